@@ -1,0 +1,106 @@
+/* ovs.h — C ABI of the B200-native oversampling sample sort (arXiv 1608.08648).
+ *
+ * The library sorts n keys of X ("sort n keys of X") by the paper's
+ * partitioning pipeline, partition-first:
+ *   ROS (random oversampling, Algorithm 2's sampling):
+ *     sample ps-1 keys uniformly at random, sort the sample, the p-1 splitters are the
+ *     (i*s)-th smallest sample keys, every key is classified by binary search over the
+ *     splitters with the (key, index) duplicate tie-break, the keys are
+ *     scattered into p buckets, every bucket is sorted independently and the buckets are
+ *     concatenated.
+ *   DRO (deterministic regular oversampling, Algorithm 1 = SqDet):
+ *     p contiguous sequences are sorted, rp regular samples per sequence, splitters are the
+ *     (i*rp)-th smallest of the rp^2 samples, each sorted sequence is split by binary search,
+ *     and bucket j gathers its p runs and is sorted (instead of the paper's p-way merge).
+ *
+ * Conventions (all entry points):
+ *   - Plain pointers and sizes only; no C++ or torch types cross this boundary, no exceptions.
+ *   - d_* pointers are DEVICE memory on the current CUDA device; h_* / report pointers are HOST.
+ *   - The caller owns every buffer.  The library never allocates device memory on the sort
+ *     path: scratch is the caller's workspace d_ws of ws_bytes >= ovs_workspace_bytes(...).
+ *   - Sorting is in place: d_keys (and d_vals) hold the input on entry, the output on return.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  All work is
+ *     enqueued on it and the call returns after enqueue (it is CUDA-graph capturable) unless
+ *     `rep` is non-NULL, in which case it synchronises `stream` and fills the report.
+ *   - Parameters are validated before any launch: a failing call does no work.
+ *   - Preconditions: f64 inputs contain no NaN and no -0.0 (BASELINE.json north_star); n < 2^32.
+ *   - Determinism: the same input bytes and parameters give bit-identical output, splitters
+ *     and bucket counts (the oracle's, see oracle/ovs_oracle.cpp).
+ */
+#ifndef OVS_H
+#define OVS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    OVS_OK = 0,
+    OVS_EINVAL = 1,      /* p == 0, NULL pointer with n > 0, n >= 2^32, bad method/flags     */
+    OVS_EDTYPE = 2,      /* unsupported dtype                                                   */
+    OVS_ESAMPLE = 3,     /* ROS: s == 0 or p*s-1 > n ("ps-1 <= n");
+                            DRO: r == 0 or r*p > floor(n/p) (distinct positions) */
+    OVS_EWORKSPACE = 4,  /* ws_bytes < ovs_workspace_bytes(...)                                  */
+    OVS_ECUDA = 5,       /* a CUDA runtime error; see ovs_last_error()                           */
+    OVS_ECAPACITY = 7,   /* distributed: output larger than out_capacity                         */
+    OVS_EINTERNAL = 8    /* a device-side check failed (reported only when rep != NULL)          */
+} ovs_status;
+
+typedef enum { OVS_U32 = 0, OVS_I32 = 1, OVS_F64 = 2 } ovs_dtype;
+typedef enum { OVS_ROS = 0, OVS_DRO = 1 } ovs_method;
+
+/* flags */
+#define OVS_DRO_PADDED_POSITIONS 1u /* DRO sample positions of the Lemma 1 proof's padding
+                                        instead of balanced segments (Q9)   */
+
+typedef struct {
+    uint32_t method; /* OVS_ROS or OVS_DRO                                                      */
+    uint32_t p;      /* number of buckets (sequences) p >= 1; p == 1 is a plain stable sort   */
+    uint32_t s;      /* ROS: oversampling factor s (sample = p*s-1 keys);
+                        DRO: r = ceil(omega_n) (T_k = r*p keys)                 */
+    uint32_t flags;  /* OVS_DRO_PADDED_POSITIONS                                              */
+    uint64_t seed;   /* ROS sample stream seed (reading Q1 of DESIGN.md); ignored by DRO       */
+} ovs_params;
+
+typedef struct {          /* optional, caller-owned HOST memory; each array pointer may be NULL */
+    void* splitter_keys;      /* p-1 keys of the input dtype                                    */
+    uint64_t* splitter_tags;  /* p-1 tags: ROS original index; DRO position in the sorted X_k
+                                 array (start_k + t)  (reading Q6)           */
+    uint64_t* bucket_counts;  /* p bucket sizes |Y_j|                                           */
+    float phase_ms[8];        /* sample, sample_sort, classify_hist, scatter, bucket_sort,
+                                 resplit, exchange, total  (CUDA events on `stream`)            */
+    uint32_t max_bucket;      /* max_j |Y_j|                                                    */
+    uint32_t kernel_launches; /* kernels this call enqueued                                     */
+    uint32_t device_status;   /* 0, or a device-side failure bit set                            */
+    uint32_t reserved;
+} ovs_report;
+
+/* Bytes of workspace ovs_sort_keys / ovs_sort_pairs_stable need for these arguments
+ * (0 on invalid arguments).  with_values: 0 keys only, 1 key-value pairs. */
+size_t ovs_workspace_bytes(size_t n, int dtype, int with_values, const ovs_params* prm);
+
+/* Sort n keys of dtype in place in d_keys (device).  Output is the unique nondecreasing
+ * permutation; splitters and bucket counts follow the method (see top). */
+int ovs_sort_keys(void* d_keys, size_t n, int dtype, const ovs_params* prm, void* d_ws, size_t ws_bytes,
+                  void* stream, ovs_report* rep);
+
+/* Stable key-value sort: d_vals (uint32, device) ride with their keys; equal keys keep their
+ * input order ("equally valued keys retain in the output their relative input order",
+ * PAPER.md:45-47). */
+int ovs_sort_pairs_stable(void* d_keys, uint32_t* d_vals, size_t n, int dtype, const ovs_params* prm, void* d_ws,
+                          size_t ws_bytes, void* stream, ovs_report* rep);
+
+/* Thread-local message of the last failure on this thread ("" if none). */
+const char* ovs_last_error(void);
+
+/* Library build identification, e.g. "ovs 0.1 sm_100a". */
+const char* ovs_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* OVS_H */

@@ -1,0 +1,159 @@
+"""Thin ctypes binding of libovs.so (include/ovs.h): argument marshalling only.
+
+Every step of the sort runs in the library's sm_100a kernels.  PyTorch is used for device
+memory (tensors, the workspace) and streams only.  There is no CPU fallback: if the
+extension is missing or no CUDA device is present the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libovs.so")
+
+OVS_OK, OVS_EINVAL, OVS_EDTYPE, OVS_ESAMPLE, OVS_EWORKSPACE, OVS_ECUDA, OVS_ECAPACITY, OVS_EINTERNAL = 0, 1, 2, 3, 4, 5, 7, 8
+OVS_U32, OVS_I32, OVS_F64 = 0, 1, 2
+OVS_ROS, OVS_DRO = 0, 1
+OVS_DRO_PADDED_POSITIONS = 1
+METHODS = {"ros": OVS_ROS, "dro": OVS_DRO}
+
+
+_NP = {OVS_U32: np.uint32, OVS_I32: np.int32, OVS_F64: np.float64}
+
+
+class Params(ctypes.Structure):
+    _fields_ = [("method", ctypes.c_uint32), ("p", ctypes.c_uint32), ("s", ctypes.c_uint32),
+                ("flags", ctypes.c_uint32), ("seed", ctypes.c_uint64)]
+
+
+class Report(ctypes.Structure):
+    _fields_ = [("splitter_keys", ctypes.c_void_p), ("splitter_tags", ctypes.c_void_p),
+                ("bucket_counts", ctypes.c_void_p), ("phase_ms", ctypes.c_float * 8),
+                ("max_bucket", ctypes.c_uint32), ("kernel_launches", ctypes.c_uint32),
+                ("device_status", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
+
+
+class OvsError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"ovs status {code}: {msg}")
+        self.code = code
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load the in-tree libovs.so; raise loudly if it has not been built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, sz, i32 = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int
+        L.ovs_workspace_bytes.restype = sz
+        L.ovs_workspace_bytes.argtypes = [sz, i32, i32, ctypes.POINTER(Params)]
+        L.ovs_sort_keys.restype = i32
+        L.ovs_sort_keys.argtypes = [vp, sz, i32, ctypes.POINTER(Params), vp, sz, vp, ctypes.POINTER(Report)]
+        L.ovs_sort_pairs_stable.restype = i32
+        L.ovs_sort_pairs_stable.argtypes = [vp, vp, sz, i32, ctypes.POINTER(Params), vp, sz, vp,
+                                            ctypes.POINTER(Report)]
+        L.ovs_last_error.restype = ctypes.c_char_p
+        L.ovs_version.restype = ctypes.c_char_p
+        _lib = L
+    return _lib
+
+
+def version() -> str:
+    return lib().ovs_version().decode()
+
+
+def _dtype_code(dt) -> int:
+    import torch
+    m = {torch.uint32: OVS_U32, torch.int32: OVS_I32, torch.float64: OVS_F64}
+    if dt not in m:
+        raise OvsError(OVS_EDTYPE, f"unsupported dtype {dt}")
+    return m[dt]
+
+
+def params(method: str = "ros", p: int = 64, s: int = 32, seed: int = 1, padded: bool = False) -> Params:
+    return Params(METHODS[method], p, s, OVS_DRO_PADDED_POSITIONS if padded else 0, seed)
+
+
+def workspace_bytes(n: int, dtype_code: int, with_values: bool, prm: Params) -> int:
+    return int(lib().ovs_workspace_bytes(n, dtype_code, 1 if with_values else 0, ctypes.byref(prm)))
+
+
+@dataclass
+class SortReport:
+    splitter_keys: np.ndarray
+    splitter_tags: np.ndarray
+    counts: np.ndarray
+    total_ms: float
+    max_bucket: int
+    kernel_launches: int
+    device_status: int
+    phase_ms: list = field(default_factory=list)
+
+
+class Sorter:
+    """Holds a workspace tensor sized for (n, dtype, kv, params) and sorts tensors in place."""
+
+    def __init__(self, n: int, dtype, with_values: bool = False, method: str = "ros", p: int = 64, s: int = 32,
+                 seed: int = 1, padded: bool = False, device=None):
+        import torch
+        self.prm = params(method, p, s, seed, padded)
+        self.dt = _dtype_code(dtype)
+        self.kv = with_values
+        self.n = n
+        nb = workspace_bytes(n, self.dt, with_values, self.prm)
+        if n > 0 and nb == 0:
+            self._raise(OVS_EINVAL)
+        self.ws = torch.empty(max(nb, 1), dtype=torch.uint8, device=device or "cuda")
+        self.ws_bytes = nb
+
+    def _raise(self, rc):
+        raise OvsError(rc, lib().ovs_last_error().decode())
+
+    def __call__(self, keys, vals=None, stream=None, report: bool = False):
+        import torch
+        assert keys.is_cuda and keys.is_contiguous() and keys.numel() == self.n
+        st = ctypes.c_void_p(stream.cuda_stream if stream is not None else torch.cuda.current_stream().cuda_stream)
+        rep = None
+        p = self.prm.p
+        kbuf = tbuf = cbuf = None
+        if report:
+            kbuf = np.zeros(max(p - 1, 0), dtype=_NP[self.dt])
+            tbuf = np.zeros(max(p - 1, 0), dtype=np.uint64)
+            cbuf = np.zeros(p, dtype=np.uint64)
+            rep = Report(kbuf.ctypes.data if kbuf.size else None, tbuf.ctypes.data if tbuf.size else None,
+                         cbuf.ctypes.data)
+        rp = ctypes.byref(rep) if rep is not None else None
+        if self.kv:
+            assert vals is not None and vals.is_cuda and vals.dtype == torch.uint32 and vals.numel() == self.n
+            rc = lib().ovs_sort_pairs_stable(keys.data_ptr(), vals.data_ptr(), self.n, self.dt, ctypes.byref(self.prm),
+                                             self.ws.data_ptr(), self.ws_bytes, st, rp)
+        else:
+            rc = lib().ovs_sort_keys(keys.data_ptr(), self.n, self.dt, ctypes.byref(self.prm), self.ws.data_ptr(),
+                                     self.ws_bytes, st, rp)
+        if rc != OVS_OK:
+            self._raise(rc)
+        if report:
+            return SortReport(kbuf, tbuf, cbuf, rep.phase_ms[7], rep.max_bucket, rep.kernel_launches,
+                              rep.device_status, list(rep.phase_ms))
+        return None
+
+
+def sort_keys(keys, method: str = "ros", p: int = 64, s: int = 32, seed: int = 1, padded: bool = False,
+              report: bool = True):
+    """Sort a CUDA tensor (uint32 / int32 / float64) in place; returns the report."""
+    return Sorter(keys.numel(), keys.dtype, False, method, p, s, seed, padded, keys.device)(keys, report=report)
+
+
+def sort_pairs_stable(keys, vals, method: str = "ros", p: int = 64, s: int = 32, seed: int = 1,
+                      padded: bool = False, report: bool = True):
+    """Stable key-value sort (uint32 values) in place; returns the report."""
+    return Sorter(keys.numel(), keys.dtype, True, method, p, s, seed, padded, keys.device)(keys, vals, report=report)

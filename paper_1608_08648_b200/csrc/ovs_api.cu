@@ -1,0 +1,150 @@
+// ovs_api.cu — the C ABI of include/ovs.h: argument validation, workspace sizing (dry run of
+// the same carving code), the enqueue of the sort, and the optional report.
+#include "ovs_engine.cuh"
+
+namespace ovs {
+thread_local std::string g_err;
+DevInfo dev_info() { return dev_info_impl(); }
+int validate(size_t n, int dtype, const ovs_params* prm) { return validate_impl(n, dtype, prm); }
+}  // namespace ovs
+
+using namespace ovs;
+
+// ------------------------------------------------------------------ C ABI
+static Out plan_dispatch(Ctx& c, void* keys, u32* vals, size_t n, int dtype, const ovs_params* prm) {
+    const bool kv = vals != nullptr || (c.dry && keys == (void*)1);
+    if (dtype == OVS_U32) return plan_u32(c, keys, vals, n, prm, kv);
+    if (dtype == OVS_I32) return plan_i32(c, keys, vals, n, prm, kv);
+    return plan_f64(c, keys, vals, n, prm, kv);
+}
+
+static int sort_impl(void* d_keys, uint32_t* d_vals, bool kv, size_t n, int dtype, const ovs_params* prm, void* d_ws,
+                     size_t ws_bytes, void* stream, ovs_report* rep) {
+    g_err.clear();
+    int v = validate(n, dtype, prm);
+    if (v != OVS_OK) { g_err = "invalid arguments"; return v; }
+    if (n > 0 && (d_keys == nullptr || (kv && d_vals == nullptr))) { g_err = "NULL buffer"; return OVS_EINVAL; }
+    try {
+        Ctx c;
+        c.di = dev_info();
+        c.st = (cudaStream_t)stream;
+        if (n == 0) {
+            if (rep) {
+                std::memset(rep->phase_ms, 0, sizeof(rep->phase_ms));
+                if (rep->bucket_counts) for (u32 j = 0; j < prm->p; ++j) rep->bucket_counts[j] = 0;
+                rep->max_bucket = 0; rep->kernel_launches = 0; rep->device_status = 0;
+            }
+            return OVS_OK;
+        }
+        // dry run: size
+        Ctx d = c;
+        d.dry = true;
+        d.take<u32>(4);           // status
+        d.take<u32>(SCAN_NT * 4); // scan block sums
+        Out od = plan_dispatch(d, kv ? (void*)1 : nullptr, nullptr, n, dtype, prm);
+        if (ws_bytes < od.ws || d_ws == nullptr) { g_err = "workspace too small"; return OVS_EWORKSPACE; }
+        // real run
+        c.dry = false;
+        c.ws = (char*)d_ws;
+        c.status = c.take<u32>(4);
+        c.bsum = c.take<u32>(SCAN_NT * 4);
+        cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+        if (rep) {
+            OVS_CK(cudaEventCreate(&ev0));
+            OVS_CK(cudaEventCreate(&ev1));
+            OVS_CK(cudaEventRecord(ev0, c.st));
+        }
+        OVS_CK(cudaMemsetAsync(c.status, 0, 16, c.st));
+        Out o = plan_dispatch(c, d_keys, kv ? d_vals : nullptr, n, dtype, prm);
+        if (rep) {
+            OVS_CK(cudaEventRecord(ev1, c.st));
+            OVS_CK(cudaStreamSynchronize(c.st));
+            float ms = 0;
+            cudaEventElapsedTime(&ms, ev0, ev1);
+            std::memset(rep->phase_ms, 0, sizeof(rep->phase_ms));
+            rep->phase_ms[7] = ms;
+            cudaEventDestroy(ev0);
+            cudaEventDestroy(ev1);
+            u32 stv = 0;
+            OVS_CK(cudaMemcpy(&stv, c.status, 4, cudaMemcpyDeviceToHost));
+            rep->device_status = stv;
+            rep->kernel_launches = c.launches;
+            const u32 p = prm->p;
+            std::vector<u64> cnt(p, 0);
+            if (p > 1) OVS_CK(cudaMemcpy(cnt.data(), o.counts, 8 * (size_t)p, cudaMemcpyDeviceToHost));
+            else cnt[0] = n;
+            u64 mx = 0;
+            for (u64 x : cnt) mx = std::max(mx, x);
+            rep->max_bucket = (u32)mx;
+            if (rep->bucket_counts) std::memcpy(rep->bucket_counts, cnt.data(), 8 * (size_t)p);
+            if (p > 1 && (rep->splitter_keys || rep->splitter_tags)) {
+                const size_t kb = dtype == OVS_F64 ? 8 : 4;
+                std::vector<unsigned char> kbuf(kb * (p - 1));
+                std::vector<u32> tbuf(p - 1);
+                OVS_CK(cudaMemcpy(kbuf.data(), o.sk, kb * (p - 1), cudaMemcpyDeviceToHost));
+                OVS_CK(cudaMemcpy(tbuf.data(), o.st, 4 * (size_t)(p - 1), cudaMemcpyDeviceToHost));
+                if (rep->splitter_keys) {
+                    // splitters are held as ordered bits: convert back to the raw dtype
+                    if (dtype == OVS_U32) std::memcpy(rep->splitter_keys, kbuf.data(), kbuf.size());
+                    else if (dtype == OVS_I32) {
+                        u32* d = (u32*)rep->splitter_keys;
+                        const u32* s = (const u32*)kbuf.data();
+                        for (u32 q = 0; q + 1 < p; ++q) d[q] = s[q] ^ 0x80000000u;
+                    } else {
+                        u64* d = (u64*)rep->splitter_keys;
+                        const u64* s = (const u64*)kbuf.data();
+                        for (u32 q = 0; q + 1 < p; ++q)
+                            d[q] = (s[q] >> 63) ? (s[q] & 0x7fffffffffffffffull) : ~s[q];
+                    }
+                }
+                if (rep->splitter_tags)
+                    for (u32 q = 0; q + 1 < p; ++q) rep->splitter_tags[q] = tbuf[q];
+            }
+            if (stv != 0) { g_err = "device-side check failed (status bits " + std::to_string(stv) + ")"; return OVS_EINTERNAL; }
+        }
+        return OVS_OK;
+    } catch (const CudaFail& e) {
+        g_err = e.what();
+        return OVS_ECUDA;
+    } catch (const StatusFail& e) {
+        g_err = e.msg;
+        return e.code;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return OVS_ECUDA;
+    }
+}
+
+extern "C" {
+
+size_t ovs_workspace_bytes(size_t n, int dtype, int with_values, const ovs_params* prm) {
+    if (validate(n, dtype, prm) != OVS_OK) return 0;
+    if (n == 0) return 0;
+    try {
+        Ctx d;
+        d.di = dev_info();
+        d.dry = true;
+        d.take<u32>(4);
+        d.take<u32>(SCAN_NT * 4);
+        Out o = plan_dispatch(d, with_values ? (void*)1 : nullptr, nullptr, n, dtype, prm);
+        return o.ws;
+    } catch (...) {
+        return 0;
+    }
+}
+
+int ovs_sort_keys(void* d_keys, size_t n, int dtype, const ovs_params* prm, void* d_ws, size_t ws_bytes, void* stream,
+                  ovs_report* rep) {
+    return sort_impl(d_keys, nullptr, false, n, dtype, prm, d_ws, ws_bytes, stream, rep);
+}
+
+int ovs_sort_pairs_stable(void* d_keys, uint32_t* d_vals, size_t n, int dtype, const ovs_params* prm, void* d_ws,
+                          size_t ws_bytes, void* stream, ovs_report* rep) {
+    return sort_impl(d_keys, d_vals, true, n, dtype, prm, d_ws, ws_bytes, stream, rep);
+}
+
+const char* ovs_last_error(void) { return g_err.c_str(); }
+
+const char* ovs_version(void) { return "ovs 0.1 sm_100a"; }
+
+}  // extern "C"

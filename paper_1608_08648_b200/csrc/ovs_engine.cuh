@@ -1,0 +1,421 @@
+#pragma once
+// ovs_engine.cuh — host orchestration (the sort engine) of the B200-native
+// partition-first oversampling sort.  Every step of the sort runs in the kernels of
+// ovs_kernels.cuh; this file only validates arguments, carves the caller's workspace and
+// enqueues kernels on the caller's stream (no host synchronisation unless a report is asked).
+#include "ovs.h"
+#include "ovs_kernels.cuh"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace ovs {
+
+
+struct CudaFail : std::runtime_error {
+    explicit CudaFail(const std::string& s) : std::runtime_error(s) {}
+};
+struct StatusFail {
+    int code;
+    std::string msg;
+};
+
+#define OVS_CK(x)                                                                                  \
+    do {                                                                                           \
+        cudaError_t e_ = (x);                                                                      \
+        if (e_ != cudaSuccess)                                                                     \
+            throw CudaFail(std::string(#x) + ": " + cudaGetErrorString(e_));                       \
+    } while (0)
+
+struct DevInfo {
+    int sms = 148;
+    int smem_optin = 232448;
+};
+
+inline DevInfo dev_info_impl() {
+    DevInfo d;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return d; }
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0) d.sms = v;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) == cudaSuccess && v > 0)
+        d.smem_optin = v;
+    cudaGetLastError();
+    return d;
+}
+
+// ------------------------------------------------------------------ workspace carving
+// The same code path sizes the workspace (dry run) and hands out pointers (real run).
+struct Ctx {
+    cudaStream_t st = nullptr;
+    char* ws = nullptr;
+    size_t off = 0;
+    bool dry = true;
+    u32 launches = 0;
+    DevInfo di;
+    u32* status = nullptr;
+    u32* bsum = nullptr;  // scratch of the device scan
+    template <class T> T* take(size_t count) {
+        off = (off + 255) & ~(size_t)255;
+        T* p = dry ? nullptr : (T*)(ws + off);
+        off += count * sizeof(T);
+        return p;
+    }
+    void check() {
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) throw CudaFail(std::string("kernel launch: ") + cudaGetErrorString(e));
+        ++launches;
+    }
+};
+
+static inline u32 cdiv(u64 a, u64 b) { return (u32)((a + b - 1) / b); }
+static inline u32 pow2_at_least(u32 x) {
+    u32 p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
+static inline u32 ilog2(u32 x) {
+    u32 l = 0;
+    while ((1u << (l + 1)) <= x) ++l;
+    return l;
+}
+
+// shared-memory capacity (items) of the bucket sorter
+template <class U, bool KV> static u32 bucket_cap(const DevInfo& di) {
+    const size_t reserve = 4096;  // static shared memory of k_bucket_sort
+    size_t avail = (size_t)di.smem_optin - bucket_smem_fixed<U, KV>() - reserve;
+    u32 cap = (u32)(avail / bucket_item_bytes<U, KV>());
+    return cap & ~31u;
+}
+template <class U, bool KV> static size_t bucket_smem(u32 cap) {
+    return bucket_smem_fixed<U, KV>() + (size_t)cap * bucket_item_bytes<U, KV>();
+}
+
+// partition tile shape: 512 threads x ITEMS per sub-tile
+constexpr int PT_NT = 512;
+template <class U, bool KV> struct PartItems { static constexpr int v = (sizeof(U) == 4 && !KV) ? 16 : 8; };
+
+// ------------------------------------------------------------------ device scan helper
+static void scan_u32(Ctx& c, const u32* in, u32* out, u32 n) {
+    const u32 nb = cdiv(n, SCAN_PER);
+    if (c.dry) return;
+    k_scan_reduce<<<nb, SCAN_NT, 0, c.st>>>(in, n, c.bsum);
+    c.check();
+    k_scan_top<<<1, SCAN_NT, 0, c.st>>>(c.bsum, nb);
+    c.check();
+    k_scan_down<<<nb, SCAN_NT, 0, c.st>>>(in, n, c.bsum, out);
+    c.check();
+}
+
+static void fill_u32(Ctx& c, u32* p, u32 v, u32 n) {
+    if (c.dry || n == 0) return;
+    k_fill_u32<<<cdiv(n, 256), 256, 0, c.st>>>(p, v, n);
+    c.check();
+}
+
+// ------------------------------------------------------------------ the sort engine
+// Sorts an array held in buffer 0 of B (codec DT: the caller's raw keys, or internal ordered
+// keys with DT_U64) into buffer 0, through a level-0 partition and the bucket sorter.
+// Splitters for level 0 come either from the caller (the contract ROS / DRO splitters) or
+// from an internal random sample (p == 1 and the internal sorts of sample arrays).
+template <int DT, bool KV> struct Engine {
+    typedef typename Codec<DT>::U U;
+
+    Ctx& c;
+    Bufs<U> B;
+    u32 n;
+    u32 cap;
+    explicit Engine(Ctx& ctx) : c(ctx) {}
+
+    struct Level0 {
+        u32 P = 1, L = 0, log2L = 0, nchunk = 0, chunk = 0;
+        U* sk = nullptr; u32* st = nullptr; u32* lut = nullptr;
+        Seg* seg = nullptr; Chunk* chunks = nullptr; u32* nchunks = nullptr;
+        u32* hist = nullptr; u32* tot = nullptr; u32* nseg = nullptr;
+    };
+    struct Lists {
+        Bucket* fit = nullptr; u32* nfit = nullptr; u32* ticket = nullptr; u32 fit_cap = 0;
+        Bucket* stack = nullptr; u32 grid = 0;
+    };
+
+    static size_t scatter_smem(u32 P, u32 L) {
+        return scatter_smem_bytes<U, KV, PartItems<U, KV>::v, PT_NT>(P, L);
+    }
+    u32 max_p_one_level() const {
+        // largest P whose scatter working set fits shared memory with L = 2P
+        u32 lo = 1, hi = 65535;
+        while (lo < hi) {
+            u32 mid = (lo + hi + 1) / 2;
+            u32 L = std::min<u32>(8192, std::max<u32>(64, pow2_at_least(2 * mid)));
+            if (scatter_smem(mid, L) + 1024 <= (size_t)c.di.smem_optin) lo = mid; else hi = mid - 1;
+        }
+        return lo;
+    }
+
+    void carve_level0(Level0& z, u32 P) {
+        z.P = P;
+        z.L = P > 1 ? std::min<u32>(8192, std::max<u32>(64, pow2_at_least(2 * P))) : 1;
+        z.log2L = ilog2(z.L);
+        // chunks: one per resident CTA slot, whole sub-tiles
+        const u32 ts = PT_NT * PartItems<U, KV>::v;
+        u32 want = (u32)c.di.sms * 2;
+        z.chunk = std::max<u32>(ts, cdiv(cdiv(n, want), ts) * ts);
+        z.nchunk = std::max<u32>(1, cdiv(n, z.chunk));
+        z.sk = c.take<U>(std::max<u32>(P, 1));
+        z.st = c.take<u32>(std::max<u32>(P, 1));
+        z.lut = c.take<u32>(z.L);
+        z.seg = c.take<Seg>(1);
+        z.chunks = c.take<Chunk>(z.nchunk);
+        z.nchunks = c.take<u32>(2);
+        z.nseg = z.nchunks + 1;
+        z.hist = c.take<u32>((size_t)z.nchunk * P);
+        z.tot = c.take<u32>(P + 1);
+    }
+    void carve_lists(Lists& l, u32 P) {
+        l.fit_cap = P + 64;
+        l.fit = c.take<Bucket>(l.fit_cap);
+        l.nfit = c.take<u32>(2);
+        l.ticket = l.nfit + 1;
+        l.grid = (u32)c.di.sms;  // bucket sorter: one CTA per SM (shared-memory bound)
+        l.stack = c.take<Bucket>((size_t)l.grid * BS_STACK);
+    }
+
+    // internal splitters for level 0 (P-1 of them) from a one-CTA sorted random sample
+    void internal_splitters(Level0& z, u64 seed) {
+        if (c.dry || z.P <= 1) return;
+        const u32 N = 8192;
+        const u32 si = std::max<u32>(1, N / z.P);
+        const size_t sm = (sizeof(U) + 4) * (size_t)N;
+        OVS_CK(cudaFuncSetAttribute(k_internal_sample<DT, KV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        k_internal_sample<DT, KV><<<1, 1024, sm, c.st>>>(B, n, z.P, si, N, seed, z.sk, z.st);
+        c.check();
+    }
+
+    // level 0: classifier build, histogram, scans, scatter buffer 0 -> buffer 1
+    void level0(Level0& z, Lists& l, u64* counts_out) {
+        if (c.dry) return;
+        const size_t sm_cls = std::max<size_t>(sizeof(U) * std::max<u32>(z.P, 1), 16);
+        OVS_CK(cudaFuncSetAttribute(k_build_cls0<U>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_cls));
+        k_build_cls0<U><<<std::max<u32>(1, std::min<u32>(z.L / 1024 + 1, 16)), 1024, sm_cls, c.st>>>(
+            z.sk, z.P, z.L, z.log2L, z.lut, z.seg, n, z.nchunk);
+        c.check();
+        k_make_chunks0<<<cdiv(z.nchunk, 256), 256, 0, c.st>>>(z.chunks, z.nchunk, n, z.chunk);
+        c.check();
+        set_pair(z.nchunks, z.nchunk, 1);  // device counts: chunks, segments
+        fill_u32(c, l.nfit, 0, 2);
+        const size_t sm_h = cls_smem_bytes<U>(z.P, z.L) + 4 * (size_t)z.P;
+        OVS_CK(cudaFuncSetAttribute(k_hist<DT, KV, true, PT_NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_h));
+        k_hist<DT, KV, true, PT_NT><<<z.nchunk, PT_NT, sm_h, c.st>>>(B, z.chunks, z.nchunks, z.seg, z.sk, z.st, z.lut,
+                                                                    z.P, z.L, z.hist);
+        c.check();
+        k_colscan<<<std::min<u32>(cdiv(z.P, 32), 4 * c.di.sms), 1024, 0, c.st>>>(z.hist, z.seg, z.nseg, z.P, z.tot);
+        c.check();
+        k_segscan<U><<<1, 1024, 0, c.st>>>(z.seg, z.nseg, z.P, z.tot, z.sk, 0, cap, l.fit, l.nfit, l.fit_cap, nullptr,
+                                          nullptr, 0, counts_out, c.status);
+        c.check();
+        constexpr int IT = PartItems<U, KV>::v;
+        const size_t sm_s = scatter_smem(z.P, z.L);
+        auto ks = k_scatter<DT, KV, true, PT_NT, IT>;
+        OVS_CK(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_s));
+        ks<<<z.nchunk, PT_NT, sm_s, c.st>>>(B, z.chunks, z.nchunks, z.seg, z.sk, z.st, z.lut, z.P, z.L, z.hist, z.tot);
+        c.check();
+    }
+
+    void set_pair(u32* p, u32 a, u32 b) {
+        k_set2<<<1, 1, 0, c.st>>>(p, a, b);
+        c.check();
+    }
+
+    void bucket_sort(Lists& l, u64 seed) {
+        if (c.dry) return;
+        const size_t sm = bucket_smem<U, KV>(cap);
+        OVS_CK(cudaFuncSetAttribute(k_bucket_sort<DT, KV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        k_bucket_sort<DT, KV><<<l.grid, BS_NT, sm, c.st>>>(l.fit, l.nfit, l.ticket, B, B.k[0], KV ? B.v[0] : nullptr,
+                                                          cap, l.stack, seed, c.status);
+        c.check();
+    }
+};
+
+// ------------------------------------------------------------------ internal sort of an array
+// keys (ordered u64) [+ u32 values, sorted stably] in buffer 0 of B; buffer 1 scratch.
+template <bool KV> struct InternalSort {
+    Engine<DT_U64, KV> e;
+    typename Engine<DT_U64, KV>::Level0 z;
+    typename Engine<DT_U64, KV>::Lists l;
+    bool direct = false;
+    InternalSort(Ctx& c, u32 n, u64* k0, u32* v0) : e(c) {
+        e.n = n;
+        e.cap = bucket_cap<u64, KV>(c.di);
+        e.B.k[0] = k0;
+        e.B.k[1] = c.take<u64>(n);
+        e.B.v[0] = v0;
+        e.B.v[1] = KV ? c.take<u32>(n) : nullptr;
+        e.B.i[0] = KV ? c.take<u32>(n) : nullptr;
+        e.B.i[1] = KV ? c.take<u32>(n) : nullptr;
+        direct = n <= e.cap;
+        u32 P = direct ? 1 : std::min<u32>(1024, cdiv(n, (u32)(e.cap * 45ull / 100)));
+        if (!direct) e.carve_level0(z, P);
+        e.carve_lists(l, direct ? 1 : P);
+    }
+    void run(u64 seed) {
+        Ctx& c = e.c;
+        if (c.dry || e.n == 0) return;
+        if (direct) {
+            if (KV) { k_iota<<<cdiv(e.n, 256), 256, 0, c.st>>>(e.B.i[0], e.n); c.check(); }
+            k_fill_u32<<<1, 2, 0, c.st>>>(l.nfit, 0, 2);
+            c.check();
+            k_push_bucket<u64><<<1, 1, 0, c.st>>>(l.fit, l.nfit, e.n);
+            c.check();
+        } else {
+            e.internal_splitters(z, seed);
+            e.level0(z, l, nullptr);
+        }
+        e.bucket_sort(l, seed);
+    }
+};
+
+// ------------------------------------------------------------------ ROS contract sort
+template <int DT, bool KV> struct RosSort {
+    typedef typename Codec<DT>::U U;
+    Ctx& c;
+    Engine<DT, KV> e;
+    typename Engine<DT, KV>::Level0 z;
+    typename Engine<DT, KV>::Lists l;
+    u32 n, p, s, m = 0, M = 0;
+    u64 seed;
+    u64* counts = nullptr;
+    // sample phase
+    u64* cand = nullptr; u32* flag = nullptr; u32* rank = nullptr; u32* keep = nullptr; u32* pos = nullptr;
+    u64* t_pack = nullptr; u64* t_key = nullptr; u32* t_tag = nullptr;
+    InternalSort<false>* cand_sort = nullptr;
+    InternalSort<false>* t_sort32 = nullptr;
+    InternalSort<true>* t_sort64 = nullptr;
+
+    RosSort(Ctx& ctx, U* keys, u32* vals, u32 n_, u32 p_, u32 s_, u64 seed_) : c(ctx), e(ctx), n(n_), p(p_), s(s_), seed(seed_) {
+        e.n = n;
+        e.cap = bucket_cap<U, KV>(c.di);
+        e.B.k[0] = keys;
+        e.B.v[0] = vals;
+        e.B.k[1] = c.take<U>(n);
+        e.B.v[1] = KV ? c.take<u32>(n) : nullptr;
+        e.B.i[0] = KV ? c.take<u32>(n) : nullptr;
+        e.B.i[1] = KV ? c.take<u32>(n) : nullptr;
+        counts = c.take<u64>(std::max<u32>(p, 1));
+        u32 P0 = p;
+        if (p == 1) P0 = n > e.cap ? std::min<u32>(std::min<u32>(1024, e.max_p_one_level()),
+                                                   cdiv(n, (u32)(e.cap * 45ull / 100))) : 1;
+        e.carve_level0(z, P0);
+        e.carve_lists(l, P0);
+        if (p > 1) {
+            m = p * s - 1;
+            // candidates: m + a margin of 8 sigma of the duplicate count + 64 (never short in
+            // practice; a shortfall is detected and reported as ST_SAMPLE_SHORT)
+            double dup = (double)m * m / (2.0 * (double)n);
+            M = (u32)std::min<double>((double)m + 8.0 * dup + 8.0 * std::sqrt(dup + 1.0) + 64.0, (double)(1u << 24) - 1);
+            cand = c.take<u64>(M);
+            flag = c.take<u32>(M);
+            rank = c.take<u32>(M);
+            keep = c.take<u32>(M);
+            pos = c.take<u32>(M);
+            cand_sort = new InternalSort<false>(c, M, cand, nullptr);
+            if (sizeof(U) == 4) {
+                t_pack = c.take<u64>(m);
+                t_sort32 = new InternalSort<false>(c, m, t_pack, nullptr);
+            } else {
+                t_key = c.take<u64>(m);
+                t_tag = c.take<u32>(m);
+                t_sort64 = new InternalSort<true>(c, m, t_key, t_tag);
+            }
+        }
+    }
+    ~RosSort() { delete cand_sort; delete t_sort32; delete t_sort64; }
+
+    void run() {
+        if (c.dry) return;
+        if (p > 1) {
+            // a1: ps-1 distinct random indices (first distinct draws of the counter stream)
+            k_ros_candidates<<<cdiv(M, 256), 256, 0, c.st>>>(cand, M, n, seed);
+            c.check();
+            cand_sort->run(seed ^ 0xc0ffee);
+            k_ros_first_flags<<<cdiv(M, 256), 256, 0, c.st>>>(cand, M, flag);
+            c.check();
+            scan_u32(c, flag, rank, M);
+            k_ros_keep<<<cdiv(M, 256), 256, 0, c.st>>>(cand, M, flag, rank, m, keep, c.status);
+            c.check();
+            scan_u32(c, keep, pos, M);
+            // a2: gather T = [(x[i], i)] in index order; a3: sort T by (key, i)
+            k_ros_gather<DT><<<cdiv(M, 256), 256, 0, c.st>>>(cand, M, keep, pos, e.B.k[0], t_pack, t_key, t_tag);
+            c.check();
+            if (t_sort32) t_sort32->run(seed ^ 0x5eed);
+            else t_sort64->run(seed ^ 0x5eed);
+            // a4: splitters S[q] = T[(q+1)s - 1]
+            k_pick_splitters<U><<<cdiv(p, 256), 256, 0, c.st>>>(t_pack, t_key, t_tag, p, s, z.sk, z.st);
+            c.check();
+        } else {
+            e.internal_splitters(z, seed);
+        }
+        // a5-a7: classify, histogram, scan, scatter;  a8: bucket sort
+        e.level0(z, l, p > 1 ? counts : nullptr);
+        e.bucket_sort(l, seed);
+    }
+};
+
+// ------------------------------------------------------------------ parameter validation
+inline int validate_impl(size_t n, int dtype, const ovs_params* prm) {
+    if (!prm) return OVS_EINVAL;
+    if (dtype != OVS_U32 && dtype != OVS_I32 && dtype != OVS_F64) return OVS_EDTYPE;
+    if (prm->p == 0) return OVS_EINVAL;
+    if (n >= 0xffffffffull) return OVS_EINVAL;
+    if (prm->method != OVS_ROS && prm->method != OVS_DRO) return OVS_EINVAL;
+    if (prm->flags & ~OVS_DRO_PADDED_POSITIONS) return OVS_EINVAL;
+    if (n == 0 || prm->p == 1) return OVS_OK;
+    if (prm->method == OVS_ROS) {
+        if (prm->s == 0) return OVS_ESAMPLE;
+        if ((uint64_t)prm->p * prm->s - 1 > n) return OVS_ESAMPLE;
+        if ((uint64_t)prm->p * prm->s > (1u << 24)) return OVS_EINVAL;
+    } else {
+        if (prm->s == 0) return OVS_ESAMPLE;
+        if ((uint64_t)prm->s * prm->p > n / prm->p) return OVS_ESAMPLE;
+    }
+    return OVS_OK;
+}
+
+struct Out {
+    void* sk = nullptr;    // device U[p-1]
+    u32* st = nullptr;     // device u32[p-1]
+    u64* counts = nullptr; // device u64[p]
+    size_t ws = 0;
+};
+
+template <int DT, bool KV>
+Out plan_or_run(Ctx& c, void* keys, u32* vals, size_t n, const ovs_params* prm) {
+    typedef typename Codec<DT>::U U;
+    if (prm->method == OVS_DRO && prm->p > 1) throw StatusFail{OVS_EINVAL, "DRO path not available in this build"};
+    RosSort<DT, KV> r(c, (U*)keys, vals, (u32)n, prm->p, prm->s, prm->seed);
+    if (prm->p > 1 && r.z.P > r.e.max_p_one_level())
+        throw StatusFail{OVS_EINVAL, "p too large for the one-level classifier in shared memory"};
+    Out o;
+    o.sk = r.z.sk;
+    o.st = r.z.st;
+    o.counts = r.counts;
+    if (!c.dry) r.run();
+    o.ws = c.off + 256;
+    return o;
+}
+
+
+// per-dtype entry points (ovs_u32.cu, ovs_i32.cu, ovs_f64.cu)
+Out plan_u32(Ctx& c, void* keys, u32* vals, size_t n, const ovs_params* prm, bool kv);
+Out plan_i32(Ctx& c, void* keys, u32* vals, size_t n, const ovs_params* prm, bool kv);
+Out plan_f64(Ctx& c, void* keys, u32* vals, size_t n, const ovs_params* prm, bool kv);
+int validate(size_t n, int dtype, const ovs_params* prm);
+DevInfo dev_info();
+extern thread_local std::string g_err;
+
+}  // namespace ovs
+

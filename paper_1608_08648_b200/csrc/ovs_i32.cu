@@ -1,0 +1,8 @@
+// ovs_i32.cu — instantiation of the sort engine for i32 keys (keys only / key-value).
+#include "ovs_engine.cuh"
+
+namespace ovs {
+Out plan_i32(Ctx& c, void* keys, u32* vals, size_t n, const ovs_params* prm, bool kv) {
+    return kv ? plan_or_run<DT_I32, true>(c, keys, vals, n, prm) : plan_or_run<DT_I32, false>(c, keys, vals, n, prm);
+}
+}  // namespace ovs

@@ -1,0 +1,1050 @@
+// ovs_kernels.cuh — sm_100a kernels of the partition-first oversampling sort.
+//
+// Citations: "P:n" = /root/reference/PAPER.md line n.  "§8(a) aN" = SURVEY.md hot-path row.
+// Design notes: all ranking inside a CTA uses shared-memory atomics
+// (measured on B200: random-address ATOMS run at LDS speed, ~9 lanes/clk/SM, while
+// __match_any_sync runs at 0.5 lanes/clk/SM — tools/ubench, profiles/r01_ubench.txt), so no
+// kernel uses warp-match ranking.  Placement inside a bucket run is therefore not in input
+// order; determinism of the OUTPUT comes from the bucket sorter, which orders every bucket
+// totally: by key (keys-only: the sorted multiset is unique) or by (key, original index)
+// (key-value: that is exactly the stable order).  Splitters and bucket counts never
+// depend on placement order.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ovs {
+// internal linkage: every translation unit gets its own copy of the kernels it launches
+namespace {
+
+typedef uint32_t u32;
+typedef uint64_t u64;
+
+// ------------------------------------------------------------------ key codecs
+// Keys are compared as "ordered bits": an order-preserving map to unsigned integers
+// (native < on u32; sign flip on i32; IEEE total order on f64 without NaN / -0, reading Q18).
+enum { DT_U32 = 0, DT_I32 = 1, DT_F64 = 2, DT_U64 = 3 /* internal, identity */ };
+
+template <int DT> struct Codec;
+template <> struct Codec<DT_U32> {
+    typedef u32 U;
+    __device__ __forceinline__ static U ord(U b) { return b; }
+    __device__ __forceinline__ static U raw(U o) { return o; }
+};
+template <> struct Codec<DT_I32> {
+    typedef u32 U;
+    __device__ __forceinline__ static U ord(U b) { return b ^ 0x80000000u; }
+    __device__ __forceinline__ static U raw(U o) { return o ^ 0x80000000u; }
+};
+template <> struct Codec<DT_F64> {
+    typedef u64 U;
+    __device__ __forceinline__ static U ord(U b) { return (b >> 63) ? ~b : (b | 0x8000000000000000ull); }
+    __device__ __forceinline__ static U raw(U o) { return (o >> 63) ? (o & 0x7fffffffffffffffull) : ~o; }
+};
+template <> struct Codec<DT_U64> {
+    typedef u64 U;
+    __device__ __forceinline__ static U ord(U b) { return b; }
+    __device__ __forceinline__ static U raw(U o) { return o; }
+};
+
+template <class U> __device__ __host__ __forceinline__ U umax_of() { return (U)~(U)0; }
+template <class U> __device__ __forceinline__ u32 bitlen(U x) {
+    return x == 0 ? 0u : (u32)(8 * sizeof(U)) - (sizeof(U) == 8 ? __clzll((long long)x) : __clz((int)x));
+}
+
+// ------------------------------------------------------------------ device status bits
+enum : u32 {
+    ST_SAMPLE_SHORT = 1u,   // fewer than ps-1 distinct candidates were drawn (never observed)
+    ST_BUCKET_OVER = 2u,    // a bucket larger than the on-chip capacity reached the sorter
+    ST_LIST_OVER = 4u,      // a work list overflowed its capacity
+};
+
+// ------------------------------------------------------------------ counter-based RNG
+// H(seed, stream, j) = SplitMix64 output number stream*2^40 + j (reading Q1).
+__device__ __forceinline__ u64 mix64(u64 z) {
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+__device__ __forceinline__ u64 rng_H(u64 seed, u64 stream, u64 j) {
+    return mix64(seed + 0x9e3779b97f4a7c15ull * ((stream << 40) + j + 1));
+}
+
+// ------------------------------------------------------------------ work descriptors
+struct Bucket {   // a contiguous range of items, in buffer `buf`, still to be sorted
+    u32 beg, len, buf, level;
+    u64 lo, hi;   // ordered-key bounds of the items (from the splitters around it)
+};
+
+struct Seg {      // a range being partitioned by one splitter set (one classifier)
+    u64 lo, hi;   // ordered-key bounds of the segment
+    u64 base;     // classifier LUT base key
+    u32 beg, len, P, shift, L, chunk0, nchunk, src, loose, pad;
+};
+
+struct Chunk { u32 beg, end, seg, pad; };
+
+// the two ping-pong buffers of a sort: buffer 0 is the caller's array (raw keys on entry,
+// raw sorted keys on exit), buffer 1 is workspace.  Key-value sorts also carry the values
+// and the original index (the stability tie-break).
+template <class U> struct Bufs {
+    U* k[2];
+    u32* v[2];
+    u32* i[2];
+};
+
+enum : u32 { BK_LOOSE = 0x80000000u };  // Bucket.level flag: lo/hi are not tight bounds
+
+// ------------------------------------------------------------------ the classifier
+// bucket(k, tag) = #{q : S[q] <lex (k, tag)}: a lower_bound over the p-1 splitters with the
+// (key, tag) tie-break.  The binary search is narrowed by a lookup
+// table over the ordered-key space: entry e covers keys [base + e<<shift, base + (e+1)<<shift)
+// and stores lo_e = #{q : S[q].key < base + e<<shift} and cnt_e = #splitter keys inside the
+// entry, so only those cnt_e splitters are binary-searched (usually 0 or 1).  The result is
+// exactly the lower_bound (tests/test_gpu_parity.py compares bucket counts with the oracle).
+template <class U> struct ClsView {
+    const U* sk; const u32* st; const u32* lut;
+    U base; u32 shift, L, P;
+};
+
+template <class U>
+__device__ __forceinline__ u32 classify(const ClsView<U>& c, U k, u32 tag) {
+    if (c.P <= 1) return 0;
+    if (k < c.base) return 0;
+    U d = (U)(k - c.base) >> c.shift;
+    if (d >= (U)c.L) return c.P - 1;
+    u32 e = c.lut[(u32)d];
+    u32 lo = e & 0xffffu, cnt = e >> 16;
+    while (cnt > 0) {
+        u32 half = cnt >> 1, mid = lo + half;
+        U s = c.sk[mid];
+        bool less = (s < k) || (s == k && c.st[mid] < tag);
+        if (less) { lo = mid + 1; cnt -= half + 1; } else { cnt = half; }
+    }
+    return lo;
+}
+
+// ------------------------------------------------------------------ block helpers
+template <int NT>
+__device__ __forceinline__ u32 block_exclusive_scan(u32 v, u32* red /*[NT/32+1]*/, u32* total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    u32 x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        u32 y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) red[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        u32 w = (lane < NT / 32) ? red[lane] : 0u;
+        u32 t = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            u32 y = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += y;
+        }
+        if (lane < NT / 32) red[lane] = t - w;
+        if (lane == NT / 32 - 1) red[NT / 32] = t;
+    }
+    __syncthreads();
+    u32 r = red[wid] + x - v;
+    if (total) *total = red[NT / 32];
+    __syncthreads();
+    return r;
+}
+
+// exclusive scan in place of a[0..cnt) (cnt arbitrary) by a CTA of NT threads; a[cnt] = total
+template <int NT>
+__device__ void block_scan_array(u32* a, u32 cnt, u32* red) {
+    u32 carry = 0;
+    for (u32 b0 = 0; b0 < cnt; b0 += NT * 4) {
+        u32 i0 = b0 + threadIdx.x * 4;
+        u32 v[4], s = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) { v[j] = (i0 + j < cnt) ? a[i0 + j] : 0u; s += v[j]; }
+        u32 tot;
+        u32 ex = block_exclusive_scan<NT>(s, red, &tot);
+        ex += carry;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (i0 + j < cnt) a[i0 + j] = ex;
+            ex += v[j];
+        }
+        carry += tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) a[cnt] = carry;
+    __syncthreads();
+}
+
+// ------------------------------------------------------------------ generic device scan (u32)
+// exclusive scan of n u32 values, 3 kernels; used by the ROS sample de-duplication (a1).
+constexpr int SCAN_NT = 1024, SCAN_PER = 4096;
+__global__ void __launch_bounds__(SCAN_NT) k_scan_reduce(const u32* in, u32 n, u32* bsum) {
+    __shared__ u32 red[SCAN_NT / 32 + 1];
+    u32 i0 = blockIdx.x * SCAN_PER + threadIdx.x * 4, s = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) s += (i0 + j < n) ? in[i0 + j] : 0u;
+    u32 tot;
+    block_exclusive_scan<SCAN_NT>(s, red, &tot);
+    if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
+}
+__global__ void __launch_bounds__(SCAN_NT) k_scan_top(u32* bsum, u32 nb) {
+    __shared__ u32 red[SCAN_NT / 32 + 1];
+    block_scan_array<SCAN_NT>(bsum, nb, red);
+}
+__global__ void __launch_bounds__(SCAN_NT) k_scan_down(const u32* in, u32 n, const u32* bsum, u32* out) {
+    __shared__ u32 red[SCAN_NT / 32 + 1];
+    u32 i0 = blockIdx.x * SCAN_PER + threadIdx.x * 4, v[4], s = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) { v[j] = (i0 + j < n) ? in[i0 + j] : 0u; s += v[j]; }
+    u32 ex = block_exclusive_scan<SCAN_NT>(s, red, nullptr) + bsum[blockIdx.x];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        if (i0 + j < n) out[i0 + j] = ex;
+        ex += v[j];
+    }
+}
+
+// ------------------------------------------------------------------ a1: ROS sample indices
+// Candidate j = (c_j << 24) | j, c_j = floor(H(seed,1,j) * n / 2^64) (reading Q1).  Sorting
+// the candidates groups equal c; the FIRST distinct draws are the candidates that are the
+// smallest j of their c-group, ranked by j.
+__global__ void k_ros_candidates(u64* cand, u32 M, u64 n, u64 seed) {
+    u32 j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= M) return;
+    u64 u = rng_H(seed, 1, j);
+    u64 c = __umul64hi(u, n);
+    cand[j] = (c << 24) | (u64)j;
+}
+
+__global__ void k_ros_first_flags(const u64* sorted, u32 M, u32* flag_by_j) {
+    u32 t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= M) return;
+    u64 x = sorted[t];
+    bool first = (t == 0) || ((sorted[t - 1] >> 24) != (x >> 24));
+    flag_by_j[(u32)(x & 0xffffffu)] = first ? 1u : 0u;
+}
+
+// keep[t] = candidate at sorted position t is one of the first m distinct draws
+__global__ void k_ros_keep(const u64* sorted, u32 M, const u32* flag_by_j, const u32* rank_by_j, u32 m,
+                           u32* keep, u32* status) {
+    u32 t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= M) return;
+    u32 j = (u32)(sorted[t] & 0xffffffu);
+    keep[t] = (flag_by_j[j] && rank_by_j[j] < m) ? 1u : 0u;
+    if (t == M - 1) {
+        u32 tot = rank_by_j[M - 1] + flag_by_j[M - 1];
+        if (tot < m) atomicOr(status, ST_SAMPLE_SHORT);
+    }
+}
+
+// a2: gather T = [(x[i], i)] in index order.  32-bit keys pack (ord key << 32 | i) into one
+// u64 (sorting it orders by (key, tag)); 64-bit keys store key and tag apart.
+template <int DT>
+__global__ void k_ros_gather(const u64* sorted, u32 M, const u32* keep, const u32* pos,
+                             const typename Codec<DT>::U* x, u64* t_pack, u64* t_key, u32* t_tag) {
+    u32 t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= M || !keep[t]) return;
+    u32 i = (u32)(sorted[t] >> 24);
+    u32 o = pos[t];
+    typename Codec<DT>::U k = Codec<DT>::ord(x[i]);
+    if (sizeof(k) == 4) {
+        t_pack[o] = ((u64)k << 32) | i;
+    } else {
+        t_key[o] = (u64)k;
+        t_tag[o] = i;
+    }
+}
+
+// a4: S[q] = T[(q+1)s - 1] (reading Q4); also the p-1 report arrays
+template <class U>
+__global__ void k_pick_splitters(const u64* t_pack, const u64* t_key, const u32* t_tag, u32 P, u32 s,
+                                 U* sk, u32* st) {
+    u32 q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q + 1 >= P) return;
+    u64 r = (u64)(q + 1) * s - 1;
+    if (sizeof(U) == 4) {
+        u64 v = t_pack[r];
+        sk[q] = (U)(v >> 32);
+        st[q] = (u32)v;
+    } else {
+        sk[q] = (U)t_key[r];
+        st[q] = t_tag[r];
+    }
+}
+
+// ------------------------------------------------------------------ classifier LUT build
+// One CTA per segment.  lo(e) = #{q : S[q].key < base + e<<shift}, cnt(e) = lo(e+1) - lo(e).
+template <class U>
+__device__ u32 count_less_key(const U* sk, u32 nsp, U thr) {
+    u32 lo = 0, cnt = nsp;
+    while (cnt > 0) {
+        u32 half = cnt >> 1, mid = lo + half;
+        if (sk[mid] < thr) { lo = mid + 1; cnt -= half + 1; } else cnt = half;
+    }
+    return lo;
+}
+
+template <class U>
+__device__ void build_lut(const U* sk, u32 P, u32 L, u32 log2L, u32* lut, U* base_out, u32* shift_out) {
+    if (P <= 1) {
+        if (threadIdx.x == 0) { *base_out = 0; *shift_out = 0; }
+        return;
+    }
+    U base = sk[0];
+    U span = sk[P - 2] - base;
+    u32 bl = bitlen<U>(span);
+    u32 shift = bl > log2L ? bl - log2L : 0u;
+    U lim = span >> shift;  // entries e > lim start above every splitter key
+    for (u32 e = threadIdx.x; e < L; e += blockDim.x) {
+        u32 a = ((U)e > lim) ? (P - 1) : count_less_key<U>(sk, P - 1, (U)(base + ((U)e << shift)));
+        u32 b = ((U)(e + 1) > lim) ? (P - 1) : count_less_key<U>(sk, P - 1, (U)(base + ((U)(e + 1) << shift)));
+        lut[e] = a | ((b - a) << 16);
+    }
+    if (threadIdx.x == 0) { *base_out = base; *shift_out = shift; }
+}
+
+// Classifier of a single segment covering [0, n) of buffer 0 (the contract level, or an
+// internal sort of a whole array): LUT entries in parallel over CTAs, splitter keys staged in
+// shared memory; CTA 0 writes the segment header.
+template <class U>
+__global__ void __launch_bounds__(1024) k_build_cls0(const U* sk, u32 P, u32 L, u32 log2L, u32* lut, Seg* seg, u32 n,
+                                                     u32 nchunk) {
+    extern __shared__ __align__(16) char smem[];
+    U* s = (U*)smem;
+    for (u32 i = threadIdx.x; i + 1 < P; i += blockDim.x) s[i] = sk[i];
+    __syncthreads();
+    U base = 0;
+    u32 shift = 0;
+    if (P > 1) {
+        base = s[0];
+        U span = s[P - 2] - base;
+        u32 bl = bitlen<U>(span);
+        shift = bl > log2L ? bl - log2L : 0u;
+        U lim = span >> shift;
+        for (u32 e = blockIdx.x * blockDim.x + threadIdx.x; e < L; e += gridDim.x * blockDim.x) {
+            u32 a = ((U)e > lim) ? (P - 1) : count_less_key<U>(s, P - 1, (U)(base + ((U)e << shift)));
+            u32 b = ((U)(e + 1) > lim) ? (P - 1) : count_less_key<U>(s, P - 1, (U)(base + ((U)(e + 1) << shift)));
+            lut[e] = a | ((b - a) << 16);
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        Seg g;
+        g.lo = (u64)umax_of<U>();  // min/max reduced by the histogram pass
+        g.hi = 0;
+        g.base = (u64)base;
+        g.beg = 0; g.len = n; g.P = P; g.shift = shift; g.L = L; g.chunk0 = 0; g.nchunk = nchunk; g.src = 0;
+        g.loose = 0; g.pad = 0;
+        *seg = g;
+    }
+}
+
+__global__ void k_make_chunks0(Chunk* ch, u32 nchunk, u32 n, u32 chunk) {
+    u32 c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= nchunk) return;
+    Chunk x;
+    x.beg = c * chunk;
+    x.end = min(n, (c + 1) * chunk);
+    x.seg = 0; x.pad = 0;
+    ch[c] = x;
+}
+
+// ------------------------------------------------------------------ partition: classifier loader
+__host__ __device__ constexpr size_t a16(size_t x) { return (x + 15) & ~(size_t)15; }
+
+template <class U>
+__device__ __forceinline__ ClsView<U> load_cls(char* sp, const Seg& sg, u32 segi, const U* sk_pool, const u32* st_pool,
+                                               const u32* lut_pool, u32 PS, u32 LS, bool load) {
+    U* sk = (U*)sp; sp += a16(sizeof(U) * (size_t)PS);
+    u32* st = (u32*)sp; sp += a16(4 * (size_t)PS);
+    u32* lut = (u32*)sp;
+    if (load) {
+        const U* gsk = sk_pool + (size_t)segi * PS;
+        const u32* gst = st_pool + (size_t)segi * PS;
+        const u32* glut = lut_pool + (size_t)segi * LS;
+        for (u32 i = threadIdx.x; i + 1 < sg.P; i += blockDim.x) { sk[i] = gsk[i]; st[i] = gst[i]; }
+        for (u32 i = threadIdx.x; i < sg.L; i += blockDim.x) lut[i] = glut[i];
+    }
+    ClsView<U> c;
+    c.sk = sk; c.st = st; c.lut = lut; c.base = (U)sg.base; c.shift = sg.shift; c.L = sg.L; c.P = sg.P;
+    return c;
+}
+template <class U> __host__ __device__ constexpr size_t cls_smem_bytes(u32 PS, u32 LS) {
+    return a16(sizeof(U) * (size_t)PS) + a16(4 * (size_t)PS) + a16(4 * (size_t)LS);
+}
+
+template <class U> __device__ __forceinline__ U shfl_xor_any(U x, int o) {
+    if (sizeof(U) == 8) return (U)__shfl_xor_sync(0xffffffffu, (unsigned long long)x, o);
+    return (U)__shfl_xor_sync(0xffffffffu, (u32)x, o);
+}
+
+// ------------------------------------------------------------------ a5+a6: classify + histogram
+// Persistent CTAs over chunks; per-chunk histogram row hist[c*PS + b].  LEVEL0 reads buffer 0
+// through the codec (the caller's raw keys) with tag = index (ROS: the original index,
+// P:524-532); later levels read ordered keys with tag = position (keys only) or the carried
+// original index (key-value).
+template <int DT, bool KV, bool LEVEL0, int NT>
+__global__ void __launch_bounds__(NT) k_hist(Bufs<typename Codec<DT>::U> B, const Chunk* chunks, const u32* nchunks,
+                                             Seg* segs, const typename Codec<DT>::U* sk_pool, const u32* st_pool,
+                                             const u32* lut_pool, u32 PS, u32 LS, u32* hist) {
+    typedef typename Codec<DT>::U U;
+    extern __shared__ __align__(16) char smem[];
+    const u32 nc = *nchunks;
+    u32 loaded = 0xffffffffu;
+    for (u32 c = blockIdx.x; c < nc; c += gridDim.x) {
+        const Chunk ch = chunks[c];
+        const Seg sg = segs[ch.seg];
+        ClsView<U> cls = load_cls<U>(smem, sg, ch.seg, sk_pool, st_pool, lut_pool, PS, LS, loaded != ch.seg);
+        loaded = ch.seg;
+        u32* h = (u32*)(smem + cls_smem_bytes<U>(PS, LS));
+        for (u32 i = threadIdx.x; i < sg.P; i += NT) h[i] = 0;
+        __syncthreads();
+        const U* src = B.k[LEVEL0 ? 0 : sg.src];
+        const u32* isrc = (KV && !LEVEL0) ? B.i[sg.src] : nullptr;
+        U mn = umax_of<U>(), mx = 0;
+        u32 i = ch.beg + threadIdx.x;
+        for (; i + 3 * NT < ch.end; i += 4 * NT) {
+            U k[4];
+            u32 tg[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                k[j] = LEVEL0 ? Codec<DT>::ord(__ldcs(src + i + j * NT)) : src[i + j * NT];
+                tg[j] = (KV && !LEVEL0) ? isrc[i + j * NT] : i + j * NT;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                atomicAdd(&h[classify<U>(cls, k[j], tg[j])], 1u);
+                if (LEVEL0) { mn = min(mn, k[j]); mx = max(mx, k[j]); }
+            }
+        }
+        for (; i < ch.end; i += NT) {
+            U k = LEVEL0 ? Codec<DT>::ord(src[i]) : src[i];
+            u32 tg = (KV && !LEVEL0) ? isrc[i] : i;
+            atomicAdd(&h[classify<U>(cls, k, tg)], 1u);
+            if (LEVEL0) { mn = min(mn, k); mx = max(mx, k); }
+        }
+        __syncthreads();
+        u32* row = hist + (size_t)c * PS;
+        for (u32 b = threadIdx.x; b < sg.P; b += NT) row[b] = h[b];
+        if (LEVEL0) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) { mn = min(mn, shfl_xor_any(mn, o)); mx = max(mx, shfl_xor_any(mx, o)); }
+            if ((threadIdx.x & 31) == 0 && ch.end > ch.beg) {
+                atomicMin((unsigned long long*)&segs[0].lo, (unsigned long long)mn);
+                atomicMax((unsigned long long*)&segs[0].hi, (unsigned long long)mx);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------ a6: column scan
+// Work item = (segment s, 32 buckets): exclusive prefix over the segment's chunks of
+// hist[c][b], in place; totals -> tot[s*(PS+1) + b].  Warp w owns a contiguous slice of
+// chunks, lane = bucket.
+__global__ void __launch_bounds__(1024) k_colscan(u32* hist, const Seg* segs, const u32* nsegs, u32 PS, u32* tot) {
+    __shared__ u32 part[32][33];
+    const u32 bgroups = (PS + 31) / 32;
+    const u32 nitems = *nsegs * bgroups;
+    const u32 lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (u32 it = blockIdx.x; it < nitems; it += gridDim.x) {
+        const u32 s = it / bgroups, bg = it % bgroups;
+        const Seg sg = segs[s];
+        if (bg * 32 >= sg.P) continue;  // uniform across the CTA
+        const u32 b = bg * 32 + lane;
+        const u32 per = (sg.nchunk + 31) / 32;
+        const u32 c0 = sg.chunk0 + min(sg.nchunk, w * per), c1 = sg.chunk0 + min(sg.nchunk, (w + 1) * per);
+        u32 sum = 0;
+        if (b < sg.P)
+            for (u32 c = c0; c < c1; ++c) sum += hist[(size_t)c * PS + b];
+        part[w][lane] = sum;
+        __syncthreads();
+        if (w == 0) {
+            u32 run = 0;
+            for (int k = 0; k < 32; ++k) { u32 v = part[k][lane]; part[k][lane] = run; run += v; }
+            if (b < sg.P) tot[(size_t)s * (PS + 1) + b] = run;
+        }
+        __syncthreads();
+        if (b < sg.P) {
+            u32 run = part[w][lane];
+            for (u32 c = c0; c < c1; ++c) {
+                u32 v = hist[(size_t)c * PS + b];
+                hist[(size_t)c * PS + b] = run;
+                run += v;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------ a6: segment scan + lists
+// Per segment: bucket starts = exclusive scan of the totals (in place in tot[]); every
+// non-empty bucket becomes a Bucket on `big` (len > cap and big != NULL) or `fit`.
+// counts_out (level 0 of the contract) receives the bucket counts.
+template <class U>
+__global__ void __launch_bounds__(1024) k_segscan(const Seg* segs, const u32* nsegs, u32 PS, u32* tot_pool,
+                                                  const U* sk_pool, u32 level, u32 cap, Bucket* fit, u32* nfit,
+                                                  u32 fit_cap, Bucket* big, u32* nbig, u32 big_cap, u64* counts_out,
+                                                  u32* status) {
+    __shared__ u32 red[33];
+    const u32 ns = *nsegs;
+    const u32 lane = threadIdx.x & 31;
+    for (u32 s = blockIdx.x; s < ns; s += gridDim.x) {
+        const Seg sg = segs[s];
+        u32* tot = tot_pool + (size_t)s * (PS + 1);
+        if (counts_out)
+            for (u32 b = threadIdx.x; b < sg.P; b += 1024) counts_out[b] = tot[b];
+        __syncthreads();
+        block_scan_array<1024>(tot, sg.P, red);
+        const U* sk = sk_pool + (size_t)s * PS;
+        for (u32 b0 = 0; b0 < sg.P; b0 += 1024) {
+            const u32 b = b0 + threadIdx.x;
+            u32 st = 0, len = 0;
+            if (b < sg.P) { st = tot[b]; len = tot[b + 1] - st; }
+            const bool isbig = big != nullptr && len > cap, isfit = len > 0 && !isbig;
+            const u32 mf = __ballot_sync(0xffffffffu, isfit), mb = __ballot_sync(0xffffffffu, isbig);
+            u32 of = 0, ob = 0;
+            if (lane == 0) {
+                if (mf) of = atomicAdd(nfit, __popc(mf));
+                if (mb) ob = atomicAdd(nbig, __popc(mb));
+            }
+            of = __shfl_sync(0xffffffffu, of, 0) + __popc(mf & ((1u << lane) - 1));
+            ob = __shfl_sync(0xffffffffu, ob, 0) + __popc(mb & ((1u << lane) - 1));
+            if (isfit || isbig) {
+                Bucket bk;
+                bk.beg = sg.beg + st; bk.len = len; bk.buf = 1 - sg.src;
+                bk.level = level | (((b == 0 || b + 1 == sg.P) && sg.loose) ? BK_LOOSE : 0u);
+                bk.lo = (b == 0) ? sg.lo : (u64)sk[b - 1];
+                bk.hi = (b + 1 == sg.P) ? sg.hi : (u64)sk[b];
+                if (isfit) { if (of < fit_cap) fit[of] = bk; else atomicOr(status, ST_LIST_OVER); }
+                else { if (ob < big_cap) big[ob] = bk; else atomicOr(status, ST_LIST_OVER); }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------ a7: scatter
+// Persistent CTAs over chunks, sub-tiles of NT*ITEMS items: classify, rank inside the sub-tile
+// with shared atomics, stage the sub-tile in bucket order in shared memory, then write every
+// bucket run contiguously at its cursor.  Cursors start at segment base + bucket start +
+// the chunk's column-scan offset, so chunks write disjoint, deterministic ranges.
+template <class U, bool KV, int ITEMS, int NT>
+__host__ __device__ constexpr size_t scatter_smem_bytes(u32 PS, u32 LS) {
+    return cls_smem_bytes<U>(PS, LS) + (sizeof(U) + (KV ? 8 : 0) + 2) * (size_t)NT * ITEMS +
+           3 * a16(4 * ((size_t)PS + 1));
+}
+
+template <int DT, bool KV, bool LEVEL0, int NT, int ITEMS>
+__global__ void __launch_bounds__(NT) k_scatter(Bufs<typename Codec<DT>::U> B, const Chunk* chunks, const u32* nchunks,
+                                                const Seg* segs, const typename Codec<DT>::U* sk_pool,
+                                                const u32* st_pool, const u32* lut_pool, u32 PS, u32 LS,
+                                                const u32* hist, const u32* tot_pool) {
+    typedef typename Codec<DT>::U U;
+    constexpr int TS = NT * ITEMS;
+    extern __shared__ __align__(16) char smem[];
+    __shared__ u32 red[NT / 32 + 1];
+    const u32 nc = *nchunks;
+    u32 loaded = 0xffffffffu;
+    char* sp0 = smem + cls_smem_bytes<U>(PS, LS);
+    U* stk = (U*)sp0; sp0 += sizeof(U) * TS;
+    u32* stv = nullptr;
+    u32* sti = nullptr;
+    if (KV) { stv = (u32*)sp0; sp0 += 4 * TS; sti = (u32*)sp0; sp0 += 4 * TS; }
+    u32* cur = (u32*)sp0; sp0 += a16(4 * ((size_t)PS + 1));
+    u32* work = (u32*)sp0; sp0 += a16(4 * ((size_t)PS + 1));
+    u32* dbase = (u32*)sp0; sp0 += a16(4 * ((size_t)PS + 1));
+    unsigned short* stb = (unsigned short*)sp0;
+    for (u32 c = blockIdx.x; c < nc; c += gridDim.x) {
+        const Chunk ch = chunks[c];
+        const Seg sg = segs[ch.seg];
+        ClsView<U> cls = load_cls<U>(smem, sg, ch.seg, sk_pool, st_pool, lut_pool, PS, LS, loaded != ch.seg);
+        loaded = ch.seg;
+        const u32 P = sg.P;
+        const u32* hrow = hist + (size_t)c * PS;
+        const u32* bst = tot_pool + (size_t)ch.seg * (PS + 1);
+        for (u32 b = threadIdx.x; b < P; b += NT) cur[b] = sg.beg + bst[b] + hrow[b];
+        const u32 srcb = LEVEL0 ? 0 : sg.src, dstb = 1 - srcb;
+        const U* src = B.k[srcb];
+        const u32* vsrc = KV ? B.v[srcb] : nullptr;
+        const u32* isrc = (KV && !LEVEL0) ? B.i[srcb] : nullptr;
+        U* dst = B.k[dstb];
+        u32* vdst = KV ? B.v[dstb] : nullptr;
+        u32* idst = KV ? B.i[dstb] : nullptr;
+        for (u32 t0 = ch.beg; t0 < ch.end; t0 += TS) {
+            const u32 nt = min((u32)TS, ch.end - t0);
+            for (u32 b = threadIdx.x; b < P; b += NT) work[b] = 0;
+            __syncthreads();
+            U k[ITEMS];
+            u32 v[ITEMS], ix[ITEMS], bk[ITEMS], rk[ITEMS];
+#pragma unroll
+            for (int j = 0; j < ITEMS; ++j) {
+                const u32 o = j * NT + threadIdx.x;
+                if (o < nt) {
+                    const u32 i = t0 + o;
+                    k[j] = LEVEL0 ? Codec<DT>::ord(__ldcs(src + i)) : src[i];
+                    if (KV) { v[j] = vsrc[i]; ix[j] = LEVEL0 ? i : isrc[i]; }
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < ITEMS; ++j) {
+                const u32 o = j * NT + threadIdx.x;
+                if (o < nt) {
+                    const u32 tag = KV ? ix[j] : t0 + o;
+                    bk[j] = classify<U>(cls, k[j], tag);
+                    rk[j] = atomicAdd(&work[bk[j]], 1u);
+                }
+            }
+            __syncthreads();
+            block_scan_array<NT>(work, P, red);
+#pragma unroll
+            for (int j = 0; j < ITEMS; ++j) {
+                const u32 o = j * NT + threadIdx.x;
+                if (o < nt) {
+                    const u32 pos = work[bk[j]] + rk[j];
+                    stk[pos] = k[j];
+                    stb[pos] = (unsigned short)bk[j];
+                    if (KV) { stv[pos] = v[j]; sti[pos] = ix[j]; }
+                }
+            }
+            for (u32 b = threadIdx.x; b < P; b += NT) {
+                const u32 st = work[b], cnt = work[b + 1] - st;
+                dbase[b] = cur[b] - st;
+                cur[b] += cnt;
+            }
+            __syncthreads();
+            for (u32 o = threadIdx.x; o < nt; o += NT) {
+                const u32 d = dbase[stb[o]] + o;
+                dst[d] = stk[o];
+                if (KV) { vdst[d] = stv[o]; idst[d] = sti[o]; }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// ------------------------------------------------------------------ CTA bitonic sort of (key, tag)
+// N a power of two, records in shared memory; ascending by (key, tag).
+template <class U>
+__device__ void cta_bitonic_kt(U* tk, u32* tt, u32 N) {
+    for (u32 kk = 2; kk <= N; kk <<= 1) {
+        for (u32 j = kk >> 1; j > 0; j >>= 1) {
+            for (u32 t = threadIdx.x; t < N; t += blockDim.x) {
+                const u32 o = t ^ j;
+                if (o > t) {
+                    const bool asc = (t & kk) == 0;
+                    const bool gt = tk[t] > tk[o] || (tk[t] == tk[o] && tt[t] > tt[o]);
+                    if (gt == asc) {
+                        U a = tk[t]; tk[t] = tk[o]; tk[o] = a;
+                        u32 b = tt[t]; tt[t] = tt[o]; tt[o] = b;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// ------------------------------------------------------------------ internal splitters
+// Splitters of an internal sort of a whole array of n items (not part of the contract; used
+// for p == 1 and for sorting the sample / candidate arrays): a random sample with
+// replacement of P*si-1 (key, index) records, sorted in one CTA, S[q] = T[(q+1)si - 1].
+template <int DT, bool KV>
+__global__ void __launch_bounds__(1024) k_internal_sample(Bufs<typename Codec<DT>::U> B, u32 n, u32 P, u32 si, u32 N,
+                                                          u64 seed, typename Codec<DT>::U* sk, u32* st) {
+    typedef typename Codec<DT>::U U;
+    extern __shared__ __align__(16) char smem[];
+    U* tk = (U*)smem;
+    u32* tt = (u32*)(smem + sizeof(U) * N);
+    const u32 m = P * si - 1;
+    for (u32 j = threadIdx.x; j < N; j += blockDim.x) {
+        if (j < m) {
+            const u32 pos = (u32)__umul64hi(rng_H(seed, 63, j), (u64)n);
+            tk[j] = Codec<DT>::ord(B.k[0][pos]);
+            tt[j] = pos;
+        } else {
+            tk[j] = umax_of<U>();
+            tt[j] = 0xffffffffu;
+        }
+    }
+    __syncthreads();
+    cta_bitonic_kt<U>(tk, tt, N);
+    for (u32 q = threadIdx.x; q + 1 < P; q += blockDim.x) {
+        sk[q] = tk[(q + 1) * si - 1];
+        st[q] = tt[(q + 1) * si - 1];
+    }
+}
+
+// ------------------------------------------------------------------ a8: bucket sort
+// Persistent CTAs pull buckets from the list.  A bucket of len <= cap is sorted on chip:
+//  1. histogram of the top digit of (key - lo) [key-value: of the composite (key, index)],
+//  2. scatter from global into shared memory grouped by digit,
+//  3. every group sorted by one warp with a register bitonic network (<= 512 items) or, for
+//     larger groups, by the CTA with an in-place bitonic network in shared memory,
+//  4. sorted groups written to the output at the bucket's final position (raw codec).
+// All global reads of a bucket finish before any write, so the source may alias the output.
+// A bucket over the capacity is re-split by the CTA itself ("sorted ... recursively by this
+// same extended method"): a random sample of it gives <= 64 sub-splitters, the
+// bucket is partitioned into the other buffer and the sub-buckets go on a per-CTA stack.
+constexpr int BS_NT = 512;
+constexpr int BS_NGMAX = 2048;
+constexpr int BS_BIGMAX = 128;
+constexpr int BS_STACK = 256;
+constexpr u32 BS_SPMAX = 64;
+constexpr u32 BS_SI = 32;
+constexpr u32 BS_SSMAX = BS_SPMAX * BS_SI;
+
+template <class U, bool KV> struct Elem;
+template <class U> struct Elem<U, false> {
+    U k;
+    __device__ __forceinline__ bool lt(const Elem& o) const { return k < o.k; }
+    __device__ __forceinline__ static Elem inf() { Elem e; e.k = umax_of<U>(); return e; }
+    __device__ __forceinline__ Elem shfl_xor(int m) const { Elem e; e.k = shfl_xor_any(k, m); return e; }
+};
+template <class U> struct Elem<U, true> {
+    U k; u32 i, v;
+    __device__ __forceinline__ bool lt(const Elem& o) const { return k < o.k || (k == o.k && i < o.i); }
+    __device__ __forceinline__ static Elem inf() { Elem e; e.k = umax_of<U>(); e.i = 0xffffffffu; e.v = 0; return e; }
+    __device__ __forceinline__ Elem shfl_xor(int m) const {
+        Elem e;
+        e.k = shfl_xor_any(k, m);
+        e.i = __shfl_xor_sync(0xffffffffu, i, m);
+        e.v = __shfl_xor_sync(0xffffffffu, v, m);
+        return e;
+    }
+};
+
+// bitonic sort of 32*R elements held as a[r] at lane: element index e = r*32 + lane
+template <class E, int R>
+__device__ __forceinline__ void warp_bitonic(E (&a)[R]) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int k = 2; k <= 32 * R; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j >= 32) {
+                const int jr = j >> 5;
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    if ((r & jr) == 0) {
+                        const int e = r * 32 + lane;
+                        const bool asc = (e & k) == 0;
+                        E x = a[r], y = a[r | jr];
+                        const bool sw = asc ? y.lt(x) : x.lt(y);
+                        if (sw) { a[r] = y; a[r | jr] = x; }
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int e = r * 32 + lane;
+                    const bool asc = (e & k) == 0;
+                    const bool lower = (lane & j) == 0;
+                    E o = a[r].shfl_xor(j);
+                    const bool keep_min = (lower == asc);
+                    const bool take = keep_min ? o.lt(a[r]) : a[r].lt(o);
+                    if (take) a[r] = o;
+                }
+            }
+        }
+    }
+}
+
+template <class U, bool KV> struct BucketSmem {
+    U* k; u32* i; u32* v; u32* gst; u32* cur;
+};
+
+template <int DT, bool KV, int R>
+__device__ __forceinline__ void warp_sort_group(const BucketSmem<typename Codec<DT>::U, KV>& S, u32 gs, u32 len,
+                                                typename Codec<DT>::U* okeys, u32* ovals, u32 obeg) {
+    typedef typename Codec<DT>::U U;
+    typedef Elem<U, KV> E;
+    const int lane = threadIdx.x & 31;
+    E a[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const u32 e = r * 32 + lane;
+        if (e < len) {
+            a[r].k = S.k[gs + e];
+            if constexpr (KV) { a[r].i = S.i[gs + e]; a[r].v = S.v[gs + e]; }
+        } else {
+            a[r] = E::inf();
+        }
+    }
+    warp_bitonic<E, R>(a);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const u32 e = r * 32 + lane;
+        if (e < len) {
+            okeys[obeg + gs + e] = Codec<DT>::raw(a[r].k);
+            if constexpr (KV) ovals[obeg + gs + e] = a[r].v;
+        }
+    }
+}
+
+template <class U, bool KV>
+__device__ __forceinline__ void smem_cex(const BucketSmem<U, KV>& S, u32 x, u32 y) {
+    bool gt;
+    if constexpr (KV) gt = S.k[y] < S.k[x] || (S.k[y] == S.k[x] && S.i[y] < S.i[x]);
+    else gt = S.k[y] < S.k[x];
+    if (gt) {
+        U t = S.k[x]; S.k[x] = S.k[y]; S.k[y] = t;
+        if constexpr (KV) {
+            u32 a = S.i[x]; S.i[x] = S.i[y]; S.i[y] = a;
+            u32 b = S.v[x]; S.v[x] = S.v[y]; S.v[y] = b;
+        }
+    }
+}
+
+template <class U> __device__ __forceinline__ u32 lower_bound_kt(const U* sk, const u32* st, u32 nsp, U k, u32 tag) {
+    u32 lo = 0, cnt = nsp;
+    while (cnt > 0) {
+        const u32 half = cnt >> 1, mid = lo + half;
+        const bool less = sk[mid] < k || (sk[mid] == k && st[mid] < tag);
+        if (less) { lo = mid + 1; cnt -= half + 1; } else cnt = half;
+    }
+    return lo;
+}
+
+template <class U, bool KV> __host__ __device__ constexpr size_t bucket_smem_fixed() {
+    return 4 * (2 * (size_t)BS_NGMAX + 4);
+}
+template <class U, bool KV> __host__ __device__ constexpr size_t bucket_item_bytes() {
+    return sizeof(U) + (KV ? 8 : 0);
+}
+
+template <int DT, bool KV>
+__global__ void __launch_bounds__(BS_NT) k_bucket_sort(const Bucket* list, const u32* nlist, u32* ticket,
+                                                        Bufs<typename Codec<DT>::U> B, typename Codec<DT>::U* okeys,
+                                                        u32* ovals, u32 cap, Bucket* stack_pool, u64 seed,
+                                                        u32* status) {
+    typedef typename Codec<DT>::U U;
+    extern __shared__ __align__(16) char smem[];
+    __shared__ u32 red[BS_NT / 32 + 1];
+    __shared__ u32 s_work, s_nbig, s_sp;
+    __shared__ u32 s_big[BS_BIGMAX];
+    __shared__ U s_mn[BS_NT / 32], s_mx[BS_NT / 32];
+    __shared__ U sp_k[BS_SPMAX];
+    __shared__ u32 sp_t[BS_SPMAX], sp_cnt[BS_SPMAX + 1], sp_cur[BS_SPMAX];
+    BucketSmem<U, KV> S;
+    {
+        char* sp = smem;
+        S.gst = (u32*)sp; sp += 4 * (BS_NGMAX + 4);
+        S.cur = (u32*)sp; sp += 4 * BS_NGMAX;
+        S.k = (U*)sp; sp += sizeof(U) * (size_t)cap;
+        if (KV) { S.i = (u32*)sp; sp += 4 * (size_t)cap; S.v = (u32*)sp; sp += 4 * (size_t)cap; }
+    }
+    Bucket* stk = stack_pool + (size_t)blockIdx.x * BS_STACK;
+    const u32 nl = *nlist;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (;;) {
+        if (threadIdx.x == 0) {
+            s_work = atomicAdd(ticket, 1u);
+            if (s_work < nl) { stk[0] = list[s_work]; s_sp = 1; }
+        }
+        __syncthreads();
+        if (s_work >= nl) break;
+        while (s_sp > 0) {
+            const Bucket bk = stk[s_sp - 1];
+            __syncthreads();
+            if (threadIdx.x == 0) { s_sp -= 1; s_nbig = 0; }
+            const u32 m = bk.len;
+            const U* src = B.k[bk.buf];
+            const u32* vsrc = KV ? B.v[bk.buf] : nullptr;
+            const u32* isrc = KV ? B.i[bk.buf] : nullptr;
+            if (m > cap) {
+                // ---------------- CTA-local re-split of an oversized bucket
+                const u32 part = (u32)((cap * 45ull) / 100);
+                u32 P = (m + part - 1) / part;
+                P = max(2u, min(BS_SPMAX, P));
+                const u32 ms = P * BS_SI - 1;
+                U* tk = S.k;
+                u32* tt = (u32*)(smem + bucket_smem_fixed<U, KV>() + sizeof(U) * BS_SSMAX);
+                for (u32 j = threadIdx.x; j < BS_SSMAX; j += BS_NT) {
+                    if (j < ms) {
+                        const u64 u = rng_H(seed ^ ((u64)bk.beg * 0x9e3779b97f4a7c15ull), 64 + (bk.level & 0xffffu), j);
+                        const u32 o = (u32)__umul64hi(u, (u64)m);
+                        tk[j] = src[bk.beg + o];
+                        tt[j] = KV ? isrc[bk.beg + o] : bk.beg + o;
+                    } else {
+                        tk[j] = umax_of<U>();
+                        tt[j] = 0xffffffffu;
+                    }
+                }
+                __syncthreads();
+                cta_bitonic_kt<U>(tk, tt, BS_SSMAX);
+                if (threadIdx.x + 1 < P) {
+                    sp_k[threadIdx.x] = tk[(threadIdx.x + 1) * BS_SI - 1];
+                    sp_t[threadIdx.x] = tt[(threadIdx.x + 1) * BS_SI - 1];
+                }
+                if (threadIdx.x <= P) sp_cnt[threadIdx.x] = 0;
+                __syncthreads();
+                for (u32 o = threadIdx.x; o < m; o += BS_NT) {
+                    const U k = src[bk.beg + o];
+                    const u32 tg = KV ? isrc[bk.beg + o] : bk.beg + o;
+                    atomicAdd(&sp_cnt[lower_bound_kt<U>(sp_k, sp_t, P - 1, k, tg)], 1u);
+                }
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    u32 run = 0;
+                    for (u32 b = 0; b < P; ++b) { const u32 c = sp_cnt[b]; sp_cnt[b] = run; sp_cur[b] = run; run += c; }
+                    sp_cnt[P] = run;
+                }
+                __syncthreads();
+                const u32 db = 1 - bk.buf;
+                for (u32 o = threadIdx.x; o < m; o += BS_NT) {
+                    const U k = src[bk.beg + o];
+                    const u32 tg = KV ? isrc[bk.beg + o] : bk.beg + o;
+                    const u32 b = lower_bound_kt<U>(sp_k, sp_t, P - 1, k, tg);
+                    const u32 d = bk.beg + atomicAdd(&sp_cur[b], 1u);
+                    B.k[db][d] = k;
+                    if (KV) { B.v[db][d] = vsrc[bk.beg + o]; B.i[db][d] = tg; }
+                }
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    u32 sp = s_sp;
+                    for (int b = (int)P - 1; b >= 0; --b) {
+                        const u32 len = sp_cnt[b + 1] - sp_cnt[b];
+                        if (len == 0) continue;
+                        if (sp >= BS_STACK) { atomicOr(status, ST_LIST_OVER); break; }
+                        Bucket nb;
+                        nb.beg = bk.beg + sp_cnt[b]; nb.len = len; nb.buf = db;
+                        const bool edge = (b == 0 || b + 1 == (int)P);
+                        nb.level = ((bk.level & 0xffffu) + 1) | ((edge && (bk.level & BK_LOOSE)) ? BK_LOOSE : 0u);
+                        nb.lo = (b == 0) ? bk.lo : (u64)sp_k[b - 1];
+                        nb.hi = (b + 1 == (int)P) ? bk.hi : (u64)sp_k[b];
+                        stk[sp++] = nb;
+                    }
+                    s_sp = sp;
+                }
+                __syncthreads();
+                continue;
+            }
+            // ---------------- on-chip sort of a bucket that fits
+            U lo = (U)bk.lo, hi = (U)bk.hi;
+            if (bk.level & BK_LOOSE) {
+                U mn = umax_of<U>(), mx = 0;
+                for (u32 o = threadIdx.x; o < m; o += BS_NT) { const U k = src[bk.beg + o]; mn = min(mn, k); mx = max(mx, k); }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) { mn = min(mn, shfl_xor_any(mn, o)); mx = max(mx, shfl_xor_any(mx, o)); }
+                if (lane == 0) { s_mn[wid] = mn; s_mx[wid] = mx; }
+                __syncthreads();
+                mn = s_mn[0]; mx = s_mx[0];
+                for (int q = 1; q < BS_NT / 32; ++q) { mn = min(mn, s_mn[q]); mx = max(mx, s_mx[q]); }
+                lo = mn; hi = mx;
+                __syncthreads();
+            }
+            u32 ng = 1;
+            while (ng < (u32)BS_NGMAX && ng * 48 < m) ng <<= 1;
+            const u32 lg = 31 - __clz(ng);
+            const u32 rb = bitlen<U>((U)(hi - lo)) + (KV ? 32u : 0u);
+            const u32 sh = rb > lg ? rb - lg : 0u;
+            auto digit = [&](U k, u32 ix) -> u32 {
+                u32 d;
+                if constexpr (KV) {
+                    if (sizeof(U) == 4) d = (u32)((((u64)(k - lo)) << 32 | ix) >> sh);
+                    else d = (u32)((((unsigned __int128)(u64)(k - lo)) << 32 | ix) >> sh);
+                } else {
+                    d = (u32)((U)(k - lo) >> sh);
+                }
+                return min(d, ng - 1);  // memory safety only: the bounds guarantee d < ng
+            };
+            for (u32 g = threadIdx.x; g < ng; g += BS_NT) S.cur[g] = 0;
+            __syncthreads();
+            for (u32 o = threadIdx.x; o < m; o += BS_NT) {
+                const U k = src[bk.beg + o];
+                const u32 ix = KV ? isrc[bk.beg + o] : 0u;
+                atomicAdd(&S.cur[digit(k, ix)], 1u);
+            }
+            __syncthreads();
+            for (u32 g = threadIdx.x; g < ng; g += BS_NT) S.gst[g] = S.cur[g];
+            __syncthreads();
+            block_scan_array<BS_NT>(S.gst, ng, red);
+            for (u32 g = threadIdx.x; g < ng; g += BS_NT) S.cur[g] = S.gst[g];
+            __syncthreads();
+            for (u32 o = threadIdx.x; o < m; o += BS_NT) {
+                const U k = src[bk.beg + o];
+                u32 ix = 0, vv = 0;
+                if (KV) { ix = isrc[bk.beg + o]; vv = vsrc[bk.beg + o]; }
+                const u32 pos = atomicAdd(&S.cur[digit(k, ix)], 1u);
+                S.k[pos] = k;
+                if (KV) { S.i[pos] = ix; S.v[pos] = vv; }
+            }
+            __syncthreads();
+            for (u32 g = wid; g < ng; g += BS_NT / 32) {
+                const u32 gs = S.gst[g], len = S.gst[g + 1] - gs;
+                if (len == 0) continue;
+                if (len <= 32) warp_sort_group<DT, KV, 1>(S, gs, len, okeys, ovals, bk.beg);
+                else if (len <= 64) warp_sort_group<DT, KV, 2>(S, gs, len, okeys, ovals, bk.beg);
+                else if (len <= 128) warp_sort_group<DT, KV, 4>(S, gs, len, okeys, ovals, bk.beg);
+                else if (len <= 256) warp_sort_group<DT, KV, 8>(S, gs, len, okeys, ovals, bk.beg);
+                else if (len <= 512) warp_sort_group<DT, KV, 16>(S, gs, len, okeys, ovals, bk.beg);
+                else if (lane == 0) {
+                    const u32 q = atomicAdd(&s_nbig, 1u);
+                    if (q < BS_BIGMAX) s_big[q] = g;
+                    else atomicOr(status, ST_LIST_OVER);
+                }
+            }
+            __syncthreads();
+            // large groups: in-place bitonic network in shared memory, all comparators
+            // ascending (the first step of each merge compares i with its mirror), so virtual
+            // +inf padding beyond len never moves and len need not be a power of two
+            const u32 nb = min(s_nbig, (u32)BS_BIGMAX);
+            for (u32 q = 0; q < nb; ++q) {
+                const u32 g = s_big[q];
+                const u32 gs = S.gst[g], len = S.gst[g + 1] - gs;
+                u32 N = 1;
+                while (N < len) N <<= 1;
+                for (u32 kk = 2; kk <= N; kk <<= 1) {
+                    const u32 hk = kk >> 1;
+                    for (u32 t = threadIdx.x; t < N / 2; t += BS_NT) {
+                        const u32 blk = t / hk, off = t % hk;
+                        const u32 x = blk * kk + off, y = blk * kk + kk - 1 - off;
+                        if (y < len) smem_cex<U, KV>(S, gs + x, gs + y);
+                    }
+                    __syncthreads();
+                    for (u32 j = kk >> 2; j > 0; j >>= 1) {
+                        for (u32 t = threadIdx.x; t < N / 2; t += BS_NT) {
+                            const u32 x = (t / j) * 2 * j + (t % j), y = x + j;
+                            if (y < len) smem_cex<U, KV>(S, gs + x, gs + y);
+                        }
+                        __syncthreads();
+                    }
+                }
+                for (u32 e = threadIdx.x; e < len; e += BS_NT) {
+                    okeys[bk.beg + gs + e] = Codec<DT>::raw(S.k[gs + e]);
+                    if (KV) ovals[bk.beg + gs + e] = S.v[gs + e];
+                }
+            }
+            __syncthreads();
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void k_fill_u32(u32* p, u32 v, u32 n) {
+    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
+__global__ void k_set2(u32* p, u32 a, u32 b) { p[0] = a; p[1] = b; }
+
+__global__ void k_iota(u32* p, u32 n) {
+    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = i;
+}
+
+// internal sorts of an array that fits the bucket sorter: one bucket with loose bounds
+template <class U>
+__global__ void k_push_bucket(Bucket* list, u32* nlist, u32 len) {
+    Bucket b;
+    b.beg = 0; b.len = len; b.buf = 0; b.level = BK_LOOSE;
+    b.lo = 0; b.hi = (u64)umax_of<U>();
+    list[0] = b;
+    *nlist = 1;
+}
+
+}  // namespace
+}  // namespace ovs

@@ -1,0 +1,8 @@
+// ovs_u32.cu — instantiation of the sort engine for u32 keys (keys only / key-value).
+#include "ovs_engine.cuh"
+
+namespace ovs {
+Out plan_u32(Ctx& c, void* keys, u32* vals, size_t n, const ovs_params* prm, bool kv) {
+    return kv ? plan_or_run<DT_U32, true>(c, keys, vals, n, prm) : plan_or_run<DT_U32, false>(c, keys, vals, n, prm);
+}
+}  // namespace ovs

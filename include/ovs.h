@@ -93,6 +93,13 @@ int ovs_sort_keys(void* d_keys, size_t n, int dtype, const ovs_params* prm, void
 int ovs_sort_pairs_stable(void* d_keys, uint32_t* d_vals, size_t n, int dtype, const ovs_params* prm, void* d_ws,
                           size_t ws_bytes, void* stream, ovs_report* rep);
 
+/* Profiling hook (thread-local): subsequent sort calls on this thread record events[k]
+ * (cudaEvent_t passed as void*) on their stream at phase boundary k, without synchronising:
+ *   0 start, 1 after the sample + splitters (a1-a4), 2 after classify + histogram + scans
+ *   (a5-a6), 3 after the scatter (a7), 4 after the bucket sort (a8) = end.
+ * count = 0 disables.  NULL entries are skipped.  The caller owns the events. */
+void ovs_set_phase_events(void* const* events, int count);
+
 /* Thread-local message of the last failure on this thread ("" if none). */
 const char* ovs_last_error(void);
 

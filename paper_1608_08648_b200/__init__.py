@@ -61,6 +61,8 @@ def lib() -> ctypes.CDLL:
         L.ovs_sort_pairs_stable.restype = i32
         L.ovs_sort_pairs_stable.argtypes = [vp, vp, sz, i32, ctypes.POINTER(Params), vp, sz, vp,
                                             ctypes.POINTER(Report)]
+        L.ovs_set_phase_events.restype = None
+        L.ovs_set_phase_events.argtypes = [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int]
         L.ovs_last_error.restype = ctypes.c_char_p
         L.ovs_version.restype = ctypes.c_char_p
         _lib = L
@@ -69,6 +71,21 @@ def lib() -> ctypes.CDLL:
 
 def version() -> str:
     return lib().ovs_version().decode()
+
+
+PHASES = ("sample", "classify_hist", "scatter", "bucket_sort")
+
+
+def set_phase_events(events) -> None:
+    """Record torch.cuda.Event objects (enable_timing=True) at the phase boundaries of every
+    following sort call on this thread: 0 start, 1 sample done, 2 histogram done, 3 scatter
+    done, 4 bucket sort done.  Pass None / [] to disable."""
+    events = list(events or [])
+    for e in events:
+        if e.cuda_event == 0:  # torch creates the event lazily
+            e.record()
+    arr = (ctypes.c_void_p * max(len(events), 1))(*[e.cuda_event for e in events])
+    lib().ovs_set_phase_events(arr, len(events))
 
 
 def _dtype_code(dt) -> int:

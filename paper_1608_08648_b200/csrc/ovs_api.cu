@@ -4,6 +4,7 @@
 
 namespace ovs {
 thread_local std::string g_err;
+thread_local std::vector<cudaEvent_t> g_marks;
 DevInfo dev_info() { return dev_info_impl(); }
 int validate(size_t n, int dtype, const ovs_params* prm) { return validate_impl(n, dtype, prm); }
 }  // namespace ovs
@@ -28,6 +29,7 @@ static int sort_impl(void* d_keys, uint32_t* d_vals, bool kv, size_t n, int dtyp
         Ctx c;
         c.di = dev_info();
         c.st = (cudaStream_t)stream;
+        c.marks = &g_marks;
         if (n == 0) {
             if (rep) {
                 std::memset(rep->phase_ms, 0, sizeof(rep->phase_ms));
@@ -144,6 +146,11 @@ int ovs_sort_pairs_stable(void* d_keys, uint32_t* d_vals, size_t n, int dtype, c
 }
 
 const char* ovs_last_error(void) { return g_err.c_str(); }
+
+void ovs_set_phase_events(void* const* events, int count) {
+    g_marks.assign(count > 0 ? count : 0, nullptr);
+    for (int i = 0; i < count; ++i) g_marks[i] = (cudaEvent_t)events[i];
+}
 
 const char* ovs_version(void) { return "ovs 0.1 sm_100a"; }
 

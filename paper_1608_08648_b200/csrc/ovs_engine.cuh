@@ -60,6 +60,10 @@ struct Ctx {
     DevInfo di;
     u32* status = nullptr;
     u32* bsum = nullptr;  // scratch of the device scan
+    const std::vector<cudaEvent_t>* marks = nullptr;  // ovs_set_phase_events
+    void mark(u32 k) {
+        if (!dry && marks && k < marks->size() && (*marks)[k]) OVS_CK(cudaEventRecord((*marks)[k], st));
+    }
     template <class T> T* take(size_t count) {
         off = (off + 255) & ~(size_t)255;
         T* p = dry ? nullptr : (T*)(ws + off);
@@ -130,6 +134,7 @@ template <int DT, bool KV> struct Engine {
     Bufs<U> B;
     u32 n;
     u32 cap;
+    bool mark_phases = false;  // the contract-level engine records the phase events
     explicit Engine(Ctx& ctx) : c(ctx) {}
 
     struct Level0 {
@@ -218,12 +223,14 @@ template <int DT, bool KV> struct Engine {
         k_segscan<U><<<1, 1024, 0, c.st>>>(z.seg, z.nseg, z.P, z.tot, z.sk, 0, cap, l.fit, l.nfit, l.fit_cap, nullptr,
                                           nullptr, 0, counts_out, c.status);
         c.check();
+        if (mark_phases) c.mark(2);
         constexpr int IT = PartItems<U, KV>::v;
         const size_t sm_s = scatter_smem(z.P, z.L);
         auto ks = k_scatter<DT, KV, true, PT_NT, IT>;
         OVS_CK(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_s));
         ks<<<z.nchunk, PT_NT, sm_s, c.st>>>(B, z.chunks, z.nchunks, z.seg, z.sk, z.st, z.lut, z.P, z.L, z.hist, z.tot);
         c.check();
+        if (mark_phases) c.mark(3);
     }
 
     void set_pair(u32* p, u32 a, u32 b) {
@@ -337,6 +344,8 @@ template <int DT, bool KV> struct RosSort {
 
     void run() {
         if (c.dry) return;
+        e.mark_phases = true;
+        c.mark(0);
         if (p > 1) {
             // a1: ps-1 distinct random indices (first distinct draws of the counter stream)
             k_ros_candidates<<<cdiv(M, 256), 256, 0, c.st>>>(cand, M, n, seed);
@@ -359,9 +368,11 @@ template <int DT, bool KV> struct RosSort {
         } else {
             e.internal_splitters(z, seed);
         }
+        c.mark(1);
         // a5-a7: classify, histogram, scan, scatter;  a8: bucket sort
         e.level0(z, l, p > 1 ? counts : nullptr);
         e.bucket_sort(l, seed);
+        c.mark(4);
     }
 };
 
@@ -416,6 +427,7 @@ Out plan_f64(Ctx& c, void* keys, u32* vals, size_t n, const ovs_params* prm, boo
 int validate(size_t n, int dtype, const ovs_params* prm);
 DevInfo dev_info();
 extern thread_local std::string g_err;
+extern thread_local std::vector<cudaEvent_t> g_marks;
 
 }  // namespace ovs
 

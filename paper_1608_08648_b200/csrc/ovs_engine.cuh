@@ -91,7 +91,7 @@ static inline u32 ilog2(u32 x) {
 
 // shared-memory capacity (items) of the bucket sorter
 template <class U, bool KV> static u32 bucket_cap(const DevInfo& di) {
-    const size_t reserve = 4096;  // static shared memory of k_bucket_sort
+    const size_t reserve = 8192;  // static shared memory of k_bucket_sort
     size_t avail = (size_t)di.smem_optin - bucket_smem_fixed<U, KV>() - reserve;
     u32 cap = (u32)(avail / bucket_item_bytes<U, KV>());
     return cap & ~31u;
@@ -120,6 +120,19 @@ static void fill_u32(Ctx& c, u32* p, u32 v, u32 n) {
     if (c.dry || n == 0) return;
     k_fill_u32<<<cdiv(n, 256), 256, 0, c.st>>>(p, v, n);
     c.check();
+}
+
+// Number of candidate draws for the ROS sample (reading Q1: the first ps-1 distinct values of
+// the counter stream): the expected number of draws to collect m distinct indices out of n
+// (coupon collector, E = n(H_n - H_{n-m})) plus 10 standard deviations and 64; a shortfall
+// (never observed) is caught on the device (ST_SAMPLE_SHORT).  0 = too many draws.
+inline u32 ros_draws(u64 n, u64 m) {
+    const double N = (double)n, a = (double)(n - m) + 0.5, b = N + 0.5;
+    const double E = N * std::log(b / a);
+    const double var = std::max(0.0, N * N * (1.0 / a - 1.0 / b) - E);
+    const double M = std::ceil(E + 10.0 * std::sqrt(var) + 64.0);
+    if (M > (double)(1u << 26)) return 0;
+    return (u32)std::max<double>(M, (double)m);
 }
 
 // ------------------------------------------------------------------ the sort engine
@@ -168,7 +181,7 @@ template <int DT, bool KV> struct Engine {
         z.log2L = ilog2(z.L);
         // chunks: one per resident CTA slot, whole sub-tiles
         const u32 ts = PT_NT * PartItems<U, KV>::v;
-        u32 want = (u32)c.di.sms * 2;
+        u32 want = (u32)c.di.sms;  // one chunk per SM: fewer concurrently open output lines
         z.chunk = std::max<u32>(ts, cdiv(cdiv(n, want), ts) * ts);
         z.nchunk = std::max<u32>(1, cdiv(n, z.chunk));
         z.sk = c.take<U>(std::max<u32>(P, 1));
@@ -320,10 +333,7 @@ template <int DT, bool KV> struct RosSort {
         e.carve_lists(l, P0);
         if (p > 1) {
             m = p * s - 1;
-            // candidates: m + a margin of 8 sigma of the duplicate count + 64 (never short in
-            // practice; a shortfall is detected and reported as ST_SAMPLE_SHORT)
-            double dup = (double)m * m / (2.0 * (double)n);
-            M = (u32)std::min<double>((double)m + 8.0 * dup + 8.0 * std::sqrt(dup + 1.0) + 64.0, (double)(1u << 24) - 1);
+            M = ros_draws(n, m);
             cand = c.take<u64>(M);
             flag = c.take<u32>(M);
             rank = c.take<u32>(M);
@@ -388,7 +398,7 @@ inline int validate_impl(size_t n, int dtype, const ovs_params* prm) {
     if (prm->method == OVS_ROS) {
         if (prm->s == 0) return OVS_ESAMPLE;
         if ((uint64_t)prm->p * prm->s - 1 > n) return OVS_ESAMPLE;
-        if ((uint64_t)prm->p * prm->s > (1u << 24)) return OVS_EINVAL;
+        if (ros_draws(n, (uint64_t)prm->p * prm->s - 1) == 0) return OVS_ESAMPLE;
     } else {
         if (prm->s == 0) return OVS_ESAMPLE;
         if ((uint64_t)prm->s * prm->p > n / prm->p) return OVS_ESAMPLE;

@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(SCAN_NT) k_scan_down(const u32* in, u32 n, con
 }
 
 // ------------------------------------------------------------------ a1: ROS sample indices
-// Candidate j = (c_j << 24) | j, c_j = floor(H(seed,1,j) * n / 2^64) (reading Q1).  Sorting
+// Candidate j = (c_j << 32) | j, c_j = floor(H(seed,1,j) * n / 2^64) (reading Q1).  Sorting
 // the candidates groups equal c; the FIRST distinct draws are the candidates that are the
 // smallest j of their c-group, ranked by j.
 __global__ void k_ros_candidates(u64* cand, u32 M, u64 n, u64 seed) {
@@ -216,15 +216,15 @@ __global__ void k_ros_candidates(u64* cand, u32 M, u64 n, u64 seed) {
     if (j >= M) return;
     u64 u = rng_H(seed, 1, j);
     u64 c = __umul64hi(u, n);
-    cand[j] = (c << 24) | (u64)j;
+    cand[j] = (c << 32) | (u64)j;
 }
 
 __global__ void k_ros_first_flags(const u64* sorted, u32 M, u32* flag_by_j) {
     u32 t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= M) return;
     u64 x = sorted[t];
-    bool first = (t == 0) || ((sorted[t - 1] >> 24) != (x >> 24));
-    flag_by_j[(u32)(x & 0xffffffu)] = first ? 1u : 0u;
+    bool first = (t == 0) || ((sorted[t - 1] >> 32) != (x >> 32));
+    flag_by_j[(u32)x] = first ? 1u : 0u;
 }
 
 // keep[t] = candidate at sorted position t is one of the first m distinct draws
@@ -232,7 +232,7 @@ __global__ void k_ros_keep(const u64* sorted, u32 M, const u32* flag_by_j, const
                            u32* keep, u32* status) {
     u32 t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= M) return;
-    u32 j = (u32)(sorted[t] & 0xffffffu);
+    u32 j = (u32)sorted[t];
     keep[t] = (flag_by_j[j] && rank_by_j[j] < m) ? 1u : 0u;
     if (t == M - 1) {
         u32 tot = rank_by_j[M - 1] + flag_by_j[M - 1];
@@ -247,7 +247,7 @@ __global__ void k_ros_gather(const u64* sorted, u32 M, const u32* keep, const u3
                              const typename Codec<DT>::U* x, u64* t_pack, u64* t_key, u32* t_tag) {
     u32 t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= M || !keep[t]) return;
-    u32 i = (u32)(sorted[t] >> 24);
+    u32 i = (u32)(sorted[t] >> 32);
     u32 o = pos[t];
     typename Codec<DT>::U k = Codec<DT>::ord(x[i]);
     if (sizeof(k) == 4) {
@@ -380,6 +380,38 @@ template <class U> __device__ __forceinline__ U shfl_xor_any(U x, int o) {
     return (U)__shfl_xor_sync(0xffffffffu, (u32)x, o);
 }
 
+// ------------------------------------------------------------------ vectorised item loops
+// for_items(src, beg, m, f): calls f(key, o) for every o in [0, m) (any order) with 16-byte
+// vector loads, UNR vectors in flight per thread (the bucket and partition passes are
+// latency bound without this: v1 kept one 4-byte load in flight per thread).
+template <class U, int NT, int UNR, class F, bool STREAM = false>
+__device__ __forceinline__ void for_items(const U* __restrict__ src, u32 beg, u32 m, F&& f) {
+    constexpr u32 V = 16 / sizeof(U);
+    const u32 mis = (u32)(((uintptr_t)(src + beg)) & 15u) / (u32)sizeof(U);
+    const u32 head = mis ? min(m, V - mis) : 0u;
+    if (threadIdx.x < head) f(src[beg + threadIdx.x], threadIdx.x);
+    const uint4* a = (const uint4*)(src + beg + head);
+    const u32 nv = (m - head) / V;
+    for (u32 v0 = 0; v0 < nv; v0 += NT * UNR) {
+        uint4 r[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const u32 idx = v0 + u * NT + threadIdx.x;
+            if (idx < nv) r[u] = STREAM ? __ldcs(a + idx) : a[idx];
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const u32 idx = v0 + u * NT + threadIdx.x;
+            if (idx < nv) {
+                const U* e = (const U*)&r[u];
+#pragma unroll
+                for (u32 q = 0; q < V; ++q) f(e[q], head + idx * V + q);
+            }
+        }
+    }
+    for (u32 o = head + nv * V + threadIdx.x; o < m; o += NT) f(src[beg + o], o);
+}
+
 // ------------------------------------------------------------------ a5+a6: classify + histogram
 // Persistent CTAs over chunks; per-chunk histogram row hist[c*PS + b].  LEVEL0 reads buffer 0
 // through the codec (the caller's raw keys) with tag = index (ROS: the original index,
@@ -404,27 +436,13 @@ __global__ void __launch_bounds__(NT) k_hist(Bufs<typename Codec<DT>::U> B, cons
         const U* src = B.k[LEVEL0 ? 0 : sg.src];
         const u32* isrc = (KV && !LEVEL0) ? B.i[sg.src] : nullptr;
         U mn = umax_of<U>(), mx = 0;
-        u32 i = ch.beg + threadIdx.x;
-        for (; i + 3 * NT < ch.end; i += 4 * NT) {
-            U k[4];
-            u32 tg[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                k[j] = LEVEL0 ? Codec<DT>::ord(__ldcs(src + i + j * NT)) : src[i + j * NT];
-                tg[j] = (KV && !LEVEL0) ? isrc[i + j * NT] : i + j * NT;
-            }
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                atomicAdd(&h[classify<U>(cls, k[j], tg[j])], 1u);
-                if (LEVEL0) { mn = min(mn, k[j]); mx = max(mx, k[j]); }
-            }
-        }
-        for (; i < ch.end; i += NT) {
-            U k = LEVEL0 ? Codec<DT>::ord(src[i]) : src[i];
-            u32 tg = (KV && !LEVEL0) ? isrc[i] : i;
+        auto body = [&](U kr, u32 o) {
+            const U k = LEVEL0 ? Codec<DT>::ord(kr) : kr;
+            const u32 tg = (KV && !LEVEL0) ? isrc[ch.beg + o] : ch.beg + o;
             atomicAdd(&h[classify<U>(cls, k, tg)], 1u);
             if (LEVEL0) { mn = min(mn, k); mx = max(mx, k); }
-        }
+        };
+        for_items<U, NT, 4, decltype(body)&, LEVEL0>(src, ch.beg, ch.end - ch.beg, body);
         __syncthreads();
         u32* row = hist + (size_t)c * PS;
         for (u32 b = threadIdx.x; b < sg.P; b += NT) row[b] = h[b];
@@ -579,18 +597,45 @@ __global__ void __launch_bounds__(NT) k_scatter(Bufs<typename Codec<DT>::U> B, c
             __syncthreads();
             U k[ITEMS];
             u32 v[ITEMS], ix[ITEMS], bk[ITEMS], rk[ITEMS];
+            // item slot j of this thread is sub-tile offset off(j): 16-byte vectors when the
+            // sub-tile is full and aligned, otherwise a strided scalar loop
+            constexpr u32 V = 16 / sizeof(U);
+            const bool vec = nt == (u32)TS && ((((uintptr_t)(src + t0)) & 15u) == 0) &&
+                             (!KV || ((((uintptr_t)(vsrc + t0)) & 15u) == 0));
+            auto off = [&](int j) -> u32 {
+                return vec ? ((j / V) * NT + threadIdx.x) * V + (j % V) : j * NT + threadIdx.x;
+            };
+            if (vec) {
 #pragma unroll
-            for (int j = 0; j < ITEMS; ++j) {
-                const u32 o = j * NT + threadIdx.x;
-                if (o < nt) {
-                    const u32 i = t0 + o;
-                    k[j] = LEVEL0 ? Codec<DT>::ord(__ldcs(src + i)) : src[i];
-                    if (KV) { v[j] = vsrc[i]; ix[j] = LEVEL0 ? i : isrc[i]; }
+                for (int jv = 0; jv < ITEMS / (int)V; ++jv) {
+                    const u32 vi = jv * NT + threadIdx.x;
+                    uint4 r = __ldcs((const uint4*)(src + t0) + vi);
+                    const U* e = (const U*)&r;
+#pragma unroll
+                    for (u32 q = 0; q < V; ++q) k[jv * V + q] = LEVEL0 ? Codec<DT>::ord(e[q]) : e[q];
+                    if (KV) {
+#pragma unroll
+                        for (u32 q = 0; q < V; ++q) {
+                            const u32 i = t0 + vi * V + q;
+                            v[jv * V + q] = vsrc[i];
+                            ix[jv * V + q] = LEVEL0 ? i : isrc[i];
+                        }
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < ITEMS; ++j) {
+                    const u32 o = off(j);
+                    if (o < nt) {
+                        const u32 i = t0 + o;
+                        k[j] = LEVEL0 ? Codec<DT>::ord(src[i]) : src[i];
+                        if (KV) { v[j] = vsrc[i]; ix[j] = LEVEL0 ? i : isrc[i]; }
+                    }
                 }
             }
 #pragma unroll
             for (int j = 0; j < ITEMS; ++j) {
-                const u32 o = j * NT + threadIdx.x;
+                const u32 o = off(j);
                 if (o < nt) {
                     const u32 tag = KV ? ix[j] : t0 + o;
                     bk[j] = classify<U>(cls, k[j], tag);
@@ -601,7 +646,7 @@ __global__ void __launch_bounds__(NT) k_scatter(Bufs<typename Codec<DT>::U> B, c
             block_scan_array<NT>(work, P, red);
 #pragma unroll
             for (int j = 0; j < ITEMS; ++j) {
-                const u32 o = j * NT + threadIdx.x;
+                const u32 o = off(j);
                 if (o < nt) {
                     const u32 pos = work[bk[j]] + rk[j];
                     stk[pos] = k[j];
@@ -679,17 +724,18 @@ __global__ void __launch_bounds__(1024) k_internal_sample(Bufs<typename Codec<DT
 
 // ------------------------------------------------------------------ a8: bucket sort
 // Persistent CTAs pull buckets from the list.  A bucket of len <= cap is sorted on chip:
-//  1. histogram of the top digit of (key - lo) [key-value: of the composite (key, index)],
-//  2. scatter from global into shared memory grouped by digit,
-//  3. every group sorted by one warp with a register bitonic network (<= 512 items) or, for
-//     larger groups, by the CTA with an in-place bitonic network in shared memory,
-//  4. sorted groups written to the output at the bucket's final position (raw codec).
+//  1. histogram of the top lg bits of (key - lo) [key-value: of the composite (key, index)]
+//     over ng ~ len/3 fine groups (the bounds come from the splitters around the bucket),
+//  2. scatter from global (L2-resident after pass 1) into shared memory grouped by digit,
+//  3. every group (mostly <= 8 items) sorted by one thread with Batcher's 19-comparator
+//     network; larger groups by a warp (bitonic, <= 512) or the CTA (bitonic in place),
+//  4. the sorted bucket copied to the output at its final position (raw codec).
 // All global reads of a bucket finish before any write, so the source may alias the output.
 // A bucket over the capacity is re-split by the CTA itself ("sorted ... recursively by this
 // same extended method"): a random sample of it gives <= 64 sub-splitters, the
 // bucket is partitioned into the other buffer and the sub-buckets go on a per-CTA stack.
 constexpr int BS_NT = 512;
-constexpr int BS_NGMAX = 2048;
+constexpr int BS_NGMAX = 8192;
 constexpr int BS_BIGMAX = 128;
 constexpr int BS_STACK = 256;
 constexpr u32 BS_SPMAX = 64;
@@ -715,6 +761,20 @@ template <class U> struct Elem<U, true> {
         return e;
     }
 };
+
+template <class E> __device__ __forceinline__ void cex(E& a, E& b) {
+    if (b.lt(a)) { E t = a; a = b; b = t; }
+}
+
+// Batcher's odd-even merge network for 8 inputs (19 comparators)
+template <class E> __device__ __forceinline__ void network8(E (&a)[8]) {
+    cex(a[0], a[1]); cex(a[2], a[3]); cex(a[4], a[5]); cex(a[6], a[7]);
+    cex(a[0], a[2]); cex(a[1], a[3]); cex(a[4], a[6]); cex(a[5], a[7]);
+    cex(a[1], a[2]); cex(a[5], a[6]);
+    cex(a[0], a[4]); cex(a[1], a[5]); cex(a[2], a[6]); cex(a[3], a[7]);
+    cex(a[2], a[4]); cex(a[3], a[5]);
+    cex(a[1], a[2]); cex(a[3], a[4]); cex(a[5], a[6]);
+}
 
 // bitonic sort of 32*R elements held as a[r] at lane: element index e = r*32 + lane
 template <class E, int R>
@@ -753,34 +813,38 @@ __device__ __forceinline__ void warp_bitonic(E (&a)[R]) {
 }
 
 template <class U, bool KV> struct BucketSmem {
-    U* k; u32* i; u32* v; u32* gst; u32* cur;
+    U* k; u32* i; u32* v; u32* cnt;
 };
 
-template <int DT, bool KV, int R>
-__device__ __forceinline__ void warp_sort_group(const BucketSmem<typename Codec<DT>::U, KV>& S, u32 gs, u32 len,
-                                                typename Codec<DT>::U* okeys, u32* ovals, u32 obeg) {
-    typedef typename Codec<DT>::U U;
+template <class U, bool KV>
+__device__ __forceinline__ Elem<U, KV> sm_get(const BucketSmem<U, KV>& S, u32 x) {
+    Elem<U, KV> e;
+    e.k = S.k[x];
+    if constexpr (KV) { e.i = S.i[x]; e.v = S.v[x]; }
+    return e;
+}
+template <class U, bool KV>
+__device__ __forceinline__ void sm_put(const BucketSmem<U, KV>& S, u32 x, const Elem<U, KV>& e) {
+    S.k[x] = e.k;
+    if constexpr (KV) { S.i[x] = e.i; S.v[x] = e.v; }
+}
+
+// a group of len <= 32*R items in shared memory, sorted in place by one warp
+template <class U, bool KV, int R>
+__device__ __forceinline__ void warp_sort_group(const BucketSmem<U, KV>& S, u32 gs, u32 len) {
     typedef Elem<U, KV> E;
     const int lane = threadIdx.x & 31;
     E a[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const u32 e = r * 32 + lane;
-        if (e < len) {
-            a[r].k = S.k[gs + e];
-            if constexpr (KV) { a[r].i = S.i[gs + e]; a[r].v = S.v[gs + e]; }
-        } else {
-            a[r] = E::inf();
-        }
+        a[r] = e < len ? sm_get<U, KV>(S, gs + e) : E::inf();
     }
     warp_bitonic<E, R>(a);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const u32 e = r * 32 + lane;
-        if (e < len) {
-            okeys[obeg + gs + e] = Codec<DT>::raw(a[r].k);
-            if constexpr (KV) ovals[obeg + gs + e] = a[r].v;
-        }
+        if (e < len) sm_put<U, KV>(S, gs + e, a[r]);
     }
 }
 
@@ -809,18 +873,19 @@ template <class U> __device__ __forceinline__ u32 lower_bound_kt(const U* sk, co
 }
 
 template <class U, bool KV> __host__ __device__ constexpr size_t bucket_smem_fixed() {
-    return 4 * (2 * (size_t)BS_NGMAX + 4);
+    return 4 * ((size_t)BS_NGMAX + 4);
 }
 template <class U, bool KV> __host__ __device__ constexpr size_t bucket_item_bytes() {
     return sizeof(U) + (KV ? 8 : 0);
 }
 
 template <int DT, bool KV>
-__global__ void __launch_bounds__(BS_NT) k_bucket_sort(const Bucket* list, const u32* nlist, u32* ticket,
-                                                        Bufs<typename Codec<DT>::U> B, typename Codec<DT>::U* okeys,
-                                                        u32* ovals, u32 cap, Bucket* stack_pool, u64 seed,
-                                                        u32* status) {
+__global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, const u32* nlist, u32* ticket,
+                                                           Bufs<typename Codec<DT>::U> B, typename Codec<DT>::U* okeys,
+                                                           u32* ovals, u32 cap, Bucket* stack_pool, u64 seed,
+                                                           u32* status) {
     typedef typename Codec<DT>::U U;
+    typedef Elem<U, KV> E;
     extern __shared__ __align__(16) char smem[];
     __shared__ u32 red[BS_NT / 32 + 1];
     __shared__ u32 s_work, s_nbig, s_sp;
@@ -831,8 +896,7 @@ __global__ void __launch_bounds__(BS_NT) k_bucket_sort(const Bucket* list, const
     BucketSmem<U, KV> S;
     {
         char* sp = smem;
-        S.gst = (u32*)sp; sp += 4 * (BS_NGMAX + 4);
-        S.cur = (u32*)sp; sp += 4 * BS_NGMAX;
+        S.cnt = (u32*)sp; sp += 4 * ((size_t)BS_NGMAX + 4);
         S.k = (U*)sp; sp += sizeof(U) * (size_t)cap;
         if (KV) { S.i = (u32*)sp; sp += 4 * (size_t)cap; S.v = (u32*)sp; sp += 4 * (size_t)cap; }
     }
@@ -881,11 +945,10 @@ __global__ void __launch_bounds__(BS_NT) k_bucket_sort(const Bucket* list, const
                 }
                 if (threadIdx.x <= P) sp_cnt[threadIdx.x] = 0;
                 __syncthreads();
-                for (u32 o = threadIdx.x; o < m; o += BS_NT) {
-                    const U k = src[bk.beg + o];
+                for_items<U, BS_NT, 4>(src, bk.beg, m, [&](U k, u32 o) {
                     const u32 tg = KV ? isrc[bk.beg + o] : bk.beg + o;
                     atomicAdd(&sp_cnt[lower_bound_kt<U>(sp_k, sp_t, P - 1, k, tg)], 1u);
-                }
+                });
                 __syncthreads();
                 if (threadIdx.x == 0) {
                     u32 run = 0;
@@ -894,14 +957,13 @@ __global__ void __launch_bounds__(BS_NT) k_bucket_sort(const Bucket* list, const
                 }
                 __syncthreads();
                 const u32 db = 1 - bk.buf;
-                for (u32 o = threadIdx.x; o < m; o += BS_NT) {
-                    const U k = src[bk.beg + o];
+                for_items<U, BS_NT, 4>(src, bk.beg, m, [&](U k, u32 o) {
                     const u32 tg = KV ? isrc[bk.beg + o] : bk.beg + o;
                     const u32 b = lower_bound_kt<U>(sp_k, sp_t, P - 1, k, tg);
                     const u32 d = bk.beg + atomicAdd(&sp_cur[b], 1u);
                     B.k[db][d] = k;
                     if (KV) { B.v[db][d] = vsrc[bk.beg + o]; B.i[db][d] = tg; }
-                }
+                });
                 __syncthreads();
                 if (threadIdx.x == 0) {
                     u32 sp = s_sp;
@@ -926,7 +988,7 @@ __global__ void __launch_bounds__(BS_NT) k_bucket_sort(const Bucket* list, const
             U lo = (U)bk.lo, hi = (U)bk.hi;
             if (bk.level & BK_LOOSE) {
                 U mn = umax_of<U>(), mx = 0;
-                for (u32 o = threadIdx.x; o < m; o += BS_NT) { const U k = src[bk.beg + o]; mn = min(mn, k); mx = max(mx, k); }
+                for_items<U, BS_NT, 4>(src, bk.beg, m, [&](U k, u32) { mn = min(mn, k); mx = max(mx, k); });
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) { mn = min(mn, shfl_xor_any(mn, o)); mx = max(mx, shfl_xor_any(mx, o)); }
                 if (lane == 0) { s_mn[wid] = mn; s_mx[wid] = mx; }
@@ -936,51 +998,61 @@ __global__ void __launch_bounds__(BS_NT) k_bucket_sort(const Bucket* list, const
                 lo = mn; hi = mx;
                 __syncthreads();
             }
-            u32 ng = 1;
-            while (ng < (u32)BS_NGMAX && ng * 48 < m) ng <<= 1;
-            const u32 lg = 31 - __clz(ng);
-            const u32 rb = bitlen<U>((U)(hi - lo)) + (KV ? 32u : 0u);
-            const u32 sh = rb > lg ? rb - lg : 0u;
+            u32 ng = 32;
+            while (ng < (u32)BS_NGMAX && ng * 3 < m) ng <<= 1;
+            // digit = floor(x * ng / R) for x = (sort key - lo) in [0, R): monotone in the key
+            // and spreads [lo, hi] over all ng groups (computed as a 64-bit fixed-point
+            // multiply-high).  Key-value sorts of 32-bit keys use the composite (key, index);
+            // 64-bit keys use the key (equal keys then share a group, ordered by index).
+            const bool comp = KV && sizeof(U) == 4;
+            const u64 xmax = comp ? ((((u64)(hi - lo)) << 32) | 0xffffffffull) : (u64)(U)(hi - lo);
+            const unsigned __int128 R = (unsigned __int128)xmax + 1;
+            const unsigned __int128 mq = (((unsigned __int128)ng) << 64) / R;
+            const u64 mult = mq > (unsigned __int128)0xffffffffffffffffull ? 0xffffffffffffffffull : (u64)mq;
             auto digit = [&](U k, u32 ix) -> u32 {
-                u32 d;
-                if constexpr (KV) {
-                    if (sizeof(U) == 4) d = (u32)((((u64)(k - lo)) << 32 | ix) >> sh);
-                    else d = (u32)((((unsigned __int128)(u64)(k - lo)) << 32 | ix) >> sh);
-                } else {
-                    d = (u32)((U)(k - lo) >> sh);
-                }
-                return min(d, ng - 1);  // memory safety only: the bounds guarantee d < ng
+                const u64 x = comp ? ((((u64)(k - lo)) << 32) | ix) : (u64)(U)(k - lo);
+                return min((u32)__umul64hi(x, mult), ng - 1);  // min: memory safety only
             };
-            for (u32 g = threadIdx.x; g < ng; g += BS_NT) S.cur[g] = 0;
+            for (u32 g = threadIdx.x; g < ng; g += BS_NT) S.cnt[g] = 0;
             __syncthreads();
-            for (u32 o = threadIdx.x; o < m; o += BS_NT) {
-                const U k = src[bk.beg + o];
+            // 1. digit histogram
+            for_items<U, BS_NT, 4>(src, bk.beg, m, [&](U k, u32 o) {
                 const u32 ix = KV ? isrc[bk.beg + o] : 0u;
-                atomicAdd(&S.cur[digit(k, ix)], 1u);
-            }
+                atomicAdd(&S.cnt[digit(k, ix)], 1u);
+            });
             __syncthreads();
-            for (u32 g = threadIdx.x; g < ng; g += BS_NT) S.gst[g] = S.cur[g];
-            __syncthreads();
-            block_scan_array<BS_NT>(S.gst, ng, red);
-            for (u32 g = threadIdx.x; g < ng; g += BS_NT) S.cur[g] = S.gst[g];
-            __syncthreads();
-            for (u32 o = threadIdx.x; o < m; o += BS_NT) {
-                const U k = src[bk.beg + o];
+            block_scan_array<BS_NT>(S.cnt, ng, red);  // cnt[g] = start of group g
+            // 2. scatter into shared memory by digit; afterwards cnt[g] = end of group g
+            for_items<U, BS_NT, 4>(src, bk.beg, m, [&](U k, u32 o) {
                 u32 ix = 0, vv = 0;
                 if (KV) { ix = isrc[bk.beg + o]; vv = vsrc[bk.beg + o]; }
-                const u32 pos = atomicAdd(&S.cur[digit(k, ix)], 1u);
+                const u32 pos = atomicAdd(&S.cnt[digit(k, ix)], 1u);
                 S.k[pos] = k;
                 if (KV) { S.i[pos] = ix; S.v[pos] = vv; }
-            }
+            });
             __syncthreads();
+            // 3. one thread per group of <= 8: Batcher network in registers
+            for (u32 g = threadIdx.x; g < ng; g += BS_NT) {
+                const u32 gs = g ? S.cnt[g - 1] : 0u, len = S.cnt[g] - gs;
+                if (len <= 1 || len > 8) continue;
+                E a[8];
+#pragma unroll
+                for (u32 q = 0; q < 8; ++q) a[q] = q < len ? sm_get<U, KV>(S, gs + q) : E::inf();
+                network8(a);
+#pragma unroll
+                for (u32 q = 0; q < 8; ++q)
+                    if (q < len) sm_put<U, KV>(S, gs + q, a[q]);
+            }
+            // 3b. groups of 9..512: one warp each (register bitonic); over 512: listed (at most
+            // cap/512 of them, so the list cannot overflow)
             for (u32 g = wid; g < ng; g += BS_NT / 32) {
-                const u32 gs = S.gst[g], len = S.gst[g + 1] - gs;
-                if (len == 0) continue;
-                if (len <= 32) warp_sort_group<DT, KV, 1>(S, gs, len, okeys, ovals, bk.beg);
-                else if (len <= 64) warp_sort_group<DT, KV, 2>(S, gs, len, okeys, ovals, bk.beg);
-                else if (len <= 128) warp_sort_group<DT, KV, 4>(S, gs, len, okeys, ovals, bk.beg);
-                else if (len <= 256) warp_sort_group<DT, KV, 8>(S, gs, len, okeys, ovals, bk.beg);
-                else if (len <= 512) warp_sort_group<DT, KV, 16>(S, gs, len, okeys, ovals, bk.beg);
+                const u32 gs = g ? S.cnt[g - 1] : 0u, len = S.cnt[g] - gs;
+                if (len <= 8) continue;
+                if (len <= 32) warp_sort_group<U, KV, 1>(S, gs, len);
+                else if (len <= 64) warp_sort_group<U, KV, 2>(S, gs, len);
+                else if (len <= 128) warp_sort_group<U, KV, 4>(S, gs, len);
+                else if (len <= 256) warp_sort_group<U, KV, 8>(S, gs, len);
+                else if (len <= 512) warp_sort_group<U, KV, 16>(S, gs, len);
                 else if (lane == 0) {
                     const u32 q = atomicAdd(&s_nbig, 1u);
                     if (q < BS_BIGMAX) s_big[q] = g;
@@ -988,13 +1060,13 @@ __global__ void __launch_bounds__(BS_NT) k_bucket_sort(const Bucket* list, const
                 }
             }
             __syncthreads();
-            // large groups: in-place bitonic network in shared memory, all comparators
+            // 3c. groups over 512: in-place bitonic network in shared memory, all comparators
             // ascending (the first step of each merge compares i with its mirror), so virtual
             // +inf padding beyond len never moves and len need not be a power of two
-            const u32 nb = min(s_nbig, (u32)BS_BIGMAX);
-            for (u32 q = 0; q < nb; ++q) {
+            const u32 nhuge = min(s_nbig, (u32)BS_BIGMAX);
+            for (u32 q = 0; q < nhuge; ++q) {
                 const u32 g = s_big[q];
-                const u32 gs = S.gst[g], len = S.gst[g + 1] - gs;
+                const u32 gs = g ? S.cnt[g - 1] : 0u, len = S.cnt[g] - gs;
                 u32 N = 1;
                 while (N < len) N <<= 1;
                 for (u32 kk = 2; kk <= N; kk <<= 1) {
@@ -1013,10 +1085,27 @@ __global__ void __launch_bounds__(BS_NT) k_bucket_sort(const Bucket* list, const
                         __syncthreads();
                     }
                 }
-                for (u32 e = threadIdx.x; e < len; e += BS_NT) {
-                    okeys[bk.beg + gs + e] = Codec<DT>::raw(S.k[gs + e]);
-                    if (KV) ovals[bk.beg + gs + e] = S.v[gs + e];
+            }
+            __syncthreads();
+            // 4. write the sorted bucket (16-byte stores where the output is aligned)
+            {
+                constexpr u32 V = 16 / sizeof(U);
+                U* out = okeys + bk.beg;
+                const u32 mis = (u32)(((uintptr_t)out) & 15u) / (u32)sizeof(U);
+                const u32 head = mis ? min(m, V - mis) : 0u;
+                if (threadIdx.x < head) out[threadIdx.x] = Codec<DT>::raw(S.k[threadIdx.x]);
+                const u32 nv = (m - head) / V;
+                uint4* o4 = (uint4*)(out + head);
+                for (u32 v = threadIdx.x; v < nv; v += BS_NT) {
+                    uint4 r;
+                    U* e = (U*)&r;
+#pragma unroll
+                    for (u32 q = 0; q < V; ++q) e[q] = Codec<DT>::raw(S.k[head + v * V + q]);
+                    o4[v] = r;
                 }
+                for (u32 o = head + nv * V + threadIdx.x; o < m; o += BS_NT) out[o] = Codec<DT>::raw(S.k[o]);
+                if (KV)
+                    for (u32 o = threadIdx.x; o < m; o += BS_NT) ovals[bk.beg + o] = S.v[o];
             }
             __syncthreads();
         }

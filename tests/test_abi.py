@@ -1,0 +1,71 @@
+"""The C-ABI library loads and exports every symbol include/ovs.h declares; host-side argument
+validation (no kernel launches: these run without a GPU)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "ovs.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(ovs_[a-z_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    import paper_1608_08648_b200 as ovs
+    L = ovs.lib()
+    names = header_functions()
+    assert {"ovs_sort_keys", "ovs_sort_pairs_stable", "ovs_workspace_bytes", "ovs_last_error"} <= set(names)
+    for nm in names:
+        assert hasattr(L, nm), nm
+    assert ovs.version().startswith("ovs")
+
+
+def test_library_is_sm100a():
+    out = os.popen(f"cuobjdump --list-elf {os.path.join(ROOT, 'paper_1608_08648_b200', 'libovs.so')}").read()
+    assert "sm_100a" in out
+
+
+def _prm(ovs, method="ros", p=64, s=32):
+    return ovs.params(method, p, s, 1)
+
+
+def test_workspace_bytes_validation():
+    import paper_1608_08648_b200 as ovs
+    P = lambda **kw: _prm(ovs, **kw)
+    assert ovs.workspace_bytes(1 << 20, ovs.OVS_U32, False, P()) > 4 * (1 << 20)
+    assert ovs.workspace_bytes(1 << 20, ovs.OVS_F64, True, P()) > 16 * (1 << 20)
+    assert ovs.workspace_bytes(100, ovs.OVS_U32, False, P(p=11, s=10)) == 0     # ps-1 > n
+    assert ovs.workspace_bytes(100, ovs.OVS_U32, False, P(p=0)) == 0            # p == 0
+    assert ovs.workspace_bytes(100, 7, False, P()) == 0                          # dtype
+    assert ovs.workspace_bytes(100, ovs.OVS_U32, False, P(method="dro", p=8, s=2)) == 0  # rp > n/p
+    assert ovs.workspace_bytes(0, ovs.OVS_U32, False, P()) == 0                  # nothing to do
+
+
+def test_sort_rejects_bad_arguments_before_any_launch():
+    import paper_1608_08648_b200 as ovs
+    L = ovs.lib()
+    prm = _prm(ovs, p=11, s=10)
+    rc = L.ovs_sort_keys(None, 100, ovs.OVS_U32, ctypes.byref(prm), None, 0, None, None)
+    assert rc == ovs.OVS_ESAMPLE
+    prm = _prm(ovs, p=0)
+    assert L.ovs_sort_keys(None, 100, ovs.OVS_U32, ctypes.byref(prm), None, 0, None, None) == ovs.OVS_EINVAL
+    prm = _prm(ovs)
+    assert L.ovs_sort_keys(None, 100, 9, ctypes.byref(prm), None, 0, None, None) == ovs.OVS_EDTYPE
+    prm = _prm(ovs, p=4, s=8)
+    assert L.ovs_sort_keys(None, 1000, ovs.OVS_U32, ctypes.byref(prm), None, 0, None, None) == ovs.OVS_EINVAL  # NULL
+    assert L.ovs_sort_keys(None, 0, ovs.OVS_U32, ctypes.byref(prm), None, 0, None, None) == ovs.OVS_OK
+    assert L.ovs_last_error() is not None
+
+
+def test_binding_raises_without_cuda():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("has a GPU")
+    import paper_1608_08648_b200 as ovs
+    with pytest.raises(Exception):
+        ovs.Sorter(1000, torch.uint32, False, "ros", 4, 8, 1)

@@ -1,0 +1,135 @@
+"""Parity of the CUDA path (called through the C ABI) with the CPU oracle.
+
+Bit-exact comparison: sorted output, values of stable key-value sorts,
+the p-1 splitters (key AND tag) and the p bucket counts, element by element, on seeded
+inputs from ovs_inputs.  Sizes span several tiles, sub-tiles and buckets with ragged tails;
+the full-size BASELINE.json configurations run in the launch configuration bench.py times.
+"""
+import numpy as np
+import pytest
+import torch
+
+import ovs_inputs
+
+pytestmark = pytest.mark.gpu
+
+TORCH = {np.dtype(np.uint32): torch.uint32, np.dtype(np.int32): torch.int32, np.dtype(np.float64): torch.float64}
+
+
+@pytest.fixture(scope="module")
+def ovs():
+    import paper_1608_08648_b200 as m
+    assert torch.cuda.is_available()
+    m.lib()
+    return m
+
+
+def gpu_sort(ovs, x, method, p, s, seed, vals=None, stream=None):
+    xt = torch.from_numpy(x).cuda()
+    if vals is not None:
+        vt = torch.from_numpy(vals).cuda()
+        srt = ovs.Sorter(len(x), xt.dtype, True, method, p, s, seed)
+        rep = srt(xt, vt, stream=stream, report=True)
+        torch.cuda.synchronize()
+        return xt.cpu().numpy(), vt.cpu().numpy(), rep
+    srt = ovs.Sorter(len(x), xt.dtype, False, method, p, s, seed)
+    rep = srt(xt, stream=stream, report=True)
+    torch.cuda.synchronize()
+    return xt.cpu().numpy(), None, rep
+
+
+def check(ref, out, vout, rep, p):
+    assert rep.device_status == 0
+    np.testing.assert_array_equal(out, ref.keys)
+    if vout is not None:
+        np.testing.assert_array_equal(vout, ref.vals)
+    np.testing.assert_array_equal(rep.counts, ref.counts)
+    if p > 1:
+        np.testing.assert_array_equal(rep.splitter_keys, ref.split_keys)
+        np.testing.assert_array_equal(rep.splitter_tags, ref.split_tags)
+
+
+def ros_case(ovs, orc, dist, n, p, s, seed=1, kv=False, dseed=3):
+    x = ovs_inputs.keys(dist, n, seed=dseed)
+    v = ovs_inputs.index_values(n) if kv else None
+    ref = orc.ros_sort(x, p, s, seed, vals=v)
+    out, vout, rep = gpu_sort(ovs, x, "ros", p, s, seed, v)
+    check(ref, out, vout, rep, p)
+    return rep
+
+
+def test_c1_full(ovs, orc):
+    """BASELINE configs[0]: n=2^20 u32 uniform [0,2^31) seed 1, ROS p=64 s=32."""
+    c = ovs_inputs.CONFIGS["C1"]
+    ros_case(ovs, orc, "u32_u31", c["n"], c["p"], c["s"], c["seed"], dseed=1)
+
+
+EDGE = [
+    ("u32_u31", 1, 1, 1), ("u32_u31", 2, 1, 1), ("u32_u31", 2, 2, 1), ("u32_u31", 7, 4, 2), ("u32_u31", 1000, 4, 8),
+    ("u32", 4097, 64, 64), ("u32_const", 100_000, 64, 32), ("u32_few4", 300_001, 16, 8), ("u32_few4", 70_000, 256, 16),
+    ("i32_gauss", 100_003, 16, 16), ("i32_sorted", 500_000, 128, 32), ("i32_reverse", 500_000, 128, 32),
+    ("i32_few", 1_000_003, 1000, 16), ("f64_normal", 200_000, 64, 32), ("f64_uniform", 1_000_003, 7, 64),
+    ("u32_u31", 100_000, 1, 1), ("f64_normal", 300_000, 1, 1), ("u32", 3_000_017, 4096, 64), ("u32_u31", 65_536, 2, 1),
+    ("u32", 2_000_000, 2, 1_000_000),
+]
+
+
+@pytest.mark.parametrize("dist,n,p,s", EDGE)
+def test_ros_keys_edge_matrix(ovs, orc, dist, n, p, s):
+    ros_case(ovs, orc, dist, n, p, s, seed=n % 97 + 1)
+
+
+KV_EDGE = [("u16key", 100_000, 8, 8), ("u32_few4", 200_000, 16, 16), ("f64_uniform", 100_000, 32, 16),
+           ("u32_const", 150_000, 64, 8), ("i32_sorted", 300_000, 16, 16), ("f64_normal", 400_001, 1, 1),
+           ("u16key", 1_000_000, 512, 32), ("u32_few4", 5, 2, 2)]
+
+
+@pytest.mark.parametrize("dist,n,p,s", KV_EDGE)
+def test_ros_pairs_stable_edge_matrix(ovs, orc, dist, n, p, s):
+    rep = ros_case(ovs, orc, dist, n, p, s, seed=5, kv=True)
+    assert rep.device_status == 0
+
+
+def test_exhaustive_sample_closed_form(ovs, orc):
+    """ps-1 = n: splitter q is the element of rank (q+1)s; counts = [s,..,s,s-1]."""
+    n, p, s = 4095, 64, 64
+    x = ovs_inputs.keys("u32_few4", n, seed=9)
+    out, _, rep = gpu_sort(ovs, x, "ros", p, s, 2)
+    assert rep.counts.tolist() == [s] * (p - 1) + [s - 1]
+    np.testing.assert_array_equal(out, np.sort(x))
+
+
+def test_determinism_and_streams(ovs):
+    x = ovs_inputs.keys("u32", 1 << 22, seed=4)
+    st = torch.cuda.Stream()
+    a = gpu_sort(ovs, x, "ros", 512, 32, 7, stream=st)
+    b = gpu_sort(ovs, x, "ros", 512, 32, 7)
+    np.testing.assert_array_equal(a[0], b[0])
+    np.testing.assert_array_equal(a[2].counts, b[2].counts)
+    np.testing.assert_array_equal(a[2].splitter_tags, b[2].splitter_tags)
+
+
+def test_error_codes(ovs):
+    x = torch.zeros(100, dtype=torch.uint32, device="cuda")
+    with pytest.raises(ovs.OvsError) as e:
+        ovs.Sorter(100, torch.uint32, False, "ros", 11, 10, 1)
+    assert e.value.code in (ovs.OVS_EINVAL, ovs.OVS_ESAMPLE)
+    import ctypes
+    prm = ovs.params("ros", 4, 8, 1)
+    ws = torch.empty(16, dtype=torch.uint8, device="cuda")
+    rc = ovs.lib().ovs_sort_keys(x.data_ptr(), 100, ovs.OVS_U32, ctypes.byref(prm), ws.data_ptr(), 16, None, None)
+    assert rc == ovs.OVS_EWORKSPACE
+
+
+def test_c5_metric_full(ovs, orc):
+    """The bench workload (metric): 2^27 u32 uniform [0,2^32) data seed 51, ROS p=4096 s=64,
+    same launch configuration as bench.py; full element-wise comparison with the oracle."""
+    c = ovs_inputs.CONFIGS["C5"]
+    ros_case(ovs, orc, "u32", c["n"], c["p"], c["s"], c["seed"], dseed=51)
+
+
+@pytest.mark.parametrize("dist,dseed", [("f64_uniform", 31), ("f64_normal", 32)])
+def test_c3_full(ovs, orc, dist, dseed):
+    """BASELINE configs[2]: 2^27 f64, ROS p=1024 s=64 (uniform [0,1) and N(0,1))."""
+    c = ovs_inputs.CONFIGS["C3"]
+    ros_case(ovs, orc, dist, c["n"], c["p"], c["s"], c["seed"], dseed=dseed)

@@ -91,7 +91,7 @@ static inline u32 ilog2(u32 x) {
 
 // shared-memory capacity (items) of the bucket sorter
 template <class U, bool KV> static u32 bucket_cap(const DevInfo& di) {
-    const size_t reserve = 8192;  // static shared memory of k_bucket_sort
+    const size_t reserve = 8192;  // static shared memory of k_bucket_sort (~5.5 KB)
     size_t avail = (size_t)di.smem_optin - bucket_smem_fixed<U, KV>() - reserve;
     u32 cap = (u32)(avail / bucket_item_bytes<U, KV>());
     return cap & ~31u;
@@ -227,9 +227,9 @@ template <int DT, bool KV> struct Engine {
         set_pair(z.nchunks, z.nchunk, 1);  // device counts: chunks, segments
         fill_u32(c, l.nfit, 0, 2);
         const size_t sm_h = cls_smem_bytes<U>(z.P, z.L) + 4 * (size_t)z.P;
-        OVS_CK(cudaFuncSetAttribute(k_hist<DT, KV, true, PT_NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_h));
-        k_hist<DT, KV, true, PT_NT><<<z.nchunk, PT_NT, sm_h, c.st>>>(B, z.chunks, z.nchunks, z.seg, z.sk, z.st, z.lut,
-                                                                    z.P, z.L, z.hist);
+        OVS_CK(cudaFuncSetAttribute(k_hist<DT, KV, true, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_h));
+        k_hist<DT, KV, true, 1024><<<z.nchunk, 1024, sm_h, c.st>>>(B, z.chunks, z.nchunks, z.seg, z.sk, z.st, z.lut,
+                                                                  z.P, z.L, z.hist);
         c.check();
         k_colscan<<<std::min<u32>(cdiv(z.P, 32), 4 * c.di.sms), 1024, 0, c.st>>>(z.hist, z.seg, z.nseg, z.P, z.tot);
         c.check();

@@ -178,6 +178,22 @@ __device__ void block_scan_array(u32* a, u32 cnt, u32* red) {
     __syncthreads();
 }
 
+// exclusive scan in place of a[0..cnt), cnt <= NT*16, one round (16 consecutive per thread)
+template <int NT>
+__device__ void block_scan_small(u32* a, u32 cnt, u32* red) {
+    const u32 i0 = threadIdx.x * 16;
+    u32 v[16], s = 0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) { v[j] = (i0 + j < cnt) ? a[i0 + j] : 0u; s += v[j]; }
+    u32 ex = block_exclusive_scan<NT>(s, red, nullptr);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        if (i0 + j < cnt) a[i0 + j] = ex;
+        ex += v[j];
+    }
+    __syncthreads();
+}
+
 // ------------------------------------------------------------------ generic device scan (u32)
 // exclusive scan of n u32 values, 3 kernels; used by the ROS sample de-duplication (a1).
 constexpr int SCAN_NT = 1024, SCAN_PER = 4096;
@@ -736,7 +752,8 @@ __global__ void __launch_bounds__(1024) k_internal_sample(Bufs<typename Codec<DT
 // bucket is partitioned into the other buffer and the sub-buckets go on a per-CTA stack.
 constexpr int BS_NT = 512;
 constexpr int BS_NGMAX = 8192;
-constexpr int BS_BIGMAX = 128;
+constexpr int BS_BIGMAX = 768;
+constexpr int BS_HUGEMAX = 128;  // groups > 512 items: at most cap/512 exist
 constexpr int BS_STACK = 256;
 constexpr u32 BS_SPMAX = 64;
 constexpr u32 BS_SI = 32;
@@ -888,8 +905,9 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
     typedef Elem<U, KV> E;
     extern __shared__ __align__(16) char smem[];
     __shared__ u32 red[BS_NT / 32 + 1];
-    __shared__ u32 s_work, s_nbig, s_sp;
+    __shared__ u32 s_work, s_next, s_nbig, s_nhuge, s_over, s_sp;
     __shared__ u32 s_big[BS_BIGMAX];
+    __shared__ u32 s_huge[BS_HUGEMAX];
     __shared__ U s_mn[BS_NT / 32], s_mx[BS_NT / 32];
     __shared__ U sp_k[BS_SPMAX];
     __shared__ u32 sp_t[BS_SPMAX], sp_cnt[BS_SPMAX + 1], sp_cur[BS_SPMAX];
@@ -903,17 +921,29 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
     Bucket* stk = stack_pool + (size_t)blockIdx.x * BS_STACK;
     const u32 nl = *nlist;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_next = atomicAdd(ticket, 1u);
     for (;;) {
         if (threadIdx.x == 0) {
-            s_work = atomicAdd(ticket, 1u);
-            if (s_work < nl) { stk[0] = list[s_work]; s_sp = 1; }
+            s_work = s_next;
+            if (s_work < nl) {
+                stk[0] = list[s_work];
+                s_sp = 1;
+                s_next = atomicAdd(ticket, 1u);  // claim the next bucket now and prefetch it
+            }
         }
         __syncthreads();
         if (s_work >= nl) break;
+        if (s_next < nl) {
+            const Bucket nx = list[s_next];
+            const char* base = (const char*)(B.k[nx.buf] + nx.beg);
+            const u32 bytes = nx.len * (u32)sizeof(U);
+            for (u32 off = threadIdx.x * 128; off < bytes; off += BS_NT * 128)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(base + off));
+        }
         while (s_sp > 0) {
             const Bucket bk = stk[s_sp - 1];
             __syncthreads();
-            if (threadIdx.x == 0) { s_sp -= 1; s_nbig = 0; }
+            if (threadIdx.x == 0) { s_sp -= 1; s_nbig = 0; s_nhuge = 0; s_over = 0; }
             const u32 m = bk.len;
             const U* src = B.k[bk.buf];
             const u32* vsrc = KV ? B.v[bk.buf] : nullptr;
@@ -1021,7 +1051,7 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                 atomicAdd(&S.cnt[digit(k, ix)], 1u);
             });
             __syncthreads();
-            block_scan_array<BS_NT>(S.cnt, ng, red);  // cnt[g] = start of group g
+            block_scan_small<BS_NT>(S.cnt, ng, red);  // cnt[g] = start of group g
             // 2. scatter into shared memory by digit; afterwards cnt[g] = end of group g
             for_items<U, BS_NT, 4>(src, bk.beg, m, [&](U k, u32 o) {
                 u32 ix = 0, vv = 0;
@@ -1031,21 +1061,39 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                 if (KV) { S.i[pos] = ix; S.v[pos] = vv; }
             });
             __syncthreads();
-            // 3. one thread per group of <= 8: Batcher network in registers
-            for (u32 g = threadIdx.x; g < ng; g += BS_NT) {
-                const u32 gs = g ? S.cnt[g - 1] : 0u, len = S.cnt[g] - gs;
-                if (len <= 1 || len > 8) continue;
-                E a[8];
+            // 3. one thread per group of <= 8: Batcher network in registers; larger groups are
+            // appended (warp-aggregated) to a list for 3b
+            for (u32 g0 = 0; g0 < ng; g0 += BS_NT) {
+                const u32 g = g0 + threadIdx.x;
+                u32 gs = 0, len = 0;
+                if (g < ng) { gs = g ? S.cnt[g - 1] : 0u; len = S.cnt[g] - gs; }
+                if (len > 1 && len <= 8) {
+                    E a[8];
 #pragma unroll
-                for (u32 q = 0; q < 8; ++q) a[q] = q < len ? sm_get<U, KV>(S, gs + q) : E::inf();
-                network8(a);
+                    for (u32 q = 0; q < 8; ++q) a[q] = q < len ? sm_get<U, KV>(S, gs + q) : E::inf();
+                    network8(a);
 #pragma unroll
-                for (u32 q = 0; q < 8; ++q)
-                    if (q < len) sm_put<U, KV>(S, gs + q, a[q]);
+                    for (u32 q = 0; q < 8; ++q)
+                        if (q < len) sm_put<U, KV>(S, gs + q, a[q]);
+                }
+                const u32 mb = __ballot_sync(0xffffffffu, len > 8);
+                if (mb) {
+                    u32 base = 0;
+                    if (lane == 0) base = atomicAdd(&s_nbig, __popc(mb));
+                    base = __shfl_sync(0xffffffffu, base, 0) + __popc(mb & ((1u << lane) - 1));
+                    if (len > 8) {
+                        if (base < BS_BIGMAX) s_big[base] = g;
+                        else atomicOr(&s_over, 1u);
+                    }
+                }
             }
-            // 3b. groups of 9..512: one warp each (register bitonic); over 512: listed (at most
-            // cap/512 of them, so the list cannot overflow)
-            for (u32 g = wid; g < ng; g += BS_NT / 32) {
+            __syncthreads();
+            // 3b. listed groups of 9..512: one warp each (register bitonic); over 512: the CTA
+            const u32 nlisted = min(s_nbig, (u32)BS_BIGMAX);
+            const bool rescan = s_over != 0;  // list overflow (pathological skew): scan all groups
+            const u32 nwork = rescan ? ng : nlisted;
+            for (u32 q = wid; q < nwork; q += BS_NT / 32) {
+                const u32 g = rescan ? q : s_big[q];
                 const u32 gs = g ? S.cnt[g - 1] : 0u, len = S.cnt[g] - gs;
                 if (len <= 8) continue;
                 if (len <= 32) warp_sort_group<U, KV, 1>(S, gs, len);
@@ -1054,8 +1102,8 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                 else if (len <= 256) warp_sort_group<U, KV, 8>(S, gs, len);
                 else if (len <= 512) warp_sort_group<U, KV, 16>(S, gs, len);
                 else if (lane == 0) {
-                    const u32 q = atomicAdd(&s_nbig, 1u);
-                    if (q < BS_BIGMAX) s_big[q] = g;
+                    const u32 h = atomicAdd(&s_nhuge, 1u);
+                    if (h < BS_HUGEMAX) s_huge[h] = g;
                     else atomicOr(status, ST_LIST_OVER);
                 }
             }
@@ -1063,9 +1111,9 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
             // 3c. groups over 512: in-place bitonic network in shared memory, all comparators
             // ascending (the first step of each merge compares i with its mirror), so virtual
             // +inf padding beyond len never moves and len need not be a power of two
-            const u32 nhuge = min(s_nbig, (u32)BS_BIGMAX);
+            const u32 nhuge = min(s_nhuge, (u32)BS_HUGEMAX);
             for (u32 q = 0; q < nhuge; ++q) {
-                const u32 g = s_big[q];
+                const u32 g = s_huge[q];
                 const u32 gs = g ? S.cnt[g - 1] : 0u, len = S.cnt[g] - gs;
                 u32 N = 1;
                 while (N < len) N <<= 1;

@@ -251,11 +251,15 @@ template <int DT, bool KV> struct Engine {
         c.check();
     }
 
-    void bucket_sort(Lists& l, u64 seed) {
+    // sorts every bucket of the list into okeys (+ ovals, + oidx) at the bucket's position;
+    // out_raw applies the codec's inverse (the caller's dtype) on the way out
+    void bucket_sort(Lists& l, u64 seed, U* okeys = nullptr, u32* ovals = nullptr, u32* oidx = nullptr,
+                     bool out_raw = true) {
         if (c.dry) return;
+        if (!okeys) { okeys = B.k[0]; ovals = KV ? B.v[0] : nullptr; }
         const size_t sm = bucket_smem<U, KV>(cap);
         OVS_CK(cudaFuncSetAttribute(k_bucket_sort<DT, KV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        k_bucket_sort<DT, KV><<<l.grid, BS_NT, sm, c.st>>>(l.fit, l.nfit, l.ticket, B, B.k[0], KV ? B.v[0] : nullptr,
+        k_bucket_sort<DT, KV><<<l.grid, BS_NT, sm, c.st>>>(l.fit, l.nfit, l.ticket, B, okeys, ovals, oidx, out_raw,
                                                           cap, l.stack, seed, c.status);
         c.check();
     }
@@ -413,10 +417,115 @@ struct Out {
     size_t ws = 0;
 };
 
+
+// ------------------------------------------------------------------ DRO contract sort (SqDet)
+// Algorithm 1 on the device: (a9) the p sequences are sorted stably by the
+// bucket sorter into buffer 1; (a10) rp regular samples per sequence; (a11) the rp^2 samples
+// are sorted; (a12) S[q] = T[(q+1)rp - 1]; (a13) every splitter is binary-searched into every
+// sorted sequence; (a14) bucket j gathers its runs X_{k,j} in k order and is sorted (instead
+// of the paper's p-way merge; the result is the same stable order).
+template <int DT, bool KV> struct DroSort {
+    typedef typename Codec<DT>::U U;
+    Ctx& c;
+    Engine<DT, KV> e;
+    typename Engine<DT, KV>::Lists l1, l2;
+    u32 n, p, r, s, ns, flags;
+    u64* counts = nullptr;
+    U* sk = nullptr;
+    u32* st = nullptr;
+    u64* t_pack = nullptr; u64* t_key = nullptr; u32* t_tag = nullptr;
+    InternalSort<false>* ts32 = nullptr;
+    InternalSort<true>* ts64 = nullptr;
+    u32* bound = nullptr; u32* cnt = nullptr; u32* tot = nullptr; u32* nseg = nullptr;
+    Seg* seg = nullptr;
+
+    DroSort(Ctx& ctx, U* keys, u32* vals, u32 n_, u32 p_, u32 r_, u32 flags_)
+        : c(ctx), e(ctx), n(n_), p(p_), r(r_), flags(flags_) {
+        e.n = n;
+        e.cap = bucket_cap<U, KV>(c.di);
+        e.B.k[0] = keys;
+        e.B.v[0] = vals;
+        e.B.k[1] = c.take<U>(n);
+        e.B.v[1] = KV ? c.take<u32>(n) : nullptr;
+        e.B.i[0] = KV ? c.take<u32>(n) : nullptr;
+        e.B.i[1] = KV ? c.take<u32>(n) : nullptr;
+        s = r * p;
+        ns = s * p;
+        counts = c.take<u64>(p);
+        sk = c.take<U>(p);
+        st = c.take<u32>(p);
+        if (sizeof(U) == 4) {
+            t_pack = c.take<u64>(ns);
+            ts32 = new InternalSort<false>(c, ns, t_pack, nullptr);
+        } else {
+            t_key = c.take<u64>(ns);
+            t_tag = c.take<u32>(ns);
+            ts64 = new InternalSort<true>(c, ns, t_key, t_tag);
+        }
+        bound = c.take<u32>((size_t)p * (p + 1));
+        cnt = c.take<u32>((size_t)p * p);
+        tot = c.take<u32>(p + 1);
+        seg = c.take<Seg>(1);
+        nseg = c.take<u32>(2);
+        e.carve_lists(l1, p);
+        e.carve_lists(l2, p);
+    }
+    ~DroSort() { delete ts32; delete ts64; }
+
+    void run() {
+        if (c.dry) return;
+        Bufs<U>& B = e.B;
+        c.mark(0);
+        // a9: BaselineSorting of the p sequences -> buffer 1 (ordered keys, values, indices)
+        fill_u32(c, l1.nfit, 0, 2);
+        k_dro_segments<<<cdiv(p, 256), 256, 0, c.st>>>(l1.fit, l1.nfit, n, p);
+        c.check();
+        e.bucket_sort(l1, 0x5e9u, B.k[1], KV ? B.v[1] : nullptr, KV ? B.i[1] : nullptr, false);
+        // a10-a12: regular sample, sample sort, splitters
+        k_dro_sample<U><<<cdiv((u64)ns, 256), 256, 0, c.st>>>(B.k[1], n, p, s, flags & OVS_DRO_PADDED_POSITIONS,
+                                                             t_pack, t_key, t_tag);
+        c.check();
+        if (ts32) ts32->run(0xd0d0);
+        else ts64->run(0xd0d0);
+        k_pick_splitters<U><<<cdiv(p, 256), 256, 0, c.st>>>(t_pack, t_key, t_tag, p, s, sk, st);
+        c.check();
+        c.mark(1);
+        // a13: split every sorted sequence by binary search; bucket starts and run offsets
+        k_dro_bounds<U><<<cdiv((u64)p * (p + 1), 256), 256, 0, c.st>>>(B.k[1], n, p, sk, st, bound);
+        c.check();
+        k_dro_counts<<<cdiv((u64)p * p, 256), 256, 0, c.st>>>(bound, p, cnt);
+        c.check();
+        k_dro_seg<U><<<1, 1024, 0, c.st>>>(B.k[1], n, p, sk, 0, seg, nseg);
+        c.check();
+        k_colscan<<<std::min<u32>(cdiv(p, 32), 4 * c.di.sms), 1024, 0, c.st>>>(cnt, seg, nseg, p, tot);
+        c.check();
+        fill_u32(c, l2.nfit, 0, 2);
+        k_segscan<U><<<1, 1024, 0, c.st>>>(seg, nseg, p, tot, sk, 0, e.cap, l2.fit, l2.nfit, l2.fit_cap, nullptr,
+                                          nullptr, 0, counts, c.status);
+        c.check();
+        c.mark(2);
+        // a14: gather the runs X_{k,j} of every bucket (k order) into buffer 0, sort each bucket
+        k_dro_gather<U, KV><<<cdiv((u64)p * p * 32, 256), 256, 0, c.st>>>(B, n, p, bound, cnt, tot);
+        c.check();
+        c.mark(3);
+        e.bucket_sort(l2, 0x5e9u);
+        c.mark(4);
+    }
+};
+
 template <int DT, bool KV>
 Out plan_or_run(Ctx& c, void* keys, u32* vals, size_t n, const ovs_params* prm) {
     typedef typename Codec<DT>::U U;
-    if (prm->method == OVS_DRO && prm->p > 1) throw StatusFail{OVS_EINVAL, "DRO path not available in this build"};
+    if (prm->method == OVS_DRO && prm->p > 1) {
+        DroSort<DT, KV> d(c, (U*)keys, vals, (u32)n, prm->p, prm->s, prm->flags);
+        Out o;
+        o.sk = d.sk;
+        o.st = d.st;
+        o.counts = d.counts;
+        if (!c.dry) d.run();
+        o.ws = c.off + 256;
+        return o;
+    }
     RosSort<DT, KV> r(c, (U*)keys, vals, (u32)n, prm->p, prm->s, prm->seed);
     if (prm->p > 1 && r.z.P > r.e.max_p_one_level())
         throw StatusFail{OVS_EINVAL, "p too large for the one-level classifier in shared memory"};

@@ -93,7 +93,9 @@ template <class U> struct Bufs {
     u32* i[2];
 };
 
-enum : u32 { BK_LOOSE = 0x80000000u };  // Bucket.level flag: lo/hi are not tight bounds
+// Bucket.level flags: lo/hi are not tight bounds; the items are the caller's raw keys (codec
+// not applied yet, value/index arrays not built yet: index = position)
+enum : u32 { BK_LOOSE = 0x80000000u, BK_RAW = 0x40000000u };
 
 // ------------------------------------------------------------------ the classifier
 // bucket(k, tag) = #{q : S[q] <lex (k, tag)}: a lower_bound over the p-1 splitters with the
@@ -899,8 +901,8 @@ template <class U, bool KV> __host__ __device__ constexpr size_t bucket_item_byt
 template <int DT, bool KV>
 __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, const u32* nlist, u32* ticket,
                                                            Bufs<typename Codec<DT>::U> B, typename Codec<DT>::U* okeys,
-                                                           u32* ovals, u32 cap, Bucket* stack_pool, u64 seed,
-                                                           u32* status) {
+                                                           u32* ovals, u32* oidx, bool out_raw, u32 cap,
+                                                           Bucket* stack_pool, u64 seed, u32* status) {
     typedef typename Codec<DT>::U U;
     typedef Elem<U, KV> E;
     extern __shared__ __align__(16) char smem[];
@@ -948,6 +950,9 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
             const U* src = B.k[bk.buf];
             const u32* vsrc = KV ? B.v[bk.buf] : nullptr;
             const u32* isrc = KV ? B.i[bk.buf] : nullptr;
+            const bool rawin = (bk.level & BK_RAW) != 0;
+            auto K = [&](U x) -> U { return rawin ? Codec<DT>::ord(x) : x; };
+            auto IX = [&](u32 pos) -> u32 { return (KV && !rawin) ? isrc[pos] : pos; };
             if (m > cap) {
                 // ---------------- CTA-local re-split of an oversized bucket
                 const u32 part = (u32)((cap * 45ull) / 100);
@@ -960,8 +965,8 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                     if (j < ms) {
                         const u64 u = rng_H(seed ^ ((u64)bk.beg * 0x9e3779b97f4a7c15ull), 64 + (bk.level & 0xffffu), j);
                         const u32 o = (u32)__umul64hi(u, (u64)m);
-                        tk[j] = src[bk.beg + o];
-                        tt[j] = KV ? isrc[bk.beg + o] : bk.beg + o;
+                        tk[j] = K(src[bk.beg + o]);
+                        tt[j] = IX(bk.beg + o);
                     } else {
                         tk[j] = umax_of<U>();
                         tt[j] = 0xffffffffu;
@@ -975,8 +980,9 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                 }
                 if (threadIdx.x <= P) sp_cnt[threadIdx.x] = 0;
                 __syncthreads();
-                for_items<U, BS_NT, 4>(src, bk.beg, m, [&](U k, u32 o) {
-                    const u32 tg = KV ? isrc[bk.beg + o] : bk.beg + o;
+                for_items<U, BS_NT, 4>(src, bk.beg, m, [&](U kr, u32 o) {
+                    const U k = K(kr);
+                    const u32 tg = IX(bk.beg + o);
                     atomicAdd(&sp_cnt[lower_bound_kt<U>(sp_k, sp_t, P - 1, k, tg)], 1u);
                 });
                 __syncthreads();
@@ -987,8 +993,9 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                 }
                 __syncthreads();
                 const u32 db = 1 - bk.buf;
-                for_items<U, BS_NT, 4>(src, bk.beg, m, [&](U k, u32 o) {
-                    const u32 tg = KV ? isrc[bk.beg + o] : bk.beg + o;
+                for_items<U, BS_NT, 4>(src, bk.beg, m, [&](U kr, u32 o) {
+                    const U k = K(kr);
+                    const u32 tg = IX(bk.beg + o);
                     const u32 b = lower_bound_kt<U>(sp_k, sp_t, P - 1, k, tg);
                     const u32 d = bk.beg + atomicAdd(&sp_cur[b], 1u);
                     B.k[db][d] = k;
@@ -1018,7 +1025,7 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
             U lo = (U)bk.lo, hi = (U)bk.hi;
             if (bk.level & BK_LOOSE) {
                 U mn = umax_of<U>(), mx = 0;
-                for_items<U, BS_NT, 4>(src, bk.beg, m, [&](U k, u32) { mn = min(mn, k); mx = max(mx, k); });
+                for_items<U, BS_NT, 4>(src, bk.beg, m, [&](U kr, u32) { const U k = K(kr); mn = min(mn, k); mx = max(mx, k); });
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) { mn = min(mn, shfl_xor_any(mn, o)); mx = max(mx, shfl_xor_any(mx, o)); }
                 if (lane == 0) { s_mn[wid] = mn; s_mx[wid] = mx; }
@@ -1046,16 +1053,17 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
             for (u32 g = threadIdx.x; g < ng; g += BS_NT) S.cnt[g] = 0;
             __syncthreads();
             // 1. digit histogram
-            for_items<U, BS_NT, 4>(src, bk.beg, m, [&](U k, u32 o) {
-                const u32 ix = KV ? isrc[bk.beg + o] : 0u;
-                atomicAdd(&S.cnt[digit(k, ix)], 1u);
+            for_items<U, BS_NT, 4>(src, bk.beg, m, [&](U kr, u32 o) {
+                const u32 ix = KV ? IX(bk.beg + o) : 0u;
+                atomicAdd(&S.cnt[digit(K(kr), ix)], 1u);
             });
             __syncthreads();
             block_scan_small<BS_NT>(S.cnt, ng, red);  // cnt[g] = start of group g
             // 2. scatter into shared memory by digit; afterwards cnt[g] = end of group g
-            for_items<U, BS_NT, 4>(src, bk.beg, m, [&](U k, u32 o) {
+            for_items<U, BS_NT, 4>(src, bk.beg, m, [&](U kr, u32 o) {
+                const U k = K(kr);
                 u32 ix = 0, vv = 0;
-                if (KV) { ix = isrc[bk.beg + o]; vv = vsrc[bk.beg + o]; }
+                if (KV) { ix = IX(bk.beg + o); vv = vsrc[bk.beg + o]; }
                 const u32 pos = atomicAdd(&S.cnt[digit(k, ix)], 1u);
                 S.k[pos] = k;
                 if (KV) { S.i[pos] = ix; S.v[pos] = vv; }
@@ -1141,23 +1149,151 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                 U* out = okeys + bk.beg;
                 const u32 mis = (u32)(((uintptr_t)out) & 15u) / (u32)sizeof(U);
                 const u32 head = mis ? min(m, V - mis) : 0u;
-                if (threadIdx.x < head) out[threadIdx.x] = Codec<DT>::raw(S.k[threadIdx.x]);
+                auto R = [&](U x) -> U { return out_raw ? Codec<DT>::raw(x) : x; };
+                if (threadIdx.x < head) out[threadIdx.x] = R(S.k[threadIdx.x]);
                 const u32 nv = (m - head) / V;
                 uint4* o4 = (uint4*)(out + head);
                 for (u32 v = threadIdx.x; v < nv; v += BS_NT) {
                     uint4 r;
                     U* e = (U*)&r;
 #pragma unroll
-                    for (u32 q = 0; q < V; ++q) e[q] = Codec<DT>::raw(S.k[head + v * V + q]);
+                    for (u32 q = 0; q < V; ++q) e[q] = R(S.k[head + v * V + q]);
                     o4[v] = r;
                 }
-                for (u32 o = head + nv * V + threadIdx.x; o < m; o += BS_NT) out[o] = Codec<DT>::raw(S.k[o]);
-                if (KV)
+                for (u32 o = head + nv * V + threadIdx.x; o < m; o += BS_NT) out[o] = R(S.k[o]);
+                if (KV) {
                     for (u32 o = threadIdx.x; o < m; o += BS_NT) ovals[bk.beg + o] = S.v[o];
+                    if (oidx)
+                        for (u32 o = threadIdx.x; o < m; o += BS_NT) oidx[bk.beg + o] = S.i[o];
+                }
             }
             __syncthreads();
         }
         __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------ DRO (Algorithm 1, SqDet)
+// a9: the p baseline sequences X_k (first n mod p get ceil(n/p) keys, reading Q8), as
+// buckets of the caller's raw keys (sorted stably by the bucket sorter into buffer 1)
+__global__ void k_dro_segments(Bucket* list, u32* nlist, u32 n, u32 p) {
+    const u32 k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= p) return;
+    const u32 q = n / p, rm = n % p;
+    Bucket b;
+    b.beg = k * q + min(k, rm);
+    b.len = q + (k < rm ? 1u : 0u);
+    b.buf = 0;
+    b.level = BK_RAW | BK_LOOSE;
+    b.lo = 0; b.hi = ~0ull;
+    list[k] = b;
+    if (k == 0) *nlist = p;
+}
+
+// a10: T_k = the s = rp regular samples of the sorted X_k: the last key of each of s evenly
+// sized segments (balanced reading Q9), or the Lemma 1 proof's padded positions
+// (flag).  Tag = start_k + position (the (sequence id, index) order, Q6).
+// 32-bit keys are packed (ord key << 32 | tag); 64-bit keys stored with a separate tag.
+template <class U>
+__global__ void k_dro_sample(const U* xs, u32 n, u32 p, u32 s, u32 padded, u64* t_pack, u64* t_key, u32* t_tag) {
+    const u64 id = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (id >= (u64)s * p) return;
+    const u32 k = (u32)(id / s), j = (u32)(id % s);
+    const u32 q = n / p, rm = n % p;
+    const u32 beg = k * q + min(k, rm), m = q + (k < rm ? 1u : 0u);
+    u32 e;
+    if (padded) {
+        const u32 x = ((n + p - 1) / p + s - 1) / s;
+        e = (j + 1 == s) ? m - 1 : (u32)min((u64)(j + 1) * x, (u64)m) - 1;
+    } else {
+        const u32 qq = m / s, rr = m % s;
+        e = (j + 1) * qq + min(j + 1, rr) - 1;
+    }
+    const U key = xs[beg + e];
+    const u32 tag = beg + e;
+    if (sizeof(U) == 4) t_pack[id] = ((u64)key << 32) | tag;
+    else { t_key[id] = (u64)key; t_tag[id] = tag; }
+}
+
+// a13: bound[k][j+1] = #{t : (X_k[t], start_k + t) <=lex S[j]} by binary search of splitter j
+// into the sorted X_k; count matrix cnt[k][j] = bound[k][j+1]-bound[k][j]
+template <class U>
+__global__ void k_dro_bounds(const U* xs, u32 n, u32 p, const U* sk, const u32* st, u32* bound) {
+    const u64 id = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (id >= (u64)p * (p + 1)) return;
+    const u32 k = (u32)(id / (p + 1)), j = (u32)(id % (p + 1));
+    const u32 q = n / p, rm = n % p;
+    const u32 beg = k * q + min(k, rm), m = q + (k < rm ? 1u : 0u);
+    u32 r;
+    if (j == 0) r = 0;
+    else if (j == p) r = m;
+    else {
+        const U key = sk[j - 1];
+        const u32 tag = st[j - 1];
+        // upper bound: first t with (X_k[t], beg + t) >lex (key, tag)
+        u32 lo = 0, cnt = m;
+        while (cnt > 0) {
+            const u32 half = cnt >> 1, mid = lo + half;
+            const U x = xs[beg + mid];
+            const bool le = x < key || (x == key && beg + mid <= tag);
+            if (le) { lo = mid + 1; cnt -= half + 1; } else cnt = half;
+        }
+        r = lo;
+    }
+    bound[id] = r;
+}
+
+__global__ void k_dro_counts(const u32* bound, u32 p, u32* cnt) {
+    const u64 id = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (id >= (u64)p * p) return;
+    const u32 k = (u32)(id / p), j = (u32)(id % p);
+    cnt[id] = bound[(u64)k * (p + 1) + j + 1] - bound[(u64)k * (p + 1) + j];
+}
+
+// the single "segment" of the DRO split: p chunks (the sequences) x p buckets; key bounds of
+// the whole input from the sorted sequences' first and last keys
+template <class U>
+__global__ void k_dro_seg(const U* xs, u32 n, u32 p, const U* sk, u32 L, Seg* seg, u32* nseg) {
+    __shared__ U smn[32], smx[32];
+    const u32 q = n / p, rm = n % p;
+    U mn = umax_of<U>(), mx = 0;
+    for (u32 k = threadIdx.x; k < p; k += blockDim.x) {
+        const u32 beg = k * q + min(k, rm), m = q + (k < rm ? 1u : 0u);
+        mn = min(mn, xs[beg]);
+        mx = max(mx, xs[beg + m - 1]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) { mn = min(mn, shfl_xor_any(mn, o)); mx = max(mx, shfl_xor_any(mx, o)); }
+    if ((threadIdx.x & 31) == 0) { smn[threadIdx.x >> 5] = mn; smx[threadIdx.x >> 5] = mx; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (u32 w = 1; w < blockDim.x / 32; ++w) { mn = min(mn, smn[w]); mx = max(mx, smx[w]); }
+        mn = min(mn, smn[0]); mx = max(mx, smx[0]);
+        Seg g;
+        g.lo = (u64)mn; g.hi = (u64)mx; g.base = 0;
+        g.beg = 0; g.len = n; g.P = p; g.shift = 0; g.L = L; g.chunk0 = 0; g.nchunk = p;
+        g.src = 1;  // buckets land in buffer 0
+        g.loose = 0; g.pad = 0;
+        *seg = g;
+        nseg[0] = 1;
+    }
+}
+
+// a14 (gather): run X_{k,j} (sorted X_k[bound[k][j] .. bound[k][j+1])) goes to bucket j at
+// offset start_j + sum_{k'<k} cnt[k'][j] (column-scanned cnt); one warp per run
+template <class U, bool KV>
+__global__ void k_dro_gather(Bufs<U> B, u32 n, u32 p, const u32* bound, const u32* off, const u32* bstart) {
+    const u64 w = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const u32 lane = threadIdx.x & 31;
+    if (w >= (u64)p * p) return;
+    const u32 k = (u32)(w / p), j = (u32)(w % p);
+    const u32 q = n / p, rm = n % p;
+    const u32 beg = k * q + min(k, rm);
+    const u32 a = bound[(u64)k * (p + 1) + j], b = bound[(u64)k * (p + 1) + j + 1];
+    const u32 d = bstart[j] + off[w];
+    for (u32 t = a + lane; t < b; t += 32) {
+        B.k[0][d + t - a] = B.k[1][beg + t];
+        if (KV) { B.v[0][d + t - a] = B.v[1][beg + t]; B.i[0][d + t - a] = B.i[1][beg + t]; }
     }
 }
 

@@ -133,3 +133,66 @@ def test_c3_full(ovs, orc, dist, dseed):
     """BASELINE configs[2]: 2^27 f64, ROS p=1024 s=64 (uniform [0,1) and N(0,1))."""
     c = ovs_inputs.CONFIGS["C3"]
     ros_case(ovs, orc, dist, c["n"], c["p"], c["s"], c["seed"], dseed=dseed)
+
+
+# ---------------------------------------------------------------- DRO (Algorithm 1, SqDet)
+def dro_case(ovs, orc, x, p, r, kv=False, padded=False):
+    n = len(x)
+    v = ovs_inputs.index_values(n) if kv else None
+    ref = orc.dro_sort(x, p, r, vals=v, padded=padded)
+    xt = torch.from_numpy(x).cuda()
+    if kv:
+        vt = torch.from_numpy(v).cuda()
+        rep = ovs.Sorter(n, xt.dtype, True, "dro", p, r, 0, padded)(xt, vt, report=True)
+    else:
+        vt = None
+        rep = ovs.Sorter(n, xt.dtype, False, "dro", p, r, 0, padded)(xt, report=True)
+    torch.cuda.synchronize()
+    check(ref, xt.cpu().numpy(), None if vt is None else vt.cpu().numpy(), rep, p)
+    # Lemma 1 (PAPER.md:421-423) on the GPU's own bucket counts
+    assert int(rep.counts.max()) <= orc.lemma1_bound(n, p, r)
+    return rep
+
+
+DRO_EDGE = [("u32_u31", 1000, 4, 1), ("u32_u31", 1003, 5, 2), ("i32_gauss", 100_003, 16, 3), ("u32_const", 65_536, 8, 4),
+            ("u32_few4", 200_000, 32, 5), ("f64_normal", 300_001, 64, 2), ("i32_few", 1_000_000, 100, 24),
+            ("u32", 3_000_000, 256, 8), ("f64_uniform", 50_000, 2, 1), ("u32_u31", 10, 1, 1)]
+
+
+@pytest.mark.parametrize("dist,n,p,r", DRO_EDGE)
+@pytest.mark.parametrize("padded", [False, True])
+def test_dro_keys_edge_matrix(ovs, orc, dist, n, p, r, padded):
+    dro_case(ovs, orc, ovs_inputs.keys(dist, n, seed=n % 31), p, r, padded=padded)
+
+
+@pytest.mark.parametrize("dist,n,p,r", [("u16key", 200_000, 16, 3), ("u32_few4", 100_000, 8, 8),
+                                         ("f64_normal", 150_000, 32, 2), ("u32_const", 70_000, 4, 2)])
+def test_dro_pairs_stable_edge_matrix(ovs, orc, dist, n, p, r):
+    dro_case(ovs, orc, ovs_inputs.keys(dist, n, seed=3), p, r, kv=True)
+
+
+def test_dro_closed_forms(ovs):
+    """Sorted input: counts = m_j; reverse: m_{p-1-j}; constant: m_j (tags order equal keys)."""
+    n, p, r = 1_000_003, 64, 3
+    m = [n // p + (1 if k < n % p else 0) for k in range(p)]
+    base = np.sort(ovs_inputs.keys("i32_uniform", n, seed=8))
+    for x, want in [(base, m), (base[::-1].copy(), m[::-1]), (np.full(n, 5, np.int32), m)]:
+        xt = torch.from_numpy(x).cuda()
+        rep = ovs.Sorter(n, xt.dtype, False, "dro", p, r, 0)(xt, report=True)
+        assert rep.counts.tolist() == want
+        np.testing.assert_array_equal(xt.cpu().numpy(), np.sort(x))
+
+
+@pytest.mark.parametrize("dist,dseed", [("i32_uniform", 21), ("i32_gauss", 22), ("i32_sorted", 23),
+                                        ("i32_reverse", 24), ("i32_few", 25)])
+def test_c2_full(ovs, orc, dist, dseed):
+    """BASELINE configs[1]: 2^24 i32, DRO p=256, r=log2 n=24 (reading Q7), five distributions."""
+    c = ovs_inputs.CONFIGS["C2"]
+    dro_case(ovs, orc, ovs_inputs.keys(dist, c["n"], seed=dseed), c["p"], c["s"])
+
+
+def test_c4_full(ovs, orc):
+    """BASELINE configs[3]: 2^27 stable key-value pairs (u32 key uniform [0,2^16), value =
+    original index), DRO p=512, r=ceil(log2 n)=27; checks stability element by element."""
+    c = ovs_inputs.CONFIGS["C4"]
+    dro_case(ovs, orc, ovs_inputs.keys("u16key", c["n"], seed=41), c["p"], c["s"], kv=True)

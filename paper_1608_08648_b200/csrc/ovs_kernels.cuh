@@ -795,6 +795,24 @@ template <class E> __device__ __forceinline__ void network8(E (&a)[8]) {
     cex(a[1], a[2]); cex(a[3], a[4]); cex(a[5], a[6]);
 }
 
+// Batcher's odd-even merge sort for 16 inputs: two 8-sorts (19 + 19 comparators) and the
+// odd-even merge of the halves (25 comparators), 63 in all
+template <class E> __device__ __forceinline__ void network16(E (&a)[16]) {
+    E* lo = a;
+    E* hi = a + 8;
+    E (&l8)[8] = *reinterpret_cast<E(*)[8]>(lo);
+    E (&h8)[8] = *reinterpret_cast<E(*)[8]>(hi);
+    network8(l8);
+    network8(h8);
+    // odd-even merge of a[0..8) and a[8..16)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) cex(a[i], a[i + 8]);
+    cex(a[4], a[8]); cex(a[5], a[9]); cex(a[6], a[10]); cex(a[7], a[11]);
+    cex(a[2], a[4]); cex(a[3], a[5]); cex(a[6], a[8]); cex(a[7], a[9]); cex(a[10], a[12]); cex(a[11], a[13]);
+    cex(a[1], a[2]); cex(a[3], a[4]); cex(a[5], a[6]); cex(a[7], a[8]); cex(a[9], a[10]); cex(a[11], a[12]);
+    cex(a[13], a[14]);
+}
+
 // bitonic sort of 32*R elements held as a[r] at lane: element index e = r*32 + lane
 template <class E, int R>
 __device__ __forceinline__ void warp_bitonic(E (&a)[R]) {
@@ -1046,9 +1064,15 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
             const unsigned __int128 R = (unsigned __int128)xmax + 1;
             const unsigned __int128 mq = (((unsigned __int128)ng) << 64) / R;
             const u64 mult = mq > (unsigned __int128)0xffffffffffffffffull ? 0xffffffffffffffffull : (u64)mq;
+            const unsigned __int128 mq32 = mq >> 32;
+            const u32 mult32 = mq32 > (unsigned __int128)0xffffffffu ? 0xffffffffu : (u32)mq32;
             auto digit = [&](U k, u32 ix) -> u32 {
-                const u64 x = comp ? ((((u64)(k - lo)) << 32) | ix) : (u64)(U)(k - lo);
-                return min((u32)__umul64hi(x, mult), ng - 1);  // min: memory safety only
+                if constexpr (!KV && sizeof(U) == 4) {
+                    return min(__umulhi((u32)(k - lo), mult32), ng - 1);  // min: memory safety only
+                } else {
+                    const u64 x = comp ? ((((u64)(k - lo)) << 32) | ix) : (u64)(U)(k - lo);
+                    return min((u32)__umul64hi(x, mult), ng - 1);
+                }
             };
             for (u32 g = threadIdx.x; g < ng; g += BS_NT) S.cnt[g] = 0;
             __syncthreads();
@@ -1096,14 +1120,27 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                 }
             }
             __syncthreads();
-            // 3b. listed groups of 9..512: one warp each (register bitonic); over 512: the CTA
+            // 3b. listed groups of 9..16: one thread each (63-comparator network)
             const u32 nlisted = min(s_nbig, (u32)BS_BIGMAX);
             const bool rescan = s_over != 0;  // list overflow (pathological skew): scan all groups
             const u32 nwork = rescan ? ng : nlisted;
+            for (u32 q = threadIdx.x; q < nwork; q += BS_NT) {
+                const u32 g = rescan ? q : s_big[q];
+                const u32 gs = g ? S.cnt[g - 1] : 0u, len = S.cnt[g] - gs;
+                if (len <= 8 || len > 16) continue;
+                E a[16];
+#pragma unroll
+                for (u32 t = 0; t < 16; ++t) a[t] = t < len ? sm_get<U, KV>(S, gs + t) : E::inf();
+                network16(a);
+#pragma unroll
+                for (u32 t = 0; t < 16; ++t)
+                    if (t < len) sm_put<U, KV>(S, gs + t, a[t]);
+            }
+            // 3c'. groups of 17..512: one warp each (register bitonic); over 512: the CTA
             for (u32 q = wid; q < nwork; q += BS_NT / 32) {
                 const u32 g = rescan ? q : s_big[q];
                 const u32 gs = g ? S.cnt[g - 1] : 0u, len = S.cnt[g] - gs;
-                if (len <= 8) continue;
+                if (len <= 16) continue;
                 if (len <= 32) warp_sort_group<U, KV, 1>(S, gs, len);
                 else if (len <= 64) warp_sort_group<U, KV, 2>(S, gs, len);
                 else if (len <= 128) warp_sort_group<U, KV, 4>(S, gs, len);

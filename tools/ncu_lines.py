@@ -19,7 +19,10 @@ for r in rows:
         continue
     if h is None or len(r) < len(h) or r[0] == "" or not r[0].isdigit():
         continue
-    lines.append([fname + ":" + r[0], r[1], float(r[ws] or 0), float(r[ie] or 0)])
+    try:
+        lines.append([fname + ":" + r[0], r[1], float(r[ws] or 0), float(r[ie] or 0)])
+    except ValueError:
+        continue
 ti = sum(l[3] for l in lines) or 1
 ts = sum(l[2] for l in lines) or 1
 print(f"total warp-inst {ti:.3e}  stall samples {ts:.0f}")

@@ -161,6 +161,10 @@ template <int DT, bool KV> struct Engine {
         Bucket* stack = nullptr; u32 grid = 0;
     };
 
+    // keys-only sorts use the write-combining scatter when its shared memory fits
+    bool use_wc(u32 P, u32 L) const {
+        return !KV && P > 1 && wc_smem_bytes<U>(P, L) + 512 <= (size_t)c.di.smem_optin;
+    }
     static size_t scatter_smem(u32 P, u32 L) {
         return scatter_smem_bytes<U, KV, PartItems<U, KV>::v, PT_NT>(P, L);
     }
@@ -178,6 +182,9 @@ template <int DT, bool KV> struct Engine {
     void carve_level0(Level0& z, u32 P) {
         z.P = P;
         z.L = P > 1 ? std::min<u32>(8192, std::max<u32>(64, pow2_at_least(2 * P))) : 1;
+        // keys-only: shrink the table until the write-combining scatter fits shared memory
+        if (!KV && P > 1)
+            while (z.L > 64 && wc_smem_bytes<U>(P, z.L) + 512 > (size_t)c.di.smem_optin) z.L >>= 1;
         z.log2L = ilog2(z.L);
         // chunks: one per resident CTA slot, whole sub-tiles
         const u32 ts = PT_NT * PartItems<U, KV>::v;
@@ -227,9 +234,11 @@ template <int DT, bool KV> struct Engine {
         set_pair(z.nchunks, z.nchunk, 1);  // device counts: chunks, segments
         fill_u32(c, l.nfit, 0, 2);
         const size_t sm_h = cls_smem_bytes<U>(z.P, z.L) + 4 * (size_t)z.P;
+        const u32 hsplit = 2;  // two 1024-thread CTAs per chunk
+        OVS_CK(cudaMemsetAsync(z.hist, 0, sizeof(u32) * (size_t)z.nchunk * z.P, c.st));
         OVS_CK(cudaFuncSetAttribute(k_hist<DT, KV, true, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_h));
-        k_hist<DT, KV, true, 1024><<<z.nchunk, 1024, sm_h, c.st>>>(B, z.chunks, z.nchunks, z.seg, z.sk, z.st, z.lut,
-                                                                  z.P, z.L, z.hist);
+        k_hist<DT, KV, true, 1024><<<z.nchunk * hsplit, 1024, sm_h, c.st>>>(B, z.chunks, z.nchunks, z.seg, z.sk, z.st,
+                                                                           z.lut, z.P, z.L, z.hist, hsplit);
         c.check();
         k_colscan<<<std::min<u32>(cdiv(z.P, 32), 4 * c.di.sms), 1024, 0, c.st>>>(z.hist, z.seg, z.nseg, z.P, z.tot);
         c.check();
@@ -237,12 +246,22 @@ template <int DT, bool KV> struct Engine {
                                           nullptr, 0, counts_out, c.status);
         c.check();
         if (mark_phases) c.mark(2);
-        constexpr int IT = PartItems<U, KV>::v;
-        const size_t sm_s = scatter_smem(z.P, z.L);
-        auto ks = k_scatter<DT, KV, true, PT_NT, IT>;
-        OVS_CK(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_s));
-        ks<<<z.nchunk, PT_NT, sm_s, c.st>>>(B, z.chunks, z.nchunks, z.seg, z.sk, z.st, z.lut, z.P, z.L, z.hist, z.tot);
-        c.check();
+        if (use_wc(z.P, z.L)) {
+            constexpr int IT = 32 / (int)sizeof(U) * 2;  // 16 u32 / 8 u64 keys per thread
+            const size_t sm_w = wc_smem_bytes<U>(z.P, z.L);
+            auto kw = k_scatter_wc<DT, PT_NT, IT>;
+            OVS_CK(cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_w));
+            kw<<<z.nchunk, PT_NT, sm_w, c.st>>>(B, z.chunks, z.nchunks, z.seg, z.sk, z.st, z.lut, z.P, z.L, z.hist, z.tot);
+            c.check();
+        } else {
+            constexpr int IT = PartItems<U, KV>::v;
+            const size_t sm_s = scatter_smem(z.P, z.L);
+            auto ks = k_scatter<DT, KV, true, PT_NT, IT>;
+            OVS_CK(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_s));
+            ks<<<z.nchunk, PT_NT, sm_s, c.st>>>(B, z.chunks, z.nchunks, z.seg, z.sk, z.st, z.lut, z.P, z.L, z.hist,
+                                                z.tot);
+            c.check();
+        }
         if (mark_phases) c.mark(3);
     }
 

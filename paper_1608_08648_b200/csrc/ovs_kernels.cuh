@@ -438,12 +438,14 @@ __device__ __forceinline__ void for_items(const U* __restrict__ src, u32 beg, u3
 template <int DT, bool KV, bool LEVEL0, int NT>
 __global__ void __launch_bounds__(NT) k_hist(Bufs<typename Codec<DT>::U> B, const Chunk* chunks, const u32* nchunks,
                                              Seg* segs, const typename Codec<DT>::U* sk_pool, const u32* st_pool,
-                                             const u32* lut_pool, u32 PS, u32 LS, u32* hist) {
+                                             const u32* lut_pool, u32 PS, u32 LS, u32* hist, u32 split) {
+    // `split` CTAs share a chunk (each a contiguous part) and add into its (zeroed) row
     typedef typename Codec<DT>::U U;
     extern __shared__ __align__(16) char smem[];
     const u32 nc = *nchunks;
     u32 loaded = 0xffffffffu;
-    for (u32 c = blockIdx.x; c < nc; c += gridDim.x) {
+    for (u32 w = blockIdx.x; w < nc * split; w += gridDim.x) {
+        const u32 c = w / split, part = w % split;
         const Chunk ch = chunks[c];
         const Seg sg = segs[ch.seg];
         ClsView<U> cls = load_cls<U>(smem, sg, ch.seg, sk_pool, st_pool, lut_pool, PS, LS, loaded != ch.seg);
@@ -451,23 +453,31 @@ __global__ void __launch_bounds__(NT) k_hist(Bufs<typename Codec<DT>::U> B, cons
         u32* h = (u32*)(smem + cls_smem_bytes<U>(PS, LS));
         for (u32 i = threadIdx.x; i < sg.P; i += NT) h[i] = 0;
         __syncthreads();
+        const u32 len = ch.end - ch.beg;
+        const u32 pbeg = ch.beg + (u32)(((u64)len * part / split) & ~15ull);
+        const u32 pend = (part + 1 == split) ? ch.end : ch.beg + (u32)(((u64)len * (part + 1) / split) & ~15ull);
         const U* src = B.k[LEVEL0 ? 0 : sg.src];
         const u32* isrc = (KV && !LEVEL0) ? B.i[sg.src] : nullptr;
         U mn = umax_of<U>(), mx = 0;
         auto body = [&](U kr, u32 o) {
             const U k = LEVEL0 ? Codec<DT>::ord(kr) : kr;
-            const u32 tg = (KV && !LEVEL0) ? isrc[ch.beg + o] : ch.beg + o;
+            const u32 tg = (KV && !LEVEL0) ? isrc[pbeg + o] : pbeg + o;
             atomicAdd(&h[classify<U>(cls, k, tg)], 1u);
             if (LEVEL0) { mn = min(mn, k); mx = max(mx, k); }
         };
-        for_items<U, NT, 4, decltype(body)&, LEVEL0>(src, ch.beg, ch.end - ch.beg, body);
+        for_items<U, NT, 4, decltype(body)&, LEVEL0>(src, pbeg, pend - pbeg, body);
         __syncthreads();
         u32* row = hist + (size_t)c * PS;
-        for (u32 b = threadIdx.x; b < sg.P; b += NT) row[b] = h[b];
+        if (split == 1) {
+            for (u32 b = threadIdx.x; b < sg.P; b += NT) row[b] = h[b];
+        } else {
+            for (u32 b = threadIdx.x; b < sg.P; b += NT)
+                if (h[b]) atomicAdd(&row[b], h[b]);
+        }
         if (LEVEL0) {
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) { mn = min(mn, shfl_xor_any(mn, o)); mx = max(mx, shfl_xor_any(mx, o)); }
-            if ((threadIdx.x & 31) == 0 && ch.end > ch.beg) {
+            if ((threadIdx.x & 31) == 0 && pend > pbeg) {
                 atomicMin((unsigned long long*)&segs[0].lo, (unsigned long long)mn);
                 atomicMax((unsigned long long*)&segs[0].hi, (unsigned long long)mx);
             }
@@ -685,6 +695,171 @@ __global__ void __launch_bounds__(NT) k_scatter(Bufs<typename Codec<DT>::U> B, c
             }
             __syncthreads();
         }
+    }
+}
+
+// ------------------------------------------------------------------ a7: write-combining scatter
+// Keys-only level-0 scatter.  The sub-tile's keys stay in registers (the next sub-tile is
+// loaded while the current one is processed).  Every bucket owns one 32-byte sector of
+// shared memory holding the keys of its current, incomplete output sector; a sector is
+// written to global memory only when complete, as one 32-byte store, so DRAM never sees a
+// partially written sector (no read-modify-write) and L2 sees one request per 32 bytes.
+// Per sub-tile and bucket b with cursor c0 and n_b new keys (positions [c0, c0+n_b)):
+//   W1: keys of the current sector (until it completes) -> the bucket's shared sector;
+//       keys of complete middle sectors -> global directly (a whole sector per sub-tile);
+//   FL: the completed sector is flushed (partially only at the chunk's first sector for b);
+//   W2: keys past the last complete sector -> the (now empty) shared sector.
+// The chunk's last incomplete sectors are flushed at the end.  Ranks come from shared
+// atomics; positions inside a (chunk, bucket) range are therefore not in input order, which
+// the bucket sorter makes irrelevant (module notes).
+template <class U> __host__ __device__ constexpr size_t wc_smem_bytes(u32 PS, u32 LS) {
+    return cls_smem_bytes<U>(PS, LS) + 32 * (size_t)PS + 2 * a16(4 * ((size_t)PS + 1)) + a16((PS + 31) / 32 * 4);
+}
+
+template <int DT, int NT, int ITEMS>
+__global__ void __launch_bounds__(NT, 1) k_scatter_wc(Bufs<typename Codec<DT>::U> B, const Chunk* chunks,
+                                                       const u32* nchunks, const Seg* segs,
+                                                       const typename Codec<DT>::U* sk_pool, const u32* st_pool,
+                                                       const u32* lut_pool, u32 PS, u32 LS, const u32* hist,
+                                                       const u32* tot_pool) {
+    typedef typename Codec<DT>::U U;
+    constexpr u32 SV = 32 / sizeof(U);  // keys per 32-byte sector
+    constexpr u32 V = 16 / sizeof(U);   // keys per 16-byte vector
+    constexpr u32 TS = NT * ITEMS;
+    static_assert(ITEMS % V == 0, "whole vectors per thread");
+    extern __shared__ __align__(16) char smem[];
+    char* sp = smem + cls_smem_bytes<U>(PS, LS);
+    U* wc = (U*)sp; sp += 32 * (size_t)PS;
+    u32* cnt = (u32*)sp; sp += a16(4 * ((size_t)PS + 1));
+    u32* cur = (u32*)sp; sp += a16(4 * ((size_t)PS + 1));
+    u32* headdone = (u32*)sp;  // bit b: the chunk's first (shared) sector of bucket b was flushed
+    const u32 nc = *nchunks;
+    U* dst = B.k[1];
+    const U* src = B.k[0];
+    for (u32 c = blockIdx.x; c < nc; c += gridDim.x) {
+        const Chunk ch = chunks[c];
+        const Seg sg = segs[ch.seg];
+        ClsView<U> cls = load_cls<U>(smem, sg, ch.seg, sk_pool, st_pool, lut_pool, PS, LS, true);
+        const u32 P = sg.P;
+        const u32* hrow = hist + (size_t)c * PS;
+        const u32* bst = tot_pool + (size_t)ch.seg * (PS + 1);
+        for (u32 b = threadIdx.x; b < P; b += NT) { cur[b] = sg.beg + bst[b] + hrow[b]; cnt[b] = 0; }
+        for (u32 w = threadIdx.x; w < (P + 31) / 32; w += NT) headdone[w] = 0;
+        auto chunk_start = [&](u32 b) -> u32 { return sg.beg + bst[b] + hrow[b]; };
+        // flush the bucket's shared sector covering [s0, s0+SV), valid keys [from, to)
+        auto flush = [&](u32 b, u32 s0, u32 to) {
+            const U* w = wc + (size_t)b * SV;
+            u32 from = s0;
+            if (!(headdone[b >> 5] & (1u << (b & 31)))) {
+                atomicOr(&headdone[b >> 5], 1u << (b & 31));
+                from = max(s0, chunk_start(b));
+            }
+            if (from == s0 && to == s0 + SV) {
+                const uint4* w4 = (const uint4*)w;
+                uint4* g4 = (uint4*)(dst + s0);
+                g4[0] = w4[0];
+                g4[1] = w4[1];
+            } else {
+                for (u32 d = from; d < to; ++d) dst[d] = w[d - s0];
+            }
+        };
+        __syncthreads();
+        const bool vec_ok = ((((uintptr_t)(src + ch.beg)) & 15u) == 0);
+        U nk[ITEMS];
+        auto load = [&](u32 t0, U (&k)[ITEMS]) {
+            const u32 nt = min(TS, ch.end - t0);
+            if (vec_ok && nt == TS) {
+#pragma unroll
+                for (u32 jv = 0; jv < ITEMS / V; ++jv) {
+                    const uint4 r = __ldcs((const uint4*)(src + t0) + jv * NT + threadIdx.x);
+                    const U* e = (const U*)&r;
+#pragma unroll
+                    for (u32 q = 0; q < V; ++q) k[jv * V + q] = e[q];
+                }
+            } else {
+#pragma unroll
+                for (u32 j = 0; j < ITEMS; ++j) {
+                    const u32 o = ((j / V) * NT + threadIdx.x) * V + (j % V);
+                    k[j] = o < nt ? src[t0 + o] : (U)0;
+                }
+            }
+        };
+        if (ch.beg < ch.end) load(ch.beg, nk);
+        for (u32 t0 = ch.beg; t0 < ch.end; t0 += TS) {
+            const u32 nt = min(TS, ch.end - t0);
+            U k[ITEMS];
+#pragma unroll
+            for (u32 j = 0; j < ITEMS; ++j) k[j] = nk[j];
+            if (t0 + TS < ch.end) load(t0 + TS, nk);  // in flight while this sub-tile is processed
+            u32 bk[ITEMS], rk[ITEMS];
+#pragma unroll
+            for (u32 j = 0; j < ITEMS; ++j) {
+                const u32 o = ((j / V) * NT + threadIdx.x) * V + (j % V);
+                if (o < nt) {
+                    k[j] = Codec<DT>::ord(k[j]);
+                    bk[j] = classify<U>(cls, k[j], t0 + o);
+                    rk[j] = atomicAdd(&cnt[bk[j]], 1u);
+                }
+            }
+            __syncthreads();
+            // W1 (and remember the tail keys for W2)
+            u32 dd[ITEMS];
+#pragma unroll
+            for (u32 j = 0; j < ITEMS; ++j) {
+                const u32 o = ((j / V) * NT + threadIdx.x) * V + (j % V);
+                dd[j] = 0xffffffffu;
+                if (o < nt) {
+                    const u32 b = bk[j], c0 = cur[b], end = c0 + cnt[b];
+                    const u32 d = c0 + rk[j];
+                    const u32 s0 = c0 & ~(SV - 1), e1 = s0 + SV, T = end & ~(SV - 1);
+                    if (end < e1 || d < e1) {
+                        wc[(size_t)b * SV + (d - s0)] = k[j];         // current sector
+                    } else if (d < T) {
+                        dst[d] = k[j];                                 // a complete middle sector
+                    } else {
+                        dd[j] = d;                                     // tail: after the flush
+                    }
+                }
+            }
+            __syncthreads();
+            // FL: the leader (rank 0) of every bucket whose current sector completed flushes it
+#pragma unroll
+            for (u32 j = 0; j < ITEMS; ++j) {
+                const u32 o = ((j / V) * NT + threadIdx.x) * V + (j % V);
+                if (o < nt && rk[j] == 0) {
+                    const u32 b = bk[j], c0 = cur[b], end = c0 + cnt[b];
+                    const u32 s0 = c0 & ~(SV - 1);
+                    if (end >= s0 + SV) flush(b, s0, s0 + SV);
+                }
+            }
+            __syncthreads();
+            // W2: tail keys into the emptied sector; leaders advance the cursor
+#pragma unroll
+            for (u32 j = 0; j < ITEMS; ++j) {
+                const u32 o = ((j / V) * NT + threadIdx.x) * V + (j % V);
+                if (o < nt && dd[j] != 0xffffffffu) {
+                    const u32 b = bk[j], end = cur[b] + cnt[b];
+                    wc[(size_t)b * SV + (dd[j] - (end & ~(SV - 1)))] = k[j];
+                }
+            }
+            __syncthreads();
+#pragma unroll
+            for (u32 j = 0; j < ITEMS; ++j) {
+                const u32 o = ((j / V) * NT + threadIdx.x) * V + (j % V);
+                if (o < nt && rk[j] == 0) {
+                    const u32 b = bk[j];
+                    cur[b] += cnt[b];
+                    cnt[b] = 0;
+                }
+            }
+            __syncthreads();
+        }
+        // the chunk's last, incomplete sectors
+        for (u32 b = threadIdx.x; b < P; b += NT) {
+            const u32 c1 = cur[b], s0 = c1 & ~(SV - 1);
+            if (c1 > s0) flush(b, s0, c1);
+        }
+        __syncthreads();
     }
 }
 

@@ -152,7 +152,7 @@ template <int DT, bool KV> struct Engine {
 
     struct Level0 {
         u32 P = 1, L = 0, log2L = 0, nchunk = 0, chunk = 0;
-        U* sk = nullptr; u32* st = nullptr; u32* lut = nullptr;
+        U* sk = nullptr; u32* st = nullptr; u16* lut = nullptr;
         Seg* seg = nullptr; Chunk* chunks = nullptr; u32* nchunks = nullptr;
         u32* hist = nullptr; u32* tot = nullptr; u32* nseg = nullptr;
     };
@@ -170,10 +170,10 @@ template <int DT, bool KV> struct Engine {
     }
     u32 max_p_one_level() const {
         // largest P whose scatter working set fits shared memory with L = 2P
-        u32 lo = 1, hi = 65535;
+        u32 lo = 1, hi = 8192;  // 13-bit classifier table entries
         while (lo < hi) {
             u32 mid = (lo + hi + 1) / 2;
-            u32 L = std::min<u32>(8192, std::max<u32>(64, pow2_at_least(2 * mid)));
+            u32 L = std::min<u32>(16384, std::max<u32>(64, pow2_at_least(4 * mid)));
             if (scatter_smem(mid, L) + 1024 <= (size_t)c.di.smem_optin) lo = mid; else hi = mid - 1;
         }
         return lo;
@@ -181,7 +181,7 @@ template <int DT, bool KV> struct Engine {
 
     void carve_level0(Level0& z, u32 P) {
         z.P = P;
-        z.L = P > 1 ? std::min<u32>(8192, std::max<u32>(64, pow2_at_least(2 * P))) : 1;
+        z.L = P > 1 ? std::min<u32>(16384, std::max<u32>(64, pow2_at_least(4 * P))) : 1;
         // keys-only: shrink the table until the write-combining scatter fits shared memory
         if (!KV && P > 1)
             while (z.L > 64 && wc_smem_bytes<U>(P, z.L) + 512 > (size_t)c.di.smem_optin) z.L >>= 1;
@@ -193,7 +193,7 @@ template <int DT, bool KV> struct Engine {
         z.nchunk = std::max<u32>(1, cdiv(n, z.chunk));
         z.sk = c.take<U>(std::max<u32>(P, 1));
         z.st = c.take<u32>(std::max<u32>(P, 1));
-        z.lut = c.take<u32>(z.L);
+        z.lut = c.take<u16>(z.L + 1);
         z.seg = c.take<Seg>(1);
         z.chunks = c.take<Chunk>(z.nchunk);
         z.nchunks = c.take<u32>(2);

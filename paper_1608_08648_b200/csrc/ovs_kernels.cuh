@@ -19,6 +19,7 @@ namespace {
 
 typedef uint32_t u32;
 typedef uint64_t u64;
+typedef uint16_t u16;
 
 // ------------------------------------------------------------------ key codecs
 // Keys are compared as "ordered bits": an order-preserving map to unsigned integers
@@ -101,11 +102,12 @@ enum : u32 { BK_LOOSE = 0x80000000u, BK_RAW = 0x40000000u };
 // bucket(k, tag) = #{q : S[q] <lex (k, tag)}: a lower_bound over the p-1 splitters with the
 // (key, tag) tie-break.  The binary search is narrowed by a lookup
 // table over the ordered-key space: entry e covers keys [base + e<<shift, base + (e+1)<<shift)
-// and stores lo_e = #{q : S[q].key < base + e<<shift} and cnt_e = #splitter keys inside the
-// entry, so only those cnt_e splitters are binary-searched (usually 0 or 1).  The result is
+// and stores (16 bits) lo_e = #{q : S[q].key < base + e<<shift} (13 bits, p <= 8192) and
+// cnt_e = #splitter keys inside the entry (3 bits, 7 = "see entry e+1"), so only those cnt_e
+// splitters are binary-searched (usually none).  The result is
 // exactly the lower_bound (tests/test_gpu_parity.py compares bucket counts with the oracle).
 template <class U> struct ClsView {
-    const U* sk; const u32* st; const u32* lut;
+    const U* sk; const u32* st; const u16* lut;
     U base; u32 shift, L, P;
 };
 
@@ -115,8 +117,9 @@ __device__ __forceinline__ u32 classify(const ClsView<U>& c, U k, u32 tag) {
     if (k < c.base) return 0;
     U d = (U)(k - c.base) >> c.shift;
     if (d >= (U)c.L) return c.P - 1;
-    u32 e = c.lut[(u32)d];
-    u32 lo = e & 0xffffu, cnt = e >> 16;
+    const u32 e = c.lut[(u32)d];
+    u32 lo = e & 0x1fffu, cnt = e >> 13;
+    if (cnt == 7) cnt = (c.lut[(u32)d + 1] & 0x1fffu) - lo;  // saturated: the next entry's lo bounds it
     while (cnt > 0) {
         u32 half = cnt >> 1, mid = lo + half;
         U s = c.sk[mid];
@@ -306,7 +309,7 @@ __device__ u32 count_less_key(const U* sk, u32 nsp, U thr) {
 }
 
 template <class U>
-__device__ void build_lut(const U* sk, u32 P, u32 L, u32 log2L, u32* lut, U* base_out, u32* shift_out) {
+__device__ void build_lut(const U* sk, u32 P, u32 L, u32 log2L, u16* lut, U* base_out, u32* shift_out) {
     if (P <= 1) {
         if (threadIdx.x == 0) { *base_out = 0; *shift_out = 0; }
         return;
@@ -319,16 +322,16 @@ __device__ void build_lut(const U* sk, u32 P, u32 L, u32 log2L, u32* lut, U* bas
     for (u32 e = threadIdx.x; e < L; e += blockDim.x) {
         u32 a = ((U)e > lim) ? (P - 1) : count_less_key<U>(sk, P - 1, (U)(base + ((U)e << shift)));
         u32 b = ((U)(e + 1) > lim) ? (P - 1) : count_less_key<U>(sk, P - 1, (U)(base + ((U)(e + 1) << shift)));
-        lut[e] = a | ((b - a) << 16);
+        lut[e] = (u16)(a | (min(b - a, 7u) << 13));
     }
-    if (threadIdx.x == 0) { *base_out = base; *shift_out = shift; }
+    if (threadIdx.x == 0) { lut[L] = (u16)(P - 1); *base_out = base; *shift_out = shift; }
 }
 
 // Classifier of a single segment covering [0, n) of buffer 0 (the contract level, or an
 // internal sort of a whole array): LUT entries in parallel over CTAs, splitter keys staged in
 // shared memory; CTA 0 writes the segment header.
 template <class U>
-__global__ void __launch_bounds__(1024) k_build_cls0(const U* sk, u32 P, u32 L, u32 log2L, u32* lut, Seg* seg, u32 n,
+__global__ void __launch_bounds__(1024) k_build_cls0(const U* sk, u32 P, u32 L, u32 log2L, u16* lut, Seg* seg, u32 n,
                                                      u32 nchunk) {
     extern __shared__ __align__(16) char smem[];
     U* s = (U*)smem;
@@ -345,8 +348,9 @@ __global__ void __launch_bounds__(1024) k_build_cls0(const U* sk, u32 P, u32 L, 
         for (u32 e = blockIdx.x * blockDim.x + threadIdx.x; e < L; e += gridDim.x * blockDim.x) {
             u32 a = ((U)e > lim) ? (P - 1) : count_less_key<U>(s, P - 1, (U)(base + ((U)e << shift)));
             u32 b = ((U)(e + 1) > lim) ? (P - 1) : count_less_key<U>(s, P - 1, (U)(base + ((U)(e + 1) << shift)));
-            lut[e] = a | ((b - a) << 16);
+            lut[e] = (u16)(a | (min(b - a, 7u) << 13));
         }
+        if (blockIdx.x == 0 && threadIdx.x == 0) lut[L] = (u16)(P - 1);
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         Seg g;
@@ -374,23 +378,23 @@ __host__ __device__ constexpr size_t a16(size_t x) { return (x + 15) & ~(size_t)
 
 template <class U>
 __device__ __forceinline__ ClsView<U> load_cls(char* sp, const Seg& sg, u32 segi, const U* sk_pool, const u32* st_pool,
-                                               const u32* lut_pool, u32 PS, u32 LS, bool load) {
+                                               const u16* lut_pool, u32 PS, u32 LS, bool load) {
     U* sk = (U*)sp; sp += a16(sizeof(U) * (size_t)PS);
     u32* st = (u32*)sp; sp += a16(4 * (size_t)PS);
-    u32* lut = (u32*)sp;
+    u16* lut = (u16*)sp;
     if (load) {
         const U* gsk = sk_pool + (size_t)segi * PS;
         const u32* gst = st_pool + (size_t)segi * PS;
-        const u32* glut = lut_pool + (size_t)segi * LS;
+        const u16* glut = lut_pool + (size_t)segi * (LS + 1);
         for (u32 i = threadIdx.x; i + 1 < sg.P; i += blockDim.x) { sk[i] = gsk[i]; st[i] = gst[i]; }
-        for (u32 i = threadIdx.x; i < sg.L; i += blockDim.x) lut[i] = glut[i];
+        for (u32 i = threadIdx.x; i <= sg.L; i += blockDim.x) lut[i] = glut[i];
     }
     ClsView<U> c;
     c.sk = sk; c.st = st; c.lut = lut; c.base = (U)sg.base; c.shift = sg.shift; c.L = sg.L; c.P = sg.P;
     return c;
 }
 template <class U> __host__ __device__ constexpr size_t cls_smem_bytes(u32 PS, u32 LS) {
-    return a16(sizeof(U) * (size_t)PS) + a16(4 * (size_t)PS) + a16(4 * (size_t)LS);
+    return a16(sizeof(U) * (size_t)PS) + a16(4 * (size_t)PS) + a16(2 * ((size_t)LS + 1));
 }
 
 template <class U> __device__ __forceinline__ U shfl_xor_any(U x, int o) {
@@ -438,7 +442,7 @@ __device__ __forceinline__ void for_items(const U* __restrict__ src, u32 beg, u3
 template <int DT, bool KV, bool LEVEL0, int NT>
 __global__ void __launch_bounds__(NT) k_hist(Bufs<typename Codec<DT>::U> B, const Chunk* chunks, const u32* nchunks,
                                              Seg* segs, const typename Codec<DT>::U* sk_pool, const u32* st_pool,
-                                             const u32* lut_pool, u32 PS, u32 LS, u32* hist, u32 split) {
+                                             const u16* lut_pool, u32 PS, u32 LS, u32* hist, u32 split) {
     // `split` CTAs share a chunk (each a contiguous part) and add into its (zeroed) row
     typedef typename Codec<DT>::U U;
     extern __shared__ __align__(16) char smem[];
@@ -586,7 +590,7 @@ __host__ __device__ constexpr size_t scatter_smem_bytes(u32 PS, u32 LS) {
 template <int DT, bool KV, bool LEVEL0, int NT, int ITEMS>
 __global__ void __launch_bounds__(NT) k_scatter(Bufs<typename Codec<DT>::U> B, const Chunk* chunks, const u32* nchunks,
                                                 const Seg* segs, const typename Codec<DT>::U* sk_pool,
-                                                const u32* st_pool, const u32* lut_pool, u32 PS, u32 LS,
+                                                const u32* st_pool, const u16* lut_pool, u32 PS, u32 LS,
                                                 const u32* hist, const u32* tot_pool) {
     typedef typename Codec<DT>::U U;
     constexpr int TS = NT * ITEMS;
@@ -720,7 +724,7 @@ template <int DT, int NT, int ITEMS>
 __global__ void __launch_bounds__(NT, 1) k_scatter_wc(Bufs<typename Codec<DT>::U> B, const Chunk* chunks,
                                                        const u32* nchunks, const Seg* segs,
                                                        const typename Codec<DT>::U* sk_pool, const u32* st_pool,
-                                                       const u32* lut_pool, u32 PS, u32 LS, const u32* hist,
+                                                       const u16* lut_pool, u32 PS, u32 LS, const u32* hist,
                                                        const u32* tot_pool) {
     typedef typename Codec<DT>::U U;
     constexpr u32 SV = 32 / sizeof(U);  // keys per 32-byte sector
@@ -787,6 +791,7 @@ __global__ void __launch_bounds__(NT, 1) k_scatter_wc(Bufs<typename Codec<DT>::U
         if (ch.beg < ch.end) load(ch.beg, nk);
         for (u32 t0 = ch.beg; t0 < ch.end; t0 += TS) {
             const u32 nt = min(TS, ch.end - t0);
+            const bool full = nt == TS;
             U k[ITEMS];
 #pragma unroll
             for (u32 j = 0; j < ITEMS; ++j) k[j] = nk[j];
@@ -795,65 +800,50 @@ __global__ void __launch_bounds__(NT, 1) k_scatter_wc(Bufs<typename Codec<DT>::U
 #pragma unroll
             for (u32 j = 0; j < ITEMS; ++j) {
                 const u32 o = ((j / V) * NT + threadIdx.x) * V + (j % V);
-                if (o < nt) {
+                if (full || o < nt) {
                     k[j] = Codec<DT>::ord(k[j]);
                     bk[j] = classify<U>(cls, k[j], t0 + o);
                     rk[j] = atomicAdd(&cnt[bk[j]], 1u);
                 }
             }
             __syncthreads();
-            // W1 (and remember the tail keys for W2)
+            // W1: current-sector keys -> the shared sector, middle-sector keys -> global; tail keys
+            // remember their slot in the sector that follows the last complete one
             u32 dd[ITEMS];
 #pragma unroll
             for (u32 j = 0; j < ITEMS; ++j) {
                 const u32 o = ((j / V) * NT + threadIdx.x) * V + (j % V);
                 dd[j] = 0xffffffffu;
-                if (o < nt) {
+                if (full || o < nt) {
                     const u32 b = bk[j], c0 = cur[b], end = c0 + cnt[b];
                     const u32 d = c0 + rk[j];
                     const u32 s0 = c0 & ~(SV - 1), e1 = s0 + SV, T = end & ~(SV - 1);
-                    if (end < e1 || d < e1) {
-                        wc[(size_t)b * SV + (d - s0)] = k[j];         // current sector
-                    } else if (d < T) {
-                        dst[d] = k[j];                                 // a complete middle sector
-                    } else {
-                        dd[j] = d;                                     // tail: after the flush
-                    }
+                    if (end < e1 || d < e1) wc[(size_t)b * SV + (d - s0)] = k[j];  // current sector
+                    else if (d < T) dst[d] = k[j];                                  // complete middle sector
+                    else dd[j] = d - T;                                             // tail (after the flush)
                 }
             }
             __syncthreads();
-            // FL: the leader (rank 0) of every bucket whose current sector completed flushes it
+            // FL: the leader (rank 0) of every bucket flushes its completed sector and advances the
+            // cursor (nobody reads cur/cnt again in this sub-tile)
 #pragma unroll
             for (u32 j = 0; j < ITEMS; ++j) {
                 const u32 o = ((j / V) * NT + threadIdx.x) * V + (j % V);
-                if (o < nt && rk[j] == 0) {
+                if ((full || o < nt) && rk[j] == 0) {
                     const u32 b = bk[j], c0 = cur[b], end = c0 + cnt[b];
                     const u32 s0 = c0 & ~(SV - 1);
                     if (end >= s0 + SV) flush(b, s0, s0 + SV);
-                }
-            }
-            __syncthreads();
-            // W2: tail keys into the emptied sector; leaders advance the cursor
-#pragma unroll
-            for (u32 j = 0; j < ITEMS; ++j) {
-                const u32 o = ((j / V) * NT + threadIdx.x) * V + (j % V);
-                if (o < nt && dd[j] != 0xffffffffu) {
-                    const u32 b = bk[j], end = cur[b] + cnt[b];
-                    wc[(size_t)b * SV + (dd[j] - (end & ~(SV - 1)))] = k[j];
-                }
-            }
-            __syncthreads();
-#pragma unroll
-            for (u32 j = 0; j < ITEMS; ++j) {
-                const u32 o = ((j / V) * NT + threadIdx.x) * V + (j % V);
-                if (o < nt && rk[j] == 0) {
-                    const u32 b = bk[j];
-                    cur[b] += cnt[b];
+                    cur[b] = end;
                     cnt[b] = 0;
                 }
             }
             __syncthreads();
+            // W2: tail keys into the emptied sector
+#pragma unroll
+            for (u32 j = 0; j < ITEMS; ++j)
+                if (dd[j] != 0xffffffffu) wc[(size_t)bk[j] * SV + dd[j]] = k[j];
         }
+        __syncthreads();
         // the chunk's last, incomplete sectors
         for (u32 b = threadIdx.x; b < P; b += NT) {
             const u32 c1 = cur[b], s0 = c1 & ~(SV - 1);

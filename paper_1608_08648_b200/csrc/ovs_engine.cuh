@@ -213,8 +213,9 @@ template <int DT, bool KV> struct Engine {
     // internal splitters for level 0 (P-1 of them) from a one-CTA sorted random sample
     void internal_splitters(Level0& z, u64 seed) {
         if (c.dry || z.P <= 1) return;
-        const u32 N = 8192;
-        const u32 si = std::max<u32>(1, N / z.P);
+        // 32 samples per internal splitter, sorted by one CTA (a power-of-two bitonic network)
+        const u32 si = std::max<u32>(1, std::min<u32>(32, 8192 / z.P));
+        const u32 N = pow2_at_least(z.P * si);
         const size_t sm = (sizeof(U) + 4) * (size_t)N;
         OVS_CK(cudaFuncSetAttribute(k_internal_sample<DT, KV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         k_internal_sample<DT, KV><<<1, 1024, sm, c.st>>>(B, n, z.P, si, N, seed, z.sk, z.st);
@@ -301,7 +302,8 @@ template <bool KV> struct InternalSort {
         e.B.i[0] = KV ? c.take<u32>(n) : nullptr;
         e.B.i[1] = KV ? c.take<u32>(n) : nullptr;
         direct = n <= e.cap;
-        u32 P = direct ? 1 : std::min<u32>(1024, cdiv(n, (u32)(e.cap * 45ull / 100)));
+        // internal buckets of ~cap/8 keys: enough of them to occupy every SM
+        u32 P = direct ? 1 : std::min<u32>(1024, cdiv(n, e.cap / 8));
         if (!direct) e.carve_level0(z, P);
         e.carve_lists(l, direct ? 1 : P);
     }

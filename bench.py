@@ -133,6 +133,78 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def run_dist(args, x, src, work, dev, rank, world, local):
+    """N > 1: weak scaling, 2^27 keys per GPU; the distributed ROS sort (sample all-reduce,
+    count all-gather, all-to-all-v over NVLink, local sort); device time, max over ranks."""
+    import torch
+    import torch.distributed as dist
+    from paper_1608_08648_b200.dist import CudaBackend, dist_sort
+    n = args.n
+    p = min(8192, max(args.p, 4096 * world)) // world * world
+    s, seed = args.s, WORKLOAD["seed"]
+    be = CudaBackend(n, n * world, torch.uint32, False, p, s, seed, world, 2 * n, dev)
+    res = dist_sort(src, None, p, s, seed, backend=be)
+    host = res.keys.cpu().numpy()
+    assert bool(np.all(host[1:] >= host[:-1]))
+    for _ in range(args.warmup):
+        dist_sort(src, None, p, s, seed, backend=be)
+    torch.cuda.synchronize(dev)
+    sampler = ClockSampler(local)
+    sampler.start()
+    ms = []
+    sent = 0
+    for _ in range(args.steps):
+        dist.barrier()
+        torch.cuda.synchronize(dev)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        r = dist_sort(src, None, p, s, seed, backend=be)
+        b.record()
+        b.synchronize()
+        ms.append(a.elapsed_time(b))
+        sent += r.exchange_bytes
+    clocks = sampler.stop()
+    t = torch.tensor([sum(ms)], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_per_step = float(t.item()) / args.steps
+    nv = torch.tensor([sent / args.steps], device=dev, dtype=torch.float64)
+    dist.all_reduce(nv, op=dist.ReduceOp.SUM)
+    value = n * world / (ms_per_step * 1e-3) / 1e9
+    # end to end: pinned host shard -> device -> distributed sort -> host slice
+    hx = torch.from_numpy(x).pin_memory()
+    e2e = []
+    for k in range(args.e2e_steps + 1):
+        dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        work.copy_(hx, non_blocking=True)
+        r = dist_sort(work, None, p, s, seed, backend=be)
+        out_h = r.keys.to("cpu")
+        b.record()
+        b.synchronize()
+        if k > 0:
+            e2e.append(a.elapsed_time(b))
+    te = torch.tensor([statistics.mean(e2e)], device=dev, dtype=torch.float64)
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        line = {"metric": "sort throughput (BASELINE.json: Gkeys/s for 2^27 uint32 keys per B200)",
+                "value": value, "unit": "Gkeys/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "u32", "data": "synthetic (ovs_inputs, seeded)",
+                "config": {"workload": f"C5: 2^27 uint32 keys per GPU x {world}, uniform on [0,2^32) (data seed 51), "
+                                       f"ROS p={p} s={s}", "global_batch": n * world, "seq_len": None,
+                           "parallelism": f"dp{world}: sample all-reduce, count all-gather, all-to-all-v (NCCL)",
+                           "n_per_gpu": n, "p": p, "s": s,
+                           "l2": "input 512 MiB per GPU > 126 MB L2"},
+                "nvlink_bytes_per_step": float(nv.item()),
+                "roofline": None, "cpu_baseline": None,
+                "e2e": {"value": n * world / (float(te.item()) * 1e-3) / 1e9, "unit": "Gkeys/s",
+                        "h2d_bytes_per_step": int(n * 4 * world), "d2h_bytes_per_step": int(n * 4 * world)},
+                "gpu_launches": None, "clocks": clocks}
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -167,8 +239,11 @@ def main():
     x = ovs_inputs.keys(WORKLOAD["dist"], n, seed=WORKLOAD["data_seed"], start=rank * n)
     src = torch.from_numpy(x).to(dev)
     work = torch.empty_like(src)
-    sorter = ovs.Sorter(n, torch.uint32, False, "ros", p, s, seed, device=dev)
     stream = torch.cuda.current_stream(dev)
+    if world > 1:
+        run_dist(args, x, src, work, dev, rank, world, local)
+        return
+    sorter = ovs.Sorter(n, torch.uint32, False, "ros", p, s, seed, device=dev)
 
     # one reported call: launch count, device status, and a correctness spot check
     work.copy_(src)

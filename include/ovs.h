@@ -93,6 +93,44 @@ int ovs_sort_keys(void* d_keys, size_t n, int dtype, const ovs_params* prm, void
 int ovs_sort_pairs_stable(void* d_keys, uint32_t* d_vals, size_t n, int dtype, const ovs_params* prm, void* d_ws,
                           size_t ws_bytes, void* stream, ovs_report* rep);
 
+/* ---------------------------------------------------------------------------------------
+ * Multi-GPU building blocks (ROS).  One process per GPU; rank r holds the contiguous shard
+ * [offset, offset + n_local) of a global array of n_global keys (ranks in index order).  The
+ * caller runs the NCCL collectives between the three calls (paper_1608_08648_b200/dist.py
+ * does it with torch.distributed), the way the paper's multi-core method splits the work
+ * (PAPER.md:656-681): each GPU samples its shard, the sample is assembled everywhere, every
+ * GPU classifies its keys against the same splitters, buckets are exchanged (bucket j goes to
+ * rank floor(j*world/p); p must be a multiple of world), and each GPU sorts
+ * the buckets it received.  Tags are global indices, so rank r's output is exactly the
+ * [sum_{j<j0} n_j, sum_{j<j1} n_j) slice of the single-GPU sort of the concatenated input.
+ *   1. ovs_dist_sample: d_sample (ovs_dist_sample_words u64 words, device) receives this
+ *      shard's records of the global sample, zero elsewhere -> caller: all-reduce SUM.
+ *   2. ovs_dist_partition: splitters from the assembled sample, local bucket counts d_counts
+ *      (p u32, device) and the local keys (order-preserving bits; + values and global indices
+ *      for key-value sorts) in bucket order in d_send_* (n_local items each) -> caller:
+ *      all-gather of the counts (world x p, rank-major) and an all-to-all-v of the send buffers
+ *      (to rank d: its buckets, in bucket order; from rank s: concatenated in rank order).
+ *   3. ovs_dist_finish: the received items (<= recv_capacity) are gathered bucket by bucket
+ *      (source-rank order) and sorted into d_out_keys (+ d_out_vals), raw dtype.
+ * The three calls must use the same workspace and the same (n_local, n_global, dtype,
+ * with_values, params, world, recv_capacity).  Errors: OVS_EINVAL also for DRO, p % world,
+ * rank out of range; device-side overflow of recv_capacity sets a status bit (the caller
+ * can size recv_capacity from the all-gathered counts before calling finish). */
+size_t ovs_dist_workspace_bytes(size_t n_local, uint64_t n_global, int dtype, int with_values, const ovs_params* prm,
+                                int world, size_t recv_capacity);
+size_t ovs_dist_sample_words(uint64_t n_global, int dtype, const ovs_params* prm);
+int ovs_dist_sample(const void* d_keys, size_t n_local, uint64_t offset, uint64_t n_global, int dtype, int with_values,
+                    const ovs_params* prm, int world, size_t recv_capacity, uint64_t* d_sample, void* d_ws,
+                    size_t ws_bytes, void* stream);
+int ovs_dist_partition(const void* d_keys, const uint32_t* d_vals, size_t n_local, uint64_t offset, uint64_t n_global,
+                       int dtype, const ovs_params* prm, int world, size_t recv_capacity, const uint64_t* d_sample,
+                       void* d_send_keys, uint32_t* d_send_vals, uint32_t* d_send_idx, uint32_t* d_counts, void* d_ws,
+                       size_t ws_bytes, void* stream);
+int ovs_dist_finish(const void* d_recv_keys, const uint32_t* d_recv_vals, const uint32_t* d_recv_idx, size_t n_local,
+                    uint64_t n_global, int dtype, const ovs_params* prm, int world, int rank, size_t recv_capacity,
+                    const uint32_t* d_all_counts, void* d_out_keys, uint32_t* d_out_vals, void* d_ws, size_t ws_bytes,
+                    void* stream);
+
 /* Profiling hook (thread-local): subsequent sort calls on this thread record events[k]
  * (cudaEvent_t passed as void*) on their stream at phase boundary k, without synchronising:
  *   0 start, 1 after the sample + splitters (a1-a4), 2 after classify + histogram + scans

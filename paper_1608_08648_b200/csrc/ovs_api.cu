@@ -145,6 +145,111 @@ int ovs_sort_pairs_stable(void* d_keys, uint32_t* d_vals, size_t n, int dtype, c
     return sort_impl(d_keys, d_vals, true, n, dtype, prm, d_ws, ws_bytes, stream, rep);
 }
 
+// ------------------------------------------------------------------ multi-GPU building blocks
+static int dist_validate(uint64_t n_local, uint64_t n_global, int dtype, const ovs_params* prm, int world) {
+    if (!prm || world < 1) return OVS_EINVAL;
+    if (dtype != OVS_U32 && dtype != OVS_I32 && dtype != OVS_F64) return OVS_EDTYPE;
+    if (prm->method != OVS_ROS) return OVS_EINVAL;               // DRO: single GPU in this revision
+    if (prm->p < 2 || prm->p % (uint32_t)world != 0) return OVS_EINVAL;  // "p ... a multiple of m"
+    if (n_global >= 0xffffffffull || n_local > n_global) return OVS_EINVAL;
+    if (prm->s == 0 || (uint64_t)prm->p * prm->s - 1 > n_global) return OVS_ESAMPLE;
+    if (ros_draws(n_global, (uint64_t)prm->p * prm->s - 1) == 0) return OVS_ESAMPLE;
+    return OVS_OK;
+}
+
+static size_t dist_dispatch(Ctx& c, int step, int dtype, bool kv, const ovs_params* prm, const DistArgs& a) {
+    if (dtype == OVS_U32) return dist_u32(c, step, prm, a, kv);
+    if (dtype == OVS_I32) return dist_i32(c, step, prm, a, kv);
+    return dist_f64(c, step, prm, a, kv);
+}
+
+static int dist_call(int step, int dtype, bool kv, const ovs_params* prm, DistArgs a, void* d_ws, size_t ws_bytes,
+                     void* stream) {
+    g_err.clear();
+    int v = dist_validate(a.n_local, a.n_global, dtype, prm, (int)a.world);
+    if (v != OVS_OK) { g_err = "invalid arguments"; return v; }
+    try {
+        Ctx d;
+        d.di = dev_info();
+        d.dry = true;
+        d.take<u32>(4);
+        d.take<u32>(SCAN_NT * 4);
+        const size_t need = dist_dispatch(d, step, dtype, kv, prm, a);
+        if (ws_bytes < need || !d_ws) { g_err = "workspace too small"; return OVS_EWORKSPACE; }
+        Ctx c;
+        c.di = d.di;
+        c.dry = false;
+        c.ws = (char*)d_ws;
+        c.st = (cudaStream_t)stream;
+        c.status = c.take<u32>(4);
+        c.bsum = c.take<u32>(SCAN_NT * 4);
+        dist_dispatch(c, step, dtype, kv, prm, a);
+        return OVS_OK;
+    } catch (const CudaFail& e) {
+        g_err = e.what();
+        return OVS_ECUDA;
+    } catch (const StatusFail& e) {
+        g_err = e.msg;
+        return e.code;
+    }
+}
+
+size_t ovs_dist_workspace_bytes(size_t n_local, uint64_t n_global, int dtype, int with_values, const ovs_params* prm,
+                                int world, size_t recv_capacity) {
+    if (dist_validate(n_local, n_global, dtype, prm, world) != OVS_OK || recv_capacity >= 0xffffffffull) return 0;
+    try {
+        Ctx d;
+        d.di = dev_info();
+        d.dry = true;
+        d.take<u32>(4);
+        d.take<u32>(SCAN_NT * 4);
+        DistArgs a{};
+        a.n_local = n_local; a.n_global = n_global; a.world = (u32)world; a.recv_cap = (u32)recv_capacity;
+        return dist_dispatch(d, 0, dtype, with_values != 0, prm, a);
+    } catch (...) {
+        return 0;
+    }
+}
+
+size_t ovs_dist_sample_words(uint64_t n_global, int dtype, const ovs_params* prm) {
+    if (!prm || prm->p < 2 || prm->s == 0) return 0;
+    return ((size_t)prm->p * prm->s - 1) * (dtype == OVS_F64 ? 2 : 1);
+}
+
+int ovs_dist_sample(const void* d_keys, size_t n_local, uint64_t offset, uint64_t n_global, int dtype, int with_values,
+                    const ovs_params* prm, int world, size_t recv_capacity, uint64_t* d_sample, void* d_ws,
+                    size_t ws_bytes, void* stream) {
+    DistArgs a{};
+    a.keys = d_keys; a.n_local = n_local; a.offset = offset; a.n_global = n_global; a.world = (u32)world;
+    a.recv_cap = (u32)recv_capacity; a.rec = d_sample;
+    if (offset + n_local > n_global) return OVS_EINVAL;
+    return dist_call(0, dtype, with_values != 0, prm, a, d_ws, ws_bytes, stream);
+}
+
+int ovs_dist_partition(const void* d_keys, const uint32_t* d_vals, size_t n_local, uint64_t offset, uint64_t n_global,
+                       int dtype, const ovs_params* prm, int world, size_t recv_capacity, const uint64_t* d_sample,
+                       void* d_send_keys, uint32_t* d_send_vals, uint32_t* d_send_idx, uint32_t* d_counts, void* d_ws,
+                       size_t ws_bytes, void* stream) {
+    DistArgs a{};
+    a.keys = d_keys; a.vals = d_vals; a.n_local = n_local; a.offset = offset; a.n_global = n_global;
+    a.world = (u32)world; a.recv_cap = (u32)recv_capacity; a.rec = (u64*)d_sample;
+    a.send_k = d_send_keys; a.send_v = d_send_vals; a.send_i = d_send_idx; a.counts = d_counts;
+    if (offset + n_local > n_global) return OVS_EINVAL;
+    return dist_call(1, dtype, d_vals != nullptr, prm, a, d_ws, ws_bytes, stream);
+}
+
+int ovs_dist_finish(const void* d_recv_keys, const uint32_t* d_recv_vals, const uint32_t* d_recv_idx, size_t n_local,
+                    uint64_t n_global, int dtype, const ovs_params* prm, int world, int rank, size_t recv_capacity,
+                    const uint32_t* d_all_counts, void* d_out_keys, uint32_t* d_out_vals, void* d_ws, size_t ws_bytes,
+                    void* stream) {
+    DistArgs a{};
+    a.n_local = n_local; a.n_global = n_global; a.world = (u32)world; a.rank = (u32)rank;
+    a.recv_cap = (u32)recv_capacity; a.recv_k = d_recv_keys; a.recv_v = d_recv_vals; a.recv_i = d_recv_idx;
+    a.C = d_all_counts; a.out_k = d_out_keys; a.out_v = d_out_vals;
+    if (rank < 0 || rank >= world) return OVS_EINVAL;
+    return dist_call(2, dtype, d_recv_vals != nullptr, prm, a, d_ws, ws_bytes, stream);
+}
+
 const char* ovs_last_error(void) { return g_err.c_str(); }
 
 void ovs_set_phase_events(void* const* events, int count) {

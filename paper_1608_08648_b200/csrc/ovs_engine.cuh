@@ -148,6 +148,7 @@ template <int DT, bool KV> struct Engine {
     u32 n;
     u32 cap;
     bool mark_phases = false;  // the contract-level engine records the phase events
+    u32 tag_base = 0;          // level-0 tag of item i = tag_base + i (multi-GPU: global index)
     explicit Engine(Ctx& ctx) : c(ctx) {}
 
     struct Level0 {
@@ -239,7 +240,7 @@ template <int DT, bool KV> struct Engine {
         OVS_CK(cudaMemsetAsync(z.hist, 0, sizeof(u32) * (size_t)z.nchunk * z.P, c.st));
         OVS_CK(cudaFuncSetAttribute(k_hist<DT, KV, true, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_h));
         k_hist<DT, KV, true, 1024><<<z.nchunk * hsplit, 1024, sm_h, c.st>>>(B, z.chunks, z.nchunks, z.seg, z.sk, z.st,
-                                                                           z.lut, z.P, z.L, z.hist, hsplit);
+                                                                           z.lut, z.P, z.L, z.hist, hsplit, tag_base);
         c.check();
         k_colscan<<<std::min<u32>(cdiv(z.P, 32), 4 * c.di.sms), 1024, 0, c.st>>>(z.hist, z.seg, z.nseg, z.P, z.tot);
         c.check();
@@ -252,7 +253,8 @@ template <int DT, bool KV> struct Engine {
             const size_t sm_w = wc_smem_bytes<U>(z.P, z.L);
             auto kw = k_scatter_wc<DT, PT_NT, IT>;
             OVS_CK(cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_w));
-            kw<<<z.nchunk, PT_NT, sm_w, c.st>>>(B, z.chunks, z.nchunks, z.seg, z.sk, z.st, z.lut, z.P, z.L, z.hist, z.tot);
+            kw<<<z.nchunk, PT_NT, sm_w, c.st>>>(B, z.chunks, z.nchunks, z.seg, z.sk, z.st, z.lut, z.P, z.L, z.hist, z.tot,
+                                                tag_base);
             c.check();
         } else {
             constexpr int IT = PartItems<U, KV>::v;
@@ -260,7 +262,7 @@ template <int DT, bool KV> struct Engine {
             auto ks = k_scatter<DT, KV, true, PT_NT, IT>;
             OVS_CK(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_s));
             ks<<<z.nchunk, PT_NT, sm_s, c.st>>>(B, z.chunks, z.nchunks, z.seg, z.sk, z.st, z.lut, z.P, z.L, z.hist,
-                                                z.tot);
+                                                z.tot, tag_base);
             c.check();
         }
         if (mark_phases) c.mark(3);
@@ -534,6 +536,114 @@ template <int DT, bool KV> struct DroSort {
     }
 };
 
+// ------------------------------------------------------------------ multi-GPU building blocks
+// One process per GPU; the caller moves bytes between the steps with NCCL collectives
+// (paper_1608_08648_b200/dist.py does it with torch.distributed).  The layout of the
+// workspace depends only on (n_local, n_global, dtype, kv, params, world, recv_capacity), so
+// the three calls share it (splitters written by partition are read by finish).
+template <int DT, bool KV> struct DistSort {
+    typedef typename Codec<DT>::U U;
+    Ctx& c;
+    Engine<DT, KV> e;   // local partition: buffer 0 = local shard, buffer 1 = send buffers
+    Engine<DT, KV> f;   // finish: buffer 0 = output, buffer 1 = scratch
+    typename Engine<DT, KV>::Level0 z;
+    typename Engine<DT, KV>::Lists l, lf;
+    u32 nl, p, s, world, m, M, words, recv_cap;
+    u64 ng, offset = 0, seed;
+    u64* counts64 = nullptr;
+    u64* cand = nullptr; u32* flag = nullptr; u32* rank = nullptr; u32* keep = nullptr; u32* pos = nullptr;
+    u64* t_pack = nullptr; u64* t_key = nullptr; u32* t_tag = nullptr;
+    InternalSort<false>* cand_sort = nullptr;
+    InternalSort<false>* t_sort32 = nullptr;
+    InternalSort<true>* t_sort64 = nullptr;
+    u32* bstart = nullptr; u32* srcoff = nullptr;
+
+    DistSort(Ctx& ctx, u32 n_local, u64 n_global, u32 p_, u32 s_, u64 seed_, u32 world_, u32 recv_capacity)
+        : c(ctx), e(ctx), f(ctx), nl(n_local), p(p_), s(s_), world(world_), recv_cap(recv_capacity), ng(n_global),
+          seed(seed_) {
+        e.n = nl;
+        e.cap = bucket_cap<U, KV>(c.di);
+        f.n = recv_cap;
+        f.cap = e.cap;
+        m = p * s - 1;
+        M = ros_draws(ng, m);
+        words = sizeof(U) == 4 ? 1 : 2;
+        counts64 = c.take<u64>(p);
+        cand = c.take<u64>(M);
+        flag = c.take<u32>(M);
+        rank = c.take<u32>(M);
+        keep = c.take<u32>(M);
+        pos = c.take<u32>(M);
+        cand_sort = new InternalSort<false>(c, M, cand, nullptr);
+        if (words == 1) {
+            t_pack = c.take<u64>(m);
+            t_sort32 = new InternalSort<false>(c, m, t_pack, nullptr);
+        } else {
+            t_key = c.take<u64>(m);
+            t_tag = c.take<u32>(m);
+            t_sort64 = new InternalSort<true>(c, m, t_key, t_tag);
+        }
+        e.carve_level0(z, p);
+        e.carve_lists(l, p);
+        // finish side
+        f.B.k[1] = c.take<U>(recv_cap);
+        f.B.v[1] = KV ? c.take<u32>(recv_cap) : nullptr;
+        f.B.i[0] = KV ? c.take<u32>(recv_cap) : nullptr;
+        f.B.i[1] = KV ? c.take<u32>(recv_cap) : nullptr;
+        bstart = c.take<u32>(p + 2);
+        srcoff = c.take<u32>(world + 1);
+        f.carve_lists(lf, p);
+    }
+    ~DistSort() { delete cand_sort; delete t_sort32; delete t_sort64; }
+
+    void sample(const U* keys, u64* rec) {
+        if (c.dry) return;
+        OVS_CK(cudaMemsetAsync(rec, 0, sizeof(u64) * (size_t)m * words, c.st));
+        k_ros_candidates<<<cdiv(M, 256), 256, 0, c.st>>>(cand, M, ng, seed);
+        c.check();
+        cand_sort->run(seed ^ 0xc0ffee);
+        k_ros_first_flags<<<cdiv(M, 256), 256, 0, c.st>>>(cand, M, flag);
+        c.check();
+        scan_u32(c, flag, rank, M);
+        k_ros_keep<<<cdiv(M, 256), 256, 0, c.st>>>(cand, M, flag, rank, m, keep, c.status);
+        c.check();
+        scan_u32(c, keep, pos, M);
+        k_dist_sample_gather<DT><<<cdiv(M, 256), 256, 0, c.st>>>(cand, M, keep, pos, keys, offset, nl, rec);
+        c.check();
+    }
+
+    void partition(U* keys, u32* vals, const u64* rec, U* send_k, u32* send_v, u32* send_i, u32* counts) {
+        if (c.dry) return;
+        k_dist_unpack<<<cdiv(m, 256), 256, 0, c.st>>>(rec, m, words, t_pack, t_key, t_tag);
+        c.check();
+        if (t_sort32) t_sort32->run(seed ^ 0x5eed);
+        else t_sort64->run(seed ^ 0x5eed);
+        k_pick_splitters<U><<<cdiv(p, 256), 256, 0, c.st>>>(t_pack, t_key, t_tag, p, s, z.sk, z.st);
+        c.check();
+        e.B.k[0] = keys; e.B.v[0] = vals;
+        e.B.k[1] = send_k; e.B.v[1] = send_v; e.B.i[1] = send_i;
+        e.B.i[0] = nullptr;
+        e.tag_base = (u32)offset;
+        e.level0(z, l, counts64);
+        k_u64_to_u32<<<cdiv(p, 256), 256, 0, c.st>>>(counts64, counts, p);
+        c.check();
+    }
+
+    void finish(const U* rk, const u32* rv, const u32* ri, const u32* C, u32 rnk, U* out_k, u32* out_v) {
+        if (c.dry) return;
+        k_dist_plan<U><<<1, 1024, 0, c.st>>>(C, world, p, rnk, z.sk, bstart, srcoff, lf.fit, lf.nfit, recv_cap, c.status);
+        c.check();
+        const u32 nb = (u32)((u64)(rnk + 1) * p / world) - (u32)((u64)rnk * p / world);
+        f.B.k[0] = out_k;
+        f.B.v[0] = out_v;
+        k_dist_gather<U, KV><<<cdiv((u64)world * nb * 32, 256), 256, 0, c.st>>>(
+            rk, rv, ri, out_k, out_v, f.B.i[0], C, world, p, rnk, bstart, srcoff);
+        c.check();
+        fill_u32(c, lf.ticket, 0, 1);
+        f.bucket_sort(lf, seed ^ 0xf1);
+    }
+};
+
 template <int DT, bool KV>
 Out plan_or_run(Ctx& c, void* keys, u32* vals, size_t n, const ovs_params* prm) {
     typedef typename Codec<DT>::U U;
@@ -559,6 +669,29 @@ Out plan_or_run(Ctx& c, void* keys, u32* vals, size_t n, const ovs_params* prm) 
     return o;
 }
 
+
+// multi-GPU entry (step 0 sample, 1 partition, 2 finish)
+struct DistArgs {
+    const void* keys; const u32* vals; u64 n_local, n_global, offset; u32 world, rank, recv_cap;
+    u64* rec; void* send_k; u32* send_v; u32* send_i; u32* counts;
+    const void* recv_k; const u32* recv_v; const u32* recv_i; const u32* C; void* out_k; u32* out_v;
+};
+template <int DT, bool KV>
+size_t dist_run(Ctx& c, int step, const ovs_params* prm, const DistArgs& a) {
+    typedef typename Codec<DT>::U U;
+    DistSort<DT, KV> d(c, (u32)a.n_local, a.n_global, prm->p, prm->s, prm->seed, a.world, a.recv_cap);
+    d.offset = a.offset;
+    if (prm->p > d.e.max_p_one_level()) throw StatusFail{OVS_EINVAL, "p too large for the one-level classifier"};
+    if (!c.dry) {
+        if (step == 0) d.sample((const U*)a.keys, a.rec);
+        else if (step == 1) d.partition((U*)a.keys, (u32*)a.vals, a.rec, (U*)a.send_k, a.send_v, a.send_i, a.counts);
+        else d.finish((const U*)a.recv_k, a.recv_v, a.recv_i, a.C, a.rank, (U*)a.out_k, a.out_v);
+    }
+    return c.off + 256;
+}
+size_t dist_u32(Ctx& c, int step, const ovs_params* prm, const DistArgs& a, bool kv);
+size_t dist_i32(Ctx& c, int step, const ovs_params* prm, const DistArgs& a, bool kv);
+size_t dist_f64(Ctx& c, int step, const ovs_params* prm, const DistArgs& a, bool kv);
 
 // per-dtype entry points (ovs_u32.cu, ovs_i32.cu, ovs_f64.cu)
 Out plan_u32(Ctx& c, void* keys, u32* vals, size_t n, const ovs_params* prm, bool kv);

@@ -5,4 +5,7 @@ namespace ovs {
 Out plan_f64(Ctx& c, void* keys, u32* vals, size_t n, const ovs_params* prm, bool kv) {
     return kv ? plan_or_run<DT_F64, true>(c, keys, vals, n, prm) : plan_or_run<DT_F64, false>(c, keys, vals, n, prm);
 }
+size_t dist_f64(Ctx& c, int step, const ovs_params* prm, const DistArgs& a, bool kv) {
+    return kv ? dist_run<DT_F64, true>(c, step, prm, a) : dist_run<DT_F64, false>(c, step, prm, a);
+}
 }  // namespace ovs

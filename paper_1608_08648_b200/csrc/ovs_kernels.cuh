@@ -442,7 +442,8 @@ __device__ __forceinline__ void for_items(const U* __restrict__ src, u32 beg, u3
 template <int DT, bool KV, bool LEVEL0, int NT>
 __global__ void __launch_bounds__(NT) k_hist(Bufs<typename Codec<DT>::U> B, const Chunk* chunks, const u32* nchunks,
                                              Seg* segs, const typename Codec<DT>::U* sk_pool, const u32* st_pool,
-                                             const u16* lut_pool, u32 PS, u32 LS, u32* hist, u32 split) {
+                                             const u16* lut_pool, u32 PS, u32 LS, u32* hist, u32 split,
+                                             u32 tag_base) {
     // `split` CTAs share a chunk (each a contiguous part) and add into its (zeroed) row
     typedef typename Codec<DT>::U U;
     extern __shared__ __align__(16) char smem[];
@@ -465,7 +466,7 @@ __global__ void __launch_bounds__(NT) k_hist(Bufs<typename Codec<DT>::U> B, cons
         U mn = umax_of<U>(), mx = 0;
         auto body = [&](U kr, u32 o) {
             const U k = LEVEL0 ? Codec<DT>::ord(kr) : kr;
-            const u32 tg = (KV && !LEVEL0) ? isrc[pbeg + o] : pbeg + o;
+            const u32 tg = (KV && !LEVEL0) ? isrc[pbeg + o] : (LEVEL0 ? tag_base : 0u) + pbeg + o;
             atomicAdd(&h[classify<U>(cls, k, tg)], 1u);
             if (LEVEL0) { mn = min(mn, k); mx = max(mx, k); }
         };
@@ -591,7 +592,7 @@ template <int DT, bool KV, bool LEVEL0, int NT, int ITEMS>
 __global__ void __launch_bounds__(NT) k_scatter(Bufs<typename Codec<DT>::U> B, const Chunk* chunks, const u32* nchunks,
                                                 const Seg* segs, const typename Codec<DT>::U* sk_pool,
                                                 const u32* st_pool, const u16* lut_pool, u32 PS, u32 LS,
-                                                const u32* hist, const u32* tot_pool) {
+                                                const u32* hist, const u32* tot_pool, u32 tag_base) {
     typedef typename Codec<DT>::U U;
     constexpr int TS = NT * ITEMS;
     extern __shared__ __align__(16) char smem[];
@@ -650,7 +651,7 @@ __global__ void __launch_bounds__(NT) k_scatter(Bufs<typename Codec<DT>::U> B, c
                         for (u32 q = 0; q < V; ++q) {
                             const u32 i = t0 + vi * V + q;
                             v[jv * V + q] = vsrc[i];
-                            ix[jv * V + q] = LEVEL0 ? i : isrc[i];
+                            ix[jv * V + q] = LEVEL0 ? tag_base + i : isrc[i];
                         }
                     }
                 }
@@ -661,7 +662,7 @@ __global__ void __launch_bounds__(NT) k_scatter(Bufs<typename Codec<DT>::U> B, c
                     if (o < nt) {
                         const u32 i = t0 + o;
                         k[j] = LEVEL0 ? Codec<DT>::ord(src[i]) : src[i];
-                        if (KV) { v[j] = vsrc[i]; ix[j] = LEVEL0 ? i : isrc[i]; }
+                        if (KV) { v[j] = vsrc[i]; ix[j] = LEVEL0 ? tag_base + i : isrc[i]; }
                     }
                 }
             }
@@ -669,7 +670,7 @@ __global__ void __launch_bounds__(NT) k_scatter(Bufs<typename Codec<DT>::U> B, c
             for (int j = 0; j < ITEMS; ++j) {
                 const u32 o = off(j);
                 if (o < nt) {
-                    const u32 tag = KV ? ix[j] : t0 + o;
+                    const u32 tag = KV ? ix[j] : (LEVEL0 ? tag_base : 0u) + t0 + o;
                     bk[j] = classify<U>(cls, k[j], tag);
                     rk[j] = atomicAdd(&work[bk[j]], 1u);
                 }
@@ -725,7 +726,7 @@ __global__ void __launch_bounds__(NT, 1) k_scatter_wc(Bufs<typename Codec<DT>::U
                                                        const u32* nchunks, const Seg* segs,
                                                        const typename Codec<DT>::U* sk_pool, const u32* st_pool,
                                                        const u16* lut_pool, u32 PS, u32 LS, const u32* hist,
-                                                       const u32* tot_pool) {
+                                                       const u32* tot_pool, u32 tag_base) {
     typedef typename Codec<DT>::U U;
     constexpr u32 SV = 32 / sizeof(U);  // keys per 32-byte sector
     constexpr u32 V = 16 / sizeof(U);   // keys per 16-byte vector
@@ -802,7 +803,7 @@ __global__ void __launch_bounds__(NT, 1) k_scatter_wc(Bufs<typename Codec<DT>::U
                 const u32 o = ((j / V) * NT + threadIdx.x) * V + (j % V);
                 if (full || o < nt) {
                     k[j] = Codec<DT>::ord(k[j]);
-                    bk[j] = classify<U>(cls, k[j], t0 + o);
+                    bk[j] = classify<U>(cls, k[j], tag_base + t0 + o);
                     rk[j] = atomicAdd(&cnt[bk[j]], 1u);
                 }
             }
@@ -1496,6 +1497,97 @@ __global__ void k_dro_gather(Bufs<U> B, u32 n, u32 p, const u32* bound, const u3
     for (u32 t = a + lane; t < b; t += 32) {
         B.k[0][d + t - a] = B.k[1][beg + t];
         if (KV) { B.v[0][d + t - a] = B.v[1][beg + t]; B.i[0][d + t - a] = B.i[1][beg + t]; }
+    }
+}
+
+// ------------------------------------------------------------------ multi-GPU building blocks
+// (SURVEY.md §8(e)).  Every rank computes the same global ROS index set over n_global keys;
+// rank r contributes the records of the indices inside its shard [offset, offset + n_local)
+// at their rank in the sorted index set (other slots stay zero, so an all-reduce SUM over the
+// ranks assembles T exactly).  Records: 32-bit keys one word (ord key << 32 | global index),
+// 64-bit keys two words (ord key, global index).
+template <int DT>
+__global__ void k_dist_sample_gather(const u64* sorted, u32 M, const u32* keep, const u32* pos,
+                                     const typename Codec<DT>::U* x, u64 offset, u32 n_local, u64* rec) {
+    const u32 t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= M || !keep[t]) return;
+    const u64 gi = sorted[t] >> 32;
+    if (gi < offset || gi >= offset + n_local) return;
+    const typename Codec<DT>::U k = Codec<DT>::ord(x[gi - offset]);
+    const u32 o = pos[t];
+    if (sizeof(k) == 4) rec[o] = ((u64)k << 32) | gi;
+    else { rec[2 * (u64)o] = (u64)k; rec[2 * (u64)o + 1] = gi; }
+}
+
+// unpack the all-reduced records into the internal sort's arrays
+__global__ void k_dist_unpack(const u64* rec, u32 m, u32 words, u64* t_pack, u64* t_key, u32* t_tag) {
+    const u32 t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= m) return;
+    if (words == 1) t_pack[t] = rec[t];
+    else { t_key[t] = rec[2 * (u64)t]; t_tag[t] = (u32)rec[2 * (u64)t + 1]; }
+}
+
+__global__ void k_u64_to_u32(const u64* a, u32* b, u32 n) {
+    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) b[i] = (u32)a[i];
+}
+
+// owned buckets [b0, b1) of rank `rank`: totals, bucket starts, source offsets; one CTA
+template <class U>
+__global__ void __launch_bounds__(1024) k_dist_plan(const u32* C /*world x p*/, u32 world, u32 p, u32 rank, const U* sk,
+                                                    u32* bstart /*nb+1*/, u32* srcoff /*world*/, Bucket* list, u32* nlist,
+                                                    u32 cap_items, u32* status) {
+    __shared__ u32 red[33];
+    const u32 b0 = (u32)((u64)rank * p / world), b1 = (u32)((u64)(rank + 1) * p / world), nb = b1 - b0;
+    for (u32 b = threadIdx.x; b < nb; b += 1024) {
+        u32 t = 0;
+        for (u32 s = 0; s < world; ++s) t += C[(u64)s * p + b0 + b];
+        bstart[b] = t;
+    }
+    __syncthreads();
+    block_scan_array<1024>(bstart, nb, red);  // bstart[nb] = items received
+    if (threadIdx.x == 0) {
+        u32 o = 0;
+        for (u32 s = 0; s < world; ++s) {
+            srcoff[s] = o;
+            for (u32 b = b0; b < b1; ++b) o += C[(u64)s * p + b];
+        }
+        *nlist = 0;
+        if (bstart[nb] > cap_items) atomicOr(status, ST_LIST_OVER);
+    }
+    __syncthreads();
+    for (u32 b = threadIdx.x; b < nb; b += 1024) {
+        const u32 len = bstart[b + 1] - bstart[b];
+        if (len == 0) continue;
+        const u32 q = atomicAdd(nlist, 1u);
+        Bucket bk;
+        bk.beg = bstart[b]; bk.len = len; bk.buf = 0;
+        const u32 g = b0 + b;  // global bucket id
+        const bool lo_open = (g == 0), hi_open = (g + 1 == p);
+        bk.level = (lo_open || hi_open) ? BK_LOOSE : 0u;
+        bk.lo = lo_open ? 0 : (u64)sk[g - 1];
+        bk.hi = hi_open ? (u64)umax_of<U>() : (u64)sk[g];
+        list[q] = bk;
+    }
+}
+
+// run (s, b): source s's items of owned bucket b -> output bucket b at offset sum_{s'<s} C[s'][b]
+template <class U, bool KV>
+__global__ void k_dist_gather(const U* rk, const u32* rv, const u32* ri, U* ok, u32* ov, u32* oi, const u32* C, u32 world,
+                              u32 p, u32 rank, const u32* bstart, const u32* srcoff) {
+    const u32 b0 = (u32)((u64)rank * p / world), b1 = (u32)((u64)(rank + 1) * p / world), nb = b1 - b0;
+    const u64 w = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const u32 lane = threadIdx.x & 31;
+    if (w >= (u64)world * nb) return;
+    const u32 s = (u32)(w / nb), b = (u32)(w % nb);
+    u32 a = srcoff[s];
+    for (u32 q = b0; q < b0 + b; ++q) a += C[(u64)s * p + q];
+    u32 d = bstart[b];
+    for (u32 q = 0; q < s; ++q) d += C[(u64)q * p + b0 + b];
+    const u32 len = C[(u64)s * p + b0 + b];
+    for (u32 t = lane; t < len; t += 32) {
+        ok[d + t] = rk[a + t];
+        if (KV) { ov[d + t] = rv[a + t]; oi[d + t] = ri[a + t]; }
     }
 }
 

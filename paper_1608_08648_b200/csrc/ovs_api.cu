@@ -42,14 +42,12 @@ static int sort_impl(void* d_keys, uint32_t* d_vals, bool kv, size_t n, int dtyp
         Ctx d = c;
         d.dry = true;
         d.take<u32>(4);           // status
-        d.take<u32>(SCAN_NT * 4); // scan block sums
         Out od = plan_dispatch(d, kv ? (void*)1 : nullptr, nullptr, n, dtype, prm);
         if (ws_bytes < od.ws || d_ws == nullptr) { g_err = "workspace too small"; return OVS_EWORKSPACE; }
         // real run
         c.dry = false;
         c.ws = (char*)d_ws;
         c.status = c.take<u32>(4);
-        c.bsum = c.take<u32>(SCAN_NT * 4);
         cudaEvent_t ev0 = nullptr, ev1 = nullptr;
         if (rep) {
             OVS_CK(cudaEventCreate(&ev0));
@@ -127,7 +125,6 @@ size_t ovs_workspace_bytes(size_t n, int dtype, int with_values, const ovs_param
         d.di = dev_info();
         d.dry = true;
         d.take<u32>(4);
-        d.take<u32>(SCAN_NT * 4);
         Out o = plan_dispatch(d, with_values ? (void*)1 : nullptr, nullptr, n, dtype, prm);
         return o.ws;
     } catch (...) {
@@ -173,7 +170,6 @@ static int dist_call(int step, int dtype, bool kv, const ovs_params* prm, DistAr
         d.di = dev_info();
         d.dry = true;
         d.take<u32>(4);
-        d.take<u32>(SCAN_NT * 4);
         const size_t need = dist_dispatch(d, step, dtype, kv, prm, a);
         if (ws_bytes < need || !d_ws) { g_err = "workspace too small"; return OVS_EWORKSPACE; }
         Ctx c;
@@ -182,7 +178,6 @@ static int dist_call(int step, int dtype, bool kv, const ovs_params* prm, DistAr
         c.ws = (char*)d_ws;
         c.st = (cudaStream_t)stream;
         c.status = c.take<u32>(4);
-        c.bsum = c.take<u32>(SCAN_NT * 4);
         dist_dispatch(c, step, dtype, kv, prm, a);
         return OVS_OK;
     } catch (const CudaFail& e) {
@@ -202,7 +197,6 @@ size_t ovs_dist_workspace_bytes(size_t n_local, uint64_t n_global, int dtype, in
         d.di = dev_info();
         d.dry = true;
         d.take<u32>(4);
-        d.take<u32>(SCAN_NT * 4);
         DistArgs a{};
         a.n_local = n_local; a.n_global = n_global; a.world = (u32)world; a.recv_cap = (u32)recv_capacity;
         return dist_dispatch(d, 0, dtype, with_values != 0, prm, a);

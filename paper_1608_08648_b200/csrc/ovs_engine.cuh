@@ -59,7 +59,6 @@ struct Ctx {
     u32 launches = 0;
     DevInfo di;
     u32* status = nullptr;
-    u32* bsum = nullptr;  // scratch of the device scan
     const std::vector<cudaEvent_t>* marks = nullptr;  // ovs_set_phase_events
     void mark(u32 k) {
         if (!dry && marks && k < marks->size() && (*marks)[k]) OVS_CK(cudaEventRecord((*marks)[k], st));
@@ -103,18 +102,6 @@ template <class U, bool KV> static size_t bucket_smem(u32 cap) {
 // partition tile shape: 512 threads x ITEMS per sub-tile
 constexpr int PT_NT = 512;
 template <class U, bool KV> struct PartItems { static constexpr int v = (sizeof(U) == 4 && !KV) ? 16 : 8; };
-
-// ------------------------------------------------------------------ device scan helper
-static void scan_u32(Ctx& c, const u32* in, u32* out, u32 n) {
-    const u32 nb = cdiv(n, SCAN_PER);
-    if (c.dry) return;
-    k_scan_reduce<<<nb, SCAN_NT, 0, c.st>>>(in, n, c.bsum);
-    c.check();
-    k_scan_top<<<1, SCAN_NT, 0, c.st>>>(c.bsum, nb);
-    c.check();
-    k_scan_down<<<nb, SCAN_NT, 0, c.st>>>(in, n, c.bsum, out);
-    c.check();
-}
 
 static void fill_u32(Ctx& c, u32* p, u32 v, u32 n) {
     if (c.dry || n == 0) return;
@@ -326,6 +313,98 @@ template <bool KV> struct InternalSort {
     }
 };
 
+// ------------------------------------------------------------------ a3+a4: sample sort + splitters
+// The m sample records (key word [, tag]) in draw order -> G coarse buckets (k_sel_count,
+// k_sel_scatter) -> every coarse bucket sorted by the bucket sorter -> S[q] = T[(q+1)s - 1].
+// 32-bit keys: one word (ord key << 32 | tag), sorted as u64 keys; 64-bit keys: key word + tag,
+// sorted as (key, tag) pairs (the tag rides as the value and is the tie-break index).
+template <bool TAG> struct Selector {
+    Engine<DT_U64, TAG> e;
+    typename Engine<DT_U64, TAG>::Lists l;
+    u32 m, G;
+    const u64* tk = nullptr;
+    const u32* tt = nullptr;
+    u64* csk = nullptr; u32* cst = nullptr; uint8_t* cb = nullptr;
+    u32* gcnt = nullptr; u32* gcur = nullptr;  // zeroed by the owner before run()
+    Selector(Ctx& c, u32 m_, const u64* tk_, const u32* tt_, u32* gcnt_, u32* gcur_)
+        : e(c), m(m_), tk(tk_), tt(tt_), gcnt(gcnt_), gcur(gcur_) {
+        u32 g = 1;
+        while (g * 2 <= m / 2048 && g * 2 <= SEL_GMAX) g *= 2;
+        G = g;
+        e.n = m;
+        e.cap = bucket_cap<u64, TAG>(c.di);
+        e.B.k[0] = c.take<u64>(m);
+        e.B.k[1] = c.take<u64>(m);
+        e.B.v[0] = TAG ? c.take<u32>(m) : nullptr;
+        e.B.v[1] = TAG ? c.take<u32>(m) : nullptr;
+        e.B.i[0] = TAG ? c.take<u32>(m) : nullptr;
+        e.B.i[1] = TAG ? c.take<u32>(m) : nullptr;
+        csk = c.take<u64>(SEL_GMAX);
+        cst = c.take<u32>(SEL_GMAX);
+        cb = c.take<uint8_t>(m);
+        e.carve_lists(l, G);
+    }
+    template <class U> void run(u32 P, u32 s, u64 seed, U* sk, u32* st) {
+        Ctx& c = e.c;
+        if (c.dry) return;
+        const u32 grid = cdiv(m, SEL_PER);
+        k_sel_count<TAG><<<grid, 1024, 0, c.st>>>(tk, tt, m, G, csk, cst, cb, gcnt);
+        c.check();
+        k_sel_scatter<TAG><<<grid, 1024, 0, c.st>>>(tk, tt, m, G, cb, gcnt, gcur, csk, e.B.k[0], e.B.v[0], e.B.i[0],
+                                                    l.fit, l.nfit);
+        c.check();
+        e.bucket_sort(l, seed);
+        k_pick_splitters<U><<<cdiv(P, 256), 256, 0, c.st>>>(e.B.k[0], e.B.k[0], e.B.v[0], P, s, sk, st);
+        c.check();
+    }
+};
+
+// a1+a2: the ROS sample index set I (first ps-1 distinct draws, reading Q1) and the records
+// T = [(x[i], i)], hash-set form (k_ros_draw, k_ros_first, k_ros_take); DIST: the global index
+// set over n_global keys, each rank contributing the records of its own shard.
+template <int DT, bool DIST> struct RosSampler {
+    typedef typename Codec<DT>::U U;
+    static constexpr bool TAG = sizeof(U) == 8;
+    Ctx& c;
+    u64 n;
+    u32 m, M, lg, nb;
+    u64* zero = nullptr; u32* bits = nullptr; u32* bcnt = nullptr;
+    u64* tk = nullptr; u32* tt = nullptr;
+    Selector<TAG>* sel = nullptr;
+    RosSampler(Ctx& ctx, u64 n_, u32 p, u32 s) : c(ctx), n(n_) {
+        m = p * s - 1;
+        M = ros_draws(n, m);
+        lg = ilog2(pow2_at_least(std::max<u32>(1024, M + M / 2)));
+        nb = cdiv(M, TK_NT);
+        zero = c.take<u64>(((size_t)1 << lg) + SEL_GMAX);
+        bits = c.take<u32>((size_t)nb * (TK_NT / 32));
+        bcnt = c.take<u32>(nb);
+        tk = c.take<u64>(m);
+        tt = TAG ? c.take<u32>(m) : nullptr;
+        u32* gcnt = zero ? (u32*)(zero + ((size_t)1 << lg)) : nullptr;
+        sel = new Selector<TAG>(c, m, tk, tt, gcnt, gcnt ? gcnt + SEL_GMAX : nullptr);
+    }
+    ~RosSampler() { delete sel; }
+    size_t zero_bytes() const { return 8 * (((size_t)1 << lg) + SEL_GMAX); }
+    // the hash set of the draws and the first-draw masks
+    void draw(u64 seed) {
+        if (c.dry) return;
+        OVS_CK(cudaMemsetAsync(zero, 0, zero_bytes(), c.st));
+        k_ros_draw<<<cdiv(M, 256), 256, 0, c.st>>>(zero, lg, M, n, seed);
+        c.check();
+        k_ros_first<<<nb, TK_NT, 0, c.st>>>(zero, lg, M, n, seed, bits, bcnt);
+        c.check();
+    }
+    // records of the members of I (DIST: of the shard [offset, offset + nl), into rec)
+    void take(u64 seed, const U* x, u64 offset, u32 nl, u64* rec) {
+        if (c.dry) return;
+        k_ros_take<DT, DIST><<<nb, TK_NT, 0, c.st>>>(bits, bcnt, M, n, seed, m, x, offset, nl, DIST ? rec : tk, tt,
+                                                      c.status);
+        c.check();
+    }
+    void select(u32 P, u32 s, u64 seed, U* sk, u32* st) { sel->template run<U>(P, s, seed, sk, st); }
+};
+
 // ------------------------------------------------------------------ ROS contract sort
 template <int DT, bool KV> struct RosSort {
     typedef typename Codec<DT>::U U;
@@ -333,15 +412,10 @@ template <int DT, bool KV> struct RosSort {
     Engine<DT, KV> e;
     typename Engine<DT, KV>::Level0 z;
     typename Engine<DT, KV>::Lists l;
-    u32 n, p, s, m = 0, M = 0;
+    u32 n, p, s;
     u64 seed;
     u64* counts = nullptr;
-    // sample phase
-    u64* cand = nullptr; u32* flag = nullptr; u32* rank = nullptr; u32* keep = nullptr; u32* pos = nullptr;
-    u64* t_pack = nullptr; u64* t_key = nullptr; u32* t_tag = nullptr;
-    InternalSort<false>* cand_sort = nullptr;
-    InternalSort<false>* t_sort32 = nullptr;
-    InternalSort<true>* t_sort64 = nullptr;
+    RosSampler<DT, false>* smp = nullptr;  // a1-a4
 
     RosSort(Ctx& ctx, U* keys, u32* vals, u32 n_, u32 p_, u32 s_, u64 seed_) : c(ctx), e(ctx), n(n_), p(p_), s(s_), seed(seed_) {
         e.n = n;
@@ -358,50 +432,20 @@ template <int DT, bool KV> struct RosSort {
                                                    cdiv(n, (u32)(e.cap * 45ull / 100))) : 1;
         e.carve_level0(z, P0);
         e.carve_lists(l, P0);
-        if (p > 1) {
-            m = p * s - 1;
-            M = ros_draws(n, m);
-            cand = c.take<u64>(M);
-            flag = c.take<u32>(M);
-            rank = c.take<u32>(M);
-            keep = c.take<u32>(M);
-            pos = c.take<u32>(M);
-            cand_sort = new InternalSort<false>(c, M, cand, nullptr);
-            if (sizeof(U) == 4) {
-                t_pack = c.take<u64>(m);
-                t_sort32 = new InternalSort<false>(c, m, t_pack, nullptr);
-            } else {
-                t_key = c.take<u64>(m);
-                t_tag = c.take<u32>(m);
-                t_sort64 = new InternalSort<true>(c, m, t_key, t_tag);
-            }
-        }
+        if (p > 1) smp = new RosSampler<DT, false>(c, n, p, s);
     }
-    ~RosSort() { delete cand_sort; delete t_sort32; delete t_sort64; }
+    ~RosSort() { delete smp; }
 
     void run() {
         if (c.dry) return;
         e.mark_phases = true;
         c.mark(0);
         if (p > 1) {
-            // a1: ps-1 distinct random indices (first distinct draws of the counter stream)
-            k_ros_candidates<<<cdiv(M, 256), 256, 0, c.st>>>(cand, M, n, seed);
-            c.check();
-            cand_sort->run(seed ^ 0xc0ffee);
-            k_ros_first_flags<<<cdiv(M, 256), 256, 0, c.st>>>(cand, M, flag);
-            c.check();
-            scan_u32(c, flag, rank, M);
-            k_ros_keep<<<cdiv(M, 256), 256, 0, c.st>>>(cand, M, flag, rank, m, keep, c.status);
-            c.check();
-            scan_u32(c, keep, pos, M);
-            // a2: gather T = [(x[i], i)] in index order; a3: sort T by (key, i)
-            k_ros_gather<DT><<<cdiv(M, 256), 256, 0, c.st>>>(cand, M, keep, pos, e.B.k[0], t_pack, t_key, t_tag);
-            c.check();
-            if (t_sort32) t_sort32->run(seed ^ 0x5eed);
-            else t_sort64->run(seed ^ 0x5eed);
-            // a4: splitters S[q] = T[(q+1)s - 1]
-            k_pick_splitters<U><<<cdiv(p, 256), 256, 0, c.st>>>(t_pack, t_key, t_tag, p, s, z.sk, z.st);
-            c.check();
+            // a1+a2: ps-1 distinct random indices and their records T = [(x[i], i)]
+            smp->draw(seed);
+            smp->take(seed, e.B.k[0], 0, n, nullptr);
+            // a3+a4: sort T by (key, i); S[q] = T[(q+1)s - 1]
+            smp->select(p, s, seed ^ 0x5eed, z.sk, z.st);
         } else {
             e.internal_splitters(z, seed);
         }
@@ -551,11 +595,7 @@ template <int DT, bool KV> struct DistSort {
     u32 nl, p, s, world, m, M, words, recv_cap;
     u64 ng, offset = 0, seed;
     u64* counts64 = nullptr;
-    u64* cand = nullptr; u32* flag = nullptr; u32* rank = nullptr; u32* keep = nullptr; u32* pos = nullptr;
-    u64* t_pack = nullptr; u64* t_key = nullptr; u32* t_tag = nullptr;
-    InternalSort<false>* cand_sort = nullptr;
-    InternalSort<false>* t_sort32 = nullptr;
-    InternalSort<true>* t_sort64 = nullptr;
+    RosSampler<DT, true>* smp = nullptr;  // a1-a4 over the global index set
     u32* bstart = nullptr; u32* srcoff = nullptr;
 
     DistSort(Ctx& ctx, u32 n_local, u64 n_global, u32 p_, u32 s_, u64 seed_, u32 world_, u32 recv_capacity)
@@ -569,20 +609,7 @@ template <int DT, bool KV> struct DistSort {
         M = ros_draws(ng, m);
         words = sizeof(U) == 4 ? 1 : 2;
         counts64 = c.take<u64>(p);
-        cand = c.take<u64>(M);
-        flag = c.take<u32>(M);
-        rank = c.take<u32>(M);
-        keep = c.take<u32>(M);
-        pos = c.take<u32>(M);
-        cand_sort = new InternalSort<false>(c, M, cand, nullptr);
-        if (words == 1) {
-            t_pack = c.take<u64>(m);
-            t_sort32 = new InternalSort<false>(c, m, t_pack, nullptr);
-        } else {
-            t_key = c.take<u64>(m);
-            t_tag = c.take<u32>(m);
-            t_sort64 = new InternalSort<true>(c, m, t_key, t_tag);
-        }
+        smp = new RosSampler<DT, true>(c, ng, p, s);
         e.carve_level0(z, p);
         e.carve_lists(l, p);
         // finish side
@@ -594,32 +621,22 @@ template <int DT, bool KV> struct DistSort {
         srcoff = c.take<u32>(world + 1);
         f.carve_lists(lf, p);
     }
-    ~DistSort() { delete cand_sort; delete t_sort32; delete t_sort64; }
+    ~DistSort() { delete smp; }
 
     void sample(const U* keys, u64* rec) {
         if (c.dry) return;
         OVS_CK(cudaMemsetAsync(rec, 0, sizeof(u64) * (size_t)m * words, c.st));
-        k_ros_candidates<<<cdiv(M, 256), 256, 0, c.st>>>(cand, M, ng, seed);
-        c.check();
-        cand_sort->run(seed ^ 0xc0ffee);
-        k_ros_first_flags<<<cdiv(M, 256), 256, 0, c.st>>>(cand, M, flag);
-        c.check();
-        scan_u32(c, flag, rank, M);
-        k_ros_keep<<<cdiv(M, 256), 256, 0, c.st>>>(cand, M, flag, rank, m, keep, c.status);
-        c.check();
-        scan_u32(c, keep, pos, M);
-        k_dist_sample_gather<DT><<<cdiv(M, 256), 256, 0, c.st>>>(cand, M, keep, pos, keys, offset, nl, rec);
-        c.check();
+        smp->draw(seed);
+        smp->take(seed, keys, offset, nl, rec);
     }
 
     void partition(U* keys, u32* vals, const u64* rec, U* send_k, u32* send_v, u32* send_i, u32* counts) {
         if (c.dry) return;
-        k_dist_unpack<<<cdiv(m, 256), 256, 0, c.st>>>(rec, m, words, t_pack, t_key, t_tag);
+        k_dist_unpack<<<cdiv(m, 256), 256, 0, c.st>>>(rec, m, words, smp->tk, smp->tk, smp->tt);
         c.check();
-        if (t_sort32) t_sort32->run(seed ^ 0x5eed);
-        else t_sort64->run(seed ^ 0x5eed);
-        k_pick_splitters<U><<<cdiv(p, 256), 256, 0, c.st>>>(t_pack, t_key, t_tag, p, s, z.sk, z.st);
-        c.check();
+        // the coarse-bucket counters are zeroed here too: this call may run on a fresh process
+        OVS_CK(cudaMemsetAsync(smp->sel->gcnt, 0, 8 * SEL_GMAX, c.st));
+        smp->select(p, s, seed ^ 0x5eed, z.sk, z.st);
         e.B.k[0] = keys; e.B.v[0] = vals;
         e.B.k[1] = send_k; e.B.v[1] = send_v; e.B.i[1] = send_i;
         e.B.i[0] = nullptr;

@@ -184,98 +184,270 @@ __device__ void block_scan_array(u32* a, u32 cnt, u32* red) {
 }
 
 // exclusive scan in place of a[0..cnt), cnt <= NT*16, one round (16 consecutive per thread)
+// Thread t owns a[16t .. 16t+16) but visits them rotated by r = (t/2) mod 16 (element
+// (j + r) mod 16 at step j), so the 32 lanes of a warp hit 32 distinct banks at every step.
 template <int NT>
 __device__ void block_scan_small(u32* a, u32 cnt, u32* red) {
-    const u32 i0 = threadIdx.x * 16;
-    u32 v[16], s = 0;
-#pragma unroll
-    for (int j = 0; j < 16; ++j) { v[j] = (i0 + j < cnt) ? a[i0 + j] : 0u; s += v[j]; }
-    u32 ex = block_exclusive_scan<NT>(s, red, nullptr);
+    const u32 i0 = threadIdx.x * 16, r = (threadIdx.x >> 1) & 15;
+    u32 v[16], s = 0, head = 0;
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-        if (i0 + j < cnt) a[i0 + j] = ex;
-        ex += v[j];
+        const u32 e = (j + r) & 15;
+        v[j] = (i0 + e < cnt) ? a[i0 + e] : 0u;
+        s += v[j];
+        if (e < r) head += v[j];
+    }
+    const u32 base = block_exclusive_scan<NT>(s, red, nullptr);
+    u32 run = base + head;  // prefix of element r
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const u32 e = (j + r) & 15;
+        if (e == 0) run = base;
+        if (i0 + e < cnt) a[i0 + e] = run;
+        run += v[j];
     }
     __syncthreads();
 }
 
-// ------------------------------------------------------------------ generic device scan (u32)
-// exclusive scan of n u32 values, 3 kernels; used by the ROS sample de-duplication (a1).
-constexpr int SCAN_NT = 1024, SCAN_PER = 4096;
-__global__ void __launch_bounds__(SCAN_NT) k_scan_reduce(const u32* in, u32 n, u32* bsum) {
-    __shared__ u32 red[SCAN_NT / 32 + 1];
-    u32 i0 = blockIdx.x * SCAN_PER + threadIdx.x * 4, s = 0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) s += (i0 + j < n) ? in[i0 + j] : 0u;
-    u32 tot;
-    block_exclusive_scan<SCAN_NT>(s, red, &tot);
-    if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
-}
-__global__ void __launch_bounds__(SCAN_NT) k_scan_top(u32* bsum, u32 nb) {
-    __shared__ u32 red[SCAN_NT / 32 + 1];
-    block_scan_array<SCAN_NT>(bsum, nb, red);
-}
-__global__ void __launch_bounds__(SCAN_NT) k_scan_down(const u32* in, u32 n, const u32* bsum, u32* out) {
-    __shared__ u32 red[SCAN_NT / 32 + 1];
-    u32 i0 = blockIdx.x * SCAN_PER + threadIdx.x * 4, v[4], s = 0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) { v[j] = (i0 + j < n) ? in[i0 + j] : 0u; s += v[j]; }
-    u32 ex = block_exclusive_scan<SCAN_NT>(s, red, nullptr) + bsum[blockIdx.x];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        if (i0 + j < n) out[i0 + j] = ex;
-        ex += v[j];
+// ------------------------------------------------------------------ CTA bitonic sort of (key, tag)
+// N a power of two, records in shared memory; ascending by (key, tag).
+template <class U>
+__device__ void cta_bitonic_kt(U* tk, u32* tt, u32 N) {
+    for (u32 kk = 2; kk <= N; kk <<= 1) {
+        for (u32 j = kk >> 1; j > 0; j >>= 1) {
+            for (u32 t = threadIdx.x; t < N; t += blockDim.x) {
+                const u32 o = t ^ j;
+                if (o > t) {
+                    const bool asc = (t & kk) == 0;
+                    const bool gt = tk[t] > tk[o] || (tk[t] == tk[o] && tt[t] > tt[o]);
+                    if (gt == asc) {
+                        U a = tk[t]; tk[t] = tk[o]; tk[o] = a;
+                        u32 b = tt[t]; tt[t] = tt[o]; tt[o] = b;
+                    }
+                }
+            }
+            __syncthreads();
+        }
     }
 }
 
-// ------------------------------------------------------------------ a1: ROS sample indices
-// Candidate j = (c_j << 32) | j, c_j = floor(H(seed,1,j) * n / 2^64) (reading Q1).  Sorting
-// the candidates groups equal c; the FIRST distinct draws are the candidates that are the
-// smallest j of their c-group, ranked by j.
-__global__ void k_ros_candidates(u64* cand, u32 M, u64 n, u64 seed) {
-    u32 j = blockIdx.x * blockDim.x + threadIdx.x;
+// ------------------------------------------------------------------ a1+a2: hash-set form
+// I = the first m distinct values of c_j = floor(H(seed,1,j) n / 2^64), j = 0, 1, ... (reading
+// Q1).  Draw j is "first" iff no j' < j has c_j' = c_j.  An open-addressing hash set keyed by c
+// keeps the smallest j of every c; an entry holds ~((c << 32) | j) so that the empty slot is 0
+// (one memset) and "smallest j" is an atomicMax.  The first draws ranked by j are the members of
+// I; the records T[rank] = (x[c], c) are written in draw order, a uniformly random order that
+// the coarse level of the sample sort relies on (T's order is not part of any result).
+__device__ __forceinline__ u32 ht_slot(u64 c, u32 lg) { return (u32)((c * 0x9e3779b97f4a7c15ull) >> (64 - lg)); }
+__device__ __forceinline__ u64 ros_draw_c(u64 seed, u32 j, u64 n) { return __umul64hi(rng_H(seed, 1, j), n); }
+
+__global__ void k_ros_draw(u64* tab, u32 lg, u32 M, u64 n, u64 seed) {
+    const u32 j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= M) return;
-    u64 u = rng_H(seed, 1, j);
-    u64 c = __umul64hi(u, n);
-    cand[j] = (c << 32) | (u64)j;
-}
-
-__global__ void k_ros_first_flags(const u64* sorted, u32 M, u32* flag_by_j) {
-    u32 t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= M) return;
-    u64 x = sorted[t];
-    bool first = (t == 0) || ((sorted[t - 1] >> 32) != (x >> 32));
-    flag_by_j[(u32)x] = first ? 1u : 0u;
-}
-
-// keep[t] = candidate at sorted position t is one of the first m distinct draws
-__global__ void k_ros_keep(const u64* sorted, u32 M, const u32* flag_by_j, const u32* rank_by_j, u32 m,
-                           u32* keep, u32* status) {
-    u32 t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= M) return;
-    u32 j = (u32)sorted[t];
-    keep[t] = (flag_by_j[j] && rank_by_j[j] < m) ? 1u : 0u;
-    if (t == M - 1) {
-        u32 tot = rank_by_j[M - 1] + flag_by_j[M - 1];
-        if (tot < m) atomicOr(status, ST_SAMPLE_SHORT);
+    const u64 c = ros_draw_c(seed, j, n);
+    const u64 e = ~((c << 32) | j);
+    const u32 mask = (1u << lg) - 1;
+    for (u32 s = ht_slot(c, lg);; s = (s + 1) & mask) {
+        u64 v = __ldcg(tab + s);
+        if (v == 0) {
+            v = atomicCAS((unsigned long long*)(tab + s), 0ull, (unsigned long long)e);
+            if (v == 0) return;
+        }
+        if ((~v >> 32) == c) {
+            atomicMax((unsigned long long*)(tab + s), (unsigned long long)e);
+            return;
+        }
     }
 }
 
-// a2: gather T = [(x[i], i)] in index order.  32-bit keys pack (ord key << 32 | i) into one
-// u64 (sorting it orders by (key, tag)); 64-bit keys store key and tag apart.
-template <int DT>
-__global__ void k_ros_gather(const u64* sorted, u32 M, const u32* keep, const u32* pos,
-                             const typename Codec<DT>::U* x, u64* t_pack, u64* t_key, u32* t_tag) {
-    u32 t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= M || !keep[t]) return;
-    u32 i = (u32)(sorted[t] >> 32);
-    u32 o = pos[t];
-    typename Codec<DT>::U k = Codec<DT>::ord(x[i]);
-    if (sizeof(k) == 4) {
-        t_pack[o] = ((u64)k << 32) | i;
+__device__ __forceinline__ u32 ht_min_j(const u64* tab, u32 lg, u64 c) {
+    const u32 mask = (1u << lg) - 1;
+    for (u32 s = ht_slot(c, lg);; s = (s + 1) & mask) {
+        const u64 v = ~__ldcg(tab + s);
+        if ((v >> 32) == c) return (u32)v;
+    }
+}
+
+constexpr int TK_NT = 1024;
+// per block of TK_NT draws: the warps' masks of first draws, and the block's count
+__global__ void __launch_bounds__(TK_NT) k_ros_first(const u64* tab, u32 lg, u32 M, u64 n, u64 seed, u32* bits, u32* bcnt) {
+    __shared__ u32 wcnt[TK_NT / 32];
+    const u32 j = blockIdx.x * TK_NT + threadIdx.x;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    bool first = false;
+    if (j < M) first = ht_min_j(tab, lg, ros_draw_c(seed, j, n)) == j;
+    const u32 mask = __ballot_sync(0xffffffffu, first);
+    if (lane == 0) { bits[j >> 5] = mask; wcnt[wid] = __popc(mask); }
+    __syncthreads();
+    if (wid == 0) {
+        u32 v = wcnt[lane];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) bcnt[blockIdx.x] = v;
+    }
+}
+
+// rank(j) among the first draws = the blocks before + the warps before + the lanes before; a
+// first draw of rank < m is a member of I.  Record layout: 32-bit keys one word
+// (ord key << 32 | c), 64-bit keys a key word and a tag (c).  DIST: only indices inside the
+// shard [offset, offset + nl) contribute (rec slots of other ranks stay zero; the all-reduce SUM
+// over ranks assembles T, 2 words per record for 64-bit keys).
+template <int DT, bool DIST>
+__global__ void __launch_bounds__(TK_NT) k_ros_take(const u32* bits, const u32* bcnt, u32 M, u64 n, u64 seed, u32 m,
+                                                     const typename Codec<DT>::U* x, u64 offset, u32 nl, u64* tk, u32* tt,
+                                                     u32* status) {
+    typedef typename Codec<DT>::U U;
+    __shared__ u32 red[TK_NT / 32], wpre[TK_NT / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    u32 s = 0;
+    for (u32 b = threadIdx.x; b < blockIdx.x; b += TK_NT) s += bcnt[b];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const u32 j = blockIdx.x * TK_NT + threadIdx.x;
+    const u32 mask = bits[j >> 5];
+    if (lane == 0) { red[wid] = s; wpre[wid] = __popc(mask); }
+    __syncthreads();
+    if (wid == 0) {
+        u32 b = red[lane], w = wpre[lane], x2 = w;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) b += __shfl_xor_sync(0xffffffffu, b, o);
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u32 y = __shfl_up_sync(0xffffffffu, x2, o);
+            if (lane >= o) x2 += y;
+        }
+        wpre[lane] = b + x2 - w;  // exclusive prefix of warp `lane` in the whole draw order
+        if (blockIdx.x + 1 == gridDim.x && lane == 31 && b + x2 < m) atomicOr(status, ST_SAMPLE_SHORT);
+    }
+    __syncthreads();
+    if (!((mask >> lane) & 1u)) return;
+    const u32 rank = wpre[wid] + __popc(mask & ((1u << lane) - 1));
+    if (rank >= m) return;
+    const u64 c = ros_draw_c(seed, j, n);
+    if (DIST && (c < offset || c >= offset + nl)) return;
+    const U k = Codec<DT>::ord(x[c - offset]);
+    if (sizeof(U) == 4) {
+        tk[rank] = ((u64)k << 32) | c;
+    } else if (DIST) {
+        tk[2 * (u64)rank] = (u64)k;
+        tk[2 * (u64)rank + 1] = c;
     } else {
-        t_key[o] = (u64)k;
-        t_tag[o] = i;
+        tk[rank] = (u64)k;
+        tt[rank] = (u32)c;
+    }
+}
+
+// ------------------------------------------------------------------ a3: sample sort (coarse level)
+// The m sample records (key word, tag) are sorted by (key, tag) in two steps: G coarse buckets,
+// then every coarse bucket by the bucket sorter.  Coarse splitter i = CS[(i+1)Q/G - 1], CS =
+// the first Q = min(m, 1024) records of T sorted (a uniform random subset, T being in draw
+// order).  Every CTA of k_sel_count sorts CS itself (a 1024-record bitonic network, ~1 us) so
+// no separate launch is needed; CTA 0 stores the coarse splitters for k_sel_scatter.
+constexpr u32 SEL_Q = 1024, SEL_PER = 4096, SEL_GMAX = 128;
+
+__device__ __forceinline__ bool rec_lt(u64 ak, u32 at, u64 bk, u32 bt) { return ak < bk || (ak == bk && at < bt); }
+
+__device__ __forceinline__ u32 coarse_of(const u64* ck, const u32* ct, u32 nc, u64 k, u32 t) {
+    u32 lo = 0, cnt = nc;
+    while (cnt > 0) {
+        const u32 half = cnt >> 1, mid = lo + half;
+        if (rec_lt(ck[mid], ct[mid], k, t)) { lo = mid + 1; cnt -= half + 1; } else cnt = half;
+    }
+    return lo;
+}
+
+template <bool TAG>
+__global__ void __launch_bounds__(1024) k_sel_count(const u64* tk, const u32* tt, u32 m, u32 G, u64* csk, u32* cst,
+                                                    uint8_t* cb, u32* gcnt) {
+    __shared__ u64 qk[SEL_Q];
+    __shared__ u32 qt[SEL_Q];
+    __shared__ u32 h[SEL_GMAX];
+    const u32 Q = min(m, SEL_Q);
+    if (G > 1) {
+        u32 N = 1;
+        while (N < Q) N <<= 1;
+        for (u32 i = threadIdx.x; i < N; i += blockDim.x) {
+            qk[i] = i < Q ? tk[i] : ~0ull;
+            qt[i] = i < Q ? (TAG ? tt[i] : 0u) : 0xffffffffu;
+        }
+        __syncthreads();
+        cta_bitonic_kt<u64>(qk, qt, N);
+        // coarse splitters in place at the front (reads before writes: ranks are increasing)
+        u64 ck = 0;
+        u32 ct = 0;
+        if (threadIdx.x + 1 < G) {
+            const u32 r = (u32)(((u64)(threadIdx.x + 1) * Q) / G) - 1;
+            ck = qk[r];
+            ct = qt[r];
+        }
+        __syncthreads();
+        if (threadIdx.x + 1 < G) {
+            qk[threadIdx.x] = ck;
+            qt[threadIdx.x] = ct;
+            if (blockIdx.x == 0) { csk[threadIdx.x] = ck; cst[threadIdx.x] = ct; }
+        }
+    }
+    for (u32 g = threadIdx.x; g < G; g += blockDim.x) h[g] = 0;
+    __syncthreads();
+    const u32 b0 = blockIdx.x * SEL_PER, b1 = min(m, b0 + SEL_PER);
+    for (u32 i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
+        const u32 g = coarse_of(qk, qt, G - 1, tk[i], TAG ? tt[i] : 0u);
+        cb[i] = (uint8_t)g;
+        atomicAdd(&h[g], 1u);
+    }
+    __syncthreads();
+    for (u32 g = threadIdx.x; g < G; g += blockDim.x)
+        if (h[g]) atomicAdd(&gcnt[g], h[g]);
+}
+
+// coarse buckets -> T2 (bucket-contiguous, order inside a bucket irrelevant: every bucket is
+// sorted next); CTA 0 writes the bucket sorter's work list (bounds = the coarse splitters' keys)
+template <bool TAG>
+__global__ void __launch_bounds__(1024) k_sel_scatter(const u64* tk, const u32* tt, u32 m, u32 G, const uint8_t* cb,
+                                                      const u32* gcnt, u32* gcur, const u64* csk, u64* ok, u32* ot,
+                                                      u32* oi, Bucket* list, u32* nlist) {
+    __shared__ u32 st[SEL_GMAX + 1], h[SEL_GMAX], base[SEL_GMAX];
+    if (threadIdx.x == 0) {
+        u32 run = 0;
+        for (u32 g = 0; g < G; ++g) { st[g] = run; run += gcnt[g]; }
+        st[G] = run;
+    }
+    for (u32 g = threadIdx.x; g < G; g += blockDim.x) h[g] = 0;
+    __syncthreads();
+    const u32 b0 = blockIdx.x * SEL_PER, b1 = min(m, b0 + SEL_PER);
+    constexpr u32 IT = SEL_PER / 1024;
+    u32 gg[IT], rr[IT];
+#pragma unroll
+    for (u32 q = 0; q < IT; ++q) {
+        const u32 i = b0 + q * 1024 + threadIdx.x;
+        if (i < b1) { gg[q] = cb[i]; rr[q] = atomicAdd(&h[gg[q]], 1u); }
+    }
+    __syncthreads();
+    for (u32 g = threadIdx.x; g < G; g += blockDim.x) base[g] = h[g] ? atomicAdd(&gcur[g], h[g]) : 0u;
+    __syncthreads();
+#pragma unroll
+    for (u32 q = 0; q < IT; ++q) {
+        const u32 i = b0 + q * 1024 + threadIdx.x;
+        if (i < b1) {
+            const u32 d = st[gg[q]] + base[gg[q]] + rr[q];
+            ok[d] = tk[i];
+            if (TAG) { ot[d] = tt[i]; oi[d] = tt[i]; }
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        u32 nb = 0;
+        for (u32 g = 0; g < G; ++g) {
+            const u32 len = st[g + 1] - st[g];
+            if (len == 0) continue;
+            Bucket b;
+            b.beg = st[g]; b.len = len; b.buf = 0;
+            b.level = (g == 0 || g + 1 == G) ? BK_LOOSE : 0u;
+            b.lo = g ? csk[g - 1] : 0ull;
+            b.hi = g + 1 < G ? csk[g] : ~0ull;
+            list[nb++] = b;
+        }
+        nlist[0] = nb;
+        nlist[1] = 0;
     }
 }
 
@@ -854,28 +1026,6 @@ __global__ void __launch_bounds__(NT, 1) k_scatter_wc(Bufs<typename Codec<DT>::U
     }
 }
 
-// ------------------------------------------------------------------ CTA bitonic sort of (key, tag)
-// N a power of two, records in shared memory; ascending by (key, tag).
-template <class U>
-__device__ void cta_bitonic_kt(U* tk, u32* tt, u32 N) {
-    for (u32 kk = 2; kk <= N; kk <<= 1) {
-        for (u32 j = kk >> 1; j > 0; j >>= 1) {
-            for (u32 t = threadIdx.x; t < N; t += blockDim.x) {
-                const u32 o = t ^ j;
-                if (o > t) {
-                    const bool asc = (t & kk) == 0;
-                    const bool gt = tk[t] > tk[o] || (tk[t] == tk[o] && tt[t] > tt[o]);
-                    if (gt == asc) {
-                        U a = tk[t]; tk[t] = tk[o]; tk[o] = a;
-                        u32 b = tt[t]; tt[t] = tt[o]; tt[o] = b;
-                    }
-                }
-            }
-            __syncthreads();
-        }
-    }
-}
-
 // ------------------------------------------------------------------ internal splitters
 // Splitters of an internal sort of a whole array of n items (not part of the contract; used
 // for p == 1 and for sorting the sample / candidate arrays): a random sample with
@@ -1076,7 +1226,7 @@ template <class U> __device__ __forceinline__ u32 lower_bound_kt(const U* sk, co
 }
 
 template <class U, bool KV> __host__ __device__ constexpr size_t bucket_smem_fixed() {
-    return 4 * ((size_t)BS_NGMAX + 4);
+    return 4 * ((size_t)BS_NGMAX + 4) + 16;  // group counters + alignment slack of the items
 }
 template <class U, bool KV> __host__ __device__ constexpr size_t bucket_item_bytes() {
     return sizeof(U) + (KV ? 8 : 0);
@@ -1101,7 +1251,7 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
     {
         char* sp = smem;
         S.cnt = (u32*)sp; sp += 4 * ((size_t)BS_NGMAX + 4);
-        S.k = (U*)sp; sp += sizeof(U) * (size_t)cap;
+        S.k = (U*)sp; sp += sizeof(U) * (size_t)cap + 16;
         if (KV) { S.i = (u32*)sp; sp += 4 * (size_t)cap; S.v = (u32*)sp; sp += 4 * (size_t)cap; }
     }
     Bucket* stk = stack_pool + (size_t)blockIdx.x * BS_STACK;
@@ -1206,6 +1356,10 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                 continue;
             }
             // ---------------- on-chip sort of a bucket that fits
+            // items sit at shared index = global index mod 16 bytes, so the write-out is aligned
+            // 16-byte shared loads and global stores
+            BucketSmem<U, KV> Sa = S;
+            Sa.k = S.k + (bk.beg & (16 / sizeof(U) - 1));
             U lo = (U)bk.lo, hi = (U)bk.hi;
             if (bk.level & BK_LOOSE) {
                 U mn = umax_of<U>(), mx = 0;
@@ -1240,23 +1394,23 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                     return min((u32)__umul64hi(x, mult), ng - 1);
                 }
             };
-            for (u32 g = threadIdx.x; g < ng; g += BS_NT) S.cnt[g] = 0;
+            for (u32 g = threadIdx.x; g < ng; g += BS_NT) Sa.cnt[g] = 0;
             __syncthreads();
             // 1. digit histogram
             for_items<U, BS_NT, 4>(src, bk.beg, m, [&](U kr, u32 o) {
                 const u32 ix = KV ? IX(bk.beg + o) : 0u;
-                atomicAdd(&S.cnt[digit(K(kr), ix)], 1u);
+                atomicAdd(&Sa.cnt[digit(K(kr), ix)], 1u);
             });
             __syncthreads();
-            block_scan_small<BS_NT>(S.cnt, ng, red);  // cnt[g] = start of group g
+            block_scan_small<BS_NT>(Sa.cnt, ng, red);  // cnt[g] = start of group g
             // 2. scatter into shared memory by digit; afterwards cnt[g] = end of group g
             for_items<U, BS_NT, 4>(src, bk.beg, m, [&](U kr, u32 o) {
                 const U k = K(kr);
                 u32 ix = 0, vv = 0;
                 if (KV) { ix = IX(bk.beg + o); vv = vsrc[bk.beg + o]; }
-                const u32 pos = atomicAdd(&S.cnt[digit(k, ix)], 1u);
-                S.k[pos] = k;
-                if (KV) { S.i[pos] = ix; S.v[pos] = vv; }
+                const u32 pos = atomicAdd(&Sa.cnt[digit(k, ix)], 1u);
+                Sa.k[pos] = k;
+                if (KV) { Sa.i[pos] = ix; Sa.v[pos] = vv; }
             });
             __syncthreads();
             // 3. one thread per group of <= 8: Batcher network in registers; larger groups are
@@ -1264,15 +1418,15 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
             for (u32 g0 = 0; g0 < ng; g0 += BS_NT) {
                 const u32 g = g0 + threadIdx.x;
                 u32 gs = 0, len = 0;
-                if (g < ng) { gs = g ? S.cnt[g - 1] : 0u; len = S.cnt[g] - gs; }
+                if (g < ng) { gs = g ? Sa.cnt[g - 1] : 0u; len = Sa.cnt[g] - gs; }
                 if (len > 1 && len <= 8) {
                     E a[8];
 #pragma unroll
-                    for (u32 q = 0; q < 8; ++q) a[q] = q < len ? sm_get<U, KV>(S, gs + q) : E::inf();
+                    for (u32 q = 0; q < 8; ++q) a[q] = q < len ? sm_get<U, KV>(Sa, gs + q) : E::inf();
                     network8(a);
 #pragma unroll
                     for (u32 q = 0; q < 8; ++q)
-                        if (q < len) sm_put<U, KV>(S, gs + q, a[q]);
+                        if (q < len) sm_put<U, KV>(Sa, gs + q, a[q]);
                 }
                 const u32 mb = __ballot_sync(0xffffffffu, len > 8);
                 if (mb) {
@@ -1292,26 +1446,26 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
             const u32 nwork = rescan ? ng : nlisted;
             for (u32 q = threadIdx.x; q < nwork; q += BS_NT) {
                 const u32 g = rescan ? q : s_big[q];
-                const u32 gs = g ? S.cnt[g - 1] : 0u, len = S.cnt[g] - gs;
+                const u32 gs = g ? Sa.cnt[g - 1] : 0u, len = Sa.cnt[g] - gs;
                 if (len <= 8 || len > 16) continue;
                 E a[16];
 #pragma unroll
-                for (u32 t = 0; t < 16; ++t) a[t] = t < len ? sm_get<U, KV>(S, gs + t) : E::inf();
+                for (u32 t = 0; t < 16; ++t) a[t] = t < len ? sm_get<U, KV>(Sa, gs + t) : E::inf();
                 network16(a);
 #pragma unroll
                 for (u32 t = 0; t < 16; ++t)
-                    if (t < len) sm_put<U, KV>(S, gs + t, a[t]);
+                    if (t < len) sm_put<U, KV>(Sa, gs + t, a[t]);
             }
             // 3c'. groups of 17..512: one warp each (register bitonic); over 512: the CTA
             for (u32 q = wid; q < nwork; q += BS_NT / 32) {
                 const u32 g = rescan ? q : s_big[q];
-                const u32 gs = g ? S.cnt[g - 1] : 0u, len = S.cnt[g] - gs;
+                const u32 gs = g ? Sa.cnt[g - 1] : 0u, len = Sa.cnt[g] - gs;
                 if (len <= 16) continue;
-                if (len <= 32) warp_sort_group<U, KV, 1>(S, gs, len);
-                else if (len <= 64) warp_sort_group<U, KV, 2>(S, gs, len);
-                else if (len <= 128) warp_sort_group<U, KV, 4>(S, gs, len);
-                else if (len <= 256) warp_sort_group<U, KV, 8>(S, gs, len);
-                else if (len <= 512) warp_sort_group<U, KV, 16>(S, gs, len);
+                if (len <= 32) warp_sort_group<U, KV, 1>(Sa, gs, len);
+                else if (len <= 64) warp_sort_group<U, KV, 2>(Sa, gs, len);
+                else if (len <= 128) warp_sort_group<U, KV, 4>(Sa, gs, len);
+                else if (len <= 256) warp_sort_group<U, KV, 8>(Sa, gs, len);
+                else if (len <= 512) warp_sort_group<U, KV, 16>(Sa, gs, len);
                 else if (lane == 0) {
                     const u32 h = atomicAdd(&s_nhuge, 1u);
                     if (h < BS_HUGEMAX) s_huge[h] = g;
@@ -1325,7 +1479,7 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
             const u32 nhuge = min(s_nhuge, (u32)BS_HUGEMAX);
             for (u32 q = 0; q < nhuge; ++q) {
                 const u32 g = s_huge[q];
-                const u32 gs = g ? S.cnt[g - 1] : 0u, len = S.cnt[g] - gs;
+                const u32 gs = g ? Sa.cnt[g - 1] : 0u, len = Sa.cnt[g] - gs;
                 u32 N = 1;
                 while (N < len) N <<= 1;
                 for (u32 kk = 2; kk <= N; kk <<= 1) {
@@ -1333,13 +1487,13 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                     for (u32 t = threadIdx.x; t < N / 2; t += BS_NT) {
                         const u32 blk = t / hk, off = t % hk;
                         const u32 x = blk * kk + off, y = blk * kk + kk - 1 - off;
-                        if (y < len) smem_cex<U, KV>(S, gs + x, gs + y);
+                        if (y < len) smem_cex<U, KV>(Sa, gs + x, gs + y);
                     }
                     __syncthreads();
                     for (u32 j = kk >> 2; j > 0; j >>= 1) {
                         for (u32 t = threadIdx.x; t < N / 2; t += BS_NT) {
                             const u32 x = (t / j) * 2 * j + (t % j), y = x + j;
-                            if (y < len) smem_cex<U, KV>(S, gs + x, gs + y);
+                            if (y < len) smem_cex<U, KV>(Sa, gs + x, gs + y);
                         }
                         __syncthreads();
                     }
@@ -1353,21 +1507,22 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                 const u32 mis = (u32)(((uintptr_t)out) & 15u) / (u32)sizeof(U);
                 const u32 head = mis ? min(m, V - mis) : 0u;
                 auto R = [&](U x) -> U { return out_raw ? Codec<DT>::raw(x) : x; };
-                if (threadIdx.x < head) out[threadIdx.x] = R(S.k[threadIdx.x]);
+                if (threadIdx.x < head) out[threadIdx.x] = R(Sa.k[threadIdx.x]);
                 const u32 nv = (m - head) / V;
                 uint4* o4 = (uint4*)(out + head);
+                const uint4* s4 = (const uint4*)(Sa.k + head);
                 for (u32 v = threadIdx.x; v < nv; v += BS_NT) {
-                    uint4 r;
+                    uint4 r = s4[v];
                     U* e = (U*)&r;
 #pragma unroll
-                    for (u32 q = 0; q < V; ++q) e[q] = R(S.k[head + v * V + q]);
+                    for (u32 q = 0; q < V; ++q) e[q] = R(e[q]);
                     o4[v] = r;
                 }
-                for (u32 o = head + nv * V + threadIdx.x; o < m; o += BS_NT) out[o] = R(S.k[o]);
+                for (u32 o = head + nv * V + threadIdx.x; o < m; o += BS_NT) out[o] = R(Sa.k[o]);
                 if (KV) {
-                    for (u32 o = threadIdx.x; o < m; o += BS_NT) ovals[bk.beg + o] = S.v[o];
+                    for (u32 o = threadIdx.x; o < m; o += BS_NT) ovals[bk.beg + o] = Sa.v[o];
                     if (oidx)
-                        for (u32 o = threadIdx.x; o < m; o += BS_NT) oidx[bk.beg + o] = S.i[o];
+                        for (u32 o = threadIdx.x; o < m; o += BS_NT) oidx[bk.beg + o] = Sa.i[o];
                 }
             }
             __syncthreads();
@@ -1501,25 +1656,9 @@ __global__ void k_dro_gather(Bufs<U> B, u32 n, u32 p, const u32* bound, const u3
 }
 
 // ------------------------------------------------------------------ multi-GPU building blocks
-// (SURVEY.md §8(e)).  Every rank computes the same global ROS index set over n_global keys;
-// rank r contributes the records of the indices inside its shard [offset, offset + n_local)
-// at their rank in the sorted index set (other slots stay zero, so an all-reduce SUM over the
-// ranks assembles T exactly).  Records: 32-bit keys one word (ord key << 32 | global index),
-// 64-bit keys two words (ord key, global index).
-template <int DT>
-__global__ void k_dist_sample_gather(const u64* sorted, u32 M, const u32* keep, const u32* pos,
-                                     const typename Codec<DT>::U* x, u64 offset, u32 n_local, u64* rec) {
-    const u32 t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= M || !keep[t]) return;
-    const u64 gi = sorted[t] >> 32;
-    if (gi < offset || gi >= offset + n_local) return;
-    const typename Codec<DT>::U k = Codec<DT>::ord(x[gi - offset]);
-    const u32 o = pos[t];
-    if (sizeof(k) == 4) rec[o] = ((u64)k << 32) | gi;
-    else { rec[2 * (u64)o] = (u64)k; rec[2 * (u64)o + 1] = gi; }
-}
-
-// unpack the all-reduced records into the internal sort's arrays
+// (SURVEY.md §8(e)).  Every rank computes the same global ROS index set over n_global keys and
+// contributes the records of its own shard (k_ros_take<DT, true>); after the all-reduce SUM
+// the records are unpacked into the sample sort's arrays.
 __global__ void k_dist_unpack(const u64* rec, u32 m, u32 words, u64* t_pack, u64* t_key, u32* t_tag) {
     const u32 t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= m) return;

@@ -876,21 +876,23 @@ __global__ void __launch_bounds__(NT) k_scatter(Bufs<typename Codec<DT>::U> B, c
 }
 
 // ------------------------------------------------------------------ a7: write-combining scatter
-// Keys-only level-0 scatter.  The sub-tile's keys stay in registers (the next sub-tile is
-// loaded while the current one is processed).  Every bucket owns one 32-byte sector of
-// shared memory holding the keys of its current, incomplete output sector; a sector is
-// written to global memory only when complete, as one 32-byte store, so DRAM never sees a
-// partially written sector (no read-modify-write) and L2 sees one request per 32 bytes.
-// Per sub-tile and bucket b with cursor c0 and n_b new keys (positions [c0, c0+n_b)):
-//   W1: keys of the current sector (until it completes) -> the bucket's shared sector;
-//       keys of complete middle sectors -> global directly (a whole sector per sub-tile);
-//   FL: the completed sector is flushed (partially only at the chunk's first sector for b);
-//   W2: keys past the last complete sector -> the (now empty) shared sector.
-// The chunk's last incomplete sectors are flushed at the end.  Ranks come from shared
-// atomics; positions inside a (chunk, bucket) range are therefore not in input order, which
-// the bucket sorter makes irrelevant (module notes).
+// Keys-only level-0 scatter.  Per chunk and bucket b the chunk's keys of b go to the global
+// positions [r_b, r_b + n_b) (r_b from the histogram scans, so chunks write disjoint,
+// deterministic ranges).  q[b] = the next position to hand out: a shared atomic gives every key
+// its absolute output position.  sb[b] = the 32-byte global sector whose keys are gathered in
+// b's shared sector wc[b] (low 3 bits: the first valid slot, non-zero only for the chunk's first
+// sector of b, whose front belongs to the previous chunk).  A sector goes to global memory only
+// when complete, as one 32-byte store, so DRAM never sees a partially written sector except the
+// (at most two) boundary sectors of every (chunk, bucket) run.
+// Per sub-tile (keys in registers; the next sub-tile's loads are in flight meanwhile):
+//   P1: pos = atomicAdd(q[b], 1); pos inside the current sector -> wc[b][pos - sector]
+//   P2: the key at the sector's last slot flushes wc[b] and moves sb[b] to the sector of the
+//       final q[b]; keys of complete sectors beyond it -> global directly (whole sectors)
+//   P3: keys of the new, incomplete sector -> wc[b]
+// Ranks come from shared atomics: positions inside a (chunk, bucket) run are not in input
+// order, which the bucket sorter makes irrelevant (module notes).
 template <class U> __host__ __device__ constexpr size_t wc_smem_bytes(u32 PS, u32 LS) {
-    return cls_smem_bytes<U>(PS, LS) + 32 * (size_t)PS + 2 * a16(4 * ((size_t)PS + 1)) + a16((PS + 31) / 32 * 4);
+    return cls_smem_bytes<U>(PS, LS) + 32 * (size_t)PS + 2 * a16(4 * ((size_t)PS + 1));
 }
 
 template <int DT, int NT, int ITEMS>
@@ -903,13 +905,12 @@ __global__ void __launch_bounds__(NT, 1) k_scatter_wc(Bufs<typename Codec<DT>::U
     constexpr u32 SV = 32 / sizeof(U);  // keys per 32-byte sector
     constexpr u32 V = 16 / sizeof(U);   // keys per 16-byte vector
     constexpr u32 TS = NT * ITEMS;
-    static_assert(ITEMS % V == 0, "whole vectors per thread");
+    static_assert(ITEMS % V == 0 && ITEMS <= 32, "whole vectors per thread, one mask bit per item");
     extern __shared__ __align__(16) char smem[];
     char* sp = smem + cls_smem_bytes<U>(PS, LS);
     U* wc = (U*)sp; sp += 32 * (size_t)PS;
-    u32* cnt = (u32*)sp; sp += a16(4 * ((size_t)PS + 1));
-    u32* cur = (u32*)sp; sp += a16(4 * ((size_t)PS + 1));
-    u32* headdone = (u32*)sp;  // bit b: the chunk's first (shared) sector of bucket b was flushed
+    u32* q = (u32*)sp; sp += a16(4 * ((size_t)PS + 1));
+    u32* sb = (u32*)sp;
     const u32 nc = *nchunks;
     U* dst = B.k[1];
     const U* src = B.k[0];
@@ -920,26 +921,11 @@ __global__ void __launch_bounds__(NT, 1) k_scatter_wc(Bufs<typename Codec<DT>::U
         const u32 P = sg.P;
         const u32* hrow = hist + (size_t)c * PS;
         const u32* bst = tot_pool + (size_t)ch.seg * (PS + 1);
-        for (u32 b = threadIdx.x; b < P; b += NT) { cur[b] = sg.beg + bst[b] + hrow[b]; cnt[b] = 0; }
-        for (u32 w = threadIdx.x; w < (P + 31) / 32; w += NT) headdone[w] = 0;
-        auto chunk_start = [&](u32 b) -> u32 { return sg.beg + bst[b] + hrow[b]; };
-        // flush the bucket's shared sector covering [s0, s0+SV), valid keys [from, to)
-        auto flush = [&](u32 b, u32 s0, u32 to) {
-            const U* w = wc + (size_t)b * SV;
-            u32 from = s0;
-            if (!(headdone[b >> 5] & (1u << (b & 31)))) {
-                atomicOr(&headdone[b >> 5], 1u << (b & 31));
-                from = max(s0, chunk_start(b));
-            }
-            if (from == s0 && to == s0 + SV) {
-                const uint4* w4 = (const uint4*)w;
-                uint4* g4 = (uint4*)(dst + s0);
-                g4[0] = w4[0];
-                g4[1] = w4[1];
-            } else {
-                for (u32 d = from; d < to; ++d) dst[d] = w[d - s0];
-            }
-        };
+        for (u32 b = threadIdx.x; b < P; b += NT) {
+            const u32 r = sg.beg + bst[b] + hrow[b];
+            q[b] = r;
+            sb[b] = r;  // sector r & ~(SV-1), first valid slot r & (SV-1)
+        }
         __syncthreads();
         const bool vec_ok = ((((uintptr_t)(src + ch.beg)) & 15u) == 0);
         U nk[ITEMS];
@@ -951,7 +937,7 @@ __global__ void __launch_bounds__(NT, 1) k_scatter_wc(Bufs<typename Codec<DT>::U
                     const uint4 r = __ldcs((const uint4*)(src + t0) + jv * NT + threadIdx.x);
                     const U* e = (const U*)&r;
 #pragma unroll
-                    for (u32 q = 0; q < V; ++q) k[jv * V + q] = e[q];
+                    for (u32 x = 0; x < V; ++x) k[jv * V + x] = e[x];
                 }
             } else {
 #pragma unroll
@@ -964,63 +950,64 @@ __global__ void __launch_bounds__(NT, 1) k_scatter_wc(Bufs<typename Codec<DT>::U
         if (ch.beg < ch.end) load(ch.beg, nk);
         for (u32 t0 = ch.beg; t0 < ch.end; t0 += TS) {
             const u32 nt = min(TS, ch.end - t0);
-            const bool full = nt == TS;
             U k[ITEMS];
 #pragma unroll
             for (u32 j = 0; j < ITEMS; ++j) k[j] = nk[j];
             if (t0 + TS < ch.end) load(t0 + TS, nk);  // in flight while this sub-tile is processed
-            u32 bk[ITEMS], rk[ITEMS];
+            u32 bk[ITEMS], pos[ITEMS];
+            u32 valid = 0, inmask = 0, lead = 0;
+            // P1: classify, take a position, park it in the bucket's current sector if it is there
 #pragma unroll
             for (u32 j = 0; j < ITEMS; ++j) {
                 const u32 o = ((j / V) * NT + threadIdx.x) * V + (j % V);
-                if (full || o < nt) {
+                if (o < nt) {
+                    valid |= 1u << j;
                     k[j] = Codec<DT>::ord(k[j]);
-                    bk[j] = classify<U>(cls, k[j], tag_base + t0 + o);
-                    rk[j] = atomicAdd(&cnt[bk[j]], 1u);
+                    const u32 b = classify<U>(cls, k[j], tag_base + t0 + o);
+                    bk[j] = b;
+                    pos[j] = atomicAdd(&q[b], 1u);
+                    const u32 d = pos[j] - (sb[b] & ~(SV - 1));
+                    if (d < SV) {
+                        wc[(size_t)b * SV + d] = k[j];
+                        inmask |= 1u << j;
+                        if (d == SV - 1) lead |= 1u << j;
+                    }
                 }
             }
             __syncthreads();
-            // W1: current-sector keys -> the shared sector, middle-sector keys -> global; tail keys
-            // remember their slot in the sector that follows the last complete one
-            u32 dd[ITEMS];
+            // P2: flush completed sectors; keys of complete sectors past them go straight out
+            u32 tail = 0;
 #pragma unroll
             for (u32 j = 0; j < ITEMS; ++j) {
-                const u32 o = ((j / V) * NT + threadIdx.x) * V + (j % V);
-                dd[j] = 0xffffffffu;
-                if (full || o < nt) {
-                    const u32 b = bk[j], c0 = cur[b], end = c0 + cnt[b];
-                    const u32 d = c0 + rk[j];
-                    const u32 s0 = c0 & ~(SV - 1), e1 = s0 + SV, T = end & ~(SV - 1);
-                    if (end < e1 || d < e1) wc[(size_t)b * SV + (d - s0)] = k[j];  // current sector
-                    else if (d < T) dst[d] = k[j];                                  // complete middle sector
-                    else dd[j] = d - T;                                             // tail (after the flush)
+                const u32 b = bk[j];
+                if (lead & (1u << j)) {
+                    const u32 sv = sb[b], s0 = sv & ~(SV - 1), front = sv & (SV - 1);
+                    const U* w = wc + (size_t)b * SV;
+                    if (front == 0) {
+                        const uint4* w4 = (const uint4*)w;
+                        uint4* g4 = (uint4*)(dst + s0);
+                        g4[0] = w4[0];
+                        g4[1] = w4[1];
+                    } else {
+                        for (u32 x = front; x < SV; ++x) dst[s0 + x] = w[x];
+                    }
+                    sb[b] = q[b] & ~(SV - 1);
+                } else if ((valid & ~inmask) & (1u << j)) {
+                    if (pos[j] < (q[b] & ~(SV - 1))) dst[pos[j]] = k[j];
+                    else tail |= 1u << j;
                 }
             }
             __syncthreads();
-            // FL: the leader (rank 0) of every bucket flushes its completed sector and advances the
-            // cursor (nobody reads cur/cnt again in this sub-tile)
-#pragma unroll
-            for (u32 j = 0; j < ITEMS; ++j) {
-                const u32 o = ((j / V) * NT + threadIdx.x) * V + (j % V);
-                if ((full || o < nt) && rk[j] == 0) {
-                    const u32 b = bk[j], c0 = cur[b], end = c0 + cnt[b];
-                    const u32 s0 = c0 & ~(SV - 1);
-                    if (end >= s0 + SV) flush(b, s0, s0 + SV);
-                    cur[b] = end;
-                    cnt[b] = 0;
-                }
-            }
-            __syncthreads();
-            // W2: tail keys into the emptied sector
+            // P3: keys of the new incomplete sector
 #pragma unroll
             for (u32 j = 0; j < ITEMS; ++j)
-                if (dd[j] != 0xffffffffu) wc[(size_t)bk[j] * SV + dd[j]] = k[j];
+                if (tail & (1u << j)) wc[(size_t)bk[j] * SV + (pos[j] & (SV - 1))] = k[j];
         }
         __syncthreads();
-        // the chunk's last, incomplete sectors
+        // the chunk's last, incomplete sectors (and runs inside one sector)
         for (u32 b = threadIdx.x; b < P; b += NT) {
-            const u32 c1 = cur[b], s0 = c1 & ~(SV - 1);
-            if (c1 > s0) flush(b, s0, c1);
+            const u32 sv = sb[b], s0 = sv & ~(SV - 1), front = sv & (SV - 1), qe = q[b];
+            for (u32 x = front; s0 + x < qe; ++x) dst[s0 + x] = wc[(size_t)b * SV + x];
         }
         __syncthreads();
     }

@@ -129,6 +129,64 @@ __device__ __forceinline__ u32 classify(const ClsView<U>& c, U k, u32 tag) {
     return lo;
 }
 
+// Batched form for N keys held in registers: the table lookups, then three unrolled,
+// predicated binary-search steps (enough for the <= 7 splitter keys a table entry can name),
+// then a loop only for saturated entries (rare).  Separate passes over the N keys keep N
+// independent shared-memory loads in flight instead of one dependent chain per key.
+#ifndef OVS_CLS_MODE
+#define OVS_CLS_MODE 1
+#endif
+template <class U, int N, class TagF>
+__device__ __forceinline__ void classify_n(const ClsView<U>& c, const U (&k)[N], TagF&& tag, u32 (&b)[N]) {
+#if OVS_CLS_MODE == 0
+#pragma unroll
+    for (int j = 0; j < N; ++j) b[j] = classify<U>(c, k[j], tag(j));
+#else
+    if (c.P <= 1) {
+#pragma unroll
+        for (int j = 0; j < N; ++j) b[j] = 0;
+        return;
+    }
+    u32 cnt[N], dd[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+        const U kk = k[j];
+        const U d = (U)(kk - c.base) >> c.shift;
+        const bool below = kk < c.base, above = !below && d >= (U)c.L;
+        dd[j] = (below || above) ? 0xffffffffu : (u32)d;
+        const u32 e = (below || above) ? 0u : c.lut[(u32)d];
+        b[j] = below ? 0u : above ? c.P - 1 : (e & 0x1fffu);
+        cnt[j] = e >> 13;
+    }
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+        if (cnt[j] == 7) cnt[j] = (c.lut[dd[j] + 1] & 0x1fffu) - b[j];  // saturated entry
+#if OVS_CLS_MODE == 2
+#pragma unroll
+    for (int step = 0; step < 3; ++step) {
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            if (cnt[j] > 0) {
+                const u32 half = cnt[j] >> 1, mid = b[j] + half;
+                const U s = c.sk[mid];
+                const bool less = (s < k[j]) || (s == k[j] && c.st[mid] < tag(j));
+                if (less) { b[j] = mid + 1; cnt[j] -= half + 1; } else { cnt[j] = half; }
+            }
+        }
+    }
+#endif
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+        while (cnt[j] > 0) {
+            const u32 half = cnt[j] >> 1, mid = b[j] + half;
+            const U s = c.sk[mid];
+            const bool less = (s < k[j]) || (s == k[j] && c.st[mid] < tag(j));
+            if (less) { b[j] = mid + 1; cnt[j] -= half + 1; } else { cnt[j] = half; }
+        }
+    }
+#endif
+}
+
 // ------------------------------------------------------------------ block helpers
 template <int NT>
 __device__ __forceinline__ u32 block_exclusive_scan(u32 v, u32* red /*[NT/32+1]*/, u32* total) {
@@ -615,8 +673,9 @@ template <int DT, bool KV, bool LEVEL0, int NT>
 __global__ void __launch_bounds__(NT) k_hist(Bufs<typename Codec<DT>::U> B, const Chunk* chunks, const u32* nchunks,
                                              Seg* segs, const typename Codec<DT>::U* sk_pool, const u32* st_pool,
                                              const u16* lut_pool, u32 PS, u32 LS, u32* hist, u32 split,
-                                             u32 tag_base) {
-    // `split` CTAs share a chunk (each a contiguous part) and add into its (zeroed) row
+                                             u32 tag_base, u16* bid) {
+    // `split` CTAs share a chunk (each a contiguous part) and add into its (zeroed) row;
+    // bid != NULL: every key's bucket is also stored (bid[i], the two-level scatter's input)
     typedef typename Codec<DT>::U U;
     extern __shared__ __align__(16) char smem[];
     const u32 nc = *nchunks;
@@ -636,13 +695,67 @@ __global__ void __launch_bounds__(NT) k_hist(Bufs<typename Codec<DT>::U> B, cons
         const U* src = B.k[LEVEL0 ? 0 : sg.src];
         const u32* isrc = (KV && !LEVEL0) ? B.i[sg.src] : nullptr;
         U mn = umax_of<U>(), mx = 0;
+        auto tag_at = [&](u32 o) -> u32 { return (KV && !LEVEL0) ? isrc[pbeg + o] : (LEVEL0 ? tag_base : 0u) + pbeg + o; };
         auto body = [&](U kr, u32 o) {
             const U k = LEVEL0 ? Codec<DT>::ord(kr) : kr;
-            const u32 tg = (KV && !LEVEL0) ? isrc[pbeg + o] : (LEVEL0 ? tag_base : 0u) + pbeg + o;
-            atomicAdd(&h[classify<U>(cls, k, tg)], 1u);
+            const u32 b = classify<U>(cls, k, tag_at(o));
+            atomicAdd(&h[b], 1u);
+            if (bid) bid[pbeg + o] = (u16)b;
             if (LEVEL0) { mn = min(mn, k); mx = max(mx, k); }
         };
-        for_items<U, NT, 4, decltype(body)&, LEVEL0>(src, pbeg, pend - pbeg, body);
+        // misaligned head and the tail one key at a time, the body in batches of UNR vectors
+        constexpr u32 V = 16 / sizeof(U);
+        constexpr int UNR = 4, NB = UNR * (int)V;
+        const u32 m = pend - pbeg;
+        const u32 mis = (u32)(((uintptr_t)(src + pbeg)) & 15u) / (u32)sizeof(U);
+        const u32 head = mis ? min(m, V - mis) : 0u;
+        if (threadIdx.x < head) body(src[pbeg + threadIdx.x], threadIdx.x);
+        const uint4* a4 = (const uint4*)(src + pbeg + head);
+        const u32 nv = (m - head) / V;
+        for (u32 v0 = 0; v0 < nv; v0 += NT * UNR) {
+            U kk[NB];
+            u32 vm = 0;
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const u32 idx = v0 + u * NT + threadIdx.x;
+                uint4 r = make_uint4(0, 0, 0, 0);
+                if (idx < nv) { r = __ldcs(a4 + idx); vm |= ((1u << V) - 1) << (u * V); }
+                const U* e = (const U*)&r;
+#pragma unroll
+                for (u32 x = 0; x < V; ++x) kk[u * V + x] = LEVEL0 ? Codec<DT>::ord(e[x]) : e[x];
+            }
+            u32 bb[NB];
+            classify_n<U, NB>(cls, kk, [&](int j) -> u32 {
+                return tag_at(head + (v0 + (j / V) * NT + threadIdx.x) * V + (j % V));
+            }, bb);
+#pragma unroll
+            for (int j = 0; j < NB; ++j) {
+                if (vm & (1u << j)) {
+                    atomicAdd(&h[bb[j]], 1u);
+                    if (LEVEL0) { mn = min(mn, kk[j]); mx = max(mx, kk[j]); }
+                }
+            }
+            if (bid) {
+                // the V ids of a vector as one 2V-byte store
+                u16* bo = bid + pbeg + head;
+#pragma unroll
+                for (int u = 0; u < UNR; ++u) {
+                    const u32 idx = v0 + u * NT + threadIdx.x;
+                    if (idx < nv) {
+                        if (V == 4) {
+                            uint2 w;
+                            w.x = bb[u * V] | (bb[u * V + 1] << 16);
+                            w.y = bb[u * V + 2] | (bb[u * V + 3] << 16);
+                            if ((((uintptr_t)(bo + idx * V)) & 7u) == 0) *(uint2*)(bo + idx * V) = w;
+                            else for (u32 x = 0; x < V; ++x) bo[idx * V + x] = (u16)bb[u * V + x];
+                        } else {
+                            for (u32 x = 0; x < V; ++x) bo[idx * V + x] = (u16)bb[u * V + x];
+                        }
+                    }
+                }
+            }
+        }
+        for (u32 o = head + nv * V + threadIdx.x; o < m; o += NT) body(src[pbeg + o], o);
         __syncthreads();
         u32* row = hist + (size_t)c * PS;
         if (split == 1) {
@@ -710,7 +823,8 @@ template <class U>
 __global__ void __launch_bounds__(1024) k_segscan(const Seg* segs, const u32* nsegs, u32 PS, u32* tot_pool,
                                                   const U* sk_pool, u32 level, u32 cap, Bucket* fit, u32* nfit,
                                                   u32 fit_cap, Bucket* big, u32* nbig, u32 big_cap, u64* counts_out,
-                                                  u32* status) {
+                                                  u32* status, u32 outbuf = 2) {
+    // outbuf: the buffer the buckets are in (2: the other one than the segment's source)
     __shared__ u32 red[33];
     const u32 ns = *nsegs;
     const u32 lane = threadIdx.x & 31;
@@ -737,7 +851,7 @@ __global__ void __launch_bounds__(1024) k_segscan(const Seg* segs, const u32* ns
             ob = __shfl_sync(0xffffffffu, ob, 0) + __popc(mb & ((1u << lane) - 1));
             if (isfit || isbig) {
                 Bucket bk;
-                bk.beg = sg.beg + st; bk.len = len; bk.buf = 1 - sg.src;
+                bk.beg = sg.beg + st; bk.len = len; bk.buf = outbuf < 2 ? outbuf : 1 - sg.src;
                 bk.level = level | (((b == 0 || b + 1 == sg.P) && sg.loose) ? BK_LOOSE : 0u);
                 bk.lo = (b == 0) ? sg.lo : (u64)sk[b - 1];
                 bk.hi = (b + 1 == sg.P) ? sg.hi : (u64)sk[b];
@@ -955,23 +1069,33 @@ __global__ void __launch_bounds__(NT, 1) k_scatter_wc(Bufs<typename Codec<DT>::U
             for (u32 j = 0; j < ITEMS; ++j) k[j] = nk[j];
             if (t0 + TS < ch.end) load(t0 + TS, nk);  // in flight while this sub-tile is processed
             u32 bk[ITEMS], pos[ITEMS];
-            u32 valid = 0, inmask = 0, lead = 0;
             // P1: classify, take a position, park it in the bucket's current sector if it is there
+            // (separate passes: every pass keeps ITEMS independent shared accesses in flight)
+            const u32 valid = nt == TS ? 0xffffffffu : 0u;
+            u32 vmask = 0;
 #pragma unroll
             for (u32 j = 0; j < ITEMS; ++j) {
+                k[j] = Codec<DT>::ord(k[j]);
                 const u32 o = ((j / V) * NT + threadIdx.x) * V + (j % V);
-                if (o < nt) {
-                    valid |= 1u << j;
-                    k[j] = Codec<DT>::ord(k[j]);
-                    const u32 b = classify<U>(cls, k[j], tag_base + t0 + o);
-                    bk[j] = b;
-                    pos[j] = atomicAdd(&q[b], 1u);
-                    const u32 d = pos[j] - (sb[b] & ~(SV - 1));
-                    if (d < SV) {
-                        wc[(size_t)b * SV + d] = k[j];
-                        inmask |= 1u << j;
-                        if (d == SV - 1) lead |= 1u << j;
-                    }
+                if (valid || o < nt) vmask |= 1u << j;
+            }
+            const u32 tb = tag_base + t0;
+            classify_n<U, ITEMS>(cls, k, [&](int j) -> u32 { return tb + ((j / V) * NT + threadIdx.x) * V + (j % V); },
+                                 bk);
+#pragma unroll
+            for (u32 j = 0; j < ITEMS; ++j)
+                if (vmask & (1u << j)) pos[j] = atomicAdd(&q[bk[j]], 1u);
+            u32 sv[ITEMS];
+#pragma unroll
+            for (u32 j = 0; j < ITEMS; ++j) sv[j] = sb[bk[j]];
+            u32 inmask = 0, lead = 0;
+#pragma unroll
+            for (u32 j = 0; j < ITEMS; ++j) {
+                const u32 d = pos[j] - (sv[j] & ~(SV - 1));
+                if ((vmask & (1u << j)) && d < SV) {
+                    wc[(size_t)bk[j] * SV + d] = k[j];
+                    inmask |= 1u << j;
+                    if (d == SV - 1) lead |= 1u << j;
                 }
             }
             __syncthreads();
@@ -992,7 +1116,7 @@ __global__ void __launch_bounds__(NT, 1) k_scatter_wc(Bufs<typename Codec<DT>::U
                         for (u32 x = front; x < SV; ++x) dst[s0 + x] = w[x];
                     }
                     sb[b] = q[b] & ~(SV - 1);
-                } else if ((valid & ~inmask) & (1u << j)) {
+                } else if ((vmask & ~inmask) & (1u << j)) {
                     if (pos[j] < (q[b] & ~(SV - 1))) dst[pos[j]] = k[j];
                     else tail |= 1u << j;
                 }
@@ -1010,6 +1134,354 @@ __global__ void __launch_bounds__(NT, 1) k_scatter_wc(Bufs<typename Codec<DT>::U
             for (u32 x = front; s0 + x < qe; ++x) dst[s0 + x] = wc[(size_t)b * SV + x];
         }
         __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------ bulk async copies (TMA)
+// 1-D cp.async.bulk global -> shared with mbarrier completion (the Blackwell copy engine; one
+// thread issues a whole tile, the other threads wait on the barrier's phase).
+__device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(u64* bar, u32 count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(u64* bar, u32 bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, u32 bytes, u64* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(u64* bar, u32 parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// ------------------------------------------------------------------ a7: two-level scatter
+// Keys-only level-0 scatter for large p, in two passes over G1 super-buckets of F = 64
+// consecutive buckets.  Pass 1 (k_part1) moves every key of a chunk to its super-bucket
+// (buffer 0 -> 1) together with a byte naming its bucket inside the super-bucket; pass 2
+// (k_part2) moves every (chunk, super-bucket) run to its buckets (buffer 1 -> 0).  Keys land at
+// exactly the positions of a one-pass scatter (bucket start + the chunk's column-scan offset +
+// rank), but every pass has a fan-out of <= 128, so a tile of 8192 keys writes runs of ~64-128
+// consecutive keys (whole sectors), and the kernels need little shared memory (two CTAs per
+// SM).  Tiles are brought into shared memory by bulk async copies, double-buffered: the copy of
+// tile i+1 runs while tile i is ranked and written; after its items are in registers a tile's
+// buffer is reused as its staging area.  Bucket ids come from the histogram pass (u16 per key).
+#ifndef OVS_TP_RANK
+#define OVS_TP_RANK 0
+#endif
+#ifndef OVS_TP_NT
+#define OVS_TP_NT 256
+#endif
+#ifndef OVS_TP_MINB
+#define OVS_TP_MINB 4
+#endif
+constexpr int TP_NT = OVS_TP_NT, TP_ITEMS = 16, TP_TS = TP_NT * TP_ITEMS, TP_F = 64, TP_GMAX = 128;
+
+// Stage one tile (ITEMS keys per thread, group g < NG <= 128, aux byte) in shared memory
+// grouped by g and write every group's keys to dst[base[g] + slot], advancing cur[g].
+// Ranking is warp-private and atomic-free (a fan-out this small makes shared atomics collide on
+// the same counters): for item j the lanes holding the same group are found with log2(NG)
+// ballots, the group's lowest lane advances the warp's counter wcnt[g][warp] and broadcasts the
+// old value.  Then one exclusive scan over (group, warp) gives every warp's slot range inside
+// every group.  Shared state: wcnt[NG * NW], cur[NG], base[NG], off[NG + 1].  The caller has
+// synchronised after its last read of stk / sta / stg.
+template <class U, int NT, int ITEMS, bool AUX>
+__device__ __forceinline__ void tile_scatter(const U (&k)[ITEMS], const u32 (&g)[ITEMS], const uint8_t (&a)[ITEMS], u32 vmask,
+                                             u32 nt, u32 NG, u32* wcnt, u32* cur, int* base, u32* off, U* stk, uint8_t* sta,
+                                             uint8_t* stg, U* dst, uint8_t* dsta, u32* red) {
+    constexpr u32 NW = NT / 32;
+    const u32 lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (u32 x = lane; x < NG; x += 32) wcnt[x * NW + wid] = 0;
+    __syncwarp();
+#if OVS_TP_RANK == 1
+    u32 nbits = 0;
+    while ((1u << nbits) < NG) ++nbits;
+    const u32 lt = (1u << lane) - 1;
+#endif
+    u32 r[ITEMS];
+#if OVS_TP_RANK == 1
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) {
+        const bool valid = (vmask >> j) & 1u;
+        const u32 gj = g[j];
+        u32 m = __ballot_sync(0xffffffffu, valid);
+        for (u32 bb = 0; bb < nbits; ++bb) {
+            const bool bit = (gj >> bb) & 1u;
+            const u32 v = __ballot_sync(0xffffffffu, bit);
+            m &= bit ? v : ~v;
+        }
+        const u32 leader = __ffs(m) - 1;
+        u32 old = 0;
+        if (valid && lane == leader) {
+            old = wcnt[gj * NW + wid];
+            wcnt[gj * NW + wid] = old + __popc(m);
+        }
+        old = __shfl_sync(0xffffffffu, old, valid ? leader : lane);
+        r[j] = old + __popc(m & lt);
+        __syncwarp();
+    }
+#else
+    // warp-private counters, shared atomics (measured: ~6.4 lanes/clk/SM even on 64 counters)
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j)
+        if (vmask & (1u << j)) r[j] = atomicAdd(&wcnt[g[j] * NW + wid], 1u);
+#endif
+    __syncthreads();
+    // exclusive scan over e = g * NW + w (group-major): 4 consecutive entries per thread
+    const u32 ne = NG * NW;
+    for (u32 e0 = 0; e0 < ne; e0 += NT * 4) {
+        const u32 eb = e0 + threadIdx.x * 4;
+        u32 v[4], s = 0;
+#pragma unroll
+        for (int x = 0; x < 4; ++x) { v[x] = eb + x < ne ? wcnt[eb + x] : 0u; s += v[x]; }
+        u32 tot;
+        u32 ex = block_exclusive_scan<NT>(s, red, &tot) + (e0 ? off[NG] : 0u);
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+            if (eb + x < ne) wcnt[eb + x] = ex;
+            ex += v[x];
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) off[NG] = (e0 ? off[NG] : 0u) + tot;
+        __syncthreads();
+    }
+    for (u32 x = threadIdx.x; x < NG; x += NT) {
+        const u32 st = wcnt[x * NW], en = x + 1 < NG ? wcnt[(x + 1) * NW] : off[NG];
+        off[x] = st;
+        base[x] = (int)cur[x] - (int)st;
+        cur[x] += en - st;
+    }
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) {
+        if (vmask & (1u << j)) {
+            const u32 s = wcnt[g[j] * NW + wid] + r[j];
+            stk[s] = k[j];
+            stg[s] = (uint8_t)g[j];
+            if (AUX) sta[s] = a[j];
+        }
+    }
+    __syncthreads();
+    for (u32 s = threadIdx.x; s < nt; s += NT) {
+        const u32 d = (u32)(base[stg[s]] + (int)s);
+        dst[d] = stk[s];
+        if (AUX) dsta[d] = sta[s];
+    }
+}
+
+// shared memory: two tile buffers of TS keys + 2*TS bytes (ids or sub bytes, and staging),
+// each with 64 bytes of alignment slack, plus the scan state
+template <class U> __host__ __device__ constexpr size_t tp_buf_bytes() {
+    return a16((size_t)TP_TS * sizeof(U) + 64) + a16((size_t)TP_TS * 2 + 64);
+}
+template <class U> __host__ __device__ constexpr size_t tp_smem_bytes() {
+    return 2 * tp_buf_bytes<U>() + 4 * (size_t)TP_GMAX * (TP_NT / 32) + 16 * (TP_GMAX + 8) + 4 * 64 + 64;
+}
+
+// pass 1: chunk c of buffer 0 (raw keys) -> super-buckets in buffer 1 (ordered keys) + sub ids
+template <int DT>
+__global__ void __launch_bounds__(TP_NT, OVS_TP_MINB) k_part1(Bufs<typename Codec<DT>::U> B, const u16* bid, uint8_t* sub,
+                                                    const Chunk* chunks, const u32* nchunks, const Seg* segs,
+                                                    const u32* hist, const u32* tot_pool, u32 PS, u32 G1) {
+    typedef typename Codec<DT>::U U;
+    constexpr int IT = TP_ITEMS;
+    extern __shared__ __align__(16) char smem[];
+    char* bufs[2] = {smem, smem + tp_buf_bytes<U>()};
+    u32* cnt = (u32*)(smem + 2 * tp_buf_bytes<U>());  // wcnt: TP_GMAX x warps
+    u32* cur = cnt + TP_GMAX * (TP_NT / 32);
+    int* base = (int*)(cur + TP_GMAX);
+    u32* off = (u32*)(base + TP_GMAX);
+    u32* red = off + TP_GMAX + 8;
+    u64* bar = (u64*)(red + 64);
+    const u32 nc = *nchunks;
+    const U* src = B.k[0];
+    U* dst = B.k[1];
+    if (threadIdx.x == 0) { mbar_init(&bar[0], 1); mbar_init(&bar[1], 1); fence_mbar_init(); }
+    __syncthreads();
+    // the CTA's tiles: chunks blockIdx.x, +gridDim.x, ...; tile t0 steps of TS inside a chunk
+    // (chunks are whole multiples of TS except the last, and 16-byte aligned)
+    auto issue = [&](u32 c, u32 t0, u32 slot) {
+        const Chunk ch = chunks[c];
+        const u32 nt = min((u32)TP_TS, ch.end - t0);
+        // whole 16-byte units of the caller's keys only (the last < 4 keys are read directly)
+        const u32 kb = (nt * (u32)sizeof(U)) & ~15u, ib = (nt * 2 + 15) & ~15u;
+        fence_proxy_async();
+        mbar_expect_tx(&bar[slot], kb + ib);
+        bulk_g2s(bufs[slot], src + t0, kb, &bar[slot]);
+        bulk_g2s(bufs[slot] + a16((size_t)TP_TS * sizeof(U) + 64), bid + t0, ib, &bar[slot]);
+    };
+    u32 c = blockIdx.x, t0 = c < nc ? chunks[c].beg : 0, it = 0;
+    if (threadIdx.x == 0 && c < nc && t0 < chunks[c].end) issue(c, t0, 0);
+    while (c < nc) {
+        const Chunk ch = chunks[c];
+        const Seg sg = segs[ch.seg];
+        if (t0 == ch.beg) {
+            const u32* hrow = hist + (size_t)c * PS;
+            const u32* bst = tot_pool + (size_t)ch.seg * (PS + 1);
+            // cursor of super-bucket g: its start + the chunk's offsets summed over its buckets
+            for (u32 g = threadIdx.x / 32; g < G1; g += TP_NT / 32) {
+                const u32 b0 = g * TP_F, b1 = min(sg.P, b0 + TP_F);
+                u32 s = 0;
+                for (u32 b = b0 + (threadIdx.x & 31); b < b1; b += 32) s += hrow[b];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+                if ((threadIdx.x & 31) == 0) cur[g] = sg.beg + bst[b0] + s;
+            }
+            __syncthreads();
+        }
+        if (t0 >= ch.end) {  // empty chunk (not produced by the engine): move on, keep one copy in flight
+            c += gridDim.x;
+            t0 = c < nc ? chunks[c].beg : 0;
+            if (threadIdx.x == 0 && c < nc && t0 < chunks[c].end) issue(c, t0, it & 1);
+            continue;
+        }
+        const u32 nt = min((u32)TP_TS, ch.end - t0);
+        // next tile of this CTA (possibly in its next chunk) -> the other buffer
+        u32 nc2 = c, nt0 = t0 + TP_TS;
+        if (nt0 >= ch.end) { nc2 = c + gridDim.x; nt0 = nc2 < nc ? chunks[nc2].beg : 0; }
+        const u32 slot = it & 1;
+        if (threadIdx.x == 0 && nc2 < nc && nt0 < chunks[nc2].end) issue(nc2, nt0, slot ^ 1);
+        mbar_wait(&bar[slot], (it >> 1) & 1);
+        const U* rk = (const U*)bufs[slot];
+        const u16* ri = (const u16*)(bufs[slot] + a16((size_t)TP_TS * sizeof(U) + 64));
+        U k[IT];
+        u32 g[IT];
+        uint8_t a[IT];
+        u32 vmask = 0;
+#pragma unroll
+        for (u32 j = 0; j < (u32)IT; ++j) {
+            const u32 o = j * TP_NT + threadIdx.x;
+            g[j] = 0; a[j] = 0; k[j] = 0;
+            if (o < nt) {
+                const u32 id = ri[o];
+                k[j] = Codec<DT>::ord(o < (nt & ~(16u / (u32)sizeof(U) - 1)) ? rk[o] : src[t0 + o]);
+                g[j] = id / TP_F;
+                a[j] = (uint8_t)(id % TP_F);
+                vmask |= 1u << j;
+            }
+        }
+        // the buffer becomes the staging area after everybody has read it (first barrier inside)
+        U* stk = (U*)bufs[slot];
+        uint8_t* sta = (uint8_t*)(bufs[slot] + a16((size_t)TP_TS * sizeof(U) + 64));
+        tile_scatter<U, TP_NT, IT, true>(k, g, a, vmask, nt, G1, cnt, cur, base, off, stk, sta, sta + TP_TS, dst, sub, red);
+        __syncthreads();
+        ++it;
+        c = nc2;
+        t0 = nt0;
+    }
+}
+
+// pass 2: run (c, g) of buffer 1 -> its buckets in buffer 0; work items w = c * G1 + g
+template <class U>
+__global__ void __launch_bounds__(TP_NT, OVS_TP_MINB) k_part2(const U* src, const uint8_t* sub, U* dst, const Seg* segs,
+                                                    const u32* nchunks, const u32* hist, const u32* tot_pool, u32 PS,
+                                                    u32 G1) {
+    constexpr int IT = TP_ITEMS;
+    constexpr u32 KV4 = 16 / sizeof(U);
+    extern __shared__ __align__(16) char smem[];
+    char* bufs[2] = {smem, smem + tp_buf_bytes<U>()};
+    u32* cnt = (u32*)(smem + 2 * tp_buf_bytes<U>());  // wcnt: TP_GMAX x warps
+    u32* cur = cnt + TP_GMAX * (TP_NT / 32);
+    int* base = (int*)(cur + TP_GMAX);
+    u32* off = (u32*)(base + TP_GMAX);
+    u32* red = off + TP_GMAX + 8;
+    u64* bar = (u64*)(red + 64);
+    __shared__ u32 s_beg[2], s_len[2];
+    const u32 nc = *nchunks;
+    const Seg sg = segs[0];
+    const u32* bst = tot_pool;
+    const u32 nw = nc * G1;
+    if (threadIdx.x == 0) { mbar_init(&bar[0], 1); mbar_init(&bar[1], 1); fence_mbar_init(); }
+    // run geometry and cursors of work item w into slot p (warp 0)
+    auto geometry = [&](u32 w, u32 p, bool cursors) {
+        const u32 c = w / G1, g = w % G1;
+        const u32 b0 = g * TP_F, F = min(sg.P, b0 + TP_F) - b0;
+        const u32* hrow = hist + (size_t)c * PS;
+        u32 s = 0, len = 0;
+        for (u32 x = threadIdx.x; x < F; x += 32) {
+            const u32 b = b0 + x, o = hrow[b];
+            const u32 nx = (c + 1 < nc) ? hrow[PS + b] : bst[b + 1] - bst[b];
+            if (cursors) cur[x] = sg.beg + bst[b] + o;
+            s += o;
+            len += nx - o;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            s += __shfl_xor_sync(0xffffffffu, s, o);
+            len += __shfl_xor_sync(0xffffffffu, len, o);
+        }
+        if (threadIdx.x == 0) { s_beg[p] = sg.beg + bst[b0] + s; s_len[p] = len; }
+    };
+    // tile copy: the 16-byte aligned superset of [beg, beg + nt) of keys and of sub bytes
+    auto issue = [&](u32 beg, u32 nt, u32 slot) {
+        const u32 ka = beg & ~(KV4 - 1), ke = (beg + nt + KV4 - 1) & ~(KV4 - 1);
+        const u32 sa = beg & ~15u, se = (beg + nt + 15) & ~15u;
+        fence_proxy_async();
+        mbar_expect_tx(&bar[slot], (ke - ka) * (u32)sizeof(U) + (se - sa));
+        bulk_g2s(bufs[slot], src + ka, (ke - ka) * (u32)sizeof(U), &bar[slot]);
+        bulk_g2s(bufs[slot] + a16((size_t)TP_TS * sizeof(U) + 64), sub + sa, se - sa, &bar[slot]);
+    };
+    u32 w = blockIdx.x, it = 0, p = 0;
+    if (threadIdx.x < 32 && w < nw) geometry(w, 0, false);
+    __syncthreads();
+    u32 t0 = 0;
+    if (threadIdx.x == 0 && w < nw && s_len[0] > 0) issue(s_beg[0], min((u32)TP_TS, s_len[0]), 0);
+    bool fresh = true;
+    while (w < nw) {
+        if (fresh) {
+            if (threadIdx.x < 32) geometry(w, p, true);
+            __syncthreads();
+            fresh = false;
+        }
+        const u32 rb = s_beg[p], rl = s_len[p];
+        if (rl == 0) { w += gridDim.x; p ^= 1; fresh = true; t0 = 0;
+            if (w < nw) { if (threadIdx.x < 32) geometry(w, p, false); __syncthreads();
+                          if (threadIdx.x == 0 && s_len[p] > 0) issue(s_beg[p], min((u32)TP_TS, s_len[p]), it & 1); }
+            continue; }
+        const u32 nt = min((u32)TP_TS, rl - t0);
+        // the next tile: the rest of this run, or the first tile of the next run
+        const u32 slot = it & 1;
+        bool more = t0 + TP_TS < rl;
+        u32 nw2 = w;
+        if (!more) {
+            nw2 = w + gridDim.x;
+            if (nw2 < nw && threadIdx.x < 32) geometry(nw2, p ^ 1, false);
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            if (more) issue(rb + t0 + TP_TS, min((u32)TP_TS, rl - t0 - TP_TS), slot ^ 1);
+            else if (nw2 < nw && s_len[p ^ 1] > 0) issue(s_beg[p ^ 1], min((u32)TP_TS, s_len[p ^ 1]), slot ^ 1);
+        }
+        mbar_wait(&bar[slot], (it >> 1) & 1);
+        const u32 beg = rb + t0;
+        const U* rk = (const U*)bufs[slot] + (beg & (KV4 - 1));
+        const uint8_t* rs = (const uint8_t*)(bufs[slot] + a16((size_t)TP_TS * sizeof(U) + 64)) + (beg & 15u);
+        U k[IT];
+        u32 gg[IT];
+        uint8_t a[IT];
+        u32 vmask = 0;
+#pragma unroll
+        for (u32 j = 0; j < (u32)IT; ++j) {
+            const u32 o = j * TP_NT + threadIdx.x;
+            gg[j] = 0; a[j] = 0; k[j] = 0;
+            if (o < nt) { k[j] = rk[o]; gg[j] = rs[o]; vmask |= 1u << j; }
+        }
+        const u32 F = min(sg.P, (w % G1) * TP_F + TP_F) - (w % G1) * TP_F;
+        U* stk = (U*)bufs[slot];
+        uint8_t* stg = (uint8_t*)(bufs[slot] + a16((size_t)TP_TS * sizeof(U) + 64));
+        tile_scatter<U, TP_NT, IT, false>(k, gg, a, vmask, nt, F, cnt, cur, base, off, stk, nullptr, stg, dst, nullptr, red);
+        __syncthreads();
+        ++it;
+        if (more) t0 += TP_TS;
+        else { w = nw2; p ^= 1; t0 = 0; fresh = true; }
     }
 }
 

@@ -1,0 +1,15 @@
+#!/bin/bash
+# build an experimental variant of libovs.so: tools/build_variant.sh <name> "<nvcc -D flags>"
+# -> tools/variants/libovs_<name>.so (u32 translation unit + api only; enough for the metric sort)
+set -e
+NAME=$1; FLAGS=$2
+D=/root/repo/tools/variants/$NAME; mkdir -p $D
+C=/root/repo/paper_1608_08648_b200/csrc
+ARCH="-gencode arch=compute_100a,code=sm_100a"
+for f in ovs_api ovs_u32 ovs_i32 ovs_f64; do
+  nvcc -O3 -std=c++17 $ARCH -lineinfo -Xcompiler -fPIC -I/root/repo/include $FLAGS -c -o $D/$f.o $C/$f.cu &
+done
+wait
+nvcc $ARCH -shared -o /root/repo/tools/variants/libovs_$NAME.so $D/*.o
+rm -rf $D
+echo built libovs_$NAME.so

@@ -1,0 +1,36 @@
+"""Phase timing of the metric sort for one or more library variants (experiments only):
+python tools/phase_bench.py [lib.so ...]   (default: the in-tree libovs.so)"""
+import statistics, sys
+sys.path.insert(0, ".")
+import numpy as np
+import torch
+import ovs_inputs
+import paper_1608_08648_b200 as ovs
+
+libs = sys.argv[1:] or [None]
+n, p, s = 1 << 27, 4096, 64
+x = torch.from_numpy(ovs_inputs.keys("u32", n, seed=51)).cuda()
+ref = None
+for path in libs:
+    if path:
+        ovs.LIB_PATH = path
+        ovs._lib = None
+    srt = ovs.Sorter(n, torch.uint32, False, "ros", p, s, 1)
+    w = x.clone()
+    srt(w)
+    torch.cuda.synchronize()
+    h = w[:: 1 << 12].cpu().numpy()
+    ok = bool(np.all(np.diff(w.cpu().numpy().astype(np.int64)) >= 0))
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(10)]
+    for k in range(13):
+        w.copy_(x)
+        if k >= 3:
+            ovs.set_phase_events(evs[k - 3])
+        srt(w)
+    ovs.set_phase_events(None)
+    torch.cuda.synchronize()
+    ph = [statistics.median(e[i].elapsed_time(e[i + 1]) for e in evs) for i in range(4)]
+    tot = statistics.median(e[0].elapsed_time(e[4]) for e in evs)
+    print(f"{path or 'libovs.so'}: sorted={ok} total {tot:.3f} ms ({n / tot / 1e6:.1f} Gkeys/s)  "
+          + "  ".join(f"{nm} {v:.3f}" for nm, v in zip(ovs.PHASES, ph)), flush=True)
+    del srt

@@ -99,9 +99,11 @@ template <class U, bool KV> static size_t bucket_smem(u32 cap) {
     return bucket_smem_fixed<U, KV>() + (size_t)cap * bucket_item_bytes<U, KV>();
 }
 
-#ifndef OVS_TP_CPS
-#define OVS_TP_CPS 4u
+#ifndef OVS_WC_NT
+#define OVS_WC_NT 1024
 #endif
+// write-combining scatter: WC_NT threads x WC_ITEMS (u32) keys per sub-tile
+constexpr int WC_NT = OVS_WC_NT, WC_ITEMS = 8192 / OVS_WC_NT;
 // partition tile shape: 512 threads x ITEMS per sub-tile
 constexpr int PT_NT = 512;
 template <class U, bool KV> struct PartItems { static constexpr int v = (sizeof(U) == 4 && !KV) ? 16 : 8; };
@@ -138,7 +140,6 @@ template <int DT, bool KV> struct Engine {
     u32 n;
     u32 cap;
     bool mark_phases = false;  // the contract-level engine records the phase events
-    bool allow_tp = true;      // keys-only two-level scatter (final layout in buffer 0)
     u32 tag_base = 0;          // level-0 tag of item i = tag_base + i (multi-GPU: global index)
     explicit Engine(Ctx& ctx) : c(ctx) {}
 
@@ -147,7 +148,6 @@ template <int DT, bool KV> struct Engine {
         U* sk = nullptr; u32* st = nullptr; u16* lut = nullptr;
         Seg* seg = nullptr; Chunk* chunks = nullptr; u32* nchunks = nullptr;
         u32* hist = nullptr; u32* tot = nullptr; u32* nseg = nullptr;
-        bool tp = false; u16* bid = nullptr; uint8_t* sub = nullptr;  // two-level scatter
     };
     struct Lists {
         Bucket* fit = nullptr; u32* nfit = nullptr; u32* ticket = nullptr; u32 fit_cap = 0;
@@ -181,10 +181,7 @@ template <int DT, bool KV> struct Engine {
         z.log2L = ilog2(z.L);
         // chunks: one per resident CTA slot, whole sub-tiles
         const u32 ts = PT_NT * PartItems<U, KV>::v;
-        // one chunk per SM (fewer concurrently open output lines of the one-pass scatters); the
-        // two-level scatter runs several CTAs per SM, one chunk each
-        const bool tp_ = allow_tp && !KV && P > 256 && cdiv(P, TP_F) <= (u32)TP_GMAX;
-        u32 want = (u32)c.di.sms * (tp_ ? OVS_TP_CPS : 1u);
+        u32 want = (u32)c.di.sms;  // one chunk per SM: fewer concurrently open output lines
         z.chunk = std::max<u32>(ts, cdiv(cdiv(n, want), ts) * ts);
         z.nchunk = std::max<u32>(1, cdiv(n, z.chunk));
         z.sk = c.take<U>(std::max<u32>(P, 1));
@@ -196,8 +193,6 @@ template <int DT, bool KV> struct Engine {
         z.nseg = z.nchunks + 1;
         z.hist = c.take<u32>((size_t)z.nchunk * P);
         z.tot = c.take<u32>(P + 1);
-        z.tp = tp_;
-        if (z.tp) { z.bid = c.take<u16>(n); z.sub = c.take<uint8_t>(n); }
     }
     void carve_lists(Lists& l, u32 P) {
         l.fit_cap = P + 64;
@@ -233,37 +228,24 @@ template <int DT, bool KV> struct Engine {
         set_pair(z.nchunks, z.nchunk, 1);  // device counts: chunks, segments
         fill_u32(c, l.nfit, 0, 2);
         const size_t sm_h = cls_smem_bytes<U>(z.P, z.L) + 4 * (size_t)z.P;
-        // two-level scatter: the bulk copies need the caller's keys 16-byte aligned
-        const bool tp = z.tp && (((uintptr_t)B.k[0]) & 15u) == 0;
-        const u32 hsplit = z.nchunk >= 2 * (u32)c.di.sms ? 1u : 2u;  // >= two 1024-thread CTAs per SM
+        const u32 hsplit = 2;  // two 1024-thread CTAs per chunk
         OVS_CK(cudaMemsetAsync(z.hist, 0, sizeof(u32) * (size_t)z.nchunk * z.P, c.st));
         OVS_CK(cudaFuncSetAttribute(k_hist<DT, KV, true, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_h));
         k_hist<DT, KV, true, 1024><<<z.nchunk * hsplit, 1024, sm_h, c.st>>>(B, z.chunks, z.nchunks, z.seg, z.sk, z.st,
-                                                                           z.lut, z.P, z.L, z.hist, hsplit, tag_base,
-                                                                           tp ? z.bid : nullptr);
+                                                                           z.lut, z.P, z.L, z.hist, hsplit, tag_base);
         c.check();
         k_colscan<<<std::min<u32>(cdiv(z.P, 32), 4 * c.di.sms), 1024, 0, c.st>>>(z.hist, z.seg, z.nseg, z.P, z.tot);
         c.check();
         k_segscan<U><<<1, 1024, 0, c.st>>>(z.seg, z.nseg, z.P, z.tot, z.sk, 0, cap, l.fit, l.nfit, l.fit_cap, nullptr,
-                                          nullptr, 0, counts_out, c.status, tp ? 0u : 2u);
+                                          nullptr, 0, counts_out, c.status);
         c.check();
         if (mark_phases) c.mark(2);
-        if (tp) {
-            const u32 G1 = cdiv(z.P, TP_F);
-            const size_t sm = tp_smem_bytes<U>();
-            OVS_CK(cudaFuncSetAttribute(k_part1<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-            OVS_CK(cudaFuncSetAttribute(k_part2<U>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-            k_part1<DT><<<z.nchunk, TP_NT, sm, c.st>>>(B, z.bid, z.sub, z.chunks, z.nchunks, z.seg, z.hist, z.tot, z.P, G1);
-            c.check();
-            const u32 grid2 = std::min<u32>(z.nchunk * G1, OVS_TP_MINB * (u32)c.di.sms);
-            k_part2<U><<<grid2, TP_NT, sm, c.st>>>(B.k[1], z.sub, B.k[0], z.seg, z.nchunks, z.hist, z.tot, z.P, G1);
-            c.check();
-        } else if (use_wc(z.P, z.L)) {
-            constexpr int IT = 32 / (int)sizeof(U) * 2;  // 16 u32 / 8 u64 keys per thread
+        if (use_wc(z.P, z.L)) {
+            constexpr int IT = WC_ITEMS * 4 / (int)sizeof(U);  // u32: WC_ITEMS keys per thread
             const size_t sm_w = wc_smem_bytes<U>(z.P, z.L);
-            auto kw = k_scatter_wc<DT, PT_NT, IT>;
+            auto kw = k_scatter_wc<DT, WC_NT, IT>;
             OVS_CK(cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_w));
-            kw<<<z.nchunk, PT_NT, sm_w, c.st>>>(B, z.chunks, z.nchunks, z.seg, z.sk, z.st, z.lut, z.P, z.L, z.hist, z.tot,
+            kw<<<z.nchunk, WC_NT, sm_w, c.st>>>(B, z.chunks, z.nchunks, z.seg, z.sk, z.st, z.lut, z.P, z.L, z.hist, z.tot,
                                                 tag_base);
             c.check();
         } else {
@@ -633,7 +615,6 @@ template <int DT, bool KV> struct DistSort {
         words = sizeof(U) == 4 ? 1 : 2;
         counts64 = c.take<u64>(p);
         smp = new RosSampler<DT, true>(c, ng, p, s);
-        e.allow_tp = false;  // the send buffers (buffer 1) receive the buckets
         e.carve_level0(z, p);
         e.carve_lists(l, p);
         // finish side

@@ -673,9 +673,8 @@ template <int DT, bool KV, bool LEVEL0, int NT>
 __global__ void __launch_bounds__(NT) k_hist(Bufs<typename Codec<DT>::U> B, const Chunk* chunks, const u32* nchunks,
                                              Seg* segs, const typename Codec<DT>::U* sk_pool, const u32* st_pool,
                                              const u16* lut_pool, u32 PS, u32 LS, u32* hist, u32 split,
-                                             u32 tag_base, u16* bid) {
-    // `split` CTAs share a chunk (each a contiguous part) and add into its (zeroed) row;
-    // bid != NULL: every key's bucket is also stored (bid[i], the two-level scatter's input)
+                                             u32 tag_base) {
+    // `split` CTAs share a chunk (each a contiguous part) and add into its (zeroed) row
     typedef typename Codec<DT>::U U;
     extern __shared__ __align__(16) char smem[];
     const u32 nc = *nchunks;
@@ -700,7 +699,6 @@ __global__ void __launch_bounds__(NT) k_hist(Bufs<typename Codec<DT>::U> B, cons
             const U k = LEVEL0 ? Codec<DT>::ord(kr) : kr;
             const u32 b = classify<U>(cls, k, tag_at(o));
             atomicAdd(&h[b], 1u);
-            if (bid) bid[pbeg + o] = (u16)b;
             if (LEVEL0) { mn = min(mn, k); mx = max(mx, k); }
         };
         // misaligned head and the tail one key at a time, the body in batches of UNR vectors
@@ -733,25 +731,6 @@ __global__ void __launch_bounds__(NT) k_hist(Bufs<typename Codec<DT>::U> B, cons
                 if (vm & (1u << j)) {
                     atomicAdd(&h[bb[j]], 1u);
                     if (LEVEL0) { mn = min(mn, kk[j]); mx = max(mx, kk[j]); }
-                }
-            }
-            if (bid) {
-                // the V ids of a vector as one 2V-byte store
-                u16* bo = bid + pbeg + head;
-#pragma unroll
-                for (int u = 0; u < UNR; ++u) {
-                    const u32 idx = v0 + u * NT + threadIdx.x;
-                    if (idx < nv) {
-                        if (V == 4) {
-                            uint2 w;
-                            w.x = bb[u * V] | (bb[u * V + 1] << 16);
-                            w.y = bb[u * V + 2] | (bb[u * V + 3] << 16);
-                            if ((((uintptr_t)(bo + idx * V)) & 7u) == 0) *(uint2*)(bo + idx * V) = w;
-                            else for (u32 x = 0; x < V; ++x) bo[idx * V + x] = (u16)bb[u * V + x];
-                        } else {
-                            for (u32 x = 0; x < V; ++x) bo[idx * V + x] = (u16)bb[u * V + x];
-                        }
-                    }
                 }
             }
         }
@@ -1164,327 +1143,6 @@ __device__ __forceinline__ void mbar_wait(u64* bar, u32 parity) {
         : "memory");
 }
 
-// ------------------------------------------------------------------ a7: two-level scatter
-// Keys-only level-0 scatter for large p, in two passes over G1 super-buckets of F = 64
-// consecutive buckets.  Pass 1 (k_part1) moves every key of a chunk to its super-bucket
-// (buffer 0 -> 1) together with a byte naming its bucket inside the super-bucket; pass 2
-// (k_part2) moves every (chunk, super-bucket) run to its buckets (buffer 1 -> 0).  Keys land at
-// exactly the positions of a one-pass scatter (bucket start + the chunk's column-scan offset +
-// rank), but every pass has a fan-out of <= 128, so a tile of 8192 keys writes runs of ~64-128
-// consecutive keys (whole sectors), and the kernels need little shared memory (two CTAs per
-// SM).  Tiles are brought into shared memory by bulk async copies, double-buffered: the copy of
-// tile i+1 runs while tile i is ranked and written; after its items are in registers a tile's
-// buffer is reused as its staging area.  Bucket ids come from the histogram pass (u16 per key).
-#ifndef OVS_TP_RANK
-#define OVS_TP_RANK 0
-#endif
-#ifndef OVS_TP_NT
-#define OVS_TP_NT 256
-#endif
-#ifndef OVS_TP_MINB
-#define OVS_TP_MINB 4
-#endif
-constexpr int TP_NT = OVS_TP_NT, TP_ITEMS = 16, TP_TS = TP_NT * TP_ITEMS, TP_F = 64, TP_GMAX = 128;
-
-// Stage one tile (ITEMS keys per thread, group g < NG <= 128, aux byte) in shared memory
-// grouped by g and write every group's keys to dst[base[g] + slot], advancing cur[g].
-// Ranking is warp-private and atomic-free (a fan-out this small makes shared atomics collide on
-// the same counters): for item j the lanes holding the same group are found with log2(NG)
-// ballots, the group's lowest lane advances the warp's counter wcnt[g][warp] and broadcasts the
-// old value.  Then one exclusive scan over (group, warp) gives every warp's slot range inside
-// every group.  Shared state: wcnt[NG * NW], cur[NG], base[NG], off[NG + 1].  The caller has
-// synchronised after its last read of stk / sta / stg.
-template <class U, int NT, int ITEMS, bool AUX>
-__device__ __forceinline__ void tile_scatter(const U (&k)[ITEMS], const u32 (&g)[ITEMS], const uint8_t (&a)[ITEMS], u32 vmask,
-                                             u32 nt, u32 NG, u32* wcnt, u32* cur, int* base, u32* off, U* stk, uint8_t* sta,
-                                             uint8_t* stg, U* dst, uint8_t* dsta, u32* red) {
-    constexpr u32 NW = NT / 32;
-    const u32 lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (u32 x = lane; x < NG; x += 32) wcnt[x * NW + wid] = 0;
-    __syncwarp();
-#if OVS_TP_RANK == 1
-    u32 nbits = 0;
-    while ((1u << nbits) < NG) ++nbits;
-    const u32 lt = (1u << lane) - 1;
-#endif
-    u32 r[ITEMS];
-#if OVS_TP_RANK == 1
-#pragma unroll
-    for (int j = 0; j < ITEMS; ++j) {
-        const bool valid = (vmask >> j) & 1u;
-        const u32 gj = g[j];
-        u32 m = __ballot_sync(0xffffffffu, valid);
-        for (u32 bb = 0; bb < nbits; ++bb) {
-            const bool bit = (gj >> bb) & 1u;
-            const u32 v = __ballot_sync(0xffffffffu, bit);
-            m &= bit ? v : ~v;
-        }
-        const u32 leader = __ffs(m) - 1;
-        u32 old = 0;
-        if (valid && lane == leader) {
-            old = wcnt[gj * NW + wid];
-            wcnt[gj * NW + wid] = old + __popc(m);
-        }
-        old = __shfl_sync(0xffffffffu, old, valid ? leader : lane);
-        r[j] = old + __popc(m & lt);
-        __syncwarp();
-    }
-#else
-    // warp-private counters, shared atomics (measured: ~6.4 lanes/clk/SM even on 64 counters)
-#pragma unroll
-    for (int j = 0; j < ITEMS; ++j)
-        if (vmask & (1u << j)) r[j] = atomicAdd(&wcnt[g[j] * NW + wid], 1u);
-#endif
-    __syncthreads();
-    // exclusive scan over e = g * NW + w (group-major): 4 consecutive entries per thread
-    const u32 ne = NG * NW;
-    for (u32 e0 = 0; e0 < ne; e0 += NT * 4) {
-        const u32 eb = e0 + threadIdx.x * 4;
-        u32 v[4], s = 0;
-#pragma unroll
-        for (int x = 0; x < 4; ++x) { v[x] = eb + x < ne ? wcnt[eb + x] : 0u; s += v[x]; }
-        u32 tot;
-        u32 ex = block_exclusive_scan<NT>(s, red, &tot) + (e0 ? off[NG] : 0u);
-#pragma unroll
-        for (int x = 0; x < 4; ++x) {
-            if (eb + x < ne) wcnt[eb + x] = ex;
-            ex += v[x];
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) off[NG] = (e0 ? off[NG] : 0u) + tot;
-        __syncthreads();
-    }
-    for (u32 x = threadIdx.x; x < NG; x += NT) {
-        const u32 st = wcnt[x * NW], en = x + 1 < NG ? wcnt[(x + 1) * NW] : off[NG];
-        off[x] = st;
-        base[x] = (int)cur[x] - (int)st;
-        cur[x] += en - st;
-    }
-#pragma unroll
-    for (int j = 0; j < ITEMS; ++j) {
-        if (vmask & (1u << j)) {
-            const u32 s = wcnt[g[j] * NW + wid] + r[j];
-            stk[s] = k[j];
-            stg[s] = (uint8_t)g[j];
-            if (AUX) sta[s] = a[j];
-        }
-    }
-    __syncthreads();
-    for (u32 s = threadIdx.x; s < nt; s += NT) {
-        const u32 d = (u32)(base[stg[s]] + (int)s);
-        dst[d] = stk[s];
-        if (AUX) dsta[d] = sta[s];
-    }
-}
-
-// shared memory: two tile buffers of TS keys + 2*TS bytes (ids or sub bytes, and staging),
-// each with 64 bytes of alignment slack, plus the scan state
-template <class U> __host__ __device__ constexpr size_t tp_buf_bytes() {
-    return a16((size_t)TP_TS * sizeof(U) + 64) + a16((size_t)TP_TS * 2 + 64);
-}
-template <class U> __host__ __device__ constexpr size_t tp_smem_bytes() {
-    return 2 * tp_buf_bytes<U>() + 4 * (size_t)TP_GMAX * (TP_NT / 32) + 16 * (TP_GMAX + 8) + 4 * 64 + 64;
-}
-
-// pass 1: chunk c of buffer 0 (raw keys) -> super-buckets in buffer 1 (ordered keys) + sub ids
-template <int DT>
-__global__ void __launch_bounds__(TP_NT, OVS_TP_MINB) k_part1(Bufs<typename Codec<DT>::U> B, const u16* bid, uint8_t* sub,
-                                                    const Chunk* chunks, const u32* nchunks, const Seg* segs,
-                                                    const u32* hist, const u32* tot_pool, u32 PS, u32 G1) {
-    typedef typename Codec<DT>::U U;
-    constexpr int IT = TP_ITEMS;
-    extern __shared__ __align__(16) char smem[];
-    char* bufs[2] = {smem, smem + tp_buf_bytes<U>()};
-    u32* cnt = (u32*)(smem + 2 * tp_buf_bytes<U>());  // wcnt: TP_GMAX x warps
-    u32* cur = cnt + TP_GMAX * (TP_NT / 32);
-    int* base = (int*)(cur + TP_GMAX);
-    u32* off = (u32*)(base + TP_GMAX);
-    u32* red = off + TP_GMAX + 8;
-    u64* bar = (u64*)(red + 64);
-    const u32 nc = *nchunks;
-    const U* src = B.k[0];
-    U* dst = B.k[1];
-    if (threadIdx.x == 0) { mbar_init(&bar[0], 1); mbar_init(&bar[1], 1); fence_mbar_init(); }
-    __syncthreads();
-    // the CTA's tiles: chunks blockIdx.x, +gridDim.x, ...; tile t0 steps of TS inside a chunk
-    // (chunks are whole multiples of TS except the last, and 16-byte aligned)
-    auto issue = [&](u32 c, u32 t0, u32 slot) {
-        const Chunk ch = chunks[c];
-        const u32 nt = min((u32)TP_TS, ch.end - t0);
-        // whole 16-byte units of the caller's keys only (the last < 4 keys are read directly)
-        const u32 kb = (nt * (u32)sizeof(U)) & ~15u, ib = (nt * 2 + 15) & ~15u;
-        fence_proxy_async();
-        mbar_expect_tx(&bar[slot], kb + ib);
-        bulk_g2s(bufs[slot], src + t0, kb, &bar[slot]);
-        bulk_g2s(bufs[slot] + a16((size_t)TP_TS * sizeof(U) + 64), bid + t0, ib, &bar[slot]);
-    };
-    u32 c = blockIdx.x, t0 = c < nc ? chunks[c].beg : 0, it = 0;
-    if (threadIdx.x == 0 && c < nc && t0 < chunks[c].end) issue(c, t0, 0);
-    while (c < nc) {
-        const Chunk ch = chunks[c];
-        const Seg sg = segs[ch.seg];
-        if (t0 == ch.beg) {
-            const u32* hrow = hist + (size_t)c * PS;
-            const u32* bst = tot_pool + (size_t)ch.seg * (PS + 1);
-            // cursor of super-bucket g: its start + the chunk's offsets summed over its buckets
-            for (u32 g = threadIdx.x / 32; g < G1; g += TP_NT / 32) {
-                const u32 b0 = g * TP_F, b1 = min(sg.P, b0 + TP_F);
-                u32 s = 0;
-                for (u32 b = b0 + (threadIdx.x & 31); b < b1; b += 32) s += hrow[b];
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-                if ((threadIdx.x & 31) == 0) cur[g] = sg.beg + bst[b0] + s;
-            }
-            __syncthreads();
-        }
-        if (t0 >= ch.end) {  // empty chunk (not produced by the engine): move on, keep one copy in flight
-            c += gridDim.x;
-            t0 = c < nc ? chunks[c].beg : 0;
-            if (threadIdx.x == 0 && c < nc && t0 < chunks[c].end) issue(c, t0, it & 1);
-            continue;
-        }
-        const u32 nt = min((u32)TP_TS, ch.end - t0);
-        // next tile of this CTA (possibly in its next chunk) -> the other buffer
-        u32 nc2 = c, nt0 = t0 + TP_TS;
-        if (nt0 >= ch.end) { nc2 = c + gridDim.x; nt0 = nc2 < nc ? chunks[nc2].beg : 0; }
-        const u32 slot = it & 1;
-        if (threadIdx.x == 0 && nc2 < nc && nt0 < chunks[nc2].end) issue(nc2, nt0, slot ^ 1);
-        mbar_wait(&bar[slot], (it >> 1) & 1);
-        const U* rk = (const U*)bufs[slot];
-        const u16* ri = (const u16*)(bufs[slot] + a16((size_t)TP_TS * sizeof(U) + 64));
-        U k[IT];
-        u32 g[IT];
-        uint8_t a[IT];
-        u32 vmask = 0;
-#pragma unroll
-        for (u32 j = 0; j < (u32)IT; ++j) {
-            const u32 o = j * TP_NT + threadIdx.x;
-            g[j] = 0; a[j] = 0; k[j] = 0;
-            if (o < nt) {
-                const u32 id = ri[o];
-                k[j] = Codec<DT>::ord(o < (nt & ~(16u / (u32)sizeof(U) - 1)) ? rk[o] : src[t0 + o]);
-                g[j] = id / TP_F;
-                a[j] = (uint8_t)(id % TP_F);
-                vmask |= 1u << j;
-            }
-        }
-        // the buffer becomes the staging area after everybody has read it (first barrier inside)
-        U* stk = (U*)bufs[slot];
-        uint8_t* sta = (uint8_t*)(bufs[slot] + a16((size_t)TP_TS * sizeof(U) + 64));
-        tile_scatter<U, TP_NT, IT, true>(k, g, a, vmask, nt, G1, cnt, cur, base, off, stk, sta, sta + TP_TS, dst, sub, red);
-        __syncthreads();
-        ++it;
-        c = nc2;
-        t0 = nt0;
-    }
-}
-
-// pass 2: run (c, g) of buffer 1 -> its buckets in buffer 0; work items w = c * G1 + g
-template <class U>
-__global__ void __launch_bounds__(TP_NT, OVS_TP_MINB) k_part2(const U* src, const uint8_t* sub, U* dst, const Seg* segs,
-                                                    const u32* nchunks, const u32* hist, const u32* tot_pool, u32 PS,
-                                                    u32 G1) {
-    constexpr int IT = TP_ITEMS;
-    constexpr u32 KV4 = 16 / sizeof(U);
-    extern __shared__ __align__(16) char smem[];
-    char* bufs[2] = {smem, smem + tp_buf_bytes<U>()};
-    u32* cnt = (u32*)(smem + 2 * tp_buf_bytes<U>());  // wcnt: TP_GMAX x warps
-    u32* cur = cnt + TP_GMAX * (TP_NT / 32);
-    int* base = (int*)(cur + TP_GMAX);
-    u32* off = (u32*)(base + TP_GMAX);
-    u32* red = off + TP_GMAX + 8;
-    u64* bar = (u64*)(red + 64);
-    __shared__ u32 s_beg[2], s_len[2];
-    const u32 nc = *nchunks;
-    const Seg sg = segs[0];
-    const u32* bst = tot_pool;
-    const u32 nw = nc * G1;
-    if (threadIdx.x == 0) { mbar_init(&bar[0], 1); mbar_init(&bar[1], 1); fence_mbar_init(); }
-    // run geometry and cursors of work item w into slot p (warp 0)
-    auto geometry = [&](u32 w, u32 p, bool cursors) {
-        const u32 c = w / G1, g = w % G1;
-        const u32 b0 = g * TP_F, F = min(sg.P, b0 + TP_F) - b0;
-        const u32* hrow = hist + (size_t)c * PS;
-        u32 s = 0, len = 0;
-        for (u32 x = threadIdx.x; x < F; x += 32) {
-            const u32 b = b0 + x, o = hrow[b];
-            const u32 nx = (c + 1 < nc) ? hrow[PS + b] : bst[b + 1] - bst[b];
-            if (cursors) cur[x] = sg.beg + bst[b] + o;
-            s += o;
-            len += nx - o;
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            s += __shfl_xor_sync(0xffffffffu, s, o);
-            len += __shfl_xor_sync(0xffffffffu, len, o);
-        }
-        if (threadIdx.x == 0) { s_beg[p] = sg.beg + bst[b0] + s; s_len[p] = len; }
-    };
-    // tile copy: the 16-byte aligned superset of [beg, beg + nt) of keys and of sub bytes
-    auto issue = [&](u32 beg, u32 nt, u32 slot) {
-        const u32 ka = beg & ~(KV4 - 1), ke = (beg + nt + KV4 - 1) & ~(KV4 - 1);
-        const u32 sa = beg & ~15u, se = (beg + nt + 15) & ~15u;
-        fence_proxy_async();
-        mbar_expect_tx(&bar[slot], (ke - ka) * (u32)sizeof(U) + (se - sa));
-        bulk_g2s(bufs[slot], src + ka, (ke - ka) * (u32)sizeof(U), &bar[slot]);
-        bulk_g2s(bufs[slot] + a16((size_t)TP_TS * sizeof(U) + 64), sub + sa, se - sa, &bar[slot]);
-    };
-    u32 w = blockIdx.x, it = 0, p = 0;
-    if (threadIdx.x < 32 && w < nw) geometry(w, 0, false);
-    __syncthreads();
-    u32 t0 = 0;
-    if (threadIdx.x == 0 && w < nw && s_len[0] > 0) issue(s_beg[0], min((u32)TP_TS, s_len[0]), 0);
-    bool fresh = true;
-    while (w < nw) {
-        if (fresh) {
-            if (threadIdx.x < 32) geometry(w, p, true);
-            __syncthreads();
-            fresh = false;
-        }
-        const u32 rb = s_beg[p], rl = s_len[p];
-        if (rl == 0) { w += gridDim.x; p ^= 1; fresh = true; t0 = 0;
-            if (w < nw) { if (threadIdx.x < 32) geometry(w, p, false); __syncthreads();
-                          if (threadIdx.x == 0 && s_len[p] > 0) issue(s_beg[p], min((u32)TP_TS, s_len[p]), it & 1); }
-            continue; }
-        const u32 nt = min((u32)TP_TS, rl - t0);
-        // the next tile: the rest of this run, or the first tile of the next run
-        const u32 slot = it & 1;
-        bool more = t0 + TP_TS < rl;
-        u32 nw2 = w;
-        if (!more) {
-            nw2 = w + gridDim.x;
-            if (nw2 < nw && threadIdx.x < 32) geometry(nw2, p ^ 1, false);
-            __syncthreads();
-        }
-        if (threadIdx.x == 0) {
-            if (more) issue(rb + t0 + TP_TS, min((u32)TP_TS, rl - t0 - TP_TS), slot ^ 1);
-            else if (nw2 < nw && s_len[p ^ 1] > 0) issue(s_beg[p ^ 1], min((u32)TP_TS, s_len[p ^ 1]), slot ^ 1);
-        }
-        mbar_wait(&bar[slot], (it >> 1) & 1);
-        const u32 beg = rb + t0;
-        const U* rk = (const U*)bufs[slot] + (beg & (KV4 - 1));
-        const uint8_t* rs = (const uint8_t*)(bufs[slot] + a16((size_t)TP_TS * sizeof(U) + 64)) + (beg & 15u);
-        U k[IT];
-        u32 gg[IT];
-        uint8_t a[IT];
-        u32 vmask = 0;
-#pragma unroll
-        for (u32 j = 0; j < (u32)IT; ++j) {
-            const u32 o = j * TP_NT + threadIdx.x;
-            gg[j] = 0; a[j] = 0; k[j] = 0;
-            if (o < nt) { k[j] = rk[o]; gg[j] = rs[o]; vmask |= 1u << j; }
-        }
-        const u32 F = min(sg.P, (w % G1) * TP_F + TP_F) - (w % G1) * TP_F;
-        U* stk = (U*)bufs[slot];
-        uint8_t* stg = (uint8_t*)(bufs[slot] + a16((size_t)TP_TS * sizeof(U) + 64));
-        tile_scatter<U, TP_NT, IT, false>(k, gg, a, vmask, nt, F, cnt, cur, base, off, stk, nullptr, stg, dst, nullptr, red);
-        __syncthreads();
-        ++it;
-        if (more) t0 += TP_TS;
-        else { w = nw2; p ^= 1; t0 = 0; fresh = true; }
-    }
-}
-
 // ------------------------------------------------------------------ internal splitters
 // Splitters of an internal sort of a whole array of n items (not part of the contract; used
 // for p == 1 and for sorting the sample / candidate arrays): a random sample with
@@ -1527,10 +1185,14 @@ __global__ void __launch_bounds__(1024) k_internal_sample(Bufs<typename Codec<DT
 // A bucket over the capacity is re-split by the CTA itself ("sorted ... recursively by this
 // same extended method"): a random sample of it gives <= 64 sub-splitters, the
 // bucket is partitioned into the other buffer and the sub-buckets go on a per-CTA stack.
-constexpr int BS_NT = 512;
+#ifndef OVS_BS_NT
+#define OVS_BS_NT 512
+#endif
+constexpr int BS_NT = OVS_BS_NT;
+constexpr u32 BS_WARPMAX = BS_NT >= 1024 ? 256 : 512;  // largest group a warp sorts in registers
 constexpr int BS_NGMAX = 8192;
 constexpr int BS_BIGMAX = 768;
-constexpr int BS_HUGEMAX = 128;  // groups > 512 items: at most cap/512 exist
+constexpr int BS_HUGEMAX = 256;  // groups > BS_WARPMAX items: at most cap/BS_WARPMAX exist
 constexpr int BS_STACK = 256;
 constexpr u32 BS_SPMAX = 64;
 constexpr u32 BS_SI = 32;
@@ -1924,7 +1586,7 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                 else if (len <= 64) warp_sort_group<U, KV, 2>(Sa, gs, len);
                 else if (len <= 128) warp_sort_group<U, KV, 4>(Sa, gs, len);
                 else if (len <= 256) warp_sort_group<U, KV, 8>(Sa, gs, len);
-                else if (len <= 512) warp_sort_group<U, KV, 16>(Sa, gs, len);
+                else if (len <= 512 && BS_WARPMAX >= 512) warp_sort_group<U, KV, BS_WARPMAX / 32>(Sa, gs, len);
                 else if (lane == 0) {
                     const u32 h = atomicAdd(&s_nhuge, 1u);
                     if (h < BS_HUGEMAX) s_huge[h] = g;
@@ -1932,7 +1594,7 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                 }
             }
             __syncthreads();
-            // 3c. groups over 512: in-place bitonic network in shared memory, all comparators
+            // 3c. groups over BS_WARPMAX: in-place bitonic network in shared memory, all comparators
             // ascending (the first step of each merge compares i with its mirror), so virtual
             // +inf padding beyond len never moves and len need not be a power of two
             const u32 nhuge = min(s_nhuge, (u32)BS_HUGEMAX);

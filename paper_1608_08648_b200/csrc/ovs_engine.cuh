@@ -99,6 +99,9 @@ template <class U, bool KV> static size_t bucket_smem(u32 cap) {
     return bucket_smem_fixed<U, KV>() + (size_t)cap * bucket_item_bytes<U, KV>();
 }
 
+#ifndef OVS_WC_IDS
+#define OVS_WC_IDS 1
+#endif
 #ifndef OVS_WC_NT
 #define OVS_WC_NT 1024
 #endif
@@ -148,6 +151,7 @@ template <int DT, bool KV> struct Engine {
         U* sk = nullptr; u32* st = nullptr; u16* lut = nullptr;
         Seg* seg = nullptr; Chunk* chunks = nullptr; u32* nchunks = nullptr;
         u32* hist = nullptr; u32* tot = nullptr; u32* nseg = nullptr;
+        u16* bid = nullptr;  // keys-only: bucket ids from the histogram pass (OVS_WC_IDS)
     };
     struct Lists {
         Bucket* fit = nullptr; u32* nfit = nullptr; u32* ticket = nullptr; u32 fit_cap = 0;
@@ -193,6 +197,7 @@ template <int DT, bool KV> struct Engine {
         z.nseg = z.nchunks + 1;
         z.hist = c.take<u32>((size_t)z.nchunk * P);
         z.tot = c.take<u32>(P + 1);
+        if (OVS_WC_IDS && !KV && P > 1) z.bid = c.take<u16>(n);
     }
     void carve_lists(Lists& l, u32 P) {
         l.fit_cap = P + 64;
@@ -232,7 +237,8 @@ template <int DT, bool KV> struct Engine {
         OVS_CK(cudaMemsetAsync(z.hist, 0, sizeof(u32) * (size_t)z.nchunk * z.P, c.st));
         OVS_CK(cudaFuncSetAttribute(k_hist<DT, KV, true, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_h));
         k_hist<DT, KV, true, 1024><<<z.nchunk * hsplit, 1024, sm_h, c.st>>>(B, z.chunks, z.nchunks, z.seg, z.sk, z.st,
-                                                                           z.lut, z.P, z.L, z.hist, hsplit, tag_base);
+                                                                           z.lut, z.P, z.L, z.hist, hsplit, tag_base,
+                                                                           use_wc(z.P, z.L) ? z.bid : nullptr);
         c.check();
         k_colscan<<<std::min<u32>(cdiv(z.P, 32), 4 * c.di.sms), 1024, 0, c.st>>>(z.hist, z.seg, z.nseg, z.P, z.tot);
         c.check();
@@ -246,7 +252,7 @@ template <int DT, bool KV> struct Engine {
             auto kw = k_scatter_wc<DT, WC_NT, IT>;
             OVS_CK(cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_w));
             kw<<<z.nchunk, WC_NT, sm_w, c.st>>>(B, z.chunks, z.nchunks, z.seg, z.sk, z.st, z.lut, z.P, z.L, z.hist, z.tot,
-                                                tag_base);
+                                                tag_base, z.bid);
             c.check();
         } else {
             constexpr int IT = PartItems<U, KV>::v;

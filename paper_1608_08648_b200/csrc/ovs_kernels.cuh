@@ -673,8 +673,9 @@ template <int DT, bool KV, bool LEVEL0, int NT>
 __global__ void __launch_bounds__(NT) k_hist(Bufs<typename Codec<DT>::U> B, const Chunk* chunks, const u32* nchunks,
                                              Seg* segs, const typename Codec<DT>::U* sk_pool, const u32* st_pool,
                                              const u16* lut_pool, u32 PS, u32 LS, u32* hist, u32 split,
-                                             u32 tag_base) {
-    // `split` CTAs share a chunk (each a contiguous part) and add into its (zeroed) row
+                                             u32 tag_base, u16* bid) {
+    // `split` CTAs share a chunk (each a contiguous part) and add into its (zeroed) row;
+    // bid != NULL: every key's bucket is also stored (bid[i]: the scatter then skips classify)
     typedef typename Codec<DT>::U U;
     extern __shared__ __align__(16) char smem[];
     const u32 nc = *nchunks;
@@ -699,6 +700,7 @@ __global__ void __launch_bounds__(NT) k_hist(Bufs<typename Codec<DT>::U> B, cons
             const U k = LEVEL0 ? Codec<DT>::ord(kr) : kr;
             const u32 b = classify<U>(cls, k, tag_at(o));
             atomicAdd(&h[b], 1u);
+            if (bid) bid[pbeg + o] = (u16)b;
             if (LEVEL0) { mn = min(mn, k); mx = max(mx, k); }
         };
         // misaligned head and the tail one key at a time, the body in batches of UNR vectors
@@ -731,6 +733,25 @@ __global__ void __launch_bounds__(NT) k_hist(Bufs<typename Codec<DT>::U> B, cons
                 if (vm & (1u << j)) {
                     atomicAdd(&h[bb[j]], 1u);
                     if (LEVEL0) { mn = min(mn, kk[j]); mx = max(mx, kk[j]); }
+                }
+            }
+            if (bid) {
+                // the V ids of a vector as one 2V-byte store
+                u16* bo = bid + pbeg + head;
+#pragma unroll
+                for (int u = 0; u < UNR; ++u) {
+                    const u32 idx = v0 + u * NT + threadIdx.x;
+                    if (idx < nv) {
+                        if (V == 4 && (((uintptr_t)(bo + idx * V)) & 7u) == 0) {
+                            uint2 w;
+                            w.x = bb[u * V] | (bb[u * V + 1] << 16);
+                            w.y = bb[u * V + 2 % V] | (bb[u * V + 3 % V] << 16);
+                            *(uint2*)(bo + idx * V) = w;
+                        } else {
+#pragma unroll
+                            for (u32 x = 0; x < V; ++x) bo[idx * V + x] = (u16)bb[u * V + x];
+                        }
+                    }
                 }
             }
         }
@@ -993,7 +1014,8 @@ __global__ void __launch_bounds__(NT, 1) k_scatter_wc(Bufs<typename Codec<DT>::U
                                                        const u32* nchunks, const Seg* segs,
                                                        const typename Codec<DT>::U* sk_pool, const u32* st_pool,
                                                        const u16* lut_pool, u32 PS, u32 LS, const u32* hist,
-                                                       const u32* tot_pool, u32 tag_base) {
+                                                       const u32* tot_pool, u32 tag_base, const u16* bid) {
+    // bid != NULL: the buckets come from the histogram pass (no classification here)
     typedef typename Codec<DT>::U U;
     constexpr u32 SV = 32 / sizeof(U);  // keys per 32-byte sector
     constexpr u32 V = 16 / sizeof(U);   // keys per 16-byte vector
@@ -1010,7 +1032,7 @@ __global__ void __launch_bounds__(NT, 1) k_scatter_wc(Bufs<typename Codec<DT>::U
     for (u32 c = blockIdx.x; c < nc; c += gridDim.x) {
         const Chunk ch = chunks[c];
         const Seg sg = segs[ch.seg];
-        ClsView<U> cls = load_cls<U>(smem, sg, ch.seg, sk_pool, st_pool, lut_pool, PS, LS, true);
+        ClsView<U> cls = load_cls<U>(smem, sg, ch.seg, sk_pool, st_pool, lut_pool, PS, LS, bid == nullptr);
         const u32 P = sg.P;
         const u32* hrow = hist + (size_t)c * PS;
         const u32* bst = tot_pool + (size_t)ch.seg * (PS + 1);
@@ -1020,9 +1042,10 @@ __global__ void __launch_bounds__(NT, 1) k_scatter_wc(Bufs<typename Codec<DT>::U
             sb[b] = r;  // sector r & ~(SV-1), first valid slot r & (SV-1)
         }
         __syncthreads();
-        const bool vec_ok = ((((uintptr_t)(src + ch.beg)) & 15u) == 0);
+        const bool vec_ok = ((((uintptr_t)(src + ch.beg)) & 15u) == 0) && (!bid || (((uintptr_t)(bid + ch.beg)) & 7u) == 0);
         U nk[ITEMS];
-        auto load = [&](u32 t0, U (&k)[ITEMS]) {
+        u32 nid[(ITEMS + 1) / 2];  // two u16 bucket ids per word
+        auto load = [&](u32 t0, U (&k)[ITEMS], u32 (&id)[(ITEMS + 1) / 2]) {
             const u32 nt = min(TS, ch.end - t0);
             if (vec_ok && nt == TS) {
 #pragma unroll
@@ -1031,22 +1054,38 @@ __global__ void __launch_bounds__(NT, 1) k_scatter_wc(Bufs<typename Codec<DT>::U
                     const U* e = (const U*)&r;
 #pragma unroll
                     for (u32 x = 0; x < V; ++x) k[jv * V + x] = e[x];
+                    if (bid) {
+                        if (V == 4) {
+                            const uint2 w = __ldcs((const uint2*)(bid + t0) + jv * NT + threadIdx.x);
+                            id[jv * 2] = w.x;
+                            id[(jv * 2 + 1) % ((ITEMS + 1) / 2)] = w.y;
+                        } else {
+                            id[jv] = __ldcs((const unsigned int*)(bid + t0) + jv * NT + threadIdx.x);
+                        }
+                    }
                 }
             } else {
 #pragma unroll
                 for (u32 j = 0; j < ITEMS; ++j) {
                     const u32 o = ((j / V) * NT + threadIdx.x) * V + (j % V);
                     k[j] = o < nt ? src[t0 + o] : (U)0;
+                    if (bid) {
+                        const u32 v = o < nt ? (u32)bid[t0 + o] : 0u;
+                        if (j & 1) id[j / 2] |= v << 16; else id[j / 2] = v;
+                    }
                 }
             }
         };
-        if (ch.beg < ch.end) load(ch.beg, nk);
+        if (ch.beg < ch.end) load(ch.beg, nk, nid);
         for (u32 t0 = ch.beg; t0 < ch.end; t0 += TS) {
             const u32 nt = min(TS, ch.end - t0);
             U k[ITEMS];
+            u32 id[(ITEMS + 1) / 2];
 #pragma unroll
             for (u32 j = 0; j < ITEMS; ++j) k[j] = nk[j];
-            if (t0 + TS < ch.end) load(t0 + TS, nk);  // in flight while this sub-tile is processed
+#pragma unroll
+            for (u32 j = 0; j < (ITEMS + 1) / 2; ++j) id[j] = nid[j];
+            if (t0 + TS < ch.end) load(t0 + TS, nk, nid);  // in flight while this sub-tile is processed
             u32 bk[ITEMS], pos[ITEMS];
             // P1: classify, take a position, park it in the bucket's current sector if it is there
             // (separate passes: every pass keeps ITEMS independent shared accesses in flight)
@@ -1059,8 +1098,13 @@ __global__ void __launch_bounds__(NT, 1) k_scatter_wc(Bufs<typename Codec<DT>::U
                 if (valid || o < nt) vmask |= 1u << j;
             }
             const u32 tb = tag_base + t0;
-            classify_n<U, ITEMS>(cls, k, [&](int j) -> u32 { return tb + ((j / V) * NT + threadIdx.x) * V + (j % V); },
-                                 bk);
+            if (bid) {
+#pragma unroll
+                for (u32 j = 0; j < ITEMS; ++j) bk[j] = (id[j / 2] >> (16 * (j & 1))) & 0xffffu;
+            } else {
+                classify_n<U, ITEMS>(cls, k, [&](int j) -> u32 { return tb + ((j / V) * NT + threadIdx.x) * V + (j % V); },
+                                     bk);
+            }
 #pragma unroll
             for (u32 j = 0; j < ITEMS; ++j)
                 if (vmask & (1u << j)) pos[j] = atomicAdd(&q[bk[j]], 1u);

@@ -99,9 +99,6 @@ template <class U, bool KV> static size_t bucket_smem(u32 cap) {
     return bucket_smem_fixed<U, KV>() + (size_t)cap * bucket_item_bytes<U, KV>();
 }
 
-#ifndef OVS_WC_IDS
-#define OVS_WC_IDS 1
-#endif
 #ifndef OVS_WC_NT
 #define OVS_WC_NT 1024
 #endif
@@ -160,7 +157,7 @@ template <int DT, bool KV> struct Engine {
 
     // keys-only sorts use the write-combining scatter when its shared memory fits
     bool use_wc(u32 P, u32 L) const {
-        return !KV && P > 1 && wc_smem_bytes<U>(P, L) + 512 <= (size_t)c.di.smem_optin;
+        return !KV && P > 1 && wc_smem_bytes<U>(P) + 512 <= (size_t)c.di.smem_optin;
     }
     static size_t scatter_smem(u32 P, u32 L) {
         return scatter_smem_bytes<U, KV, PartItems<U, KV>::v, PT_NT>(P, L);
@@ -179,9 +176,6 @@ template <int DT, bool KV> struct Engine {
     void carve_level0(Level0& z, u32 P) {
         z.P = P;
         z.L = P > 1 ? std::min<u32>(16384, std::max<u32>(64, pow2_at_least(4 * P))) : 1;
-        // keys-only: shrink the table until the write-combining scatter fits shared memory
-        if (!KV && P > 1)
-            while (z.L > 64 && wc_smem_bytes<U>(P, z.L) + 512 > (size_t)c.di.smem_optin) z.L >>= 1;
         z.log2L = ilog2(z.L);
         // chunks: one per resident CTA slot, whole sub-tiles
         const u32 ts = PT_NT * PartItems<U, KV>::v;
@@ -197,7 +191,7 @@ template <int DT, bool KV> struct Engine {
         z.nseg = z.nchunks + 1;
         z.hist = c.take<u32>((size_t)z.nchunk * P);
         z.tot = c.take<u32>(P + 1);
-        if (OVS_WC_IDS && !KV && P > 1) z.bid = c.take<u16>(n);
+        if (!KV && P > 1) z.bid = c.take<u16>(n);
     }
     void carve_lists(Lists& l, u32 P) {
         l.fit_cap = P + 64;
@@ -248,11 +242,10 @@ template <int DT, bool KV> struct Engine {
         if (mark_phases) c.mark(2);
         if (use_wc(z.P, z.L)) {
             constexpr int IT = WC_ITEMS * 4 / (int)sizeof(U);  // u32: WC_ITEMS keys per thread
-            const size_t sm_w = wc_smem_bytes<U>(z.P, z.L);
+            const size_t sm_w = wc_smem_bytes<U>(z.P);
             auto kw = k_scatter_wc<DT, WC_NT, IT>;
             OVS_CK(cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_w));
-            kw<<<z.nchunk, WC_NT, sm_w, c.st>>>(B, z.chunks, z.nchunks, z.seg, z.sk, z.st, z.lut, z.P, z.L, z.hist, z.tot,
-                                                tag_base, z.bid);
+            kw<<<z.nchunk, WC_NT, sm_w, c.st>>>(B, z.chunks, z.nchunks, z.seg, z.P, z.hist, z.tot, z.bid);
             c.check();
         } else {
             constexpr int IT = PartItems<U, KV>::v;

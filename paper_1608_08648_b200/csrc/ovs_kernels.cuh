@@ -990,13 +990,16 @@ __global__ void __launch_bounds__(NT) k_scatter(Bufs<typename Codec<DT>::U> B, c
 }
 
 // ------------------------------------------------------------------ a7: write-combining scatter
-// Keys-only level-0 scatter.  Per chunk and bucket b the chunk's keys of b go to the global
-// positions [r_b, r_b + n_b) (r_b from the histogram scans, so chunks write disjoint,
-// deterministic ranges).  q[b] = the next position to hand out: a shared atomic gives every key
-// its absolute output position.  sb[b] = the 32-byte global sector whose keys are gathered in
-// b's shared sector wc[b] (low 3 bits: the first valid slot, non-zero only for the chunk's first
-// sector of b, whose front belongs to the previous chunk).  A sector goes to global memory only
-// when complete, as one 32-byte store, so DRAM never sees a partially written sector except the
+// Keys-only level-0 scatter, driven by the bucket ids the histogram pass stored (bid[i]).  Per
+// chunk and bucket b the chunk's keys of b go to the global positions [r_b, r_b + n_b) (r_b
+// from the histogram scans, so chunks write disjoint, deterministic ranges).  q[b] = the next
+// position to hand out (a shared atomic gives every key its absolute output position); sb[b] =
+// the 32-byte global sector whose keys are gathered in b's shared sector wc[b] (low 3 bits: the
+// first valid slot, non-zero only for the chunk's first sector of b, whose front belongs to the
+// previous chunk).  (Packing q and sb into one 64-bit word for a single atomic measured 1.7x
+// slower: 64-bit shared atomics are not native-speed.)  A sector goes to global memory only when complete, as one 32-byte store, so
+// DRAM never sees a partially written sector (measured on B200: partial-sector stores cost a
+// DRAM read-modify-write even when the rest of the sector follows microseconds later) except the
 // (at most two) boundary sectors of every (chunk, bucket) run.
 // Per sub-tile (keys in registers; the next sub-tile's loads are in flight meanwhile):
 //   P1: pos = atomicAdd(q[b], 1); pos inside the current sector -> wc[b][pos - sector]
@@ -1005,34 +1008,30 @@ __global__ void __launch_bounds__(NT) k_scatter(Bufs<typename Codec<DT>::U> B, c
 //   P3: keys of the new, incomplete sector -> wc[b]
 // Ranks come from shared atomics: positions inside a (chunk, bucket) run are not in input
 // order, which the bucket sorter makes irrelevant (module notes).
-template <class U> __host__ __device__ constexpr size_t wc_smem_bytes(u32 PS, u32 LS) {
-    return cls_smem_bytes<U>(PS, LS) + 32 * (size_t)PS + 2 * a16(4 * ((size_t)PS + 1));
+template <class U> __host__ __device__ constexpr size_t wc_smem_bytes(u32 PS) {
+    return 32 * (size_t)PS + 8 * (size_t)PS;  // wc, q, sb
 }
 
 template <int DT, int NT, int ITEMS>
 __global__ void __launch_bounds__(NT, 1) k_scatter_wc(Bufs<typename Codec<DT>::U> B, const Chunk* chunks,
-                                                       const u32* nchunks, const Seg* segs,
-                                                       const typename Codec<DT>::U* sk_pool, const u32* st_pool,
-                                                       const u16* lut_pool, u32 PS, u32 LS, const u32* hist,
-                                                       const u32* tot_pool, u32 tag_base, const u16* bid) {
-    // bid != NULL: the buckets come from the histogram pass (no classification here)
+                                                       const u32* nchunks, const Seg* segs, u32 PS, const u32* hist,
+                                                       const u32* tot_pool, const u16* bid) {
     typedef typename Codec<DT>::U U;
     constexpr u32 SV = 32 / sizeof(U);  // keys per 32-byte sector
     constexpr u32 V = 16 / sizeof(U);   // keys per 16-byte vector
     constexpr u32 TS = NT * ITEMS;
+    constexpr u32 NI = (ITEMS + 1) / 2;  // two u16 bucket ids per word
     static_assert(ITEMS % V == 0 && ITEMS <= 32, "whole vectors per thread, one mask bit per item");
     extern __shared__ __align__(16) char smem[];
-    char* sp = smem + cls_smem_bytes<U>(PS, LS);
-    U* wc = (U*)sp; sp += 32 * (size_t)PS;
-    u32* q = (u32*)sp; sp += a16(4 * ((size_t)PS + 1));
-    u32* sb = (u32*)sp;
+    U* wc = (U*)smem;
+    u32* q = (u32*)(smem + 32 * (size_t)PS);
+    u32* sb = q + PS;
     const u32 nc = *nchunks;
     U* dst = B.k[1];
     const U* src = B.k[0];
     for (u32 c = blockIdx.x; c < nc; c += gridDim.x) {
         const Chunk ch = chunks[c];
         const Seg sg = segs[ch.seg];
-        ClsView<U> cls = load_cls<U>(smem, sg, ch.seg, sk_pool, st_pool, lut_pool, PS, LS, bid == nullptr);
         const u32 P = sg.P;
         const u32* hrow = hist + (size_t)c * PS;
         const u32* bst = tot_pool + (size_t)ch.seg * (PS + 1);
@@ -1042,10 +1041,10 @@ __global__ void __launch_bounds__(NT, 1) k_scatter_wc(Bufs<typename Codec<DT>::U
             sb[b] = r;  // sector r & ~(SV-1), first valid slot r & (SV-1)
         }
         __syncthreads();
-        const bool vec_ok = ((((uintptr_t)(src + ch.beg)) & 15u) == 0) && (!bid || (((uintptr_t)(bid + ch.beg)) & 7u) == 0);
+        const bool vec_ok = ((((uintptr_t)(src + ch.beg)) & 15u) == 0) && ((((uintptr_t)(bid + ch.beg)) & 7u) == 0);
         U nk[ITEMS];
-        u32 nid[(ITEMS + 1) / 2];  // two u16 bucket ids per word
-        auto load = [&](u32 t0, U (&k)[ITEMS], u32 (&id)[(ITEMS + 1) / 2]) {
+        u32 nid[NI];
+        auto load = [&](u32 t0, U (&k)[ITEMS], u32 (&id)[NI]) {
             const u32 nt = min(TS, ch.end - t0);
             if (vec_ok && nt == TS) {
 #pragma unroll
@@ -1054,14 +1053,12 @@ __global__ void __launch_bounds__(NT, 1) k_scatter_wc(Bufs<typename Codec<DT>::U
                     const U* e = (const U*)&r;
 #pragma unroll
                     for (u32 x = 0; x < V; ++x) k[jv * V + x] = e[x];
-                    if (bid) {
-                        if (V == 4) {
-                            const uint2 w = __ldcs((const uint2*)(bid + t0) + jv * NT + threadIdx.x);
-                            id[jv * 2] = w.x;
-                            id[(jv * 2 + 1) % ((ITEMS + 1) / 2)] = w.y;
-                        } else {
-                            id[jv] = __ldcs((const unsigned int*)(bid + t0) + jv * NT + threadIdx.x);
-                        }
+                    if (V == 4) {
+                        const uint2 w = __ldcs((const uint2*)(bid + t0) + jv * NT + threadIdx.x);
+                        id[jv * 2] = w.x;
+                        id[(jv * 2 + 1) % NI] = w.y;
+                    } else {
+                        id[jv] = __ldcs((const unsigned int*)(bid + t0) + jv * NT + threadIdx.x);
                     }
                 }
             } else {
@@ -1069,10 +1066,8 @@ __global__ void __launch_bounds__(NT, 1) k_scatter_wc(Bufs<typename Codec<DT>::U
                 for (u32 j = 0; j < ITEMS; ++j) {
                     const u32 o = ((j / V) * NT + threadIdx.x) * V + (j % V);
                     k[j] = o < nt ? src[t0 + o] : (U)0;
-                    if (bid) {
-                        const u32 v = o < nt ? (u32)bid[t0 + o] : 0u;
-                        if (j & 1) id[j / 2] |= v << 16; else id[j / 2] = v;
-                    }
+                    const u32 v = o < nt ? (u32)bid[t0 + o] : 0u;
+                    if (j & 1) id[j / 2] |= v << 16; else id[j / 2] = v;
                 }
             }
         };
@@ -1080,45 +1075,33 @@ __global__ void __launch_bounds__(NT, 1) k_scatter_wc(Bufs<typename Codec<DT>::U
         for (u32 t0 = ch.beg; t0 < ch.end; t0 += TS) {
             const u32 nt = min(TS, ch.end - t0);
             U k[ITEMS];
-            u32 id[(ITEMS + 1) / 2];
+            u32 id[NI];
 #pragma unroll
             for (u32 j = 0; j < ITEMS; ++j) k[j] = nk[j];
 #pragma unroll
-            for (u32 j = 0; j < (ITEMS + 1) / 2; ++j) id[j] = nid[j];
+            for (u32 j = 0; j < NI; ++j) id[j] = nid[j];
             if (t0 + TS < ch.end) load(t0 + TS, nk, nid);  // in flight while this sub-tile is processed
-            u32 bk[ITEMS], pos[ITEMS];
-            // P1: classify, take a position, park it in the bucket's current sector if it is there
-            // (separate passes: every pass keeps ITEMS independent shared accesses in flight)
-            const u32 valid = nt == TS ? 0xffffffffu : 0u;
-            u32 vmask = 0;
+            u32 vmask = 0xffffffffu;
+            if (nt < TS) {
+                vmask = 0;
+#pragma unroll
+                for (u32 j = 0; j < ITEMS; ++j)
+                    if (((j / V) * NT + threadIdx.x) * V + (j % V) < nt) vmask |= 1u << j;
+            }
+            // P1: a position and the current sector per key; park it there if it is inside
+            u32 pos[ITEMS], inmask = 0, lead = 0;
 #pragma unroll
             for (u32 j = 0; j < ITEMS; ++j) {
+                const u32 b = (id[j / 2] >> (16 * (j & 1))) & 0xffffu;
                 k[j] = Codec<DT>::ord(k[j]);
-                const u32 o = ((j / V) * NT + threadIdx.x) * V + (j % V);
-                if (valid || o < nt) vmask |= 1u << j;
-            }
-            const u32 tb = tag_base + t0;
-            if (bid) {
-#pragma unroll
-                for (u32 j = 0; j < ITEMS; ++j) bk[j] = (id[j / 2] >> (16 * (j & 1))) & 0xffffu;
-            } else {
-                classify_n<U, ITEMS>(cls, k, [&](int j) -> u32 { return tb + ((j / V) * NT + threadIdx.x) * V + (j % V); },
-                                     bk);
-            }
-#pragma unroll
-            for (u32 j = 0; j < ITEMS; ++j)
-                if (vmask & (1u << j)) pos[j] = atomicAdd(&q[bk[j]], 1u);
-            u32 sv[ITEMS];
-#pragma unroll
-            for (u32 j = 0; j < ITEMS; ++j) sv[j] = sb[bk[j]];
-            u32 inmask = 0, lead = 0;
-#pragma unroll
-            for (u32 j = 0; j < ITEMS; ++j) {
-                const u32 d = pos[j] - (sv[j] & ~(SV - 1));
-                if ((vmask & (1u << j)) && d < SV) {
-                    wc[(size_t)bk[j] * SV + d] = k[j];
-                    inmask |= 1u << j;
-                    if (d == SV - 1) lead |= 1u << j;
+                if (vmask & (1u << j)) {
+                    pos[j] = atomicAdd(&q[b], 1u);
+                    const u32 d = pos[j] - (sb[b] & ~(SV - 1));
+                    if (d < SV) {
+                        wc[(size_t)b * SV + d] = k[j];
+                        inmask |= 1u << j;
+                        if (d == SV - 1) lead |= 1u << j;
+                    }
                 }
             }
             __syncthreads();
@@ -1126,17 +1109,17 @@ __global__ void __launch_bounds__(NT, 1) k_scatter_wc(Bufs<typename Codec<DT>::U
             u32 tail = 0;
 #pragma unroll
             for (u32 j = 0; j < ITEMS; ++j) {
-                const u32 b = bk[j];
+                const u32 b = (id[j / 2] >> (16 * (j & 1))) & 0xffffu;
                 if (lead & (1u << j)) {
                     const u32 sv = sb[b], s0 = sv & ~(SV - 1), front = sv & (SV - 1);
-                    const U* w = wc + (size_t)b * SV;
+                    const U* wb = wc + (size_t)b * SV;
                     if (front == 0) {
-                        const uint4* w4 = (const uint4*)w;
+                        const uint4* w4 = (const uint4*)wb;
                         uint4* g4 = (uint4*)(dst + s0);
                         g4[0] = w4[0];
                         g4[1] = w4[1];
                     } else {
-                        for (u32 x = front; x < SV; ++x) dst[s0 + x] = w[x];
+                        for (u32 x = front; x < SV; ++x) dst[s0 + x] = wb[x];
                     }
                     sb[b] = q[b] & ~(SV - 1);
                 } else if ((vmask & ~inmask) & (1u << j)) {
@@ -1147,13 +1130,17 @@ __global__ void __launch_bounds__(NT, 1) k_scatter_wc(Bufs<typename Codec<DT>::U
             __syncthreads();
             // P3: keys of the new incomplete sector
 #pragma unroll
-            for (u32 j = 0; j < ITEMS; ++j)
-                if (tail & (1u << j)) wc[(size_t)bk[j] * SV + (pos[j] & (SV - 1))] = k[j];
+            for (u32 j = 0; j < ITEMS; ++j) {
+                if (tail & (1u << j)) {
+                    const u32 b = (id[j / 2] >> (16 * (j & 1))) & 0xffffu;
+                    wc[(size_t)b * SV + (pos[j] & (SV - 1))] = k[j];
+                }
+            }
         }
         __syncthreads();
         // the chunk's last, incomplete sectors (and runs inside one sector)
         for (u32 b = threadIdx.x; b < P; b += NT) {
-            const u32 sv = sb[b], s0 = sv & ~(SV - 1), front = sv & (SV - 1), qe = q[b];
+            const u32 qe = q[b], sv = sb[b], s0 = sv & ~(SV - 1), front = sv & (SV - 1);
             for (u32 x = front; s0 + x < qe; ++x) dst[s0 + x] = wc[(size_t)b * SV + x];
         }
         __syncthreads();

@@ -145,7 +145,7 @@ template <int DT, bool KV> struct Engine {
 
     struct Level0 {
         u32 P = 1, L = 0, log2L = 0, nchunk = 0, chunk = 0;
-        U* sk = nullptr; u32* st = nullptr; u16* lut = nullptr;
+        U* sk = nullptr; u32* st = nullptr; u32* lut = nullptr;
         Seg* seg = nullptr; Chunk* chunks = nullptr; u32* nchunks = nullptr;
         u32* hist = nullptr; u32* tot = nullptr; u32* nseg = nullptr;
         u16* bid = nullptr;  // keys-only: bucket ids from the histogram pass (OVS_WC_IDS)
@@ -156,26 +156,32 @@ template <int DT, bool KV> struct Engine {
     };
 
     // keys-only sorts use the write-combining scatter when its shared memory fits
-    bool use_wc(u32 P, u32 L) const {
+    bool use_wc(u32 P) const {
         return !KV && P > 1 && wc_smem_bytes<U>(P) + 512 <= (size_t)c.di.smem_optin;
     }
     static size_t scatter_smem(u32 P, u32 L) {
         return scatter_smem_bytes<U, KV, PartItems<U, KV>::v, PT_NT>(P, L);
     }
     u32 max_p_one_level() const {
-        // largest P whose scatter working set fits shared memory with L = 2P
+        // largest P whose scatter working set fits shared memory (with the smallest table)
         u32 lo = 1, hi = 8192;  // 13-bit classifier table entries
         while (lo < hi) {
             u32 mid = (lo + hi + 1) / 2;
-            u32 L = std::min<u32>(16384, std::max<u32>(64, pow2_at_least(4 * mid)));
-            if (scatter_smem(mid, L) + 1024 <= (size_t)c.di.smem_optin) lo = mid; else hi = mid - 1;
+            if (use_wc(mid) || scatter_smem(mid, 64) + 1024 <= (size_t)c.di.smem_optin) lo = mid; else hi = mid - 1;
         }
         return lo;
     }
 
     void carve_level0(Level0& z, u32 P) {
         z.P = P;
-        z.L = P > 1 ? std::min<u32>(16384, std::max<u32>(64, pow2_at_least(4 * P))) : 1;
+        // classifier table: ~8 entries per splitter for keys-only sorts (only the histogram pass
+        // holds it), ~4 for key-value sorts (the scatter holds it next to its staging area)
+        // (the write-combining scatter does not classify; the generic scatter does)
+        const bool wc = use_wc(P);
+        z.L = P > 1 ? std::min<u32>(wc ? 32768 : 16384, std::max<u32>(64, pow2_at_least((wc ? 8 : 4) * P))) : 1;
+        while (z.L > 64 && (wc ? cls_smem_bytes<U>(P, z.L) + 4 * (size_t)P : scatter_smem(P, z.L)) + 1024 >
+                               (size_t)c.di.smem_optin)
+            z.L >>= 1;
         z.log2L = ilog2(z.L);
         // chunks: one per resident CTA slot, whole sub-tiles
         const u32 ts = PT_NT * PartItems<U, KV>::v;
@@ -184,7 +190,7 @@ template <int DT, bool KV> struct Engine {
         z.nchunk = std::max<u32>(1, cdiv(n, z.chunk));
         z.sk = c.take<U>(std::max<u32>(P, 1));
         z.st = c.take<u32>(std::max<u32>(P, 1));
-        z.lut = c.take<u16>(z.L + 1);
+        z.lut = c.take<u32>(z.L + 1);
         z.seg = c.take<Seg>(1);
         z.chunks = c.take<Chunk>(z.nchunk);
         z.nchunks = c.take<u32>(2);
@@ -232,7 +238,7 @@ template <int DT, bool KV> struct Engine {
         OVS_CK(cudaFuncSetAttribute(k_hist<DT, KV, true, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_h));
         k_hist<DT, KV, true, 1024><<<z.nchunk * hsplit, 1024, sm_h, c.st>>>(B, z.chunks, z.nchunks, z.seg, z.sk, z.st,
                                                                            z.lut, z.P, z.L, z.hist, hsplit, tag_base,
-                                                                           use_wc(z.P, z.L) ? z.bid : nullptr);
+                                                                           use_wc(z.P) ? z.bid : nullptr);
         c.check();
         k_colscan<<<std::min<u32>(cdiv(z.P, 32), 4 * c.di.sms), 1024, 0, c.st>>>(z.hist, z.seg, z.nseg, z.P, z.tot);
         c.check();
@@ -240,7 +246,7 @@ template <int DT, bool KV> struct Engine {
                                           nullptr, 0, counts_out, c.status);
         c.check();
         if (mark_phases) c.mark(2);
-        if (use_wc(z.P, z.L)) {
+        if (use_wc(z.P)) {
             constexpr int IT = WC_ITEMS * 4 / (int)sizeof(U);  // u32: WC_ITEMS keys per thread
             const size_t sm_w = wc_smem_bytes<U>(z.P);
             auto kw = k_scatter_wc<DT, WC_NT, IT>;

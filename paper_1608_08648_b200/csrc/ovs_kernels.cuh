@@ -102,23 +102,36 @@ enum : u32 { BK_LOOSE = 0x80000000u, BK_RAW = 0x40000000u };
 // bucket(k, tag) = #{q : S[q] <lex (k, tag)}: a lower_bound over the p-1 splitters with the
 // (key, tag) tie-break.  The binary search is narrowed by a lookup
 // table over the ordered-key space: entry e covers keys [base + e<<shift, base + (e+1)<<shift)
-// and stores (16 bits) lo_e = #{q : S[q].key < base + e<<shift} (13 bits, p <= 8192) and
-// cnt_e = #splitter keys inside the entry (3 bits, 7 = "see entry e+1"), so only those cnt_e
-// splitters are binary-searched (usually none).  The result is
-// exactly the lower_bound (tests/test_gpu_parity.py compares bucket counts with the oracle).
+// and stores (32 bits) lo_e = #{q : S[q].key < base + e<<shift} (bits 0-12, p <= 8192), cnt_e =
+// #splitter keys inside the entry (bits 13-15, 7 = "see entry e+1") and frac_e = the position of
+// the first of them inside the entry at 16-bit resolution (bits 16-31).  cnt 0: the bucket is
+// lo; cnt 1: comparing the key's own 16-bit position with frac decides unless they are equal
+// (then one exact (key, tag) comparison); cnt >= 2: binary search of those cnt splitters.  The
+// result is exactly the lower_bound (tests/test_gpu_parity.py compares bucket counts with the
+// oracle).
 template <class U> struct ClsView {
-    const U* sk; const u32* st; const u16* lut;
+    const U* sk; const u32* st; const u32* lut;
     U base; u32 shift, L, P;
 };
+
+// 16-bit position of an offset inside a table entry of 2^shift keys
+template <class U> __device__ __host__ __forceinline__ u32 cls_frac(U off, u32 shift) {
+    return shift >= 16 ? (u32)(off >> (shift - 16)) : (u32)(off << (16 - shift));
+}
 
 template <class U>
 __device__ __forceinline__ u32 classify(const ClsView<U>& c, U k, u32 tag) {
     if (c.P <= 1) return 0;
     if (k < c.base) return 0;
-    U d = (U)(k - c.base) >> c.shift;
+    const U x = (U)(k - c.base);
+    const U d = x >> c.shift;
     if (d >= (U)c.L) return c.P - 1;
     const u32 e = c.lut[(u32)d];
-    u32 lo = e & 0x1fffu, cnt = e >> 13;
+    u32 lo = e & 0x1fffu, cnt = (e >> 13) & 7u;
+    if (cnt == 1) {
+        const u32 kf = cls_frac<U>(x & (((U)1 << c.shift) - 1), c.shift), sf = e >> 16;
+        if (kf != sf) return lo + (kf > sf ? 1u : 0u);
+    }
     if (cnt == 7) cnt = (c.lut[(u32)d + 1] & 0x1fffu) - lo;  // saturated: the next entry's lo bounds it
     while (cnt > 0) {
         u32 half = cnt >> 1, mid = lo + half;
@@ -129,62 +142,51 @@ __device__ __forceinline__ u32 classify(const ClsView<U>& c, U k, u32 tag) {
     return lo;
 }
 
-// Batched form for N keys held in registers: the table lookups, then three unrolled,
-// predicated binary-search steps (enough for the <= 7 splitter keys a table entry can name),
-// then a loop only for saturated entries (rare).  Separate passes over the N keys keep N
-// independent shared-memory loads in flight instead of one dependent chain per key.
-#ifndef OVS_CLS_MODE
-#define OVS_CLS_MODE 1
-#endif
+// Batched form for N keys held in registers: the table lookups for all N first (N independent
+// shared loads in flight), the 16-bit position test, then a search loop only for the keys left.
 template <class U, int N, class TagF>
 __device__ __forceinline__ void classify_n(const ClsView<U>& c, const U (&k)[N], TagF&& tag, u32 (&b)[N]) {
-#if OVS_CLS_MODE == 0
-#pragma unroll
-    for (int j = 0; j < N; ++j) b[j] = classify<U>(c, k[j], tag(j));
-#else
     if (c.P <= 1) {
 #pragma unroll
         for (int j = 0; j < N; ++j) b[j] = 0;
         return;
     }
-    u32 cnt[N], dd[N];
+    u32 e[N];
 #pragma unroll
     for (int j = 0; j < N; ++j) {
-        const U kk = k[j];
-        const U d = (U)(kk - c.base) >> c.shift;
-        const bool below = kk < c.base, above = !below && d >= (U)c.L;
-        dd[j] = (below || above) ? 0xffffffffu : (u32)d;
-        const u32 e = (below || above) ? 0u : c.lut[(u32)d];
-        b[j] = below ? 0u : above ? c.P - 1 : (e & 0x1fffu);
-        cnt[j] = e >> 13;
+        const U x = (U)(k[j] - c.base);
+        const U d = x >> c.shift;
+        const bool below = k[j] < c.base, above = !below && d >= (U)c.L;
+        e[j] = (below || above) ? 0u : c.lut[(u32)d];
+        b[j] = below ? 0u : above ? c.P - 1 : (e[j] & 0x1fffu);
     }
+    u32 left = 0;  // keys that still need splitter comparisons
 #pragma unroll
-    for (int j = 0; j < N; ++j)
-        if (cnt[j] == 7) cnt[j] = (c.lut[dd[j] + 1] & 0x1fffu) - b[j];  // saturated entry
-#if OVS_CLS_MODE == 2
-#pragma unroll
-    for (int step = 0; step < 3; ++step) {
+    for (int j = 0; j < N; ++j) {
+        const u32 cnt = (e[j] >> 13) & 7u;
+        if (cnt == 1) {
+            const U x = (U)(k[j] - c.base);
+            const u32 kf = cls_frac<U>(x & (((U)1 << c.shift) - 1), c.shift), sf = e[j] >> 16;
+            if (kf != sf) b[j] += kf > sf ? 1u : 0u;
+            else left |= 1u << j;
+        } else if (cnt > 1) {
+            left |= 1u << j;
+        }
+    }
+    if (__any_sync(0xffffffffu, left != 0)) {
 #pragma unroll
         for (int j = 0; j < N; ++j) {
-            if (cnt[j] > 0) {
-                const u32 half = cnt[j] >> 1, mid = b[j] + half;
+            if (!((left >> j) & 1u)) continue;
+            u32 cnt = (e[j] >> 13) & 7u;
+            if (cnt == 7) cnt = (c.lut[(u32)((U)(k[j] - c.base) >> c.shift) + 1] & 0x1fffu) - b[j];
+            while (cnt > 0) {
+                const u32 half = cnt >> 1, mid = b[j] + half;
                 const U s = c.sk[mid];
                 const bool less = (s < k[j]) || (s == k[j] && c.st[mid] < tag(j));
-                if (less) { b[j] = mid + 1; cnt[j] -= half + 1; } else { cnt[j] = half; }
+                if (less) { b[j] = mid + 1; cnt -= half + 1; } else { cnt = half; }
             }
         }
     }
-#endif
-#pragma unroll
-    for (int j = 0; j < N; ++j) {
-        while (cnt[j] > 0) {
-            const u32 half = cnt[j] >> 1, mid = b[j] + half;
-            const U s = c.sk[mid];
-            const bool less = (s < k[j]) || (s == k[j] && c.st[mid] < tag(j));
-            if (less) { b[j] = mid + 1; cnt[j] -= half + 1; } else { cnt[j] = half; }
-        }
-    }
-#endif
 }
 
 // ------------------------------------------------------------------ block helpers
@@ -527,7 +529,7 @@ __global__ void k_pick_splitters(const u64* t_pack, const u64* t_key, const u32*
 }
 
 // ------------------------------------------------------------------ classifier LUT build
-// One CTA per segment.  lo(e) = #{q : S[q].key < base + e<<shift}, cnt(e) = lo(e+1) - lo(e).
+// lo(e) = #{q : S[q].key < base + e<<shift}, cnt(e) = lo(e+1) - lo(e), frac(e) (see the classifier).
 template <class U>
 __device__ u32 count_less_key(const U* sk, u32 nsp, U thr) {
     u32 lo = 0, cnt = nsp;
@@ -538,30 +540,11 @@ __device__ u32 count_less_key(const U* sk, u32 nsp, U thr) {
     return lo;
 }
 
-template <class U>
-__device__ void build_lut(const U* sk, u32 P, u32 L, u32 log2L, u16* lut, U* base_out, u32* shift_out) {
-    if (P <= 1) {
-        if (threadIdx.x == 0) { *base_out = 0; *shift_out = 0; }
-        return;
-    }
-    U base = sk[0];
-    U span = sk[P - 2] - base;
-    u32 bl = bitlen<U>(span);
-    u32 shift = bl > log2L ? bl - log2L : 0u;
-    U lim = span >> shift;  // entries e > lim start above every splitter key
-    for (u32 e = threadIdx.x; e < L; e += blockDim.x) {
-        u32 a = ((U)e > lim) ? (P - 1) : count_less_key<U>(sk, P - 1, (U)(base + ((U)e << shift)));
-        u32 b = ((U)(e + 1) > lim) ? (P - 1) : count_less_key<U>(sk, P - 1, (U)(base + ((U)(e + 1) << shift)));
-        lut[e] = (u16)(a | (min(b - a, 7u) << 13));
-    }
-    if (threadIdx.x == 0) { lut[L] = (u16)(P - 1); *base_out = base; *shift_out = shift; }
-}
-
 // Classifier of a single segment covering [0, n) of buffer 0 (the contract level, or an
 // internal sort of a whole array): LUT entries in parallel over CTAs, splitter keys staged in
 // shared memory; CTA 0 writes the segment header.
 template <class U>
-__global__ void __launch_bounds__(1024) k_build_cls0(const U* sk, u32 P, u32 L, u32 log2L, u16* lut, Seg* seg, u32 n,
+__global__ void __launch_bounds__(1024) k_build_cls0(const U* sk, u32 P, u32 L, u32 log2L, u32* lut, Seg* seg, u32 n,
                                                      u32 nchunk) {
     extern __shared__ __align__(16) char smem[];
     U* s = (U*)smem;
@@ -578,9 +561,11 @@ __global__ void __launch_bounds__(1024) k_build_cls0(const U* sk, u32 P, u32 L, 
         for (u32 e = blockIdx.x * blockDim.x + threadIdx.x; e < L; e += gridDim.x * blockDim.x) {
             u32 a = ((U)e > lim) ? (P - 1) : count_less_key<U>(s, P - 1, (U)(base + ((U)e << shift)));
             u32 b = ((U)(e + 1) > lim) ? (P - 1) : count_less_key<U>(s, P - 1, (U)(base + ((U)(e + 1) << shift)));
-            lut[e] = (u16)(a | (min(b - a, 7u) << 13));
+            // position of the first splitter key inside the entry (16-bit resolution)
+            const u32 fr = b > a ? cls_frac<U>((U)(s[a] - base) & (((U)1 << shift) - 1), shift) : 0u;
+            lut[e] = a | (min(b - a, 7u) << 13) | (fr << 16);
         }
-        if (blockIdx.x == 0 && threadIdx.x == 0) lut[L] = (u16)(P - 1);
+        if (blockIdx.x == 0 && threadIdx.x == 0) lut[L] = P - 1;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         Seg g;
@@ -608,14 +593,14 @@ __host__ __device__ constexpr size_t a16(size_t x) { return (x + 15) & ~(size_t)
 
 template <class U>
 __device__ __forceinline__ ClsView<U> load_cls(char* sp, const Seg& sg, u32 segi, const U* sk_pool, const u32* st_pool,
-                                               const u16* lut_pool, u32 PS, u32 LS, bool load) {
+                                               const u32* lut_pool, u32 PS, u32 LS, bool load) {
     U* sk = (U*)sp; sp += a16(sizeof(U) * (size_t)PS);
     u32* st = (u32*)sp; sp += a16(4 * (size_t)PS);
-    u16* lut = (u16*)sp;
+    u32* lut = (u32*)sp;
     if (load) {
         const U* gsk = sk_pool + (size_t)segi * PS;
         const u32* gst = st_pool + (size_t)segi * PS;
-        const u16* glut = lut_pool + (size_t)segi * (LS + 1);
+        const u32* glut = lut_pool + (size_t)segi * (LS + 1);
         for (u32 i = threadIdx.x; i + 1 < sg.P; i += blockDim.x) { sk[i] = gsk[i]; st[i] = gst[i]; }
         for (u32 i = threadIdx.x; i <= sg.L; i += blockDim.x) lut[i] = glut[i];
     }
@@ -624,7 +609,7 @@ __device__ __forceinline__ ClsView<U> load_cls(char* sp, const Seg& sg, u32 segi
     return c;
 }
 template <class U> __host__ __device__ constexpr size_t cls_smem_bytes(u32 PS, u32 LS) {
-    return a16(sizeof(U) * (size_t)PS) + a16(4 * (size_t)PS) + a16(2 * ((size_t)LS + 1));
+    return a16(sizeof(U) * (size_t)PS) + a16(4 * (size_t)PS) + a16(4 * ((size_t)LS + 1));
 }
 
 template <class U> __device__ __forceinline__ U shfl_xor_any(U x, int o) {
@@ -672,7 +657,7 @@ __device__ __forceinline__ void for_items(const U* __restrict__ src, u32 beg, u3
 template <int DT, bool KV, bool LEVEL0, int NT>
 __global__ void __launch_bounds__(NT) k_hist(Bufs<typename Codec<DT>::U> B, const Chunk* chunks, const u32* nchunks,
                                              Seg* segs, const typename Codec<DT>::U* sk_pool, const u32* st_pool,
-                                             const u16* lut_pool, u32 PS, u32 LS, u32* hist, u32 split,
+                                             const u32* lut_pool, u32 PS, u32 LS, u32* hist, u32 split,
                                              u32 tag_base, u16* bid) {
     // `split` CTAs share a chunk (each a contiguous part) and add into its (zeroed) row;
     // bid != NULL: every key's bucket is also stored (bid[i]: the scatter then skips classify)
@@ -877,7 +862,7 @@ __host__ __device__ constexpr size_t scatter_smem_bytes(u32 PS, u32 LS) {
 template <int DT, bool KV, bool LEVEL0, int NT, int ITEMS>
 __global__ void __launch_bounds__(NT) k_scatter(Bufs<typename Codec<DT>::U> B, const Chunk* chunks, const u32* nchunks,
                                                 const Seg* segs, const typename Codec<DT>::U* sk_pool,
-                                                const u32* st_pool, const u16* lut_pool, u32 PS, u32 LS,
+                                                const u32* st_pool, const u32* lut_pool, u32 PS, u32 LS,
                                                 const u32* hist, const u32* tot_pool, u32 tag_base) {
     typedef typename Codec<DT>::U U;
     constexpr int TS = NT * ITEMS;
@@ -1221,6 +1206,14 @@ __global__ void __launch_bounds__(1024) k_internal_sample(Bufs<typename Codec<DT
 #endif
 constexpr int BS_NT = OVS_BS_NT;
 constexpr u32 BS_WARPMAX = BS_NT >= 1024 ? 256 : 512;  // largest group a warp sorts in registers
+#ifdef OVS_BS_PROF  // phase profile of the bucket sorter (experiments only): CTA-0-thread cycles per phase
+__device__ unsigned long long g_bsprof[16];
+#define BS_T0 long long bs_t_ = clock64();
+#define BS_PROBE(i) if (threadIdx.x == 0) { const long long n_ = clock64(); atomicAdd(&g_bsprof[i], (unsigned long long)(n_ - bs_t_)); bs_t_ = n_; }
+#else
+#define BS_T0
+#define BS_PROBE(i)
+#endif
 constexpr int BS_NGMAX = 8192;
 constexpr int BS_BIGMAX = 768;
 constexpr int BS_HUGEMAX = 256;  // groups > BS_WARPMAX items: at most cap/BS_WARPMAX exist
@@ -1409,29 +1402,46 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
     Bucket* stk = stack_pool + (size_t)blockIdx.x * BS_STACK;
     const u32 nl = *nlist;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    if (threadIdx.x == 0) s_next = atomicAdd(ticket, 1u);
+#ifdef OVS_BS_PROF
+    const long long bs_start_ = clock64();
+#endif
+    // Work distribution: the next bucket is claimed (ticket) and its descriptor loaded one bucket
+    // ahead, and the claim after that is issued at the start of a bucket and consumed at its end,
+    // so no global round trip sits between two buckets.  The claimed bucket is kept in shared
+    // memory; only resplit children go through the CTA's stack in global memory.
+    __shared__ Bucket s_cur, s_nxt;
+    __shared__ u32 s_base;
+    if (threadIdx.x == 0) {
+        s_work = atomicAdd(ticket, 1u);
+        if (s_work < nl) s_cur = list[s_work];
+        s_next = atomicAdd(ticket, 1u);
+        if (s_next < nl) s_nxt = list[s_next];
+    }
+    __syncthreads();
     for (;;) {
+        if (s_work >= nl) break;
+        u32 t3 = 0xffffffffu;  // thread 0: the claim after the next one (consumed at the end)
         if (threadIdx.x == 0) {
-            s_work = s_next;
-            if (s_work < nl) {
-                stk[0] = list[s_work];
-                s_sp = 1;
-                s_next = atomicAdd(ticket, 1u);  // claim the next bucket now and prefetch it
+            if (s_next < nl) {
+                // the next bucket's keys into L2 with one bulk prefetch (16-byte aligned cover)
+                const Bucket nx = s_nxt;
+                const uintptr_t a0 = (uintptr_t)(B.k[nx.buf] + nx.beg) & ~(uintptr_t)15;
+                const uintptr_t a1 = ((uintptr_t)(B.k[nx.buf] + nx.beg + nx.len) + 15) & ~(uintptr_t)15;
+                if (a1 > a0)
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((u32)(a1 - a0)) : "memory");
             }
+            t3 = atomicAdd(ticket, 1u);
+            s_sp = 0;
+            s_base = 1;
         }
         __syncthreads();
-        if (s_work >= nl) break;
-        if (s_next < nl) {
-            const Bucket nx = list[s_next];
-            const char* base = (const char*)(B.k[nx.buf] + nx.beg);
-            const u32 bytes = nx.len * (u32)sizeof(U);
-            for (u32 off = threadIdx.x * 128; off < bytes; off += BS_NT * 128)
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(base + off));
-        }
-        while (s_sp > 0) {
-            const Bucket bk = stk[s_sp - 1];
+        while (s_base || s_sp > 0) {
+            const Bucket bk = s_base ? s_cur : stk[s_sp - 1];
             __syncthreads();
-            if (threadIdx.x == 0) { s_sp -= 1; s_nbig = 0; s_nhuge = 0; s_over = 0; }
+            if (threadIdx.x == 0) {
+                if (s_base) s_base = 0; else s_sp -= 1;
+                s_nbig = 0; s_nhuge = 0; s_over = 0;
+            }
             const u32 m = bk.len;
             const U* src = B.k[bk.buf];
             const u32* vsrc = KV ? B.v[bk.buf] : nullptr;
@@ -1439,6 +1449,7 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
             const bool rawin = (bk.level & BK_RAW) != 0;
             auto K = [&](U x) -> U { return rawin ? Codec<DT>::ord(x) : x; };
             auto IX = [&](u32 pos) -> u32 { return (KV && !rawin) ? isrc[pos] : pos; };
+            BS_T0
             if (m > cap) {
                 // ---------------- CTA-local re-split of an oversized bucket
                 const u32 part = (u32)((cap * 45ull) / 100);
@@ -1505,6 +1516,7 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                     s_sp = sp;
                 }
                 __syncthreads();
+                BS_PROBE(0)
                 continue;
             }
             // ---------------- on-chip sort of a bucket that fits
@@ -1512,6 +1524,7 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
             // 16-byte shared loads and global stores
             BucketSmem<U, KV> Sa = S;
             Sa.k = S.k + (bk.beg & (16 / sizeof(U) - 1));
+            BS_PROBE(1)
             U lo = (U)bk.lo, hi = (U)bk.hi;
             if (bk.level & BK_LOOSE) {
                 U mn = umax_of<U>(), mx = 0;
@@ -1533,11 +1546,12 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
             // 64-bit keys use the key (equal keys then share a group, ordered by index).
             const bool comp = KV && sizeof(U) == 4;
             const u64 xmax = comp ? ((((u64)(hi - lo)) << 32) | 0xffffffffull) : (u64)(U)(hi - lo);
-            const unsigned __int128 R = (unsigned __int128)xmax + 1;
-            const unsigned __int128 mq = (((unsigned __int128)ng) << 64) / R;
-            const u64 mult = mq > (unsigned __int128)0xffffffffffffffffull ? 0xffffffffffffffffull : (u64)mq;
-            const unsigned __int128 mq32 = mq >> 32;
-            const u32 mult32 = mq32 > (unsigned __int128)0xffffffffu ? 0xffffffffu : (u32)mq32;
+            // multiplier ~ ng * 2^64 / R in double precision: any multiplier keeps the digit monotone
+            // (and the clamp keeps it < ng), so rounding only perturbs the group sizes slightly
+            const double mq = (double)ng * 18446744073709551616.0 / ((double)xmax + 1.0);
+            const u64 mult = mq >= 18446744073709549568.0 ? 0xffffffffffffffffull : (u64)mq;
+            const double mq32 = mq * (1.0 / 4294967296.0);
+            const u32 mult32 = mq32 >= 4294967295.0 ? 0xffffffffu : (u32)mq32;
             auto digit = [&](U k, u32 ix) -> u32 {
                 if constexpr (!KV && sizeof(U) == 4) {
                     return min(__umulhi((u32)(k - lo), mult32), ng - 1);  // min: memory safety only
@@ -1548,13 +1562,16 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
             };
             for (u32 g = threadIdx.x; g < ng; g += BS_NT) Sa.cnt[g] = 0;
             __syncthreads();
+            BS_PROBE(2)
             // 1. digit histogram
             for_items<U, BS_NT, 4>(src, bk.beg, m, [&](U kr, u32 o) {
                 const u32 ix = KV ? IX(bk.beg + o) : 0u;
                 atomicAdd(&Sa.cnt[digit(K(kr), ix)], 1u);
             });
             __syncthreads();
+            BS_PROBE(3)
             block_scan_small<BS_NT>(Sa.cnt, ng, red);  // cnt[g] = start of group g
+            BS_PROBE(4)
             // 2. scatter into shared memory by digit; afterwards cnt[g] = end of group g
             for_items<U, BS_NT, 4>(src, bk.beg, m, [&](U kr, u32 o) {
                 const U k = K(kr);
@@ -1565,6 +1582,7 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                 if (KV) { Sa.i[pos] = ix; Sa.v[pos] = vv; }
             });
             __syncthreads();
+            BS_PROBE(5)
             // 3. one thread per group of <= 8: Batcher network in registers; larger groups are
             // appended (warp-aggregated) to a list for 3b
             for (u32 g0 = 0; g0 < ng; g0 += BS_NT) {
@@ -1592,6 +1610,7 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                 }
             }
             __syncthreads();
+            BS_PROBE(6)
             // 3b. listed groups of 9..16: one thread each (63-comparator network)
             const u32 nlisted = min(s_nbig, (u32)BS_BIGMAX);
             const bool rescan = s_over != 0;  // list overflow (pathological skew): scan all groups
@@ -1625,6 +1644,7 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                 }
             }
             __syncthreads();
+            BS_PROBE(7)
             // 3c. groups over BS_WARPMAX: in-place bitonic network in shared memory, all comparators
             // ascending (the first step of each merge compares i with its mirror), so virtual
             // +inf padding beyond len never moves and len need not be a power of two
@@ -1652,6 +1672,7 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                 }
             }
             __syncthreads();
+            BS_PROBE(8)
             // 4. write the sorted bucket (16-byte stores where the output is aligned)
             {
                 constexpr u32 V = 16 / sizeof(U);
@@ -1678,9 +1699,19 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                 }
             }
             __syncthreads();
+            BS_PROBE(9)
+        }
+        if (threadIdx.x == 0) {
+            s_work = s_next;
+            s_cur = s_nxt;
+            s_next = t3;
+            if (t3 < nl) s_nxt = list[t3];
         }
         __syncthreads();
     }
+#ifdef OVS_BS_PROF
+    if (threadIdx.x == 0) atomicAdd(&g_bsprof[15], (unsigned long long)(clock64() - bs_start_));
+#endif
 }
 
 // ------------------------------------------------------------------ DRO (Algorithm 1, SqDet)

@@ -9,3 +9,14 @@ size_t dist_u32(Ctx& c, int step, const ovs_params* prm, const DistArgs& a, bool
     return kv ? dist_run<DT_U32, true>(c, step, prm, a) : dist_run<DT_U32, false>(c, step, prm, a);
 }
 }  // namespace ovs
+
+#ifdef OVS_BS_PROF
+extern "C" int ovs_debug_bsprof(unsigned long long* out, int reset) {
+    if (cudaMemcpyFromSymbol(out, ovs::g_bsprof, sizeof(unsigned long long) * 16) != cudaSuccess) return 1;
+    if (reset) {
+        unsigned long long z[16] = {0};
+        cudaMemcpyToSymbol(ovs::g_bsprof, z, sizeof(z));
+    }
+    return 0;
+}
+#endif

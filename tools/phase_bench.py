@@ -34,3 +34,18 @@ for path in libs:
     print(f"{path or 'libovs.so'}: sorted={ok} total {tot:.3f} ms ({n / tot / 1e6:.1f} Gkeys/s)  "
           + "  ".join(f"{nm} {v:.3f}" for nm, v in zip(ovs.PHASES, ph)), flush=True)
     del srt
+
+# bucket-sorter phase profile (libraries built with -DOVS_BS_PROF)
+import ctypes
+for path in libs:
+    L = ctypes.CDLL(path or ovs.LIB_PATH)
+    if not hasattr(L, "ovs_debug_bsprof"):
+        continue
+    arr = (ctypes.c_ulonglong * 16)()
+    L.ovs_debug_bsprof(arr, 1)
+    srt = ovs.Sorter(n, torch.uint32, False, "ros", p, s, 1) if False else None
+    names = ["resplit", "loose", "setup", "hist", "scan", "scatter", "net8", "net16+warp", "huge", "write"]
+    tot = arr[15]
+    print("bucket sorter cycles (sum over CTAs, thread 0), share of kernel:",
+          "  ".join(f"{nm} {arr[i] / tot * 100:.1f}%" for i, nm in enumerate(names)),
+          f" other {(tot - sum(arr[:10])) / tot * 100:.1f}%")

@@ -112,11 +112,15 @@ enum : u32 { BK_LOOSE = 0x80000000u, BK_RAW = 0x40000000u };
 template <class U> struct ClsView {
     const U* sk; const u32* st; const u32* lut;
     U base; u32 shift, L, P;
+    u32 fr, fl;  // 16-bit position of x = key - base inside its entry: ((x >> fr) << fl) & 0xffff
 };
 
 // 16-bit position of an offset inside a table entry of 2^shift keys
 template <class U> __device__ __host__ __forceinline__ u32 cls_frac(U off, u32 shift) {
     return shift >= 16 ? (u32)(off >> (shift - 16)) : (u32)(off << (16 - shift));
+}
+template <class U> __device__ __forceinline__ u32 cls_kfrac(const ClsView<U>& c, U x) {
+    return (u32)((x >> c.fr) << c.fl) & 0xffffu;
 }
 
 template <class U>
@@ -129,7 +133,7 @@ __device__ __forceinline__ u32 classify(const ClsView<U>& c, U k, u32 tag) {
     const u32 e = c.lut[(u32)d];
     u32 lo = e & 0x1fffu, cnt = (e >> 13) & 7u;
     if (cnt == 1) {
-        const u32 kf = cls_frac<U>(x & (((U)1 << c.shift) - 1), c.shift), sf = e >> 16;
+        const u32 kf = cls_kfrac<U>(c, x), sf = e >> 16;
         if (kf != sf) return lo + (kf > sf ? 1u : 0u);
     }
     if (cnt == 7) cnt = (c.lut[(u32)d + 1] & 0x1fffu) - lo;  // saturated: the next entry's lo bounds it
@@ -166,7 +170,7 @@ __device__ __forceinline__ void classify_n(const ClsView<U>& c, const U (&k)[N],
         const u32 cnt = (e[j] >> 13) & 7u;
         if (cnt == 1) {
             const U x = (U)(k[j] - c.base);
-            const u32 kf = cls_frac<U>(x & (((U)1 << c.shift) - 1), c.shift), sf = e[j] >> 16;
+            const u32 kf = cls_kfrac<U>(c, x), sf = e[j] >> 16;
             if (kf != sf) b[j] += kf > sf ? 1u : 0u;
             else left |= 1u << j;
         } else if (cnt > 1) {
@@ -606,6 +610,8 @@ __device__ __forceinline__ ClsView<U> load_cls(char* sp, const Seg& sg, u32 segi
     }
     ClsView<U> c;
     c.sk = sk; c.st = st; c.lut = lut; c.base = (U)sg.base; c.shift = sg.shift; c.L = sg.L; c.P = sg.P;
+    c.fr = sg.shift >= 16 ? sg.shift - 16 : 0u;
+    c.fl = sg.shift >= 16 ? 0u : 16 - sg.shift;
     return c;
 }
 template <class U> __host__ __device__ constexpr size_t cls_smem_bytes(u32 PS, u32 LS) {
@@ -654,8 +660,14 @@ __device__ __forceinline__ void for_items(const U* __restrict__ src, u32 beg, u3
 // through the codec (the caller's raw keys) with tag = index (ROS: the original index,
 // P:524-532); later levels read ordered keys with tag = position (keys only) or the carried
 // original index (key-value).
+#ifndef OVS_HIST_UNR
+#define OVS_HIST_UNR 2
+#endif
+#ifndef OVS_HIST_MINB
+#define OVS_HIST_MINB 1
+#endif
 template <int DT, bool KV, bool LEVEL0, int NT>
-__global__ void __launch_bounds__(NT) k_hist(Bufs<typename Codec<DT>::U> B, const Chunk* chunks, const u32* nchunks,
+__global__ void __launch_bounds__(NT, OVS_HIST_MINB) k_hist(Bufs<typename Codec<DT>::U> B, const Chunk* chunks, const u32* nchunks,
                                              Seg* segs, const typename Codec<DT>::U* sk_pool, const u32* st_pool,
                                              const u32* lut_pool, u32 PS, u32 LS, u32* hist, u32 split,
                                              u32 tag_base, u16* bid) {
@@ -690,7 +702,7 @@ __global__ void __launch_bounds__(NT) k_hist(Bufs<typename Codec<DT>::U> B, cons
         };
         // misaligned head and the tail one key at a time, the body in batches of UNR vectors
         constexpr u32 V = 16 / sizeof(U);
-        constexpr int UNR = 4, NB = UNR * (int)V;
+        constexpr int UNR = OVS_HIST_UNR, NB = UNR * (int)V;
         const u32 m = pend - pbeg;
         const u32 mis = (u32)(((uintptr_t)(src + pbeg)) & 15u) / (u32)sizeof(U);
         const u32 head = mis ? min(m, V - mis) : 0u;

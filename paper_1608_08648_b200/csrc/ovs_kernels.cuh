@@ -1532,10 +1532,10 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                 continue;
             }
             // ---------------- on-chip sort of a bucket that fits
-            // items sit at shared index = global index mod 16 bytes, so the write-out is aligned
+            // items sit at shared index = output address mod 16 bytes, so the write-out is aligned
             // 16-byte shared loads and global stores
             BucketSmem<U, KV> Sa = S;
-            Sa.k = S.k + (bk.beg & (16 / sizeof(U) - 1));
+            Sa.k = S.k + ((((uintptr_t)(okeys + bk.beg)) / sizeof(U)) & (16 / sizeof(U) - 1));
             BS_PROBE(1)
             U lo = (U)bk.lo, hi = (U)bk.hi;
             if (bk.level & BK_LOOSE) {

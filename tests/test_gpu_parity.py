@@ -90,6 +90,30 @@ def test_ros_pairs_stable_edge_matrix(ovs, orc, dist, n, p, s):
     assert rep.device_status == 0
 
 
+@pytest.mark.parametrize("dist,n,p,s", [("u32", 1_000_001, 4096, 16), ("i32_few", 777_777, 2000, 8),
+                                        ("f64_uniform", 500_001, 512, 16)])
+def test_ros_misaligned_input(ovs, orc, dist, n, p, s):
+    """The caller's keys start one element past a 16-byte boundary: the scalar head/tail paths of
+    the vectorised histogram, scatter and bucket-sort passes."""
+    x = ovs_inputs.keys(dist, n, seed=9)
+    ref = orc.ros_sort(x, p, s, 2)
+    buf = torch.empty(n + 1, dtype=TORCH[x.dtype], device="cuda")
+    xt = buf[1:]
+    xt.copy_(torch.from_numpy(x))
+    srt = ovs.Sorter(n, xt.dtype, False, "ros", p, s, 2)
+    rep = srt(xt, report=True)
+    torch.cuda.synchronize()
+    check(ref, xt.cpu().numpy(), None, rep, p)
+
+
+@pytest.mark.parametrize("dist,n,p,s", [("u32", 2_000_003, 8192, 4), ("u32_few4", 1_500_000, 6000, 4),
+                                        ("i32_gauss", 3_000_000, 5000, 8)])
+def test_ros_large_p(ovs, orc, dist, n, p, s):
+    """p beyond the write-combining scatter's shared-memory limit: the generic staged scatter
+    with a classifier table of fewer than one entry per splitter (multi-splitter entries)."""
+    ros_case(ovs, orc, dist, n, p, s, seed=4)
+
+
 def test_exhaustive_sample_closed_form(ovs, orc):
     """ps-1 = n: splitter q is the element of rank (q+1)s; counts = [s,..,s,s-1]."""
     n, p, s = 4095, 64, 64

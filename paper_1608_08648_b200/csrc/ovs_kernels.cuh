@@ -1227,6 +1227,12 @@ __device__ unsigned long long g_bsprof[16];
 #define BS_PROBE(i)
 #endif
 constexpr int BS_NGMAX = 8192;
+#ifndef OVS_BS_UNR
+#define OVS_BS_UNR 4
+#endif
+#ifndef OVS_NET8_X
+#define OVS_NET8_X 2
+#endif
 constexpr int BS_BIGMAX = 768;
 constexpr int BS_HUGEMAX = 256;  // groups > BS_WARPMAX items: at most cap/BS_WARPMAX exist
 constexpr int BS_STACK = 256;
@@ -1489,7 +1495,7 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                 }
                 if (threadIdx.x <= P) sp_cnt[threadIdx.x] = 0;
                 __syncthreads();
-                for_items<U, BS_NT, 4>(src, bk.beg, m, [&](U kr, u32 o) {
+                for_items<U, BS_NT, OVS_BS_UNR>(src, bk.beg, m, [&](U kr, u32 o) {
                     const U k = K(kr);
                     const u32 tg = IX(bk.beg + o);
                     atomicAdd(&sp_cnt[lower_bound_kt<U>(sp_k, sp_t, P - 1, k, tg)], 1u);
@@ -1502,7 +1508,7 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                 }
                 __syncthreads();
                 const u32 db = 1 - bk.buf;
-                for_items<U, BS_NT, 4>(src, bk.beg, m, [&](U kr, u32 o) {
+                for_items<U, BS_NT, OVS_BS_UNR>(src, bk.beg, m, [&](U kr, u32 o) {
                     const U k = K(kr);
                     const u32 tg = IX(bk.beg + o);
                     const u32 b = lower_bound_kt<U>(sp_k, sp_t, P - 1, k, tg);
@@ -1540,7 +1546,7 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
             U lo = (U)bk.lo, hi = (U)bk.hi;
             if (bk.level & BK_LOOSE) {
                 U mn = umax_of<U>(), mx = 0;
-                for_items<U, BS_NT, 4>(src, bk.beg, m, [&](U kr, u32) { const U k = K(kr); mn = min(mn, k); mx = max(mx, k); });
+                for_items<U, BS_NT, OVS_BS_UNR>(src, bk.beg, m, [&](U kr, u32) { const U k = K(kr); mn = min(mn, k); mx = max(mx, k); });
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) { mn = min(mn, shfl_xor_any(mn, o)); mx = max(mx, shfl_xor_any(mx, o)); }
                 if (lane == 0) { s_mn[wid] = mn; s_mx[wid] = mx; }
@@ -1576,7 +1582,7 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
             __syncthreads();
             BS_PROBE(2)
             // 1. digit histogram
-            for_items<U, BS_NT, 4>(src, bk.beg, m, [&](U kr, u32 o) {
+            for_items<U, BS_NT, OVS_BS_UNR>(src, bk.beg, m, [&](U kr, u32 o) {
                 const u32 ix = KV ? IX(bk.beg + o) : 0u;
                 atomicAdd(&Sa.cnt[digit(K(kr), ix)], 1u);
             });
@@ -1585,7 +1591,7 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
             block_scan_small<BS_NT>(Sa.cnt, ng, red);  // cnt[g] = start of group g
             BS_PROBE(4)
             // 2. scatter into shared memory by digit; afterwards cnt[g] = end of group g
-            for_items<U, BS_NT, 4>(src, bk.beg, m, [&](U kr, u32 o) {
+            for_items<U, BS_NT, OVS_BS_UNR>(src, bk.beg, m, [&](U kr, u32 o) {
                 const U k = K(kr);
                 u32 ix = 0, vv = 0;
                 if (KV) { ix = IX(bk.beg + o); vv = vsrc[bk.beg + o]; }
@@ -1597,27 +1603,43 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
             BS_PROBE(5)
             // 3. one thread per group of <= 8: Batcher network in registers; larger groups are
             // appended (warp-aggregated) to a list for 3b
-            for (u32 g0 = 0; g0 < ng; g0 += BS_NT) {
-                const u32 g = g0 + threadIdx.x;
-                u32 gs = 0, len = 0;
-                if (g < ng) { gs = g ? Sa.cnt[g - 1] : 0u; len = Sa.cnt[g] - gs; }
-                if (len > 1 && len <= 8) {
-                    E a[8];
+            // (OVS_NET8_X: groups per thread per iteration, their loads and networks interleaved)
+            for (u32 g0 = 0; g0 < ng; g0 += BS_NT * OVS_NET8_X) {
+                u32 gs[OVS_NET8_X], len[OVS_NET8_X];
+                E a[OVS_NET8_X][8];
 #pragma unroll
-                    for (u32 q = 0; q < 8; ++q) a[q] = q < len ? sm_get<U, KV>(Sa, gs + q) : E::inf();
-                    network8(a);
+                for (int x = 0; x < OVS_NET8_X; ++x) {
+                    const u32 g = g0 + x * BS_NT + threadIdx.x;
+                    gs[x] = 0; len[x] = 0;
+                    if (g < ng) { gs[x] = g ? Sa.cnt[g - 1] : 0u; len[x] = Sa.cnt[g] - gs[x]; }
+                }
+#pragma unroll
+                for (int x = 0; x < OVS_NET8_X; ++x) {
+                    const u32 lx = (len[x] > 1 && len[x] <= 8) ? len[x] : 0u;
+#pragma unroll
+                    for (u32 q = 0; q < 8; ++q) a[x][q] = q < lx ? sm_get<U, KV>(Sa, gs[x] + q) : E::inf();
+                }
+#pragma unroll
+                for (int x = 0; x < OVS_NET8_X; ++x) network8(a[x]);
+#pragma unroll
+                for (int x = 0; x < OVS_NET8_X; ++x) {
+                    const u32 lx = (len[x] > 1 && len[x] <= 8) ? len[x] : 0u;
 #pragma unroll
                     for (u32 q = 0; q < 8; ++q)
-                        if (q < len) sm_put<U, KV>(Sa, gs + q, a[q]);
+                        if (q < lx) sm_put<U, KV>(Sa, gs[x] + q, a[x][q]);
                 }
-                const u32 mb = __ballot_sync(0xffffffffu, len > 8);
-                if (mb) {
-                    u32 base = 0;
-                    if (lane == 0) base = atomicAdd(&s_nbig, __popc(mb));
-                    base = __shfl_sync(0xffffffffu, base, 0) + __popc(mb & ((1u << lane) - 1));
-                    if (len > 8) {
-                        if (base < BS_BIGMAX) s_big[base] = g;
-                        else atomicOr(&s_over, 1u);
+#pragma unroll
+                for (int x = 0; x < OVS_NET8_X; ++x) {
+                    const u32 g = g0 + x * BS_NT + threadIdx.x;
+                    const u32 mb = __ballot_sync(0xffffffffu, len[x] > 8);
+                    if (mb) {
+                        u32 base = 0;
+                        if (lane == 0) base = atomicAdd(&s_nbig, __popc(mb));
+                        base = __shfl_sync(0xffffffffu, base, 0) + __popc(mb & ((1u << lane) - 1));
+                        if (len[x] > 8) {
+                            if (base < BS_BIGMAX) s_big[base] = g;
+                            else atomicOr(&s_over, 1u);
+                        }
                     }
                 }
             }

@@ -1086,24 +1086,33 @@ __global__ void __launch_bounds__(NT, 1) k_scatter_wc(Bufs<typename Codec<DT>::U
                     if (((j / V) * NT + threadIdx.x) * V + (j % V) < nt) vmask |= 1u << j;
             }
             // P1: a position and the current sector per key; park it there if it is inside
-            u32 pos[ITEMS], inmask = 0, lead = 0;
+            // (separate passes over the ITEMS keys: all atomics, then all sector loads, then the
+            // stores, so ITEMS independent shared accesses are in flight instead of one chain)
+            u32 pos[ITEMS], sv[ITEMS], inmask = 0, lead = 0;
 #pragma unroll
             for (u32 j = 0; j < ITEMS; ++j) {
                 const u32 b = (id[j / 2] >> (16 * (j & 1))) & 0xffffu;
                 k[j] = Codec<DT>::ord(k[j]);
-                if (vmask & (1u << j)) {
-                    pos[j] = atomicAdd(&q[b], 1u);
-                    const u32 d = pos[j] - (sb[b] & ~(SV - 1));
-                    if (d < SV) {
-                        wc[(size_t)b * SV + d] = k[j];
-                        inmask |= 1u << j;
-                        if (d == SV - 1) lead |= 1u << j;
-                    }
+                if (vmask & (1u << j)) pos[j] = atomicAdd(&q[b], 1u);
+            }
+#pragma unroll
+            for (u32 j = 0; j < ITEMS; ++j) sv[j] = sb[(id[j / 2] >> (16 * (j & 1))) & 0xffffu];
+#pragma unroll
+            for (u32 j = 0; j < ITEMS; ++j) {
+                const u32 b = (id[j / 2] >> (16 * (j & 1))) & 0xffffu;
+                const u32 d = pos[j] - (sv[j] & ~(SV - 1));
+                if ((vmask & (1u << j)) && d < SV) {
+                    wc[(size_t)b * SV + d] = k[j];
+                    inmask |= 1u << j;
+                    if (d == SV - 1) lead |= 1u << j;
                 }
             }
             __syncthreads();
             // P2: flush completed sectors; keys of complete sectors past them go straight out
-            u32 tail = 0;
+            u32 tail = 0, qf[ITEMS];
+#pragma unroll
+            for (u32 j = 0; j < ITEMS; ++j)
+                if (((vmask & ~inmask) | lead) & (1u << j)) qf[j] = q[(id[j / 2] >> (16 * (j & 1))) & 0xffffu];
 #pragma unroll
             for (u32 j = 0; j < ITEMS; ++j) {
                 const u32 b = (id[j / 2] >> (16 * (j & 1))) & 0xffffu;
@@ -1118,9 +1127,9 @@ __global__ void __launch_bounds__(NT, 1) k_scatter_wc(Bufs<typename Codec<DT>::U
                     } else {
                         for (u32 x = front; x < SV; ++x) dst[s0 + x] = wb[x];
                     }
-                    sb[b] = q[b] & ~(SV - 1);
+                    sb[b] = qf[j] & ~(SV - 1);
                 } else if ((vmask & ~inmask) & (1u << j)) {
-                    if (pos[j] < (q[b] & ~(SV - 1))) dst[pos[j]] = k[j];
+                    if (pos[j] < (qf[j] & ~(SV - 1))) dst[pos[j]] = k[j];
                     else tail |= 1u << j;
                 }
             }

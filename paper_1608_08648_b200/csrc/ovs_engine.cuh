@@ -77,10 +77,35 @@ struct Ctx {
 };
 
 static inline u32 cdiv(u64 a, u64 b) { return (u32)((a + b - 1) / b); }
+
+// Kernel launch with programmatic dependent launch (PDL, cudaLaunchAttributeProgrammatic-
+// StreamSerialization): every kernel lets its successor be scheduled as soon as all of its own
+// CTAs have started (griddepcontrol.launch_dependents) and waits for its predecessor's results
+// (griddepcontrol.wait) before touching memory, so the launch latency of the ~16 kernels of a
+// sort overlaps the tail of the previous kernel instead of adding to it.
+template <class... KA, class... AA>
+static void launch(Ctx& c, void (*k)(KA...), dim3 grid, dim3 block, size_t smem, AA&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c.st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = OVS_PDL;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    OVS_CK(cudaLaunchKernelEx(&cfg, k, std::forward<AA>(args)...));
+}
 static inline u32 pow2_at_least(u32 x) {
     u32 p = 1;
     while (p < x) p <<= 1;
     return p;
+}
+static inline u32 bits_for(u64 n) {  // bits needed for the values 0 .. n-1 (>= 1)
+    u32 b = 1;
+    while (b < 32 && (1ull << b) < n) ++b;
+    return b;
 }
 static inline u32 ilog2(u32 x) {
     u32 l = 0;
@@ -110,7 +135,7 @@ template <class U, bool KV> struct PartItems { static constexpr int v = (sizeof(
 
 static void fill_u32(Ctx& c, u32* p, u32 v, u32 n) {
     if (c.dry || n == 0) return;
-    k_fill_u32<<<cdiv(n, 256), 256, 0, c.st>>>(p, v, n);
+    launch(c, k_fill_u32, cdiv(n, 256), 256, 0, p, v, n);
     c.check();
 }
 
@@ -141,6 +166,7 @@ template <int DT, bool KV> struct Engine {
     u32 cap;
     bool mark_phases = false;  // the contract-level engine records the phase events
     u32 tag_base = 0;          // level-0 tag of item i = tag_base + i (multi-GPU: global index)
+    u32 ixbits = 32;           // key-value sorts: original indices are < 2^ixbits
     explicit Engine(Ctx& ctx) : c(ctx) {}
 
     struct Level0 {
@@ -216,7 +242,7 @@ template <int DT, bool KV> struct Engine {
         const u32 N = pow2_at_least(z.P * si);
         const size_t sm = (sizeof(U) + 4) * (size_t)N;
         OVS_CK(cudaFuncSetAttribute(k_internal_sample<DT, KV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        k_internal_sample<DT, KV><<<1, 1024, sm, c.st>>>(B, n, z.P, si, N, seed, z.sk, z.st);
+        launch(c, k_internal_sample<DT, KV>, 1, 1024, sm, B, n, z.P, si, N, seed, z.sk, z.st);
         c.check();
     }
 
@@ -225,10 +251,10 @@ template <int DT, bool KV> struct Engine {
         if (c.dry) return;
         const size_t sm_cls = std::max<size_t>(sizeof(U) * std::max<u32>(z.P, 1), 16);
         OVS_CK(cudaFuncSetAttribute(k_build_cls0<U>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_cls));
-        k_build_cls0<U><<<std::max<u32>(1, std::min<u32>(z.L / 1024 + 1, 16)), 1024, sm_cls, c.st>>>(
+        launch(c, k_build_cls0<U>, std::max<u32>(1, std::min<u32>(z.L / 1024 + 1, 16)), 1024, sm_cls, 
             z.sk, z.P, z.L, z.log2L, z.lut, z.seg, n, z.nchunk);
         c.check();
-        k_make_chunks0<<<cdiv(z.nchunk, 256), 256, 0, c.st>>>(z.chunks, z.nchunk, n, z.chunk);
+        launch(c, k_make_chunks0, cdiv(z.nchunk, 256), 256, 0, z.chunks, z.nchunk, n, z.chunk);
         c.check();
         set_pair(z.nchunks, z.nchunk, 1);  // device counts: chunks, segments
         fill_u32(c, l.nfit, 0, 2);
@@ -236,13 +262,13 @@ template <int DT, bool KV> struct Engine {
         const u32 hsplit = 2;  // two 1024-thread CTAs per chunk
         OVS_CK(cudaMemsetAsync(z.hist, 0, sizeof(u32) * (size_t)z.nchunk * z.P, c.st));
         OVS_CK(cudaFuncSetAttribute(k_hist<DT, KV, true, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_h));
-        k_hist<DT, KV, true, 1024><<<z.nchunk * hsplit, 1024, sm_h, c.st>>>(B, z.chunks, z.nchunks, z.seg, z.sk, z.st,
+        launch(c, k_hist<DT, KV, true, 1024>, z.nchunk * hsplit, 1024, sm_h, B, z.chunks, z.nchunks, z.seg, z.sk, z.st,
                                                                            z.lut, z.P, z.L, z.hist, hsplit, tag_base,
                                                                            use_wc(z.P) ? z.bid : nullptr);
         c.check();
-        k_colscan<<<std::min<u32>(cdiv(z.P, 32), 4 * c.di.sms), 1024, 0, c.st>>>(z.hist, z.seg, z.nseg, z.P, z.tot);
+        launch(c, k_colscan, std::min<u32>(cdiv(z.P, 32), 4 * c.di.sms), 1024, 0, z.hist, z.seg, z.nseg, z.P, z.tot);
         c.check();
-        k_segscan<U><<<1, 1024, 0, c.st>>>(z.seg, z.nseg, z.P, z.tot, z.sk, 0, cap, l.fit, l.nfit, l.fit_cap, nullptr,
+        launch(c, k_segscan<U>, 1, 1024, 0, z.seg, z.nseg, z.P, z.tot, z.sk, 0, cap, l.fit, l.nfit, l.fit_cap, nullptr,
                                           nullptr, 0, counts_out, c.status);
         c.check();
         if (mark_phases) c.mark(2);
@@ -251,14 +277,14 @@ template <int DT, bool KV> struct Engine {
             const size_t sm_w = wc_smem_bytes<U>(z.P);
             auto kw = k_scatter_wc<DT, WC_NT, IT>;
             OVS_CK(cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_w));
-            kw<<<z.nchunk, WC_NT, sm_w, c.st>>>(B, z.chunks, z.nchunks, z.seg, z.P, z.hist, z.tot, z.bid);
+            launch(c, kw, z.nchunk, WC_NT, sm_w, B, z.chunks, z.nchunks, z.seg, z.P, z.hist, z.tot, z.bid);
             c.check();
         } else {
             constexpr int IT = PartItems<U, KV>::v;
             const size_t sm_s = scatter_smem(z.P, z.L);
             auto ks = k_scatter<DT, KV, true, PT_NT, IT>;
             OVS_CK(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_s));
-            ks<<<z.nchunk, PT_NT, sm_s, c.st>>>(B, z.chunks, z.nchunks, z.seg, z.sk, z.st, z.lut, z.P, z.L, z.hist,
+            launch(c, ks, z.nchunk, PT_NT, sm_s, B, z.chunks, z.nchunks, z.seg, z.sk, z.st, z.lut, z.P, z.L, z.hist,
                                                 z.tot, tag_base);
             c.check();
         }
@@ -266,7 +292,7 @@ template <int DT, bool KV> struct Engine {
     }
 
     void set_pair(u32* p, u32 a, u32 b) {
-        k_set2<<<1, 1, 0, c.st>>>(p, a, b);
+        launch(c, k_set2, 1, 1, 0, p, a, b);
         c.check();
     }
 
@@ -278,8 +304,8 @@ template <int DT, bool KV> struct Engine {
         if (!okeys) { okeys = B.k[0]; ovals = KV ? B.v[0] : nullptr; }
         const size_t sm = bucket_smem<U, KV>(cap);
         OVS_CK(cudaFuncSetAttribute(k_bucket_sort<DT, KV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        k_bucket_sort<DT, KV><<<l.grid, BS_NT, sm, c.st>>>(l.fit, l.nfit, l.ticket, B, okeys, ovals, oidx, out_raw,
-                                                          cap, l.stack, seed, c.status);
+        launch(c, k_bucket_sort<DT, KV>, l.grid, BS_NT, sm, l.fit, l.nfit, l.ticket, B, okeys, ovals, oidx, out_raw,
+                                                          cap, l.stack, seed, c.status, ixbits);
         c.check();
     }
 };
@@ -310,10 +336,10 @@ template <bool KV> struct InternalSort {
         Ctx& c = e.c;
         if (c.dry || e.n == 0) return;
         if (direct) {
-            if (KV) { k_iota<<<cdiv(e.n, 256), 256, 0, c.st>>>(e.B.i[0], e.n); c.check(); }
-            k_fill_u32<<<1, 2, 0, c.st>>>(l.nfit, 0, 2);
+            if (KV) { launch(c, k_iota, cdiv(e.n, 256), 256, 0, e.B.i[0], e.n); c.check(); }
+            launch(c, k_fill_u32, 1, 2, 0, l.nfit, 0, 2);
             c.check();
-            k_push_bucket<u64><<<1, 1, 0, c.st>>>(l.fit, l.nfit, e.n);
+            launch(c, k_push_bucket<u64>, 1, 1, 0, l.fit, l.nfit, e.n);
             c.check();
         } else {
             e.internal_splitters(z, seed);
@@ -358,13 +384,13 @@ template <bool TAG> struct Selector {
         Ctx& c = e.c;
         if (c.dry) return;
         const u32 grid = cdiv(m, SEL_PER);
-        k_sel_count<TAG><<<grid, 1024, 0, c.st>>>(tk, tt, m, G, csk, cst, cb, gcnt);
+        launch(c, k_sel_count<TAG>, grid, 1024, 0, tk, tt, m, G, csk, cst, cb, gcnt);
         c.check();
-        k_sel_scatter<TAG><<<grid, 1024, 0, c.st>>>(tk, tt, m, G, cb, gcnt, gcur, csk, e.B.k[0], e.B.v[0], e.B.i[0],
+        launch(c, k_sel_scatter<TAG>, grid, 1024, 0, tk, tt, m, G, cb, gcnt, gcur, csk, e.B.k[0], e.B.v[0], e.B.i[0],
                                                     l.fit, l.nfit);
         c.check();
         e.bucket_sort(l, seed);
-        k_pick_splitters<U><<<cdiv(P, 256), 256, 0, c.st>>>(e.B.k[0], e.B.k[0], e.B.v[0], P, s, sk, st);
+        launch(c, k_pick_splitters<U>, cdiv(P, 256), 256, 0, e.B.k[0], e.B.k[0], e.B.v[0], P, s, sk, st);
         c.check();
     }
 };
@@ -400,15 +426,15 @@ template <int DT, bool DIST> struct RosSampler {
     void draw(u64 seed) {
         if (c.dry) return;
         OVS_CK(cudaMemsetAsync(zero, 0, zero_bytes(), c.st));
-        k_ros_draw<<<cdiv(M, 256), 256, 0, c.st>>>(zero, lg, M, n, seed);
+        launch(c, k_ros_draw, cdiv(M, 256), 256, 0, zero, lg, M, n, seed);
         c.check();
-        k_ros_first<<<nb, TK_NT, 0, c.st>>>(zero, lg, M, n, seed, bits, bcnt);
+        launch(c, k_ros_first, nb, TK_NT, 0, zero, lg, M, n, seed, bits, bcnt);
         c.check();
     }
     // records of the members of I (DIST: of the shard [offset, offset + nl), into rec)
     void take(u64 seed, const U* x, u64 offset, u32 nl, u64* rec) {
         if (c.dry) return;
-        k_ros_take<DT, DIST><<<nb, TK_NT, 0, c.st>>>(bits, bcnt, M, n, seed, m, x, offset, nl, DIST ? rec : tk, tt,
+        launch(c, k_ros_take<DT, DIST>, nb, TK_NT, 0, bits, bcnt, M, n, seed, m, x, offset, nl, DIST ? rec : tk, tt,
                                                       c.status);
         c.check();
     }
@@ -429,6 +455,7 @@ template <int DT, bool KV> struct RosSort {
 
     RosSort(Ctx& ctx, U* keys, u32* vals, u32 n_, u32 p_, u32 s_, u64 seed_) : c(ctx), e(ctx), n(n_), p(p_), s(s_), seed(seed_) {
         e.n = n;
+        e.ixbits = bits_for(n);
         e.cap = bucket_cap<U, KV>(c.di);
         e.B.k[0] = keys;
         e.B.v[0] = vals;
@@ -519,6 +546,7 @@ template <int DT, bool KV> struct DroSort {
     DroSort(Ctx& ctx, U* keys, u32* vals, u32 n_, u32 p_, u32 r_, u32 flags_)
         : c(ctx), e(ctx), n(n_), p(p_), r(r_), flags(flags_) {
         e.n = n;
+        e.ixbits = bits_for(n);
         e.cap = bucket_cap<U, KV>(c.di);
         e.B.k[0] = keys;
         e.B.v[0] = vals;
@@ -555,34 +583,34 @@ template <int DT, bool KV> struct DroSort {
         c.mark(0);
         // a9: BaselineSorting of the p sequences -> buffer 1 (ordered keys, values, indices)
         fill_u32(c, l1.nfit, 0, 2);
-        k_dro_segments<<<cdiv(p, 256), 256, 0, c.st>>>(l1.fit, l1.nfit, n, p);
+        launch(c, k_dro_segments, cdiv(p, 256), 256, 0, l1.fit, l1.nfit, n, p);
         c.check();
         e.bucket_sort(l1, 0x5e9u, B.k[1], KV ? B.v[1] : nullptr, KV ? B.i[1] : nullptr, false);
         // a10-a12: regular sample, sample sort, splitters
-        k_dro_sample<U><<<cdiv((u64)ns, 256), 256, 0, c.st>>>(B.k[1], n, p, s, flags & OVS_DRO_PADDED_POSITIONS,
+        launch(c, k_dro_sample<U>, cdiv((u64)ns, 256), 256, 0, B.k[1], n, p, s, flags & OVS_DRO_PADDED_POSITIONS,
                                                              t_pack, t_key, t_tag);
         c.check();
         if (ts32) ts32->run(0xd0d0);
         else ts64->run(0xd0d0);
-        k_pick_splitters<U><<<cdiv(p, 256), 256, 0, c.st>>>(t_pack, t_key, t_tag, p, s, sk, st);
+        launch(c, k_pick_splitters<U>, cdiv(p, 256), 256, 0, t_pack, t_key, t_tag, p, s, sk, st);
         c.check();
         c.mark(1);
         // a13: split every sorted sequence by binary search; bucket starts and run offsets
-        k_dro_bounds<U><<<cdiv((u64)p * (p + 1), 256), 256, 0, c.st>>>(B.k[1], n, p, sk, st, bound);
+        launch(c, k_dro_bounds<U>, cdiv((u64)p * (p + 1), 256), 256, 0, B.k[1], n, p, sk, st, bound);
         c.check();
-        k_dro_counts<<<cdiv((u64)p * p, 256), 256, 0, c.st>>>(bound, p, cnt);
+        launch(c, k_dro_counts, cdiv((u64)p * p, 256), 256, 0, bound, p, cnt);
         c.check();
-        k_dro_seg<U><<<1, 1024, 0, c.st>>>(B.k[1], n, p, sk, 0, seg, nseg);
+        launch(c, k_dro_seg<U>, 1, 1024, 0, B.k[1], n, p, sk, 0, seg, nseg);
         c.check();
-        k_colscan<<<std::min<u32>(cdiv(p, 32), 4 * c.di.sms), 1024, 0, c.st>>>(cnt, seg, nseg, p, tot);
+        launch(c, k_colscan, std::min<u32>(cdiv(p, 32), 4 * c.di.sms), 1024, 0, cnt, seg, nseg, p, tot);
         c.check();
         fill_u32(c, l2.nfit, 0, 2);
-        k_segscan<U><<<1, 1024, 0, c.st>>>(seg, nseg, p, tot, sk, 0, e.cap, l2.fit, l2.nfit, l2.fit_cap, nullptr,
+        launch(c, k_segscan<U>, 1, 1024, 0, seg, nseg, p, tot, sk, 0, e.cap, l2.fit, l2.nfit, l2.fit_cap, nullptr,
                                           nullptr, 0, counts, c.status);
         c.check();
         c.mark(2);
         // a14: gather the runs X_{k,j} of every bucket (k order) into buffer 0, sort each bucket
-        k_dro_gather<U, KV><<<cdiv((u64)p * p * 32, 256), 256, 0, c.st>>>(B, n, p, bound, cnt, tot);
+        launch(c, k_dro_gather<U, KV>, cdiv((u64)p * p * 32, 256), 256, 0, B, n, p, bound, cnt, tot);
         c.check();
         c.mark(3);
         e.bucket_sort(l2, 0x5e9u);
@@ -615,6 +643,7 @@ template <int DT, bool KV> struct DistSort {
         e.cap = bucket_cap<U, KV>(c.di);
         f.n = recv_cap;
         f.cap = e.cap;
+        f.ixbits = bits_for(ng);
         m = p * s - 1;
         M = ros_draws(ng, m);
         words = sizeof(U) == 4 ? 1 : 2;
@@ -642,7 +671,7 @@ template <int DT, bool KV> struct DistSort {
 
     void partition(U* keys, u32* vals, const u64* rec, U* send_k, u32* send_v, u32* send_i, u32* counts) {
         if (c.dry) return;
-        k_dist_unpack<<<cdiv(m, 256), 256, 0, c.st>>>(rec, m, words, smp->tk, smp->tk, smp->tt);
+        launch(c, k_dist_unpack, cdiv(m, 256), 256, 0, rec, m, words, smp->tk, smp->tk, smp->tt);
         c.check();
         // the coarse-bucket counters are zeroed here too: this call may run on a fresh process
         OVS_CK(cudaMemsetAsync(smp->sel->gcnt, 0, 8 * SEL_GMAX, c.st));
@@ -652,18 +681,18 @@ template <int DT, bool KV> struct DistSort {
         e.B.i[0] = nullptr;
         e.tag_base = (u32)offset;
         e.level0(z, l, counts64);
-        k_u64_to_u32<<<cdiv(p, 256), 256, 0, c.st>>>(counts64, counts, p);
+        launch(c, k_u64_to_u32, cdiv(p, 256), 256, 0, counts64, counts, p);
         c.check();
     }
 
     void finish(const U* rk, const u32* rv, const u32* ri, const u32* C, u32 rnk, U* out_k, u32* out_v) {
         if (c.dry) return;
-        k_dist_plan<U><<<1, 1024, 0, c.st>>>(C, world, p, rnk, z.sk, bstart, srcoff, lf.fit, lf.nfit, recv_cap, c.status);
+        launch(c, k_dist_plan<U>, 1, 1024, 0, C, world, p, rnk, z.sk, bstart, srcoff, lf.fit, lf.nfit, recv_cap, c.status);
         c.check();
         const u32 nb = (u32)((u64)(rnk + 1) * p / world) - (u32)((u64)rnk * p / world);
         f.B.k[0] = out_k;
         f.B.v[0] = out_v;
-        k_dist_gather<U, KV><<<cdiv((u64)world * nb * 32, 256), 256, 0, c.st>>>(
+        launch(c, k_dist_gather<U, KV>, cdiv((u64)world * nb * 32, 256), 256, 0, 
             rk, rv, ri, out_k, out_v, f.B.i[0], C, world, p, rnk, bstart, srcoff);
         c.check();
         fill_u32(c, lf.ticket, 0, 1);

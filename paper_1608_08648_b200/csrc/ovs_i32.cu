@@ -9,3 +9,16 @@ size_t dist_i32(Ctx& c, int step, const ovs_params* prm, const DistArgs& a, bool
     return kv ? dist_run<DT_I32, true>(c, step, prm, a) : dist_run<DT_I32, false>(c, step, prm, a);
 }
 }  // namespace ovs
+
+#ifdef OVS_BS_PROF  // experiments only: bucket-sorter phase cycles of this translation unit's kernels
+extern "C" int ovs_debug_bsprof_i32(unsigned long long* out, int reset) {
+    unsigned long long v[16];
+    if (cudaMemcpyFromSymbol(v, ovs::g_bsprof, sizeof(v)) != cudaSuccess) return 1;
+    for (int i = 0; i < 16; ++i) out[i] += v[i];
+    if (reset) {
+        unsigned long long z[16] = {0};
+        cudaMemcpyToSymbol(ovs::g_bsprof, z, sizeof(z));
+    }
+    return 0;
+}
+#endif

@@ -21,6 +21,15 @@ typedef uint32_t u32;
 typedef uint64_t u64;
 typedef uint16_t u16;
 
+// ------------------------------------------------------------------ programmatic dependent launch
+// First statement of every kernel (see launch() in ovs_engine.cuh): allow the next kernel on the
+// stream to be scheduled once all CTAs of this one have started, then wait until the previous
+// kernel has completed and its memory is visible.  Both are no-ops without the PDL attribute.
+#ifndef OVS_PDL
+#define OVS_PDL 0
+#endif
+#define PDL_PROLOGUE() asm volatile("griddepcontrol.launch_dependents;\n\tgriddepcontrol.wait;" ::: "memory")
+
 // ------------------------------------------------------------------ key codecs
 // Keys are compared as "ordered bits": an order-preserving map to unsigned integers
 // (native < on u32; sign flip on i32; IEEE total order on f64 without NaN / -0, reading Q18).
@@ -306,6 +315,7 @@ __device__ __forceinline__ u32 ht_slot(u64 c, u32 lg) { return (u32)((c * 0x9e37
 __device__ __forceinline__ u64 ros_draw_c(u64 seed, u32 j, u64 n) { return __umul64hi(rng_H(seed, 1, j), n); }
 
 __global__ void k_ros_draw(u64* tab, u32 lg, u32 M, u64 n, u64 seed) {
+    PDL_PROLOGUE();
     const u32 j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= M) return;
     const u64 c = ros_draw_c(seed, j, n);
@@ -335,6 +345,7 @@ __device__ __forceinline__ u32 ht_min_j(const u64* tab, u32 lg, u64 c) {
 constexpr int TK_NT = 1024;
 // per block of TK_NT draws: the warps' masks of first draws, and the block's count
 __global__ void __launch_bounds__(TK_NT) k_ros_first(const u64* tab, u32 lg, u32 M, u64 n, u64 seed, u32* bits, u32* bcnt) {
+    PDL_PROLOGUE();
     __shared__ u32 wcnt[TK_NT / 32];
     const u32 j = blockIdx.x * TK_NT + threadIdx.x;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -360,6 +371,7 @@ template <int DT, bool DIST>
 __global__ void __launch_bounds__(TK_NT) k_ros_take(const u32* bits, const u32* bcnt, u32 M, u64 n, u64 seed, u32 m,
                                                      const typename Codec<DT>::U* x, u64 offset, u32 nl, u64* tk, u32* tt,
                                                      u32* status) {
+    PDL_PROLOGUE();
     typedef typename Codec<DT>::U U;
     __shared__ u32 red[TK_NT / 32], wpre[TK_NT / 32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -423,6 +435,7 @@ __device__ __forceinline__ u32 coarse_of(const u64* ck, const u32* ct, u32 nc, u
 template <bool TAG>
 __global__ void __launch_bounds__(1024) k_sel_count(const u64* tk, const u32* tt, u32 m, u32 G, u64* csk, u32* cst,
                                                     uint8_t* cb, u32* gcnt) {
+    PDL_PROLOGUE();
     __shared__ u64 qk[SEL_Q];
     __shared__ u32 qt[SEL_Q];
     __shared__ u32 h[SEL_GMAX];
@@ -470,6 +483,7 @@ template <bool TAG>
 __global__ void __launch_bounds__(1024) k_sel_scatter(const u64* tk, const u32* tt, u32 m, u32 G, const uint8_t* cb,
                                                       const u32* gcnt, u32* gcur, const u64* csk, u64* ok, u32* ot,
                                                       u32* oi, Bucket* list, u32* nlist) {
+    PDL_PROLOGUE();
     __shared__ u32 st[SEL_GMAX + 1], h[SEL_GMAX], base[SEL_GMAX];
     if (threadIdx.x == 0) {
         u32 run = 0;
@@ -519,6 +533,7 @@ __global__ void __launch_bounds__(1024) k_sel_scatter(const u64* tk, const u32* 
 template <class U>
 __global__ void k_pick_splitters(const u64* t_pack, const u64* t_key, const u32* t_tag, u32 P, u32 s,
                                  U* sk, u32* st) {
+    PDL_PROLOGUE();
     u32 q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q + 1 >= P) return;
     u64 r = (u64)(q + 1) * s - 1;
@@ -550,6 +565,7 @@ __device__ u32 count_less_key(const U* sk, u32 nsp, U thr) {
 template <class U>
 __global__ void __launch_bounds__(1024) k_build_cls0(const U* sk, u32 P, u32 L, u32 log2L, u32* lut, Seg* seg, u32 n,
                                                      u32 nchunk) {
+    PDL_PROLOGUE();
     extern __shared__ __align__(16) char smem[];
     U* s = (U*)smem;
     for (u32 i = threadIdx.x; i + 1 < P; i += blockDim.x) s[i] = sk[i];
@@ -583,6 +599,7 @@ __global__ void __launch_bounds__(1024) k_build_cls0(const U* sk, u32 P, u32 L, 
 }
 
 __global__ void k_make_chunks0(Chunk* ch, u32 nchunk, u32 n, u32 chunk) {
+    PDL_PROLOGUE();
     u32 c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= nchunk) return;
     Chunk x;
@@ -671,6 +688,7 @@ __global__ void __launch_bounds__(NT, OVS_HIST_MINB) k_hist(Bufs<typename Codec<
                                              Seg* segs, const typename Codec<DT>::U* sk_pool, const u32* st_pool,
                                              const u32* lut_pool, u32 PS, u32 LS, u32* hist, u32 split,
                                              u32 tag_base, u16* bid) {
+    PDL_PROLOGUE();
     // `split` CTAs share a chunk (each a contiguous part) and add into its (zeroed) row;
     // bid != NULL: every key's bucket is also stored (bid[i]: the scatter then skips classify)
     typedef typename Codec<DT>::U U;
@@ -709,17 +727,29 @@ __global__ void __launch_bounds__(NT, OVS_HIST_MINB) k_hist(Bufs<typename Codec<
         if (threadIdx.x < head) body(src[pbeg + threadIdx.x], threadIdx.x);
         const uint4* a4 = (const uint4*)(src + pbeg + head);
         const u32 nv = (m - head) / V;
+        // software pipelined: the next batch's vectors are loaded before this batch is classified
+        uint4 nr[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const u32 idx = u * NT + threadIdx.x;
+            nr[u] = idx < nv ? __ldcs(a4 + idx) : make_uint4(0, 0, 0, 0);
+        }
         for (u32 v0 = 0; v0 < nv; v0 += NT * UNR) {
             U kk[NB];
             u32 vm = 0;
 #pragma unroll
             for (int u = 0; u < UNR; ++u) {
                 const u32 idx = v0 + u * NT + threadIdx.x;
-                uint4 r = make_uint4(0, 0, 0, 0);
-                if (idx < nv) { r = __ldcs(a4 + idx); vm |= ((1u << V) - 1) << (u * V); }
+                const uint4 r = nr[u];
+                if (idx < nv) vm |= ((1u << V) - 1) << (u * V);
                 const U* e = (const U*)&r;
 #pragma unroll
                 for (u32 x = 0; x < V; ++x) kk[u * V + x] = LEVEL0 ? Codec<DT>::ord(e[x]) : e[x];
+            }
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const u32 idx = v0 + NT * UNR + u * NT + threadIdx.x;
+                nr[u] = idx < nv ? __ldcs(a4 + idx) : make_uint4(0, 0, 0, 0);
             }
             u32 bb[NB];
             classify_n<U, NB>(cls, kk, [&](int j) -> u32 {
@@ -778,6 +808,7 @@ __global__ void __launch_bounds__(NT, OVS_HIST_MINB) k_hist(Bufs<typename Codec<
 // hist[c][b], in place; totals -> tot[s*(PS+1) + b].  Warp w owns a contiguous slice of
 // chunks, lane = bucket.
 __global__ void __launch_bounds__(1024) k_colscan(u32* hist, const Seg* segs, const u32* nsegs, u32 PS, u32* tot) {
+    PDL_PROLOGUE();
     __shared__ u32 part[32][33];
     const u32 bgroups = (PS + 31) / 32;
     const u32 nitems = *nsegs * bgroups;
@@ -820,8 +851,8 @@ template <class U>
 __global__ void __launch_bounds__(1024) k_segscan(const Seg* segs, const u32* nsegs, u32 PS, u32* tot_pool,
                                                   const U* sk_pool, u32 level, u32 cap, Bucket* fit, u32* nfit,
                                                   u32 fit_cap, Bucket* big, u32* nbig, u32 big_cap, u64* counts_out,
-                                                  u32* status, u32 outbuf = 2) {
-    // outbuf: the buffer the buckets are in (2: the other one than the segment's source)
+                                                  u32* status) {
+    PDL_PROLOGUE();
     __shared__ u32 red[33];
     const u32 ns = *nsegs;
     const u32 lane = threadIdx.x & 31;
@@ -848,7 +879,7 @@ __global__ void __launch_bounds__(1024) k_segscan(const Seg* segs, const u32* ns
             ob = __shfl_sync(0xffffffffu, ob, 0) + __popc(mb & ((1u << lane) - 1));
             if (isfit || isbig) {
                 Bucket bk;
-                bk.beg = sg.beg + st; bk.len = len; bk.buf = outbuf < 2 ? outbuf : 1 - sg.src;
+                bk.beg = sg.beg + st; bk.len = len; bk.buf = 1 - sg.src;
                 bk.level = level | (((b == 0 || b + 1 == sg.P) && sg.loose) ? BK_LOOSE : 0u);
                 bk.lo = (b == 0) ? sg.lo : (u64)sk[b - 1];
                 bk.hi = (b + 1 == sg.P) ? sg.hi : (u64)sk[b];
@@ -876,6 +907,7 @@ __global__ void __launch_bounds__(NT) k_scatter(Bufs<typename Codec<DT>::U> B, c
                                                 const Seg* segs, const typename Codec<DT>::U* sk_pool,
                                                 const u32* st_pool, const u32* lut_pool, u32 PS, u32 LS,
                                                 const u32* hist, const u32* tot_pool, u32 tag_base) {
+    PDL_PROLOGUE();
     typedef typename Codec<DT>::U U;
     constexpr int TS = NT * ITEMS;
     extern __shared__ __align__(16) char smem[];
@@ -1013,6 +1045,7 @@ template <int DT, int NT, int ITEMS>
 __global__ void __launch_bounds__(NT, 1) k_scatter_wc(Bufs<typename Codec<DT>::U> B, const Chunk* chunks,
                                                        const u32* nchunks, const Seg* segs, u32 PS, const u32* hist,
                                                        const u32* tot_pool, const u16* bid) {
+    PDL_PROLOGUE();
     typedef typename Codec<DT>::U U;
     constexpr u32 SV = 32 / sizeof(U);  // keys per 32-byte sector
     constexpr u32 V = 16 / sizeof(U);   // keys per 16-byte vector
@@ -1187,6 +1220,7 @@ __device__ __forceinline__ void mbar_wait(u64* bar, u32 parity) {
 template <int DT, bool KV>
 __global__ void __launch_bounds__(1024) k_internal_sample(Bufs<typename Codec<DT>::U> B, u32 n, u32 P, u32 si, u32 N,
                                                           u64 seed, typename Codec<DT>::U* sk, u32* st) {
+    PDL_PROLOGUE();
     typedef typename Codec<DT>::U U;
     extern __shared__ __align__(16) char smem[];
     U* tk = (U*)smem;
@@ -1408,7 +1442,9 @@ template <int DT, bool KV>
 __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, const u32* nlist, u32* ticket,
                                                            Bufs<typename Codec<DT>::U> B, typename Codec<DT>::U* okeys,
                                                            u32* ovals, u32* oidx, bool out_raw, u32 cap,
-                                                           Bucket* stack_pool, u64 seed, u32* status) {
+                                                           Bucket* stack_pool, u64 seed, u32* status, u32 ixbits) {
+    // ixbits: key-value sorts' indices are < 2^ixbits
+    PDL_PROLOGUE();
     typedef typename Codec<DT>::U U;
     typedef Elem<U, KV> E;
     extern __shared__ __align__(16) char smem[];
@@ -1419,6 +1455,8 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
     __shared__ U s_mn[BS_NT / 32], s_mx[BS_NT / 32];
     __shared__ U sp_k[BS_SPMAX];
     __shared__ u32 sp_t[BS_SPMAX], sp_cnt[BS_SPMAX + 1], sp_cur[BS_SPMAX];
+    __shared__ u32 rs_cnt[BS_SPMAX], rs_off[BS_SPMAX];
+    __shared__ int rs_base[BS_SPMAX];
     BucketSmem<U, KV> S;
     {
         char* sp = smem;
@@ -1479,7 +1517,7 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
             BS_T0
             if (m > cap) {
                 // ---------------- CTA-local re-split of an oversized bucket
-                const u32 part = (u32)((cap * 45ull) / 100);
+                const u32 part = (u32)((cap * 60ull) / 100);
                 u32 P = (m + part - 1) / part;
                 P = max(2u, min(BS_SPMAX, P));
                 const u32 ms = P * BS_SI - 1;
@@ -1503,6 +1541,7 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                     sp_t[threadIdx.x] = tt[(threadIdx.x + 1) * BS_SI - 1];
                 }
                 if (threadIdx.x <= P) sp_cnt[threadIdx.x] = 0;
+                if (threadIdx.x < BS_SPMAX) rs_cnt[threadIdx.x] = 0;
                 __syncthreads();
                 for_items<U, BS_NT, OVS_BS_UNR>(src, bk.beg, m, [&](U kr, u32 o) {
                     const U k = K(kr);
@@ -1516,16 +1555,63 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                     sp_cnt[P] = run;
                 }
                 __syncthreads();
+                // scatter in tiles of RS_IT * BS_NT items staged in shared memory by sub-bucket, so
+                // every sub-bucket's items of a tile leave as one coalesced run (whole sectors)
                 const u32 db = 1 - bk.buf;
-                for_items<U, BS_NT, OVS_BS_UNR>(src, bk.beg, m, [&](U kr, u32 o) {
-                    const U k = K(kr);
-                    const u32 tg = IX(bk.beg + o);
-                    const u32 b = lower_bound_kt<U>(sp_k, sp_t, P - 1, k, tg);
-                    const u32 d = bk.beg + atomicAdd(&sp_cur[b], 1u);
-                    B.k[db][d] = k;
-                    if (KV) { B.v[db][d] = vsrc[bk.beg + o]; B.i[db][d] = tg; }
-                });
-                __syncthreads();
+                constexpr u32 RS_IT = 8, RT = RS_IT * BS_NT;
+                uint8_t* sbk = (uint8_t*)S.cnt;  // sub-bucket of each staged item
+                for (u32 t0 = 0; t0 < m; t0 += RT) {
+                    const u32 nt = min(RT, m - t0);
+                    U kk[RS_IT];
+                    u32 tg[RS_IT], vv[RS_IT], bb[RS_IT], rr[RS_IT];
+#pragma unroll
+                    for (u32 j = 0; j < RS_IT; ++j) {
+                        const u32 o = j * BS_NT + threadIdx.x;
+                        if (o < nt) {
+                            kk[j] = K(src[bk.beg + t0 + o]);
+                            tg[j] = IX(bk.beg + t0 + o);
+                            if (KV) vv[j] = vsrc[bk.beg + t0 + o];
+                        }
+                    }
+#pragma unroll
+                    for (u32 j = 0; j < RS_IT; ++j) {
+                        if (j * BS_NT + threadIdx.x < nt) {
+                            bb[j] = lower_bound_kt<U>(sp_k, sp_t, P - 1, kk[j], tg[j]);
+                            rr[j] = atomicAdd(&rs_cnt[bb[j]], 1u);
+                        }
+                    }
+                    __syncthreads();
+                    if (threadIdx.x < 32) {  // tile offsets (P <= 64: two per lane) and run bases
+                        const u32 b0 = 2 * threadIdx.x, b1 = b0 + 1;
+                        const u32 c0 = b0 < P ? rs_cnt[b0] : 0u, c1 = b1 < P ? rs_cnt[b1] : 0u;
+                        u32 x = c0 + c1;
+#pragma unroll
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const u32 y = __shfl_up_sync(0xffffffffu, x, o);
+                            if (threadIdx.x >= (u32)o) x += y;
+                        }
+                        const u32 ex = x - c0 - c1;
+                        if (b0 < P) { rs_off[b0] = ex; rs_base[b0] = (int)sp_cur[b0] - (int)ex; sp_cur[b0] += c0; rs_cnt[b0] = 0; }
+                        if (b1 < P) { rs_off[b1] = ex + c0; rs_base[b1] = (int)sp_cur[b1] - (int)(ex + c0); sp_cur[b1] += c1; rs_cnt[b1] = 0; }
+                    }
+                    __syncthreads();
+#pragma unroll
+                    for (u32 j = 0; j < RS_IT; ++j) {
+                        if (j * BS_NT + threadIdx.x < nt) {
+                            const u32 s = rs_off[bb[j]] + rr[j];
+                            S.k[s] = kk[j];
+                            sbk[s] = (uint8_t)bb[j];
+                            if (KV) { S.i[s] = tg[j]; S.v[s] = vv[j]; }
+                        }
+                    }
+                    __syncthreads();
+                    for (u32 s = threadIdx.x; s < nt; s += BS_NT) {
+                        const u32 d = bk.beg + (u32)(rs_base[sbk[s]] + (int)s);
+                        B.k[db][d] = S.k[s];
+                        if (KV) { B.v[db][d] = S.v[s]; B.i[db][d] = S.i[s]; }
+                    }
+                    __syncthreads();
+                }
                 if (threadIdx.x == 0) {
                     u32 sp = s_sp;
                     for (int b = (int)P - 1; b >= 0; --b) {
@@ -1569,10 +1655,14 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
             while (ng < (u32)BS_NGMAX && ng * 3 < m) ng <<= 1;
             // digit = floor(x * ng / R) for x = (sort key - lo) in [0, R): monotone in the key
             // and spreads [lo, hi] over all ng groups (computed as a 64-bit fixed-point
-            // multiply-high).  Key-value sorts of 32-bit keys use the composite (key, index);
-            // 64-bit keys use the key (equal keys then share a group, ordered by index).
+            // multiply-high).  Key-value sorts of 32-bit keys use the composite (key, index) with
+            // the index in its ixbits low bits (indices < 2^ixbits, so the groups spread over the
+            // indices that occur); 64-bit keys use the key (equal keys share a group, ordered by
+            // index).  R <= ng: digit = x, every group holds one key value (keys only: the groups
+            // need no sorting, e.g. few distinct keys).
             const bool comp = KV && sizeof(U) == 4;
-            const u64 xmax = comp ? ((((u64)(hi - lo)) << 32) | 0xffffffffull) : (u64)(U)(hi - lo);
+            const u64 xmax = comp ? ((((u64)(hi - lo)) << ixbits) | ((1ull << ixbits) - 1)) : (u64)(U)(hi - lo);
+            const bool direct = xmax < (u64)ng;
             // multiplier ~ ng * 2^64 / R in double precision: any multiplier keeps the digit monotone
             // (and the clamp keeps it < ng), so rounding only perturbs the group sizes slightly
             const double mq = (double)ng * 18446744073709551616.0 / ((double)xmax + 1.0);
@@ -1581,12 +1671,14 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
             const u32 mult32 = mq32 >= 4294967295.0 ? 0xffffffffu : (u32)mq32;
             auto digit = [&](U k, u32 ix) -> u32 {
                 if constexpr (!KV && sizeof(U) == 4) {
-                    return min(__umulhi((u32)(k - lo), mult32), ng - 1);  // min: memory safety only
+                    const u32 x = (u32)(k - lo);
+                    return direct ? x : min(__umulhi(x, mult32), ng - 1);  // min: memory safety only
                 } else {
-                    const u64 x = comp ? ((((u64)(k - lo)) << 32) | ix) : (u64)(U)(k - lo);
-                    return min((u32)__umul64hi(x, mult), ng - 1);
+                    const u64 x = comp ? ((((u64)(k - lo)) << ixbits) | ix) : (u64)(U)(k - lo);
+                    return direct ? (u32)x : min((u32)__umul64hi(x, mult), ng - 1);
                 }
             };
+            const bool need_sort = KV || !direct;
             for (u32 g = threadIdx.x; g < ng; g += BS_NT) Sa.cnt[g] = 0;
             __syncthreads();
             BS_PROBE(2)
@@ -1613,7 +1705,7 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
             // 3. one thread per group of <= 8: Batcher network in registers; larger groups are
             // appended (warp-aggregated) to a list for 3b
             // (OVS_NET8_X: groups per thread per iteration, their loads and networks interleaved)
-            for (u32 g0 = 0; g0 < ng; g0 += BS_NT * OVS_NET8_X) {
+            for (u32 g0 = 0; need_sort && g0 < ng; g0 += BS_NT * OVS_NET8_X) {
                 u32 gs[OVS_NET8_X], len[OVS_NET8_X];
                 E a[OVS_NET8_X][8];
 #pragma unroll
@@ -1761,6 +1853,7 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
 // a9: the p baseline sequences X_k (first n mod p get ceil(n/p) keys, reading Q8), as
 // buckets of the caller's raw keys (sorted stably by the bucket sorter into buffer 1)
 __global__ void k_dro_segments(Bucket* list, u32* nlist, u32 n, u32 p) {
+    PDL_PROLOGUE();
     const u32 k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= p) return;
     const u32 q = n / p, rm = n % p;
@@ -1780,6 +1873,7 @@ __global__ void k_dro_segments(Bucket* list, u32* nlist, u32 n, u32 p) {
 // 32-bit keys are packed (ord key << 32 | tag); 64-bit keys stored with a separate tag.
 template <class U>
 __global__ void k_dro_sample(const U* xs, u32 n, u32 p, u32 s, u32 padded, u64* t_pack, u64* t_key, u32* t_tag) {
+    PDL_PROLOGUE();
     const u64 id = (u64)blockIdx.x * blockDim.x + threadIdx.x;
     if (id >= (u64)s * p) return;
     const u32 k = (u32)(id / s), j = (u32)(id % s);
@@ -1803,6 +1897,7 @@ __global__ void k_dro_sample(const U* xs, u32 n, u32 p, u32 s, u32 padded, u64* 
 // into the sorted X_k; count matrix cnt[k][j] = bound[k][j+1]-bound[k][j]
 template <class U>
 __global__ void k_dro_bounds(const U* xs, u32 n, u32 p, const U* sk, const u32* st, u32* bound) {
+    PDL_PROLOGUE();
     const u64 id = (u64)blockIdx.x * blockDim.x + threadIdx.x;
     if (id >= (u64)p * (p + 1)) return;
     const u32 k = (u32)(id / (p + 1)), j = (u32)(id % (p + 1));
@@ -1828,6 +1923,7 @@ __global__ void k_dro_bounds(const U* xs, u32 n, u32 p, const U* sk, const u32* 
 }
 
 __global__ void k_dro_counts(const u32* bound, u32 p, u32* cnt) {
+    PDL_PROLOGUE();
     const u64 id = (u64)blockIdx.x * blockDim.x + threadIdx.x;
     if (id >= (u64)p * p) return;
     const u32 k = (u32)(id / p), j = (u32)(id % p);
@@ -1838,6 +1934,7 @@ __global__ void k_dro_counts(const u32* bound, u32 p, u32* cnt) {
 // the whole input from the sorted sequences' first and last keys
 template <class U>
 __global__ void k_dro_seg(const U* xs, u32 n, u32 p, const U* sk, u32 L, Seg* seg, u32* nseg) {
+    PDL_PROLOGUE();
     __shared__ U smn[32], smx[32];
     const u32 q = n / p, rm = n % p;
     U mn = umax_of<U>(), mx = 0;
@@ -1867,6 +1964,7 @@ __global__ void k_dro_seg(const U* xs, u32 n, u32 p, const U* sk, u32 L, Seg* se
 // offset start_j + sum_{k'<k} cnt[k'][j] (column-scanned cnt); one warp per run
 template <class U, bool KV>
 __global__ void k_dro_gather(Bufs<U> B, u32 n, u32 p, const u32* bound, const u32* off, const u32* bstart) {
+    PDL_PROLOGUE();
     const u64 w = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const u32 lane = threadIdx.x & 31;
     if (w >= (u64)p * p) return;
@@ -1886,6 +1984,7 @@ __global__ void k_dro_gather(Bufs<U> B, u32 n, u32 p, const u32* bound, const u3
 // contributes the records of its own shard (k_ros_take<DT, true>); after the all-reduce SUM
 // the records are unpacked into the sample sort's arrays.
 __global__ void k_dist_unpack(const u64* rec, u32 m, u32 words, u64* t_pack, u64* t_key, u32* t_tag) {
+    PDL_PROLOGUE();
     const u32 t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= m) return;
     if (words == 1) t_pack[t] = rec[t];
@@ -1893,6 +1992,7 @@ __global__ void k_dist_unpack(const u64* rec, u32 m, u32 words, u64* t_pack, u64
 }
 
 __global__ void k_u64_to_u32(const u64* a, u32* b, u32 n) {
+    PDL_PROLOGUE();
     const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) b[i] = (u32)a[i];
 }
@@ -1902,6 +2002,7 @@ template <class U>
 __global__ void __launch_bounds__(1024) k_dist_plan(const u32* C /*world x p*/, u32 world, u32 p, u32 rank, const U* sk,
                                                     u32* bstart /*nb+1*/, u32* srcoff /*world*/, Bucket* list, u32* nlist,
                                                     u32 cap_items, u32* status) {
+    PDL_PROLOGUE();
     __shared__ u32 red[33];
     const u32 b0 = (u32)((u64)rank * p / world), b1 = (u32)((u64)(rank + 1) * p / world), nb = b1 - b0;
     for (u32 b = threadIdx.x; b < nb; b += 1024) {
@@ -1940,6 +2041,7 @@ __global__ void __launch_bounds__(1024) k_dist_plan(const u32* C /*world x p*/, 
 template <class U, bool KV>
 __global__ void k_dist_gather(const U* rk, const u32* rv, const u32* ri, U* ok, u32* ov, u32* oi, const u32* C, u32 world,
                               u32 p, u32 rank, const u32* bstart, const u32* srcoff) {
+    PDL_PROLOGUE();
     const u32 b0 = (u32)((u64)rank * p / world), b1 = (u32)((u64)(rank + 1) * p / world), nb = b1 - b0;
     const u64 w = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const u32 lane = threadIdx.x & 31;
@@ -1957,13 +2059,16 @@ __global__ void k_dist_gather(const U* rk, const u32* rv, const u32* ri, U* ok, 
 }
 
 __global__ void k_fill_u32(u32* p, u32 v, u32 n) {
+    PDL_PROLOGUE();
     const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) p[i] = v;
 }
 
-__global__ void k_set2(u32* p, u32 a, u32 b) { p[0] = a; p[1] = b; }
+__global__ void k_set2(u32* p, u32 a, u32 b) {
+    PDL_PROLOGUE(); p[0] = a; p[1] = b; }
 
 __global__ void k_iota(u32* p, u32 n) {
+    PDL_PROLOGUE();
     const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) p[i] = i;
 }
@@ -1971,6 +2076,7 @@ __global__ void k_iota(u32* p, u32 n) {
 // internal sorts of an array that fits the bucket sorter: one bucket with loose bounds
 template <class U>
 __global__ void k_push_bucket(Bucket* list, u32* nlist, u32 len) {
+    PDL_PROLOGUE();
     Bucket b;
     b.beg = 0; b.len = len; b.buf = 0; b.level = BK_LOOSE;
     b.lo = 0; b.hi = (u64)umax_of<U>();

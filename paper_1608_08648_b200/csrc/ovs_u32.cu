@@ -10,9 +10,11 @@ size_t dist_u32(Ctx& c, int step, const ovs_params* prm, const DistArgs& a, bool
 }
 }  // namespace ovs
 
-#ifdef OVS_BS_PROF
-extern "C" int ovs_debug_bsprof(unsigned long long* out, int reset) {
-    if (cudaMemcpyFromSymbol(out, ovs::g_bsprof, sizeof(unsigned long long) * 16) != cudaSuccess) return 1;
+#ifdef OVS_BS_PROF  // experiments only: bucket-sorter phase cycles of this translation unit's kernels
+extern "C" int ovs_debug_bsprof_u32(unsigned long long* out, int reset) {
+    unsigned long long v[16];
+    if (cudaMemcpyFromSymbol(v, ovs::g_bsprof, sizeof(v)) != cudaSuccess) return 1;
+    for (int i = 0; i < 16; ++i) out[i] += v[i];
     if (reset) {
         unsigned long long z[16] = {0};
         cudaMemcpyToSymbol(ovs::g_bsprof, z, sizeof(z));

@@ -1,0 +1,53 @@
+"""Device time of one sort for each BASELINE.json configuration (C1-C4; C5 is bench.py):
+python tools/configs_bench.py [reps]   -> one JSON line per config (median of reps, after 2 warm-ups)"""
+import json, statistics, sys
+sys.path.insert(0, ".")
+import torch
+import ovs_inputs
+import paper_1608_08648_b200 as ovs
+
+reps = int(sys.argv[1]) if len(sys.argv) > 1 else 5
+only = sys.argv[2].split(",") if len(sys.argv) > 2 else None
+CASES = [  # name, dist, data seed, n, method, p, s/r, kv, algorithmic bytes per key
+    ("C1", "u32_u31", 1, 1 << 20, "ros", 64, 32, False, 20),
+    ("C2-uniform", "i32_uniform", 21, 1 << 24, "dro", 256, 24, False, 16),
+    ("C2-few", "i32_few", 25, 1 << 24, "dro", 256, 24, False, 16),
+    ("C3-uniform", "f64_uniform", 31, 1 << 27, "ros", 1024, 64, False, 40),
+    ("C4", "u16key", 41, 1 << 27, "dro", 512, 27, True, 32),
+]
+for name, dist, dseed, n, method, p, s, kv, bpk in CASES:
+    if only and name not in only:
+        continue
+    x = torch.from_numpy(ovs_inputs.keys(dist, n, seed=dseed)).cuda()
+    v = torch.from_numpy(ovs_inputs.index_values(n)).cuda() if kv else None
+    srt = ovs.Sorter(n, x.dtype, kv, method, p, s, 1)
+    wk, wv = x.clone(), (v.clone() if kv else None)
+    ms = []
+    for r in range(reps + 2):
+        wk.copy_(x)
+        if kv:
+            wv.copy_(v)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        srt(wk, wv) if kv else srt(wk)
+        b.record()
+        b.synchronize()
+        if r >= 2:
+            ms.append(a.elapsed_time(b))
+    t = statistics.median(ms)
+    print(json.dumps({"config": name, "n": n, "dtype": str(x.dtype).replace("torch.", ""), "method": method, "p": p,
+                      "s_or_r": s, "kv": kv, "ms": round(t, 4), "Gkeys_per_s": round(n / t / 1e6, 2),
+                      "algorithmic_GBps": round(n * bpk / t / 1e6, 1)}), flush=True)
+    del srt, x, v, wk, wv
+    torch.cuda.empty_cache()
+
+import ctypes
+L = ovs.lib()
+if hasattr(L, "ovs_debug_bsprof_u32"):
+    arr = (ctypes.c_ulonglong * 16)()
+    for dt in ("u32", "i32", "f64"):
+        getattr(L, "ovs_debug_bsprof_" + dt)(arr, 1)
+    names = ["resplit", "loose", "setup", "hist", "scan", "scatter", "net8", "net16+warp", "huge", "write"]
+    tot = arr[15] or 1
+    print("bucket sorter cycles:", "  ".join(f"{nm} {arr[i] / tot * 100:.1f}%" for i, nm in enumerate(names)),
+          f" other {(tot - sum(arr[:10])) / tot * 100:.1f}%")

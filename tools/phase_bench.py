@@ -39,10 +39,11 @@ for path in libs:
 import ctypes
 for path in libs:
     L = ctypes.CDLL(path or ovs.LIB_PATH)
-    if not hasattr(L, "ovs_debug_bsprof"):
+    if not hasattr(L, "ovs_debug_bsprof_u32"):
         continue
     arr = (ctypes.c_ulonglong * 16)()
-    L.ovs_debug_bsprof(arr, 1)
+    for dt in ("u32", "i32", "f64"):
+        getattr(L, "ovs_debug_bsprof_" + dt)(arr, 1)
     srt = ovs.Sorter(n, torch.uint32, False, "ros", p, s, 1) if False else None
     names = ["resplit", "loose", "setup", "hist", "scan", "scatter", "net8", "net16+warp", "huge", "write"]
     tot = arr[15]

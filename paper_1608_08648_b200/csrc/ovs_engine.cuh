@@ -390,6 +390,12 @@ template <bool TAG> struct Selector {
                                                     l.fit, l.nfit);
         c.check();
         e.bucket_sort(l, seed);
+        pick<U>(P, s, sk, st);
+    }
+    // S[q] = T[(q+1)s - 1], q < P-1, from the sorted records
+    template <class U> void pick(u32 P, u32 s, U* sk, u32* st) {
+        Ctx& c = e.c;
+        if (c.dry) return;
         launch(c, k_pick_splitters<U>, cdiv(P, 256), 256, 0, e.B.k[0], e.B.k[0], e.B.v[0], P, s, sk, st);
         c.check();
     }
@@ -452,6 +458,15 @@ template <int DT, bool KV> struct RosSort {
     u64 seed;
     u64* counts = nullptr;
     RosSampler<DT, false>* smp = nullptr;  // a1-a4
+    // Refinement: when the contract's buckets (n/p keys) cannot be sorted on chip, level 0
+    // partitions into p*f buckets with the splitters T[(i+1)s/f - 1] (f | s, >= 8 samples
+    // each), a superset of the contract's T[(q+1)s - 1] (i = (q+1)f - 1).  Contract bucket q is
+    // exactly the concatenation of level-0 buckets qf .. qf+f-1, so the output is unchanged and
+    // the contract's splitters and counts are read off (k_pick_splitters, k_fold_counts).
+    u32 f = 1;
+    U* rep_sk = nullptr;
+    u32* rep_st = nullptr;
+    u64* int_counts = nullptr;
 
     RosSort(Ctx& ctx, U* keys, u32* vals, u32 n_, u32 p_, u32 s_, u64 seed_) : c(ctx), e(ctx), n(n_), p(p_), s(s_), seed(seed_) {
         e.n = n;
@@ -467,6 +482,20 @@ template <int DT, bool KV> struct RosSort {
         u32 P0 = p;
         if (p == 1) P0 = n > e.cap ? std::min<u32>(std::min<u32>(1024, e.max_p_one_level()),
                                                    cdiv(n, (u32)(e.cap * 45ull / 100))) : 1;
+        if (p > 1) {
+            // refine while the buckets exceed the on-chip capacity, within the bucket count the
+            // fast scatter handles (keys only: the write-combining one)
+            u32 pmax = std::min<u32>(8192, e.max_p_one_level());
+            if (!KV && e.use_wc(p)) while (pmax > p && !e.use_wc(pmax)) --pmax;
+            while (s % (2 * f) == 0 && s / (2 * f) >= 8 && (u64)p * 2 * f <= pmax && (u64)n > (u64)p * f * e.cap)
+                f *= 2;
+            P0 = p * f;
+            if (f > 1) {
+                rep_sk = c.take<U>(p);
+                rep_st = c.take<u32>(p);
+                int_counts = c.take<u64>(P0);
+            }
+        }
         e.carve_level0(z, P0);
         e.carve_lists(l, P0);
         if (p > 1) smp = new RosSampler<DT, false>(c, n, p, s);
@@ -481,14 +510,19 @@ template <int DT, bool KV> struct RosSort {
             // a1+a2: ps-1 distinct random indices and their records T = [(x[i], i)]
             smp->draw(seed);
             smp->take(seed, e.B.k[0], 0, n, nullptr);
-            // a3+a4: sort T by (key, i); S[q] = T[(q+1)s - 1]
-            smp->select(p, s, seed ^ 0x5eed, z.sk, z.st);
+            // a3+a4: sort T by (key, i); S[q] = T[(q+1)s - 1] (refined: every (s/f)-th)
+            smp->select(p * f, s / f, seed ^ 0x5eed, z.sk, z.st);
+            if (f > 1) smp->sel->template pick<U>(p, s, rep_sk, rep_st);
         } else {
             e.internal_splitters(z, seed);
         }
         c.mark(1);
         // a5-a7: classify, histogram, scan, scatter;  a8: bucket sort
-        e.level0(z, l, p > 1 ? counts : nullptr);
+        e.level0(z, l, p > 1 ? (f > 1 ? int_counts : counts) : nullptr);
+        if (f > 1) {
+            launch(c, k_fold_counts, cdiv(p, 256), 256, 0, int_counts, f, p, counts);
+            c.check();
+        }
         e.bucket_sort(l, seed);
         c.mark(4);
     }
@@ -717,8 +751,8 @@ Out plan_or_run(Ctx& c, void* keys, u32* vals, size_t n, const ovs_params* prm) 
     if (prm->p > 1 && r.z.P > r.e.max_p_one_level())
         throw StatusFail{OVS_EINVAL, "p too large for the one-level classifier in shared memory"};
     Out o;
-    o.sk = r.z.sk;
-    o.st = r.z.st;
+    o.sk = r.f > 1 ? r.rep_sk : r.z.sk;
+    o.st = r.f > 1 ? r.rep_st : r.z.st;
     o.counts = r.counts;
     if (!c.dry) r.run();
     o.ws = c.off + 256;

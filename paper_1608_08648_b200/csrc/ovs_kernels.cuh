@@ -232,6 +232,49 @@ __device__ __forceinline__ u32 block_exclusive_scan(u32 v, u32* red /*[NT/32+1]*
     return r;
 }
 
+// exclusive scan of 4 words per thread at once (each word may pack independent 16-bit fields
+// whose sums stay below 2^16); total[] receives the CTA totals
+template <int NT>
+__device__ __forceinline__ void block_exclusive_scan4(u32 (&v)[4], u32 (*red)[4] /*[NT/32 + 1]*/, u32 (&total)[4]) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    u32 x[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) x[q] = v[q];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const u32 y = __shfl_up_sync(0xffffffffu, x[q], o);
+            if (lane >= o) x[q] += y;
+        }
+    }
+    if (lane == 31)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) red[wid][q] = x[q];
+    __syncthreads();
+    if (wid == 0) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const u32 w = lane < NT / 32 ? red[lane][q] : 0u;
+            u32 t = w;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const u32 y = __shfl_up_sync(0xffffffffu, t, o);
+                if (lane >= o) t += y;
+            }
+            if (lane < NT / 32) red[lane][q] = t - w;
+            if (lane == NT / 32 - 1) red[NT / 32][q] = t;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        total[q] = red[NT / 32][q];
+        v[q] = red[wid][q] + x[q] - v[q];
+    }
+    __syncthreads();
+}
+
 // exclusive scan in place of a[0..cnt) (cnt arbitrary) by a CTA of NT threads; a[cnt] = total
 template <int NT>
 __device__ void block_scan_array(u32* a, u32 cnt, u32* red) {
@@ -545,6 +588,16 @@ __global__ void k_pick_splitters(const u64* t_pack, const u64* t_key, const u32*
         sk[q] = (U)t_key[r];
         st[q] = t_tag[r];
     }
+}
+
+// contract bucket q = refined level-0 buckets qf .. qf+f-1 (RosSort refinement)
+__global__ void k_fold_counts(const u64* in, u32 f, u32 p, u64* out) {
+    PDL_PROLOGUE();
+    const u32 q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= p) return;
+    u64 s = 0;
+    for (u32 j = 0; j < f; ++j) s += in[(u64)q * f + j];
+    out[q] = s;
 }
 
 // ------------------------------------------------------------------ classifier LUT build
@@ -1456,6 +1509,7 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
     __shared__ U sp_k[BS_SPMAX];
     __shared__ u32 sp_t[BS_SPMAX], sp_cnt[BS_SPMAX + 1], sp_cur[BS_SPMAX];
     __shared__ u32 rs_cnt[BS_SPMAX], rs_off[BS_SPMAX];
+    __shared__ u32 rs_red[BS_NT / 32 + 1][4];
     __shared__ int rs_base[BS_SPMAX];
     BucketSmem<U, KV> S;
     {
@@ -1521,9 +1575,11 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                 u32 P = (m + part - 1) / part;
                 P = max(2u, min(BS_SPMAX, P));
                 const u32 ms = P * BS_SI - 1;
+                u32 NS = 32;  // the sample, padded to a power of two for the bitonic network
+                while (NS < ms) NS <<= 1;
                 U* tk = S.k;
                 u32* tt = (u32*)(smem + bucket_smem_fixed<U, KV>() + sizeof(U) * BS_SSMAX);
-                for (u32 j = threadIdx.x; j < BS_SSMAX; j += BS_NT) {
+                for (u32 j = threadIdx.x; j < NS; j += BS_NT) {
                     if (j < ms) {
                         const u64 u = rng_H(seed ^ ((u64)bk.beg * 0x9e3779b97f4a7c15ull), 64 + (bk.level & 0xffffu), j);
                         const u32 o = (u32)__umul64hi(u, (u64)m);
@@ -1535,7 +1591,7 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                     }
                 }
                 __syncthreads();
-                cta_bitonic_kt<U>(tk, tt, BS_SSMAX);
+                cta_bitonic_kt<U>(tk, tt, NS);
                 if (threadIdx.x + 1 < P) {
                     sp_k[threadIdx.x] = tk[(threadIdx.x + 1) * BS_SI - 1];
                     sp_t[threadIdx.x] = tt[(threadIdx.x + 1) * BS_SI - 1];
@@ -1543,11 +1599,28 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                 if (threadIdx.x <= P) sp_cnt[threadIdx.x] = 0;
                 if (threadIdx.x < BS_SPMAX) rs_cnt[threadIdx.x] = 0;
                 __syncthreads();
+                BS_PROBE(10)
+                // P <= 8: per-thread counters in registers, two 16-bit fields per word (a thread sees
+                // < 2^16 keys: m <= 64 * cap), one CTA reduction; otherwise shared atomics (a fan-out
+                // this small makes them collide on the same counters)
+                const bool small = P <= 8;
+                u32 pc[4] = {0u, 0u, 0u, 0u};
                 for_items<U, BS_NT, OVS_BS_UNR>(src, bk.beg, m, [&](U kr, u32 o) {
                     const U k = K(kr);
                     const u32 tg = IX(bk.beg + o);
-                    atomicAdd(&sp_cnt[lower_bound_kt<U>(sp_k, sp_t, P - 1, k, tg)], 1u);
+                    const u32 b = lower_bound_kt<U>(sp_k, sp_t, P - 1, k, tg);
+                    if (small) {
+#pragma unroll
+                        for (u32 q = 0; q < 4; ++q) pc[q] += (b >> 1) == q ? (1u << (16 * (b & 1))) : 0u;
+                    } else {
+                        atomicAdd(&sp_cnt[b], 1u);
+                    }
                 });
+                if (small) {
+                    u32 tot[4];
+                    block_exclusive_scan4<BS_NT>(pc, rs_red, tot);
+                    if (threadIdx.x < P) sp_cnt[threadIdx.x] = (tot[threadIdx.x >> 1] >> (16 * (threadIdx.x & 1))) & 0xffffu;
+                }
                 __syncthreads();
                 if (threadIdx.x == 0) {
                     u32 run = 0;
@@ -1555,6 +1628,7 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                     sp_cnt[P] = run;
                 }
                 __syncthreads();
+                BS_PROBE(11)
                 // scatter in tiles of RS_IT * BS_NT items staged in shared memory by sub-bucket, so
                 // every sub-bucket's items of a tile leave as one coalesced run (whole sectors)
                 const u32 db = 1 - bk.buf;
@@ -1574,11 +1648,41 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                         }
                     }
 #pragma unroll
-                    for (u32 j = 0; j < RS_IT; ++j) {
-                        if (j * BS_NT + threadIdx.x < nt) {
-                            bb[j] = lower_bound_kt<U>(sp_k, sp_t, P - 1, kk[j], tg[j]);
-                            rr[j] = atomicAdd(&rs_cnt[bb[j]], 1u);
+                    for (u32 j = 0; j < RS_IT; ++j)
+                        if (j * BS_NT + threadIdx.x < nt) bb[j] = lower_bound_kt<U>(sp_k, sp_t, P - 1, kk[j], tg[j]);
+                    if (small) {
+                        // rank = the thread's earlier items of the bucket + the earlier threads' (one
+                        // scan of packed 16-bit counters); tile totals -> rs_cnt
+                        u32 w[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+                        for (u32 j = 0; j < RS_IT; ++j) {
+                            if (j * BS_NT + threadIdx.x < nt) {
+                                const u32 q = bb[j] >> 1, sh = 16 * (bb[j] & 1);
+                                u32 cur = 0;
+#pragma unroll
+                                for (u32 x = 0; x < 4; ++x) cur = x == q ? w[x] : cur;
+                                rr[j] = (cur >> sh) & 0xffffu;
+#pragma unroll
+                                for (u32 x = 0; x < 4; ++x) w[x] += x == q ? (1u << sh) : 0u;
+                            }
                         }
+                        u32 ex[4] = {w[0], w[1], w[2], w[3]}, tot[4];
+                        block_exclusive_scan4<BS_NT>(ex, rs_red, tot);
+#pragma unroll
+                        for (u32 j = 0; j < RS_IT; ++j) {
+                            if (j * BS_NT + threadIdx.x < nt) {
+                                const u32 q = bb[j] >> 1, sh = 16 * (bb[j] & 1);
+                                u32 e0 = 0;
+#pragma unroll
+                                for (u32 x = 0; x < 4; ++x) e0 = x == q ? ex[x] : e0;
+                                rr[j] += (e0 >> sh) & 0xffffu;
+                            }
+                        }
+                        if (threadIdx.x < P) rs_cnt[threadIdx.x] = (tot[threadIdx.x >> 1] >> (16 * (threadIdx.x & 1))) & 0xffffu;
+                    } else {
+#pragma unroll
+                        for (u32 j = 0; j < RS_IT; ++j)
+                            if (j * BS_NT + threadIdx.x < nt) rr[j] = atomicAdd(&rs_cnt[bb[j]], 1u);
                     }
                     __syncthreads();
                     if (threadIdx.x < 32) {  // tile offsets (P <= 64: two per lane) and run bases
@@ -1612,6 +1716,7 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                     }
                     __syncthreads();
                 }
+                BS_PROBE(12)
                 if (threadIdx.x == 0) {
                     u32 sp = s_sp;
                     for (int b = (int)P - 1; b >= 0; --b) {

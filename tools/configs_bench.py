@@ -22,22 +22,24 @@ for name, dist, dseed, n, method, p, s, kv, bpk in CASES:
     v = torch.from_numpy(ovs_inputs.index_values(n)).cuda() if kv else None
     srt = ovs.Sorter(n, x.dtype, kv, method, p, s, 1)
     wk, wv = x.clone(), (v.clone() if kv else None)
-    ms = []
+    ms, ph = [], []
     for r in range(reps + 2):
         wk.copy_(x)
         if kv:
             wv.copy_(v)
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        ovs.set_phase_events(ev)
         srt(wk, wv) if kv else srt(wk)
-        b.record()
-        b.synchronize()
+        ovs.set_phase_events(None)
+        ev[4].synchronize()
         if r >= 2:
-            ms.append(a.elapsed_time(b))
+            ms.append(ev[0].elapsed_time(ev[4]))
+            ph.append([ev[i].elapsed_time(ev[i + 1]) for i in range(4)])
     t = statistics.median(ms)
+    phases = {nm: round(statistics.median(q[i] for q in ph), 3) for i, nm in enumerate(ovs.PHASES)}
     print(json.dumps({"config": name, "n": n, "dtype": str(x.dtype).replace("torch.", ""), "method": method, "p": p,
                       "s_or_r": s, "kv": kv, "ms": round(t, 4), "Gkeys_per_s": round(n / t / 1e6, 2),
-                      "algorithmic_GBps": round(n * bpk / t / 1e6, 1)}), flush=True)
+                      "algorithmic_GBps": round(n * bpk / t / 1e6, 1), "phases_ms": phases}), flush=True)
     del srt, x, v, wk, wv
     torch.cuda.empty_cache()
 
@@ -47,7 +49,7 @@ if hasattr(L, "ovs_debug_bsprof_u32"):
     arr = (ctypes.c_ulonglong * 16)()
     for dt in ("u32", "i32", "f64"):
         getattr(L, "ovs_debug_bsprof_" + dt)(arr, 1)
-    names = ["resplit", "loose", "setup", "hist", "scan", "scatter", "net8", "net16+warp", "huge", "write"]
+    names = ["resplit-push", "loose", "setup", "hist", "scan", "scatter", "net8", "net16+warp", "huge", "write", "rs-sample", "rs-count", "rs-scatter"]
     tot = arr[15] or 1
     print("bucket sorter cycles:", "  ".join(f"{nm} {arr[i] / tot * 100:.1f}%" for i, nm in enumerate(names)),
-          f" other {(tot - sum(arr[:10])) / tot * 100:.1f}%")
+          f" other {(tot - sum(arr[:13])) / tot * 100:.1f}%")

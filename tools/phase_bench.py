@@ -45,8 +45,8 @@ for path in libs:
     for dt in ("u32", "i32", "f64"):
         getattr(L, "ovs_debug_bsprof_" + dt)(arr, 1)
     srt = ovs.Sorter(n, torch.uint32, False, "ros", p, s, 1) if False else None
-    names = ["resplit", "loose", "setup", "hist", "scan", "scatter", "net8", "net16+warp", "huge", "write"]
+    names = ["resplit-push", "loose", "setup", "hist", "scan", "scatter", "net8", "net16+warp", "huge", "write", "rs-sample", "rs-count", "rs-scatter"]
     tot = arr[15]
     print("bucket sorter cycles (sum over CTAs, thread 0), share of kernel:",
           "  ".join(f"{nm} {arr[i] / tot * 100:.1f}%" for i, nm in enumerate(names)),
-          f" other {(tot - sum(arr[:10])) / tot * 100:.1f}%")
+          f" other {(tot - sum(arr[:13])) / tot * 100:.1f}%")

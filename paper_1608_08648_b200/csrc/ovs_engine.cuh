@@ -179,6 +179,7 @@ template <int DT, bool KV> struct Engine {
     struct Lists {
         Bucket* fit = nullptr; u32* nfit = nullptr; u32* ticket = nullptr; u32 fit_cap = 0;
         Bucket* stack = nullptr; u32 grid = 0;
+        Bucket* wl = nullptr; u32* nwl = nullptr; u32 wl_cap = 0;  // buckets sorted in windows
     };
 
     // keys-only sorts use the write-combining scatter when its shared memory fits
@@ -232,6 +233,9 @@ template <int DT, bool KV> struct Engine {
         l.ticket = l.nfit + 1;
         l.grid = (u32)c.di.sms;  // bucket sorter: one CTA per SM (shared-memory bound)
         l.stack = c.take<Bucket>((size_t)l.grid * BS_STACK);
+        l.wl_cap = std::max<u32>(64, n / std::max<u32>(cap, 1) + 64);  // windowed buckets exceed cap
+        l.wl = c.take<Bucket>(l.wl_cap);
+        l.nwl = c.take<u32>(2);
     }
 
     // internal splitters for level 0 (P-1 of them) from a one-CTA sorted random sample
@@ -303,9 +307,14 @@ template <int DT, bool KV> struct Engine {
         if (c.dry) return;
         if (!okeys) { okeys = B.k[0]; ovals = KV ? B.v[0] : nullptr; }
         const size_t sm = bucket_smem<U, KV>(cap);
-        OVS_CK(cudaFuncSetAttribute(k_bucket_sort<DT, KV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        launch(c, k_bucket_sort<DT, KV>, l.grid, BS_NT, sm, l.fit, l.nfit, l.ticket, B, okeys, ovals, oidx, out_raw,
-                                                          cap, l.stack, seed, c.status, ixbits);
+        OVS_CK(cudaFuncSetAttribute(k_bucket_sort<DT, KV, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        OVS_CK(cudaFuncSetAttribute(k_bucket_sort<DT, KV, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        fill_u32(c, l.nwl, 0, 2);
+        launch(c, k_bucket_sort<DT, KV, false>, l.grid, BS_NT, sm, l.fit, l.nfit, l.ticket, B, okeys, ovals, oidx, out_raw,
+                                                          cap, l.stack, seed, c.status, ixbits, l.wl, l.nwl, l.wl_cap);
+        c.check();
+        launch(c, k_bucket_sort<DT, KV, true>, l.grid, BS_NT, sm, l.wl, l.nwl, l.nwl + 1, B, okeys, ovals, oidx, out_raw,
+               cap, l.stack, seed, c.status, ixbits, l.wl, l.nwl, 0u);
         c.check();
     }
 };

@@ -1493,11 +1493,16 @@ template <class U, bool KV> __host__ __device__ constexpr size_t bucket_item_byt
     return sizeof(U) + (KV ? 8 : 0);
 }
 
-template <int DT, bool KV>
+// WIN = false: buckets that fit on chip, oversized ones re-split or (up to BS_WMAX * cap, not in
+// the output array) appended to wlist; WIN = true: the wlist buckets, sorted on chip in windows
+// of consecutive digit groups (kept out of the first kernel: its register allocation, and so the
+// common path's speed, must not pay for the window loop)
+template <int DT, bool KV, bool WIN>
 __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, const u32* nlist, u32* ticket,
                                                            Bufs<typename Codec<DT>::U> B, typename Codec<DT>::U* okeys,
                                                            u32* ovals, u32* oidx, bool out_raw, u32 cap,
-                                                           Bucket* stack_pool, u64 seed, u32* status, u32 ixbits) {
+                                                           Bucket* stack_pool, u64 seed, u32* status, u32 ixbits,
+                                                           Bucket* wlist, u32* nwlist, u32 wcap) {
     // ixbits: key-value sorts' indices are < 2^ixbits
     PDL_PROLOGUE();
     typedef typename Codec<DT>::U U;
@@ -1574,7 +1579,19 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
             // windows re-read the bucket after writing earlier windows' output: only when the
             // bucket does not live in the output array
             const bool can_window = (const void*)B.k[bk.buf] != (const void*)okeys;
-            if (m > cap && (m > BS_WMAX * cap || (bk.level & BK_FORCE) || !can_window)) {
+            // (slightly oversized buckets, m <= 1.1 cap, are re-split right here: they are rare
+            // outliers of a bucket-size distribution that fits, and the window launch only starts
+            // after this one, so a few of them would sit alone in its tail)
+            if (!WIN && m > cap + cap / 10 && m <= BS_WMAX * cap && can_window && !(bk.level & BK_FORCE)) {
+                // sorted on chip in windows by the second launch (k_bucket_sort<..., true>)
+                if (threadIdx.x == 0) {
+                    const u32 w = atomicAdd(nwlist, 1u);
+                    if (w < wcap) wlist[w] = bk; else atomicOr(status, ST_LIST_OVER);
+                }
+                __syncthreads();
+                continue;
+            }
+            if (m > cap && (m > BS_WMAX * cap || (bk.level & BK_FORCE) || !can_window || !WIN)) {
                 // ---------------- CTA-local re-split of an oversized bucket
                 const u32 part = (u32)((cap * 60ull) / 100);
                 u32 P = (m + part - 1) / part;
@@ -1742,145 +1759,88 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                 BS_PROBE(0)
                 continue;
             }
-            // ---------------- on-chip sort of a bucket that fits
-            // items sit at shared index = output address mod 16 bytes, so the write-out is aligned
-            // 16-byte shared loads and global stores
-            BucketSmem<U, KV> Sa = S;
-            Sa.k = S.k + ((((uintptr_t)(okeys + bk.beg)) / sizeof(U)) & (16 / sizeof(U) - 1));
-            BS_PROBE(1)
-            U lo = (U)bk.lo, hi = (U)bk.hi;
-            if (bk.level & BK_LOOSE) {
-                U mn = umax_of<U>(), mx = 0;
-                for_items<U, BS_NT, OVS_BS_UNR>(src, bk.beg, m, [&](U kr, u32) { const U k = K(kr); mn = min(mn, k); mx = max(mx, k); });
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) { mn = min(mn, shfl_xor_any(mn, o)); mx = max(mx, shfl_xor_any(mx, o)); }
-                if (lane == 0) { s_mn[wid] = mn; s_mx[wid] = mx; }
-                __syncthreads();
-                mn = s_mn[0]; mx = s_mx[0];
-                for (int q = 1; q < BS_NT / 32; ++q) { mn = min(mn, s_mn[q]); mx = max(mx, s_mx[q]); }
-                lo = mn; hi = mx;
-                __syncthreads();
-            }
-            u32 ng = 32;
-            while (ng < (u32)BS_NGMAX && ng * 3 < m) ng <<= 1;
-            // digit = floor(x * ng / R) for x = (sort key - lo) in [0, R): monotone in the key
-            // and spreads [lo, hi] over all ng groups (computed as a 64-bit fixed-point
-            // multiply-high).  Key-value sorts of 32-bit keys use the composite (key, index) with
-            // the index in its ixbits low bits (indices < 2^ixbits, so the groups spread over the
-            // indices that occur); 64-bit keys use the key (equal keys share a group, ordered by
-            // index).  R <= ng: digit = x, every group holds one key value (keys only: the groups
-            // need no sorting, e.g. few distinct keys).
-            const bool comp = KV && sizeof(U) == 4;
-            const u64 xmax = comp ? ((((u64)(hi - lo)) << ixbits) | ((1ull << ixbits) - 1)) : (u64)(U)(hi - lo);
-            const bool direct = xmax < (u64)ng;
-            // multiplier ~ ng * 2^64 / R in double precision: any multiplier keeps the digit monotone
-            // (and the clamp keeps it < ng), so rounding only perturbs the group sizes slightly
-            const double mq = (double)ng * 18446744073709551616.0 / ((double)xmax + 1.0);
-            const u64 mult = mq >= 18446744073709549568.0 ? 0xffffffffffffffffull : (u64)mq;
-            const double mq32 = mq * (1.0 / 4294967296.0);
-            const u32 mult32 = mq32 >= 4294967295.0 ? 0xffffffffu : (u32)mq32;
-            auto digit = [&](U k, u32 ix) -> u32 {
-                if constexpr (!KV && sizeof(U) == 4) {
-                    const u32 x = (u32)(k - lo);
-                    return direct ? x : min(__umulhi(x, mult32), ng - 1);  // min: memory safety only
-                } else {
-                    const u64 x = comp ? ((((u64)(k - lo)) << ixbits) | ix) : (u64)(U)(k - lo);
-                    return direct ? (u32)x : min((u32)__umul64hi(x, mult), ng - 1);
-                }
-            };
-            const bool need_sort = KV || !direct;
-            for (u32 g = threadIdx.x; g < ng; g += BS_NT) Sa.cnt[g] = 0;
-            __syncthreads();
-            BS_PROBE(2)
-            // 1. digit histogram
-            for_items<U, BS_NT, OVS_BS_UNR>(src, bk.beg, m, [&](U kr, u32 o) {
-                const u32 ix = KV ? IX(bk.beg + o) : 0u;
-                atomicAdd(&Sa.cnt[digit(K(kr), ix)], 1u);
-            });
-            __syncthreads();
-            BS_PROBE(3)
-            block_scan_small<BS_NT>(Sa.cnt, ng, red);  // cnt[g] = start of group g
-            BS_PROBE(4)
-            if (m > cap) {
-                // windows need every group to fit: otherwise re-split the bucket instead
-                u32 mg = 0;
-                for (u32 g = threadIdx.x; g < ng; g += BS_NT) mg = max(mg, (g + 1 < ng ? Sa.cnt[g + 1] : m) - Sa.cnt[g]);
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) mg = max(mg, __shfl_xor_sync(0xffffffffu, mg, o));
-                if (lane == 0) red[wid] = mg;
-                __syncthreads();
-                if (threadIdx.x == 0) {
-                    u32 x = 0;
-                    for (int w = 0; w < BS_NT / 32; ++w) x = max(x, red[w]);
-                    s_w[3] = x;
-                }
-                __syncthreads();
-                if (s_w[3] > cap) {
-                    if (threadIdx.x == 0) {
-                        Bucket fb = bk;
-                        fb.level |= BK_FORCE;
-                        if (s_sp < BS_STACK) stk[s_sp++] = fb; else atomicOr(status, ST_LIST_OVER);
-                    }
+            if constexpr (!WIN) {
+                // ---------------- on-chip sort of a bucket that fits
+                // items sit at shared index = output address mod 16 bytes, so the write-out is aligned
+                // 16-byte shared loads and global stores
+                BucketSmem<U, KV> Sa = S;
+                Sa.k = S.k + ((((uintptr_t)(okeys + bk.beg)) / sizeof(U)) & (16 / sizeof(U) - 1));
+                BS_PROBE(1)
+                U lo = (U)bk.lo, hi = (U)bk.hi;
+                if (bk.level & BK_LOOSE) {
+                    U mn = umax_of<U>(), mx = 0;
+                    for_items<U, BS_NT, OVS_BS_UNR>(src, bk.beg, m, [&](U kr, u32) { const U k = K(kr); mn = min(mn, k); mx = max(mx, k); });
+    #pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) { mn = min(mn, shfl_xor_any(mn, o)); mx = max(mx, shfl_xor_any(mx, o)); }
+                    if (lane == 0) { s_mn[wid] = mn; s_mx[wid] = mx; }
                     __syncthreads();
-                    continue;
+                    mn = s_mn[0]; mx = s_mx[0];
+                    for (int q = 1; q < BS_NT / 32; ++q) { mn = min(mn, s_mn[q]); mx = max(mx, s_mx[q]); }
+                    lo = mn; hi = mx;
+                    __syncthreads();
                 }
-            }
-            // 2-4 per window: consecutive groups [wg0, wg1) whose items fit on chip (one window
-            // covering every group when m <= cap; a bucket of up to BS_WMAX * cap items is sorted in
-            // several windows, each reading the bucket again (from L2) instead of re-splitting it)
-            for (u32 wg0 = 0; wg0 < ng;) {
-                if (threadIdx.x == 0) {
-                    u32 lo_g = wg0 + 1, hi_g = ng;  // largest wg1 with start(wg1) - start(wg0) <= cap
-                    const u32 s0 = Sa.cnt[wg0];
-                    while (lo_g < hi_g) {
-                        const u32 mid = (lo_g + hi_g + 1) >> 1;
-                        const u32 sm = mid < ng ? Sa.cnt[mid] : m;
-                        if (sm - s0 <= cap) lo_g = mid; else hi_g = mid - 1;
+                u32 ng = 32;
+                while (ng < (u32)BS_NGMAX && ng * 3 < m) ng <<= 1;
+                // digit = floor(x * ng / R) for x = (sort key - lo) in [0, R): monotone in the key
+                // and spreads [lo, hi] over all ng groups (computed as a 64-bit fixed-point
+                // multiply-high).  Key-value sorts of 32-bit keys use the composite (key, index) with
+                // the index in its ixbits low bits (indices < 2^ixbits, so the groups spread over the
+                // indices that occur); 64-bit keys use the key (equal keys share a group, ordered by
+                // index).  R <= ng: digit = x, every group holds one key value (keys only: the groups
+                // need no sorting, e.g. few distinct keys).
+                const bool comp = KV && sizeof(U) == 4;
+                const u64 xmax = comp ? ((((u64)(hi - lo)) << ixbits) | ((1ull << ixbits) - 1)) : (u64)(U)(hi - lo);
+                const bool direct = xmax < (u64)ng;
+                // multiplier ~ ng * 2^64 / R in double precision: any multiplier keeps the digit monotone
+                // (and the clamp keeps it < ng), so rounding only perturbs the group sizes slightly
+                const double mq = (double)ng * 18446744073709551616.0 / ((double)xmax + 1.0);
+                const u64 mult = mq >= 18446744073709549568.0 ? 0xffffffffffffffffull : (u64)mq;
+                const double mq32 = mq * (1.0 / 4294967296.0);
+                const u32 mult32 = mq32 >= 4294967295.0 ? 0xffffffffu : (u32)mq32;
+                auto digit = [&](U k, u32 ix) -> u32 {
+                    if constexpr (!KV && sizeof(U) == 4) {
+                        const u32 x = (u32)(k - lo);
+                        return direct ? x : min(__umulhi(x, mult32), ng - 1);  // min: memory safety only
+                    } else {
+                        const u64 x = comp ? ((((u64)(k - lo)) << ixbits) | ix) : (u64)(U)(k - lo);
+                        return direct ? (u32)x : min((u32)__umul64hi(x, mult), ng - 1);
                     }
-                    s_w[0] = lo_g;
-                    s_w[1] = s0;
-                    s_w[2] = (lo_g < ng ? Sa.cnt[lo_g] : m) - s0;
-                }
+                };
+                const bool need_sort = KV || !direct;
+                for (u32 g = threadIdx.x; g < ng; g += BS_NT) Sa.cnt[g] = 0;
                 __syncthreads();
-                const u32 wg1 = s_w[0], wbase = s_w[1], wm = s_w[2];
+                BS_PROBE(2)
+                // 1. digit histogram
+                for_items<U, BS_NT, OVS_BS_UNR>(src, bk.beg, m, [&](U kr, u32 o) {
+                    const u32 ix = KV ? IX(bk.beg + o) : 0u;
+                    atomicAdd(&Sa.cnt[digit(K(kr), ix)], 1u);
+                });
                 __syncthreads();
-#ifdef OVS_DEBUG_CHECKS
-                if (threadIdx.x == 0 && (wm > cap || wg1 <= wg0 || wg1 > ng)) { printf("BS window wm %u cap %u wg0 %u wg1 %u ng %u m %u\n", wm, cap, wg0, wg1, ng, m); __trap(); }
-#endif
-                if (threadIdx.x == 0) { s_nbig = 0; s_nhuge = 0; s_over = 0; }
-                BucketSmem<U, KV> Sw = S;
-                Sw.k = S.k + ((((uintptr_t)(okeys + bk.beg + wbase)) / sizeof(U)) & (16 / sizeof(U) - 1));
-                {
-                    BucketSmem<U, KV>& Sa = Sw;
+                BS_PROBE(3)
+                block_scan_small<BS_NT>(Sa.cnt, ng, red);  // cnt[g] = start of group g
+                BS_PROBE(4)
                 // 2. scatter into shared memory by digit; afterwards cnt[g] = end of group g
                 for_items<U, BS_NT, OVS_BS_UNR>(src, bk.beg, m, [&](U kr, u32 o) {
                     const U k = K(kr);
                     u32 ix = 0, vv = 0;
-                    if (KV) ix = IX(bk.beg + o);
-                    const u32 dg = digit(k, ix);
-                    if (dg >= wg0 && dg < wg1) {
-                        if (KV) vv = vsrc[bk.beg + o];
-                        const u32 pos = atomicAdd(&Sa.cnt[dg], 1u) - wbase;
-#ifdef OVS_DEBUG_CHECKS
-                        if (pos >= wm) { printf("BS pos %u wm %u dg %u wg0 %u wg1 %u wbase %u m %u\n", pos, wm, dg, wg0, wg1, wbase, m); __trap(); }
-#endif
-                        Sa.k[pos] = k;
-                        if (KV) { Sa.i[pos] = ix; Sa.v[pos] = vv; }
-                    }
+                    if (KV) { ix = IX(bk.beg + o); vv = vsrc[bk.beg + o]; }
+                    const u32 pos = atomicAdd(&Sa.cnt[digit(k, ix)], 1u);
+                    Sa.k[pos] = k;
+                    if (KV) { Sa.i[pos] = ix; Sa.v[pos] = vv; }
                 });
                 __syncthreads();
                 BS_PROBE(5)
                 // 3. one thread per group of <= 8: Batcher network in registers; larger groups are
                 // appended (warp-aggregated) to a list for 3b
                 // (OVS_NET8_X: groups per thread per iteration, their loads and networks interleaved)
-                for (u32 g0 = wg0; need_sort && g0 < wg1; g0 += BS_NT * OVS_NET8_X) {
+                for (u32 g0 = 0; need_sort && g0 < ng; g0 += BS_NT * OVS_NET8_X) {
                     u32 gs[OVS_NET8_X], len[OVS_NET8_X];
                     E a[OVS_NET8_X][8];
     #pragma unroll
                     for (int x = 0; x < OVS_NET8_X; ++x) {
                         const u32 g = g0 + x * BS_NT + threadIdx.x;
                         gs[x] = 0; len[x] = 0;
-                        if (g < wg1) { const u32 s0 = g ? Sa.cnt[g - 1] : 0u; len[x] = Sa.cnt[g] - s0; gs[x] = s0 - wbase; }
+                        if (g < ng) { gs[x] = g ? Sa.cnt[g - 1] : 0u; len[x] = Sa.cnt[g] - gs[x]; }
                     }
     #pragma unroll
                     for (int x = 0; x < OVS_NET8_X; ++x) {
@@ -1917,10 +1877,10 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                 // 3b. listed groups of 9..16: one thread each (63-comparator network)
                 const u32 nlisted = min(s_nbig, (u32)BS_BIGMAX);
                 const bool rescan = s_over != 0;  // list overflow (pathological skew): scan all groups
-                const u32 nwork = rescan ? wg1 - wg0 : nlisted;
+                const u32 nwork = rescan ? ng : nlisted;
                 for (u32 q = threadIdx.x; q < nwork; q += BS_NT) {
-                    const u32 g = rescan ? wg0 + q : s_big[q];
-                    const u32 g_s = g ? Sa.cnt[g - 1] : 0u, len = Sa.cnt[g] - g_s, gs = g_s - wbase;
+                    const u32 g = rescan ? q : s_big[q];
+                    const u32 gs = g ? Sa.cnt[g - 1] : 0u, len = Sa.cnt[g] - gs;
                     if (len <= 8 || len > 16) continue;
                     E a[16];
     #pragma unroll
@@ -1932,8 +1892,8 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                 }
                 // 3c'. groups of 17..512: one warp each (register bitonic); over 512: the CTA
                 for (u32 q = wid; q < nwork; q += BS_NT / 32) {
-                    const u32 g = rescan ? wg0 + q : s_big[q];
-                    const u32 g_s = g ? Sa.cnt[g - 1] : 0u, len = Sa.cnt[g] - g_s, gs = g_s - wbase;
+                    const u32 g = rescan ? q : s_big[q];
+                    const u32 gs = g ? Sa.cnt[g - 1] : 0u, len = Sa.cnt[g] - gs;
                     if (len <= 16) continue;
                     if (len <= 32) warp_sort_group<U, KV, 1>(Sa, gs, len);
                     else if (len <= 64) warp_sort_group<U, KV, 2>(Sa, gs, len);
@@ -1954,7 +1914,7 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                 const u32 nhuge = min(s_nhuge, (u32)BS_HUGEMAX);
                 for (u32 q = 0; q < nhuge; ++q) {
                     const u32 g = s_huge[q];
-                    const u32 g_s = g ? Sa.cnt[g - 1] : 0u, len = Sa.cnt[g] - g_s, gs = g_s - wbase;
+                    const u32 gs = g ? Sa.cnt[g - 1] : 0u, len = Sa.cnt[g] - gs;
                     u32 N = 1;
                     while (N < len) N <<= 1;
                     for (u32 kk = 2; kk <= N; kk <<= 1) {
@@ -1979,8 +1939,7 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                 // 4. write the sorted bucket (16-byte stores where the output is aligned)
                 {
                     constexpr u32 V = 16 / sizeof(U);
-                    U* out = okeys + bk.beg + wbase;
-                    const u32 m = wm;  // this window's items
+                    U* out = okeys + bk.beg;
                     const u32 mis = (u32)(((uintptr_t)out) & 15u) / (u32)sizeof(U);
                     const u32 head = mis ? min(m, V - mis) : 0u;
                     auto R = [&](U x) -> U { return out_raw ? Codec<DT>::raw(x) : x; };
@@ -1997,16 +1956,279 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                     }
                     for (u32 o = head + nv * V + threadIdx.x; o < m; o += BS_NT) out[o] = R(Sa.k[o]);
                     if (KV) {
-                        for (u32 o = threadIdx.x; o < m; o += BS_NT) ovals[bk.beg + wbase + o] = Sa.v[o];
+                        for (u32 o = threadIdx.x; o < m; o += BS_NT) ovals[bk.beg + o] = Sa.v[o];
                         if (oidx)
-                            for (u32 o = threadIdx.x; o < m; o += BS_NT) oidx[bk.beg + wbase + o] = Sa.i[o];
+                            for (u32 o = threadIdx.x; o < m; o += BS_NT) oidx[bk.beg + o] = Sa.i[o];
                     }
                 }
+                __syncthreads();
+            } else {
+                // ---------------- on-chip sort of a bucket that fits
+                // items sit at shared index = output address mod 16 bytes, so the write-out is aligned
+                // 16-byte shared loads and global stores
+                BucketSmem<U, KV> Sa = S;
+                Sa.k = S.k + ((((uintptr_t)(okeys + bk.beg)) / sizeof(U)) & (16 / sizeof(U) - 1));
+                BS_PROBE(1)
+                U lo = (U)bk.lo, hi = (U)bk.hi;
+                if (bk.level & BK_LOOSE) {
+                    U mn = umax_of<U>(), mx = 0;
+                    for_items<U, BS_NT, OVS_BS_UNR>(src, bk.beg, m, [&](U kr, u32) { const U k = K(kr); mn = min(mn, k); mx = max(mx, k); });
+    #pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) { mn = min(mn, shfl_xor_any(mn, o)); mx = max(mx, shfl_xor_any(mx, o)); }
+                    if (lane == 0) { s_mn[wid] = mn; s_mx[wid] = mx; }
+                    __syncthreads();
+                    mn = s_mn[0]; mx = s_mx[0];
+                    for (int q = 1; q < BS_NT / 32; ++q) { mn = min(mn, s_mn[q]); mx = max(mx, s_mx[q]); }
+                    lo = mn; hi = mx;
                     __syncthreads();
                 }
-                wg0 = wg1;
+                u32 ng = 32;
+                while (ng < (u32)BS_NGMAX && ng * 3 < m) ng <<= 1;
+                // digit = floor(x * ng / R) for x = (sort key - lo) in [0, R): monotone in the key
+                // and spreads [lo, hi] over all ng groups (computed as a 64-bit fixed-point
+                // multiply-high).  Key-value sorts of 32-bit keys use the composite (key, index) with
+                // the index in its ixbits low bits (indices < 2^ixbits, so the groups spread over the
+                // indices that occur); 64-bit keys use the key (equal keys share a group, ordered by
+                // index).  R <= ng: digit = x, every group holds one key value (keys only: the groups
+                // need no sorting, e.g. few distinct keys).
+                const bool comp = KV && sizeof(U) == 4;
+                const u64 xmax = comp ? ((((u64)(hi - lo)) << ixbits) | ((1ull << ixbits) - 1)) : (u64)(U)(hi - lo);
+                const bool direct = xmax < (u64)ng;
+                // multiplier ~ ng * 2^64 / R in double precision: any multiplier keeps the digit monotone
+                // (and the clamp keeps it < ng), so rounding only perturbs the group sizes slightly
+                const double mq = (double)ng * 18446744073709551616.0 / ((double)xmax + 1.0);
+                const u64 mult = mq >= 18446744073709549568.0 ? 0xffffffffffffffffull : (u64)mq;
+                const double mq32 = mq * (1.0 / 4294967296.0);
+                const u32 mult32 = mq32 >= 4294967295.0 ? 0xffffffffu : (u32)mq32;
+                auto digit = [&](U k, u32 ix) -> u32 {
+                    if constexpr (!KV && sizeof(U) == 4) {
+                        const u32 x = (u32)(k - lo);
+                        return direct ? x : min(__umulhi(x, mult32), ng - 1);  // min: memory safety only
+                    } else {
+                        const u64 x = comp ? ((((u64)(k - lo)) << ixbits) | ix) : (u64)(U)(k - lo);
+                        return direct ? (u32)x : min((u32)__umul64hi(x, mult), ng - 1);
+                    }
+                };
+                const bool need_sort = KV || !direct;
+                for (u32 g = threadIdx.x; g < ng; g += BS_NT) Sa.cnt[g] = 0;
+                __syncthreads();
+                BS_PROBE(2)
+                // 1. digit histogram
+                for_items<U, BS_NT, OVS_BS_UNR>(src, bk.beg, m, [&](U kr, u32 o) {
+                    const u32 ix = KV ? IX(bk.beg + o) : 0u;
+                    atomicAdd(&Sa.cnt[digit(K(kr), ix)], 1u);
+                });
+                __syncthreads();
+                BS_PROBE(3)
+                block_scan_small<BS_NT>(Sa.cnt, ng, red);  // cnt[g] = start of group g
+                BS_PROBE(4)
+                if (m > cap) {
+                    // windows need every group to fit: otherwise re-split the bucket instead
+                    u32 mg = 0;
+                    for (u32 g = threadIdx.x; g < ng; g += BS_NT) mg = max(mg, (g + 1 < ng ? Sa.cnt[g + 1] : m) - Sa.cnt[g]);
+    #pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) mg = max(mg, __shfl_xor_sync(0xffffffffu, mg, o));
+                    if (lane == 0) red[wid] = mg;
+                    __syncthreads();
+                    if (threadIdx.x == 0) {
+                        u32 x = 0;
+                        for (int w = 0; w < BS_NT / 32; ++w) x = max(x, red[w]);
+                        s_w[3] = x;
+                    }
+                    __syncthreads();
+                    if (s_w[3] > cap) {
+                        if (threadIdx.x == 0) {
+                            Bucket fb = bk;
+                            fb.level |= BK_FORCE;
+                            if (s_sp < BS_STACK) stk[s_sp++] = fb; else atomicOr(status, ST_LIST_OVER);
+                        }
+                        __syncthreads();
+                        continue;
+                    }
+                }
+                // 2-4 per window: consecutive groups [wg0, wg1) whose items fit on chip (one window
+                // covering every group when m <= cap; a bucket of up to BS_WMAX * cap items is sorted in
+                // several windows, each reading the bucket again (from L2) instead of re-splitting it)
+                for (u32 wg0 = 0; wg0 < ng;) {
+                    if (threadIdx.x == 0) {
+                        u32 lo_g = wg0 + 1, hi_g = ng;  // largest wg1 with start(wg1) - start(wg0) <= cap
+                        const u32 s0 = Sa.cnt[wg0];
+                        while (lo_g < hi_g) {
+                            const u32 mid = (lo_g + hi_g + 1) >> 1;
+                            const u32 sm = mid < ng ? Sa.cnt[mid] : m;
+                            if (sm - s0 <= cap) lo_g = mid; else hi_g = mid - 1;
+                        }
+                        s_w[0] = lo_g;
+                        s_w[1] = s0;
+                        s_w[2] = (lo_g < ng ? Sa.cnt[lo_g] : m) - s0;
+                    }
+                    __syncthreads();
+                    const u32 wg1 = s_w[0], wbase = s_w[1], wm = s_w[2];
+                    __syncthreads();
+    #ifdef OVS_DEBUG_CHECKS
+                    if (threadIdx.x == 0 && (wm > cap || wg1 <= wg0 || wg1 > ng)) { printf("BS window wm %u cap %u wg0 %u wg1 %u ng %u m %u\n", wm, cap, wg0, wg1, ng, m); __trap(); }
+    #endif
+                    if (threadIdx.x == 0) { s_nbig = 0; s_nhuge = 0; s_over = 0; }
+                    BucketSmem<U, KV> Sw = S;
+                    Sw.k = S.k + ((((uintptr_t)(okeys + bk.beg + wbase)) / sizeof(U)) & (16 / sizeof(U) - 1));
+                    {
+                        BucketSmem<U, KV>& Sa = Sw;
+                    // 2. scatter into shared memory by digit; afterwards cnt[g] = end of group g
+                    for_items<U, BS_NT, OVS_BS_UNR>(src, bk.beg, m, [&](U kr, u32 o) {
+                        const U k = K(kr);
+                        u32 ix = 0, vv = 0;
+                        if (KV) ix = IX(bk.beg + o);
+                        const u32 dg = digit(k, ix);
+                        if (dg >= wg0 && dg < wg1) {
+                            if (KV) vv = vsrc[bk.beg + o];
+                            const u32 pos = atomicAdd(&Sa.cnt[dg], 1u) - wbase;
+    #ifdef OVS_DEBUG_CHECKS
+                            if (pos >= wm) { printf("BS pos %u wm %u dg %u wg0 %u wg1 %u wbase %u m %u\n", pos, wm, dg, wg0, wg1, wbase, m); __trap(); }
+    #endif
+                            Sa.k[pos] = k;
+                            if (KV) { Sa.i[pos] = ix; Sa.v[pos] = vv; }
+                        }
+                    });
+                    __syncthreads();
+                    BS_PROBE(5)
+                    // 3. one thread per group of <= 8: Batcher network in registers; larger groups are
+                    // appended (warp-aggregated) to a list for 3b
+                    // (OVS_NET8_X: groups per thread per iteration, their loads and networks interleaved)
+                    for (u32 g0 = wg0; need_sort && g0 < wg1; g0 += BS_NT * OVS_NET8_X) {
+                        u32 gs[OVS_NET8_X], len[OVS_NET8_X];
+                        E a[OVS_NET8_X][8];
+        #pragma unroll
+                        for (int x = 0; x < OVS_NET8_X; ++x) {
+                            const u32 g = g0 + x * BS_NT + threadIdx.x;
+                            gs[x] = 0; len[x] = 0;
+                            if (g < wg1) { const u32 s0 = g ? Sa.cnt[g - 1] : 0u; len[x] = Sa.cnt[g] - s0; gs[x] = s0 - wbase; }
+                        }
+        #pragma unroll
+                        for (int x = 0; x < OVS_NET8_X; ++x) {
+                            const u32 lx = (len[x] > 1 && len[x] <= 8) ? len[x] : 0u;
+        #pragma unroll
+                            for (u32 q = 0; q < 8; ++q) a[x][q] = q < lx ? sm_get<U, KV>(Sa, gs[x] + q) : E::inf();
+                        }
+        #pragma unroll
+                        for (int x = 0; x < OVS_NET8_X; ++x) network8(a[x]);
+        #pragma unroll
+                        for (int x = 0; x < OVS_NET8_X; ++x) {
+                            const u32 lx = (len[x] > 1 && len[x] <= 8) ? len[x] : 0u;
+        #pragma unroll
+                            for (u32 q = 0; q < 8; ++q)
+                                if (q < lx) sm_put<U, KV>(Sa, gs[x] + q, a[x][q]);
+                        }
+        #pragma unroll
+                        for (int x = 0; x < OVS_NET8_X; ++x) {
+                            const u32 g = g0 + x * BS_NT + threadIdx.x;
+                            const u32 mb = __ballot_sync(0xffffffffu, len[x] > 8);
+                            if (mb) {
+                                u32 base = 0;
+                                if (lane == 0) base = atomicAdd(&s_nbig, __popc(mb));
+                                base = __shfl_sync(0xffffffffu, base, 0) + __popc(mb & ((1u << lane) - 1));
+                                if (len[x] > 8) {
+                                    if (base < BS_BIGMAX) s_big[base] = g;
+                                    else atomicOr(&s_over, 1u);
+                                }
+                            }
+                        }
+                    }
+                    __syncthreads();
+                    BS_PROBE(6)
+                    // 3b. listed groups of 9..16: one thread each (63-comparator network)
+                    const u32 nlisted = min(s_nbig, (u32)BS_BIGMAX);
+                    const bool rescan = s_over != 0;  // list overflow (pathological skew): scan all groups
+                    const u32 nwork = rescan ? wg1 - wg0 : nlisted;
+                    for (u32 q = threadIdx.x; q < nwork; q += BS_NT) {
+                        const u32 g = rescan ? wg0 + q : s_big[q];
+                        const u32 g_s = g ? Sa.cnt[g - 1] : 0u, len = Sa.cnt[g] - g_s, gs = g_s - wbase;
+                        if (len <= 8 || len > 16) continue;
+                        E a[16];
+        #pragma unroll
+                        for (u32 t = 0; t < 16; ++t) a[t] = t < len ? sm_get<U, KV>(Sa, gs + t) : E::inf();
+                        network16(a);
+        #pragma unroll
+                        for (u32 t = 0; t < 16; ++t)
+                            if (t < len) sm_put<U, KV>(Sa, gs + t, a[t]);
+                    }
+                    // 3c'. groups of 17..512: one warp each (register bitonic); over 512: the CTA
+                    for (u32 q = wid; q < nwork; q += BS_NT / 32) {
+                        const u32 g = rescan ? wg0 + q : s_big[q];
+                        const u32 g_s = g ? Sa.cnt[g - 1] : 0u, len = Sa.cnt[g] - g_s, gs = g_s - wbase;
+                        if (len <= 16) continue;
+                        if (len <= 32) warp_sort_group<U, KV, 1>(Sa, gs, len);
+                        else if (len <= 64) warp_sort_group<U, KV, 2>(Sa, gs, len);
+                        else if (len <= 128) warp_sort_group<U, KV, 4>(Sa, gs, len);
+                        else if (len <= 256) warp_sort_group<U, KV, 8>(Sa, gs, len);
+                        else if (len <= 512 && BS_WARPMAX >= 512) warp_sort_group<U, KV, BS_WARPMAX / 32>(Sa, gs, len);
+                        else if (lane == 0) {
+                            const u32 h = atomicAdd(&s_nhuge, 1u);
+                            if (h < BS_HUGEMAX) s_huge[h] = g;
+                            else atomicOr(status, ST_LIST_OVER);
+                        }
+                    }
+                    __syncthreads();
+                    BS_PROBE(7)
+                    // 3c. groups over BS_WARPMAX: in-place bitonic network in shared memory, all comparators
+                    // ascending (the first step of each merge compares i with its mirror), so virtual
+                    // +inf padding beyond len never moves and len need not be a power of two
+                    const u32 nhuge = min(s_nhuge, (u32)BS_HUGEMAX);
+                    for (u32 q = 0; q < nhuge; ++q) {
+                        const u32 g = s_huge[q];
+                        const u32 g_s = g ? Sa.cnt[g - 1] : 0u, len = Sa.cnt[g] - g_s, gs = g_s - wbase;
+                        u32 N = 1;
+                        while (N < len) N <<= 1;
+                        for (u32 kk = 2; kk <= N; kk <<= 1) {
+                            const u32 hk = kk >> 1;
+                            for (u32 t = threadIdx.x; t < N / 2; t += BS_NT) {
+                                const u32 blk = t / hk, off = t % hk;
+                                const u32 x = blk * kk + off, y = blk * kk + kk - 1 - off;
+                                if (y < len) smem_cex<U, KV>(Sa, gs + x, gs + y);
+                            }
+                            __syncthreads();
+                            for (u32 j = kk >> 2; j > 0; j >>= 1) {
+                                for (u32 t = threadIdx.x; t < N / 2; t += BS_NT) {
+                                    const u32 x = (t / j) * 2 * j + (t % j), y = x + j;
+                                    if (y < len) smem_cex<U, KV>(Sa, gs + x, gs + y);
+                                }
+                                __syncthreads();
+                            }
+                        }
+                    }
+                    __syncthreads();
+                    BS_PROBE(8)
+                    // 4. write the sorted bucket (16-byte stores where the output is aligned)
+                    {
+                        constexpr u32 V = 16 / sizeof(U);
+                        U* out = okeys + bk.beg + wbase;
+                        const u32 m = wm;  // this window's items
+                        const u32 mis = (u32)(((uintptr_t)out) & 15u) / (u32)sizeof(U);
+                        const u32 head = mis ? min(m, V - mis) : 0u;
+                        auto R = [&](U x) -> U { return out_raw ? Codec<DT>::raw(x) : x; };
+                        if (threadIdx.x < head) out[threadIdx.x] = R(Sa.k[threadIdx.x]);
+                        const u32 nv = (m - head) / V;
+                        uint4* o4 = (uint4*)(out + head);
+                        const uint4* s4 = (const uint4*)(Sa.k + head);
+                        for (u32 v = threadIdx.x; v < nv; v += BS_NT) {
+                            uint4 r = s4[v];
+                            U* e = (U*)&r;
+        #pragma unroll
+                            for (u32 q = 0; q < V; ++q) e[q] = R(e[q]);
+                            o4[v] = r;
+                        }
+                        for (u32 o = head + nv * V + threadIdx.x; o < m; o += BS_NT) out[o] = R(Sa.k[o]);
+                        if (KV) {
+                            for (u32 o = threadIdx.x; o < m; o += BS_NT) ovals[bk.beg + wbase + o] = Sa.v[o];
+                            if (oidx)
+                                for (u32 o = threadIdx.x; o < m; o += BS_NT) oidx[bk.beg + wbase + o] = Sa.i[o];
+                        }
+                    }
+                        __syncthreads();
+                    }
+                    wg0 = wg1;
+                }
+                __syncthreads();
             }
-            __syncthreads();
             BS_PROBE(9)
         }
         if (threadIdx.x == 0) {

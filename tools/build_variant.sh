@@ -4,7 +4,7 @@
 set -e
 NAME=$1; FLAGS=$2
 D=/root/repo/tools/variants/$NAME; mkdir -p $D
-C=/root/repo/paper_1608_08648_b200/csrc
+C=${SRC:-/root/repo/paper_1608_08648_b200/csrc}
 ARCH="-gencode arch=compute_100a,code=sm_100a"
 for f in ovs_api ovs_u32 ovs_i32 ovs_f64; do
   nvcc -O3 -std=c++17 $ARCH -lineinfo -Xcompiler -fPIC -I/root/repo/include $FLAGS -c -o $D/$f.o $C/$f.cu &

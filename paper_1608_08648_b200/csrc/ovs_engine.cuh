@@ -319,6 +319,62 @@ template <int DT, bool KV> struct Engine {
     }
 };
 
+// ------------------------------------------------------------------ level 1 (k_l1_setup, ...)
+// Re-splits every bucket of a device list by the whole GPU; the sub-buckets (in buffer
+// 1 - bucket.buf) are appended to out (its own fit list, sized for maxseg * L1_PS entries).
+template <int DT, bool KV> struct Level1 {
+    typedef typename Codec<DT>::U U;
+    static constexpr u32 PS = 256, LS = 1024, CH = 1u << 16;
+    Engine<DT, KV>& e;
+    u32 maxseg = 0, maxchunk = 0;
+    U* sk = nullptr; u32* st = nullptr; u32* lut = nullptr; Seg* segs = nullptr; u32* nsegs = nullptr;
+    Chunk* chunks = nullptr; u32* hist = nullptr; u32* tot = nullptr;
+    Level1(Engine<DT, KV>& eng, u32 max_segments) : e(eng) {
+        Ctx& c = e.c;
+        maxseg = std::max<u32>(1, max_segments);
+        maxchunk = e.n / CH + maxseg + 1;
+        sk = c.take<U>((size_t)maxseg * PS);
+        st = c.take<u32>((size_t)maxseg * PS);
+        lut = c.take<u32>((size_t)maxseg * (LS + 1));
+        segs = c.take<Seg>(maxseg);
+        nsegs = c.take<u32>(2);
+        chunks = c.take<Chunk>(maxchunk);
+        hist = c.take<u32>((size_t)maxchunk * PS);
+        tot = c.take<u32>((size_t)maxseg * (PS + 1));
+    }
+    static size_t setup_smem() { return (sizeof(U) + 4) * (size_t)PS * L1_SI; }
+    void run(const Bucket* list, const u32* nlist, typename Engine<DT, KV>::Lists& out, u64 seed) {
+        Ctx& c = e.c;
+        if (c.dry) return;
+        const u32 part = (u32)(e.cap * 6ull / 10);
+        const size_t sm0 = setup_smem();
+        OVS_CK(cudaFuncSetAttribute(k_l1_setup<DT, KV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm0));
+        launch(c, k_l1_setup<DT, KV>, maxseg, 1024, sm0, e.B, list, nlist, part, PS, LS, 10u, sk, st, lut, segs, nsegs,
+               seed, CH);
+        c.check();
+        launch(c, k_l1_chunks, 1, 1024, 0, segs, nsegs, CH, chunks, nsegs + 1);
+        c.check();
+        OVS_CK(cudaMemsetAsync(hist, 0, sizeof(u32) * (size_t)maxchunk * PS, c.st));
+        const size_t sm_h = cls_smem_bytes<U>(PS, LS) + 4 * (size_t)PS;
+        OVS_CK(cudaFuncSetAttribute(k_hist<DT, KV, false, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_h));
+        launch(c, k_hist<DT, KV, false, 1024>, std::min<u32>(maxchunk, 4 * (u32)c.di.sms), 1024, sm_h, e.B, chunks,
+               nsegs + 1, segs, sk, st, lut, PS, LS, hist, 1u, 0u, (u16*)nullptr);
+        c.check();
+        launch(c, k_colscan, std::min<u32>(maxseg * (PS / 32), 4 * (u32)c.di.sms), 1024, 0, hist, segs, nsegs, PS, tot);
+        c.check();
+        launch(c, k_segscan<U>, std::min<u32>(maxseg, 2 * (u32)c.di.sms), 1024, 0, segs, nsegs, PS, tot, sk, 1u, e.cap,
+               out.fit, out.nfit, out.fit_cap, (Bucket*)nullptr, (u32*)nullptr, 0u, (u64*)nullptr, c.status);
+        c.check();
+        constexpr int IT = PartItems<U, KV>::v;
+        const size_t sm_s = Engine<DT, KV>::scatter_smem(PS, LS);
+        auto ks = k_scatter<DT, KV, false, PT_NT, IT>;
+        OVS_CK(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_s));
+        launch(c, ks, std::min<u32>(maxchunk, 2 * (u32)c.di.sms), PT_NT, sm_s, e.B, chunks, nsegs + 1, segs, sk, st, lut,
+               PS, LS, hist, tot, 0u);
+        c.check();
+    }
+};
+
 // ------------------------------------------------------------------ internal sort of an array
 // keys (ordered u64) [+ u32 values, sorted stably] in buffer 0 of B; buffer 1 scratch.
 template <bool KV> struct InternalSort {
@@ -585,6 +641,11 @@ template <int DT, bool KV> struct DroSort {
     InternalSort<true>* ts64 = nullptr;
     u32* bound = nullptr; u32* cnt = nullptr; u32* tot = nullptr; u32* nseg = nullptr;
     Seg* seg = nullptr;
+    // sequences and buckets of n/p keys far over the on-chip capacity: level 1 re-splits them
+    // with the whole GPU before the bucket sorter (instead of one CTA re-splitting each)
+    bool big = false;
+    Level1<DT, KV>* l1x = nullptr;
+    typename Engine<DT, KV>::Lists lb;
 
     DroSort(Ctx& ctx, U* keys, u32* vals, u32 n_, u32 p_, u32 r_, u32 flags_)
         : c(ctx), e(ctx), n(n_), p(p_), r(r_), flags(flags_) {
@@ -617,8 +678,19 @@ template <int DT, bool KV> struct DroSort {
         nseg = c.take<u32>(2);
         e.carve_lists(l1, p);
         e.carve_lists(l2, p);
+        big = (n / p) > BS_WMAX * e.cap;
+        if (big) {
+            l1x = new Level1<DT, KV>(e, p);
+            e.carve_lists(lb, p * Level1<DT, KV>::PS);
+        }
     }
-    ~DroSort() { delete ts32; delete ts64; }
+    ~DroSort() { delete ts32; delete ts64; delete l1x; }
+    // sort the buckets of list l (all far over capacity) through level 1
+    void sort_big(typename Engine<DT, KV>::Lists& l, u64 seed, U* okeys, u32* ovals, u32* oidx, bool out_raw) {
+        fill_u32(c, lb.nfit, 0, 2);
+        l1x->run(l.fit, l.nfit, lb, seed);
+        e.bucket_sort(lb, seed, okeys, ovals, oidx, out_raw);
+    }
 
     void run() {
         if (c.dry) return;
@@ -628,7 +700,16 @@ template <int DT, bool KV> struct DroSort {
         fill_u32(c, l1.nfit, 0, 2);
         launch(c, k_dro_segments, cdiv(p, 256), 256, 0, l1.fit, l1.nfit, n, p);
         c.check();
-        e.bucket_sort(l1, 0x5e9u, B.k[1], KV ? B.v[1] : nullptr, KV ? B.i[1] : nullptr, false);
+        if (big) {
+            // ordered keys (+ values, indices) in buffer 1, sequences re-split 1 -> 0, sorted -> 1
+            launch(c, k_to_ordered<DT, KV>, 4 * c.di.sms, 1024, 0, B, n);
+            c.check();
+            launch(c, k_list_flip, cdiv(p, 256), 256, 0, l1.fit, l1.nfit);
+            c.check();
+            sort_big(l1, 0x5e9u, B.k[1], KV ? B.v[1] : nullptr, KV ? B.i[1] : nullptr, false);
+        } else {
+            e.bucket_sort(l1, 0x5e9u, B.k[1], KV ? B.v[1] : nullptr, KV ? B.i[1] : nullptr, false);
+        }
         // a10-a12: regular sample, sample sort, splitters
         launch(c, k_dro_sample<U>, cdiv((u64)ns, 256), 256, 0, B.k[1], n, p, s, flags & OVS_DRO_PADDED_POSITIONS,
                                                              t_pack, t_key, t_tag);
@@ -656,7 +737,8 @@ template <int DT, bool KV> struct DroSort {
         launch(c, k_dro_gather<U, KV>, cdiv((u64)p * p * 32, 256), 256, 0, B, n, p, bound, cnt, tot);
         c.check();
         c.mark(3);
-        e.bucket_sort(l2, 0x5e9u);
+        if (big) sort_big(l2, 0x5e9u, B.k[0], KV ? B.v[0] : nullptr, nullptr, true);
+        else e.bucket_sort(l2, 0x5e9u);
         c.mark(4);
     }
 };

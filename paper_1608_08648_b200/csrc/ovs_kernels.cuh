@@ -1267,6 +1267,141 @@ __device__ __forceinline__ void mbar_wait(u64* bar, u32 parity) {
         : "memory");
 }
 
+// ------------------------------------------------------------------ level 1: buckets far over capacity
+// A list of buckets much larger than one SM's shared memory is re-split by the whole GPU ("the
+// split keys are to be sorted ... recursively by this same extended method"): every
+// bucket becomes a segment with its own sub-splitters (a sorted random sample of it, 8 records per
+// sub-splitter, tie-broken by position / original index), classifier table and chunks; then the
+// segment-aware histogram, column scan, segment scan and staged scatter kernels partition all of
+// them at once (all SMs instead of one CTA per bucket), and the sub-buckets join a bucket list.
+// Sub-splitter choice only affects sub-bucket sizes: the sorted result is unique either way.
+constexpr u32 L1_SI = 8;
+
+template <int DT, bool KV>
+__global__ void __launch_bounds__(1024) k_l1_setup(Bufs<typename Codec<DT>::U> B, const Bucket* list, const u32* nlist,
+                                                   u32 part, u32 PS, u32 LS, u32 log2LS, typename Codec<DT>::U* sk_pool,
+                                                   u32* st_pool, u32* lut_pool, Seg* segs, u32* nsegs, u64 seed,
+                                                   u32 chunk) {
+    PDL_PROLOGUE();
+    typedef typename Codec<DT>::U U;
+    extern __shared__ __align__(16) char smem[];
+    const u32 nl = *nlist;
+    const u32 g = blockIdx.x;
+    if (g == 0 && threadIdx.x == 0) *nsegs = nl;
+    if (g >= nl) return;
+    const Bucket bk = list[g];
+    const u32 len = bk.len;
+    const U* src = B.k[bk.buf];
+    const u32* isrc = KV ? B.i[bk.buf] : nullptr;
+    u32 P = (len + part - 1) / part;
+    P = max(2u, min(PS, P));
+    const u32 ns = P * L1_SI - 1;
+    u32 N = 32;
+    while (N < ns) N <<= 1;
+    U* tk = (U*)smem;
+    u32* tt = (u32*)(smem + sizeof(U) * (size_t)PS * L1_SI);
+    for (u32 j = threadIdx.x; j < N; j += blockDim.x) {
+        if (j < ns) {
+            const u32 o = bk.beg + (u32)__umul64hi(rng_H(seed ^ ((u64)bk.beg * 0x9e3779b97f4a7c15ull), 80, j), (u64)len);
+            tk[j] = src[o];
+            tt[j] = KV ? isrc[o] : o;
+        } else {
+            tk[j] = umax_of<U>();
+            tt[j] = 0xffffffffu;
+        }
+    }
+    __syncthreads();
+    cta_bitonic_kt<U>(tk, tt, N);
+    // sub-splitters (rank (i+1) L1_SI - 1 of the sample) to the pool and to the front of tk
+    U ck = 0;
+    u32 ct = 0;
+    const bool mine = threadIdx.x + 1 < P;
+    if (mine) { ck = tk[(threadIdx.x + 1) * L1_SI - 1]; ct = tt[(threadIdx.x + 1) * L1_SI - 1]; }
+    __syncthreads();
+    if (mine) {
+        tk[threadIdx.x] = ck;
+        sk_pool[(size_t)g * PS + threadIdx.x] = ck;
+        st_pool[(size_t)g * PS + threadIdx.x] = ct;
+    }
+    __syncthreads();
+    // classifier table of the segment (same format as k_build_cls0)
+    u32 L = 64;
+    while (L < 4 * P && L < LS) L <<= 1;
+    u32 log2L = 6;
+    while ((1u << log2L) < L) ++log2L;
+    const U base = tk[0];
+    const U span = tk[P - 2] - base;
+    const u32 bl = bitlen<U>(span);
+    const u32 shift = bl > log2L ? bl - log2L : 0u;
+    const U lim = span >> shift;
+    u32* lut = lut_pool + (size_t)g * (LS + 1);
+    for (u32 e = threadIdx.x; e < L; e += blockDim.x) {
+        const u32 a = ((U)e > lim) ? (P - 1) : count_less_key<U>(tk, P - 1, (U)(base + ((U)e << shift)));
+        const u32 b = ((U)(e + 1) > lim) ? (P - 1) : count_less_key<U>(tk, P - 1, (U)(base + ((U)(e + 1) << shift)));
+        const u32 fr = b > a ? cls_frac<U>((U)(tk[a] - base) & (((U)1 << shift) - 1), shift) : 0u;
+        lut[e] = a | (min(b - a, 7u) << 13) | (fr << 16);
+    }
+    if (threadIdx.x == 0) {
+        lut[L] = P - 1;
+        Seg sg;
+        sg.lo = bk.lo; sg.hi = bk.hi; sg.base = (u64)base;
+        sg.beg = bk.beg; sg.len = len; sg.P = P; sg.shift = shift; sg.L = L;
+        sg.chunk0 = 0; sg.nchunk = (len + chunk - 1) / chunk; sg.src = bk.buf;
+        sg.loose = (bk.level & BK_LOOSE) ? 1u : 0u; sg.pad = (bk.level & 0xffffu) + 1;
+        segs[g] = sg;
+    }
+}
+
+// chunk list of all segments (one CTA): chunk0 = exclusive scan of the segments' chunk counts
+__global__ void __launch_bounds__(1024) k_l1_chunks(Seg* segs, const u32* nsegs, u32 chunk, Chunk* chunks, u32* nchunks) {
+    PDL_PROLOGUE();
+    __shared__ u32 red[33];
+    const u32 ns = *nsegs;
+    u32 carry = 0;
+    for (u32 s0 = 0; s0 < ns; s0 += 1024) {
+        const u32 s = s0 + threadIdx.x;
+        const u32 c = s < ns ? segs[s].nchunk : 0u;
+        u32 tot;
+        const u32 ex = block_exclusive_scan<1024>(c, red, &tot) + carry;
+        if (s < ns) {
+            segs[s].chunk0 = ex;
+            const Seg sg = segs[s];
+            for (u32 q = 0; q < c; ++q) {
+                Chunk ch;
+                ch.beg = sg.beg + q * chunk;
+                ch.end = min(sg.beg + sg.len, sg.beg + (q + 1) * chunk);
+                ch.seg = s; ch.pad = 0;
+                chunks[ex + q] = ch;
+            }
+        }
+        carry += tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *nchunks = carry;
+}
+
+// raw keys of buffer 0 -> ordered keys in buffer 1 (+ values and original indices): the DRO
+// sequences become ordinary (non-raw) buckets for level 1
+template <int DT, bool KV>
+__global__ void k_to_ordered(Bufs<typename Codec<DT>::U> B, u32 n) {
+    PDL_PROLOGUE();
+    for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        B.k[1][i] = Codec<DT>::ord(B.k[0][i]);
+        if (KV) { B.v[1][i] = B.v[0][i]; B.i[1][i] = i; }
+    }
+}
+
+// every bucket of a list moved to buffer 1 - buf (the DRO sequences after k_to_ordered)
+__global__ void k_list_flip(Bucket* list, const u32* nlist) {
+    PDL_PROLOGUE();
+    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= *nlist) return;
+    Bucket b = list[i];
+    b.buf = 1 - b.buf;
+    b.level &= ~BK_RAW;
+    list[i] = b;
+}
+
 // ------------------------------------------------------------------ internal splitters
 // Splitters of an internal sort of a whole array of n items (not part of the contract; used
 // for p == 1 and for sorting the sample / candidate arrays): a random sample with

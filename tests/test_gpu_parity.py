@@ -195,6 +195,18 @@ def test_dro_pairs_stable_edge_matrix(ovs, orc, dist, n, p, r):
     dro_case(ovs, orc, ovs_inputs.keys(dist, n, seed=3), p, r, kv=True)
 
 
+@pytest.mark.parametrize("dist,n,p,r,kv", [("u32", 2_000_003, 8, 2, False), ("i32_few", 1_600_000, 4, 3, False),
+                                           ("u16key", 600_001, 4, 2, True), ("f64_normal", 900_000, 4, 2, False)])
+def test_dro_level1(ovs, orc, dist, n, p, r, kv):
+    """Sequences and buckets of n/p keys far over the on-chip capacity: both go through the
+    GPU-wide level-1 re-split (segment-aware histogram and scatter) before the bucket sorter."""
+    x = ovs_inputs.keys(dist, n, seed=13)
+    v = ovs_inputs.index_values(n) if kv else None
+    ref = orc.dro_sort(x, p, r, vals=v)
+    out, vout, rep = gpu_sort(ovs, x, "dro", p, r, 0, v)
+    check(ref, out, vout, rep, p)
+
+
 def test_dro_closed_forms(ovs):
     """Sorted input: counts = m_j; reverse: m_{p-1-j}; constant: m_j (tags order equal keys)."""
     n, p, r = 1_000_003, 64, 3

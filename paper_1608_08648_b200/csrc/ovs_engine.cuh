@@ -760,6 +760,8 @@ template <int DT, bool KV> struct DistSort {
     u64* counts64 = nullptr;
     RosSampler<DT, true>* smp = nullptr;  // a1-a4 over the global index set
     u32* bstart = nullptr; u32* srcoff = nullptr;
+    Level1<DT, KV>* l1x = nullptr;  // owned buckets far over capacity
+    typename Engine<DT, KV>::Lists lb;
 
     DistSort(Ctx& ctx, u32 n_local, u64 n_global, u32 p_, u32 s_, u64 seed_, u32 world_, u32 recv_capacity)
         : c(ctx), e(ctx), f(ctx), nl(n_local), p(p_), s(s_), world(world_), recv_cap(recv_capacity), ng(n_global),
@@ -784,8 +786,12 @@ template <int DT, bool KV> struct DistSort {
         bstart = c.take<u32>(p + 2);
         srcoff = c.take<u32>(world + 1);
         f.carve_lists(lf, p);
+        if (ng / p > BS_WMAX * f.cap) {
+            l1x = new Level1<DT, KV>(f, p / world + 1);
+            f.carve_lists(lb, (p / world + 1) * Level1<DT, KV>::PS);
+        }
     }
-    ~DistSort() { delete smp; }
+    ~DistSort() { delete smp; delete l1x; }
 
     void sample(const U* keys, u64* rec) {
         if (c.dry) return;
@@ -812,16 +818,26 @@ template <int DT, bool KV> struct DistSort {
 
     void finish(const U* rk, const u32* rv, const u32* ri, const u32* C, u32 rnk, U* out_k, u32* out_v) {
         if (c.dry) return;
-        launch(c, k_dist_plan<U>, 1, 1024, 0, C, world, p, rnk, z.sk, bstart, srcoff, lf.fit, lf.nfit, recv_cap, c.status);
+        launch(c, k_dist_plan<U>, 1, 1024, 0, C, world, p, rnk, z.sk, bstart, srcoff, lf.fit, lf.nfit, recv_cap, c.status,
+               1u);
         c.check();
         const u32 nb = (u32)((u64)(rnk + 1) * p / world) - (u32)((u64)rnk * p / world);
         f.B.k[0] = out_k;
         f.B.v[0] = out_v;
-        launch(c, k_dist_gather<U, KV>, cdiv((u64)world * nb * 32, 256), 256, 0, 
-            rk, rv, ri, out_k, out_v, f.B.i[0], C, world, p, rnk, bstart, srcoff);
+        // the owned buckets are assembled in the scratch buffer 1 and sorted into the output
+        // (buffer 0): a bucket does not live in the output array, so oversized ones can be
+        // sorted in windows; buckets far over capacity go through level 1 first
+        launch(c, k_dist_gather<U, KV>, cdiv((u64)world * nb * 32, 256), 256, 0,
+            rk, rv, ri, f.B.k[1], f.B.v[1], f.B.i[1], C, world, p, rnk, bstart, srcoff);
         c.check();
         fill_u32(c, lf.ticket, 0, 1);
-        f.bucket_sort(lf, seed ^ 0xf1);
+        if (l1x) {
+            fill_u32(c, lb.nfit, 0, 2);
+            l1x->run(lf.fit, lf.nfit, lb, seed ^ 0xf2);
+            f.bucket_sort(lb, seed ^ 0xf1);
+        } else {
+            f.bucket_sort(lf, seed ^ 0xf1);
+        }
     }
 };
 

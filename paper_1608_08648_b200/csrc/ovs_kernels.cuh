@@ -2531,7 +2531,7 @@ __global__ void k_u64_to_u32(const u64* a, u32* b, u32 n) {
 template <class U>
 __global__ void __launch_bounds__(1024) k_dist_plan(const u32* C /*world x p*/, u32 world, u32 p, u32 rank, const U* sk,
                                                     u32* bstart /*nb+1*/, u32* srcoff /*world*/, Bucket* list, u32* nlist,
-                                                    u32 cap_items, u32* status) {
+                                                    u32 cap_items, u32* status, u32 buf) {
     PDL_PROLOGUE();
     __shared__ u32 red[33];
     const u32 b0 = (u32)((u64)rank * p / world), b1 = (u32)((u64)(rank + 1) * p / world), nb = b1 - b0;
@@ -2557,7 +2557,7 @@ __global__ void __launch_bounds__(1024) k_dist_plan(const u32* C /*world x p*/, 
         if (len == 0) continue;
         const u32 q = atomicAdd(nlist, 1u);
         Bucket bk;
-        bk.beg = bstart[b]; bk.len = len; bk.buf = 0;
+        bk.beg = bstart[b]; bk.len = len; bk.buf = buf;
         const u32 g = b0 + b;  // global bucket id
         const bool lo_open = (g == 0), hi_open = (g + 1 == p);
         bk.level = (lo_open || hi_open) ? BK_LOOSE : 0u;

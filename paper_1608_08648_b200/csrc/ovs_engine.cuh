@@ -279,7 +279,7 @@ template <int DT, bool KV> struct Engine {
         if (use_wc(z.P)) {
             constexpr int IT = WC_ITEMS * 4 / (int)sizeof(U);  // u32: WC_ITEMS keys per thread
             const size_t sm_w = wc_smem_bytes<U>(z.P);
-            auto kw = k_scatter_wc<DT, WC_NT, IT>;
+            auto kw = k_scatter_wc<DT, WC_NT, IT, true>;
             OVS_CK(cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_w));
             launch(c, kw, z.nchunk, WC_NT, sm_w, B, z.chunks, z.nchunks, z.seg, z.P, z.hist, z.tot, z.bid);
             c.check();
@@ -329,6 +329,7 @@ template <int DT, bool KV> struct Level1 {
     u32 maxseg = 0, maxchunk = 0;
     U* sk = nullptr; u32* st = nullptr; u32* lut = nullptr; Seg* segs = nullptr; u32* nsegs = nullptr;
     Chunk* chunks = nullptr; u32* hist = nullptr; u32* tot = nullptr;
+    u16* bid = nullptr;  // keys only: sub-bucket ids (the write-combining scatter's input)
     Level1(Engine<DT, KV>& eng, u32 max_segments) : e(eng) {
         Ctx& c = e.c;
         maxseg = std::max<u32>(1, max_segments);
@@ -341,6 +342,7 @@ template <int DT, bool KV> struct Level1 {
         chunks = c.take<Chunk>(maxchunk);
         hist = c.take<u32>((size_t)maxchunk * PS);
         tot = c.take<u32>((size_t)maxseg * (PS + 1));
+        if (!KV) bid = c.take<u16>(e.n);
     }
     static size_t setup_smem() { return (sizeof(U) + 4) * (size_t)PS * L1_SI; }
     void run(const Bucket* list, const u32* nlist, typename Engine<DT, KV>::Lists& out, u64 seed) {
@@ -358,19 +360,28 @@ template <int DT, bool KV> struct Level1 {
         const size_t sm_h = cls_smem_bytes<U>(PS, LS) + 4 * (size_t)PS;
         OVS_CK(cudaFuncSetAttribute(k_hist<DT, KV, false, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_h));
         launch(c, k_hist<DT, KV, false, 1024>, std::min<u32>(maxchunk, 4 * (u32)c.di.sms), 1024, sm_h, e.B, chunks,
-               nsegs + 1, segs, sk, st, lut, PS, LS, hist, 1u, 0u, (u16*)nullptr);
+               nsegs + 1, segs, sk, st, lut, PS, LS, hist, 1u, 0u, bid);
         c.check();
         launch(c, k_colscan, std::min<u32>(maxseg * (PS / 32), 4 * (u32)c.di.sms), 1024, 0, hist, segs, nsegs, PS, tot);
         c.check();
         launch(c, k_segscan<U>, std::min<u32>(maxseg, 2 * (u32)c.di.sms), 1024, 0, segs, nsegs, PS, tot, sk, 1u, e.cap,
                out.fit, out.nfit, out.fit_cap, (Bucket*)nullptr, (u32*)nullptr, 0u, (u64*)nullptr, c.status);
         c.check();
-        constexpr int IT = PartItems<U, KV>::v;
-        const size_t sm_s = Engine<DT, KV>::scatter_smem(PS, LS);
-        auto ks = k_scatter<DT, KV, false, PT_NT, IT>;
-        OVS_CK(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_s));
-        launch(c, ks, std::min<u32>(maxchunk, 2 * (u32)c.di.sms), PT_NT, sm_s, e.B, chunks, nsegs + 1, segs, sk, st, lut,
-               PS, LS, hist, tot, 0u);
+        if (!KV) {
+            constexpr int IT = WC_ITEMS * 4 / (int)sizeof(U);
+            const size_t sm_w = wc_smem_bytes<U>(PS);
+            auto kw = k_scatter_wc<DT, WC_NT, IT, false>;
+            OVS_CK(cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_w));
+            launch(c, kw, std::min<u32>(maxchunk, (u32)c.di.sms), WC_NT, sm_w, e.B, chunks, nsegs + 1, segs, PS, hist, tot,
+                   (const u16*)bid);
+        } else {
+            constexpr int IT = PartItems<U, KV>::v;
+            const size_t sm_s = Engine<DT, KV>::scatter_smem(PS, LS);
+            auto ks = k_scatter<DT, KV, false, PT_NT, IT>;
+            OVS_CK(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_s));
+            launch(c, ks, std::min<u32>(maxchunk, 2 * (u32)c.di.sms), PT_NT, sm_s, e.B, chunks, nsegs + 1, segs, sk, st,
+                   lut, PS, LS, hist, tot, 0u);
+        }
         c.check();
     }
 };

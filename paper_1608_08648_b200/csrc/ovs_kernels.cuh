@@ -1095,7 +1095,9 @@ template <class U> __host__ __device__ constexpr size_t wc_smem_bytes(u32 PS) {
     return 32 * (size_t)PS + 8 * (size_t)PS;  // wc, q, sb
 }
 
-template <int DT, int NT, int ITEMS>
+// LEVEL0: the caller's raw keys in buffer 0 -> buffer 1; otherwise ordered keys of every chunk's
+// segment source buffer -> the other buffer (level 1)
+template <int DT, int NT, int ITEMS, bool LEVEL0>
 __global__ void __launch_bounds__(NT, 1) k_scatter_wc(Bufs<typename Codec<DT>::U> B, const Chunk* chunks,
                                                        const u32* nchunks, const Seg* segs, u32 PS, const u32* hist,
                                                        const u32* tot_pool, const u16* bid) {
@@ -1111,12 +1113,12 @@ __global__ void __launch_bounds__(NT, 1) k_scatter_wc(Bufs<typename Codec<DT>::U
     u32* q = (u32*)(smem + 32 * (size_t)PS);
     u32* sb = q + PS;
     const u32 nc = *nchunks;
-    U* dst = B.k[1];
-    const U* src = B.k[0];
     for (u32 c = blockIdx.x; c < nc; c += gridDim.x) {
         const Chunk ch = chunks[c];
         const Seg sg = segs[ch.seg];
         const u32 P = sg.P;
+        const U* src = B.k[LEVEL0 ? 0 : sg.src];
+        U* dst = B.k[LEVEL0 ? 1 : 1 - sg.src];
         const u32* hrow = hist + (size_t)c * PS;
         const u32* bst = tot_pool + (size_t)ch.seg * (PS + 1);
         for (u32 b = threadIdx.x; b < P; b += NT) {
@@ -1179,7 +1181,7 @@ __global__ void __launch_bounds__(NT, 1) k_scatter_wc(Bufs<typename Codec<DT>::U
 #pragma unroll
             for (u32 j = 0; j < ITEMS; ++j) {
                 const u32 b = (id[j / 2] >> (16 * (j & 1))) & 0xffffu;
-                k[j] = Codec<DT>::ord(k[j]);
+                if (LEVEL0) k[j] = Codec<DT>::ord(k[j]);
                 if (vmask & (1u << j)) pos[j] = atomicAdd(&q[b], 1u);
             }
 #pragma unroll

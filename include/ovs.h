@@ -131,6 +131,15 @@ int ovs_dist_finish(const void* d_recv_keys, const uint32_t* d_recv_vals, const 
                     const uint32_t* d_all_counts, void* d_out_keys, uint32_t* d_out_vals, void* d_ws, size_t ws_bytes,
                     void* stream);
 
+/* Parameters for which the buckets of n keys fit one SM's shared memory in one level (SURVEY.md
+ * §8(f) f4; the paper leaves p to the user and takes s = lg^2 n).  ROS: p = the
+ * smallest power of two with n/p <= 0.6 x the on-chip capacity, capped at the largest p the fast
+ * one-level scatter handles (p = 1, a plain sort, when n fits on chip), s = 64 (or less when
+ * p*s-1 > n).  DRO: the same p (also <= sqrt(n)), r = min(ceil(log2 n), floor(n/p^2)) >= 1.  Writes
+ * method, p, s into *out (flags = 0, seed = 1); OVS_EINVAL / OVS_EDTYPE on bad arguments.  Pure
+ * host computation from the device's shared-memory size (no launch). */
+int ovs_auto_params(size_t n, int dtype, int with_values, int method, ovs_params* out);
+
 /* Profiling hook (thread-local): subsequent sort calls on this thread record events[k]
  * (cudaEvent_t passed as void*) on their stream at phase boundary k, without synchronising:
  *   0 start, 1 after the sample + splitters (a1-a4), 2 after classify + histogram + scans

@@ -63,6 +63,8 @@ def lib() -> ctypes.CDLL:
                                             ctypes.POINTER(Report)]
         L.ovs_set_phase_events.restype = None
         L.ovs_set_phase_events.argtypes = [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int]
+        L.ovs_auto_params.restype = i32
+        L.ovs_auto_params.argtypes = [sz, i32, i32, i32, ctypes.POINTER(Params)]
         L.ovs_last_error.restype = ctypes.c_char_p
         L.ovs_version.restype = ctypes.c_char_p
         _lib = L
@@ -98,6 +100,15 @@ def _dtype_code(dt) -> int:
 
 def params(method: str = "ros", p: int = 64, s: int = 32, seed: int = 1, padded: bool = False) -> Params:
     return Params(METHODS[method], p, s, OVS_DRO_PADDED_POSITIONS if padded else 0, seed)
+
+
+def auto_params(n: int, dtype, with_values: bool = False, method: str = "ros") -> Params:
+    """ovs_auto_params: p (and s or r) for which the buckets fit on chip in one level."""
+    prm = Params()
+    rc = lib().ovs_auto_params(n, _dtype_code(dtype), int(with_values), 0 if method == "ros" else 1, ctypes.byref(prm))
+    if rc != OVS_OK:
+        raise OvsError(rc, "ovs_auto_params")
+    return prm
 
 
 def workspace_bytes(n: int, dtype_code: int, with_values: bool, prm: Params) -> int:

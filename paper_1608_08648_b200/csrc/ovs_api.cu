@@ -115,6 +115,21 @@ static int sort_impl(void* d_keys, uint32_t* d_vals, bool kv, size_t n, int dtyp
     }
 }
 
+// ovs_auto_params: the smallest power-of-two p whose buckets fit on chip with margin
+template <class U, bool KV> static u32 auto_p(size_t n, const DevInfo& di) {
+    const u64 cap = bucket_cap<U, KV>(di);
+    if (n <= cap) return 1;
+    const u64 part = cap * 6 / 10;
+    u32 pmax = 8192;  // 13-bit classifier entries; keys only: the write-combining scatter's range
+    if (!KV) while (pmax > 2 && wc_smem_bytes<U>(pmax) + 512 > (size_t)di.smem_optin) pmax >>= 1;
+    else
+        while (pmax > 2 && scatter_smem_bytes<U, KV, PartItems<U, KV>::v, PT_NT>(pmax, 64) + 1024 > (size_t)di.smem_optin)
+            pmax >>= 1;
+    u32 p = 2;
+    while ((u64)p < pmax && (n + p - 1) / p > part) p <<= 1;
+    return p;
+}
+
 extern "C" {
 
 size_t ovs_workspace_bytes(size_t n, int dtype, int with_values, const ovs_params* prm) {
@@ -252,5 +267,31 @@ void ovs_set_phase_events(void* const* events, int count) {
 }
 
 const char* ovs_version(void) { return "ovs 0.1 sm_100a"; }
+
+int ovs_auto_params(size_t n, int dtype, int with_values, int method, ovs_params* out) {
+    if (!out || (method != OVS_ROS && method != OVS_DRO) || n == 0 || n >= 0xffffffffull) return OVS_EINVAL;
+    if (dtype != OVS_U32 && dtype != OVS_I32 && dtype != OVS_F64) return OVS_EDTYPE;
+    const DevInfo di = dev_info();
+    const bool kv = with_values != 0;
+    u32 p = dtype == OVS_F64 ? (kv ? auto_p<u64, true>(n, di) : auto_p<u64, false>(n, di))
+                             : (kv ? auto_p<u32, true>(n, di) : auto_p<u32, false>(n, di));
+    u32 s = 1;
+    if (method == OVS_ROS) {
+        s = 64;
+        while (p > 1 && s > 1 && (u64)p * s - 1 > n) s >>= 1;
+    } else {
+        while (p > 1 && (u64)p * p > n) p >>= 1;  // r >= 1 needs r*p <= n/p
+        u32 lg = 0;
+        while (lg < 32 && (1ull << lg) < n) ++lg;
+        const u64 rmax = p > 1 ? n / ((u64)p * p) : 1;
+        s = (u32)std::max<u64>(1, std::min<u64>(lg, rmax));
+    }
+    out->method = (uint32_t)method;
+    out->p = p;
+    out->s = s;
+    out->flags = 0;
+    out->seed = 1;
+    return OVS_OK;
+}
 
 }  // extern "C"

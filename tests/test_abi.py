@@ -69,3 +69,27 @@ def test_binding_raises_without_cuda():
     import paper_1608_08648_b200 as ovs
     with pytest.raises(Exception):
         ovs.Sorter(1000, torch.uint32, False, "ros", 4, 8, 1)
+
+
+def test_auto_params():
+    """ovs_auto_params (host only): buckets of n/p keys fit the on-chip capacity with margin, p within
+    the one-level limits, the sample-size preconditions of PAPER.md:566 (ps-1 <= n) and of the DRO
+    regular sample (r*p <= n/p) hold."""
+    import paper_1608_08648_b200 as ovs
+    import torch
+    for n in (1000, 1 << 20, 1 << 24, 1 << 27, 3_000_017):
+        for dt in (torch.uint32, torch.float64):
+            for kv in (False, True):
+                pr = ovs.auto_params(n, dt, kv, "ros")
+                assert pr.method == 0 and pr.p >= 1 and pr.p & (pr.p - 1) == 0
+                if pr.p > 1:
+                    assert pr.p * pr.s - 1 <= n and pr.s >= 1
+                    assert ovs.workspace_bytes(n, ovs._dtype_code(dt), kv, pr) > 0
+                pd = ovs.auto_params(n, dt, kv, "dro")
+                if pd.p > 1:
+                    assert pd.s >= 1 and pd.s * pd.p <= n // pd.p
+    small = ovs.auto_params(1000, torch.uint32)
+    assert small.p == 1
+    big = ovs.auto_params(1 << 27, torch.uint32)
+    assert big.p == 4096 and big.s == 64          # the metric's configuration
+    assert ovs.auto_params(1 << 27, torch.float64).p < 1 << 27

@@ -456,7 +456,7 @@ template <bool TAG> struct Selector {
         cb = c.take<uint8_t>(m);
         e.carve_lists(l, G);
     }
-    template <class U> void run(u32 P, u32 s, u64 seed, U* sk, u32* st) {
+    template <class U> void run(u32 P, u32 s, u32 f, u64 seed, U* sk, u32* st) {
         Ctx& c = e.c;
         if (c.dry) return;
         const u32 grid = cdiv(m, SEL_PER);
@@ -466,13 +466,13 @@ template <bool TAG> struct Selector {
                                                     l.fit, l.nfit);
         c.check();
         e.bucket_sort(l, seed);
-        pick<U>(P, s, sk, st);
+        pick<U>(P, s, f, sk, st);
     }
     // S[q] = T[(q+1)s - 1], q < P-1, from the sorted records
-    template <class U> void pick(u32 P, u32 s, U* sk, u32* st) {
+    template <class U> void pick(u32 P, u32 s, u32 f, U* sk, u32* st) {
         Ctx& c = e.c;
         if (c.dry) return;
-        launch(c, k_pick_splitters<U>, cdiv(P, 256), 256, 0, e.B.k[0], e.B.k[0], e.B.v[0], P, s, sk, st);
+        launch(c, k_pick_splitters<U>, cdiv(P, 256), 256, 0, e.B.k[0], e.B.k[0], e.B.v[0], P, s, f, sk, st);
         c.check();
     }
 };
@@ -520,7 +520,7 @@ template <int DT, bool DIST> struct RosSampler {
                                                       c.status);
         c.check();
     }
-    void select(u32 P, u32 s, u64 seed, U* sk, u32* st) { sel->template run<U>(P, s, seed, sk, st); }
+    void select(u32 P, u32 s, u32 f, u64 seed, U* sk, u32* st) { sel->template run<U>(P, s, f, seed, sk, st); }
 };
 
 // ------------------------------------------------------------------ ROS contract sort
@@ -535,8 +535,8 @@ template <int DT, bool KV> struct RosSort {
     u64* counts = nullptr;
     RosSampler<DT, false>* smp = nullptr;  // a1-a4
     // Refinement: when the contract's buckets (n/p keys) cannot be sorted on chip, level 0
-    // partitions into p*f buckets with the splitters T[(i+1)s/f - 1] (f | s, >= 8 samples
-    // each), a superset of the contract's T[(q+1)s - 1] (i = (q+1)f - 1).  Contract bucket q is
+    // partitions into p*f buckets with the splitters T[floor((i+1)s/f) - 1] (>= 8 samples each),
+    // a superset of the contract's T[(q+1)s - 1] (i = (q+1)f - 1).  Contract bucket q is
     // exactly the concatenation of level-0 buckets qf .. qf+f-1, so the output is unchanged and
     // the contract's splitters and counts are read off (k_pick_splitters, k_fold_counts).
     u32 f = 1;
@@ -563,7 +563,7 @@ template <int DT, bool KV> struct RosSort {
             // fast scatter handles (keys only: the write-combining one)
             u32 pmax = std::min<u32>(8192, e.max_p_one_level());
             if (!KV && e.use_wc(p)) while (pmax > p && !e.use_wc(pmax)) --pmax;
-            while (s % (2 * f) == 0 && s / (2 * f) >= 8 && (u64)p * 2 * f <= pmax && (u64)n > (u64)p * f * e.cap)
+            while (s / (2 * f) >= 8 && (u64)p * 2 * f <= pmax && (u64)n > (u64)p * f * e.cap)
                 f *= 2;
             P0 = p * f;
             if (f > 1) {
@@ -587,8 +587,8 @@ template <int DT, bool KV> struct RosSort {
             smp->draw(seed);
             smp->take(seed, e.B.k[0], 0, n, nullptr);
             // a3+a4: sort T by (key, i); S[q] = T[(q+1)s - 1] (refined: every (s/f)-th)
-            smp->select(p * f, s / f, seed ^ 0x5eed, z.sk, z.st);
-            if (f > 1) smp->sel->template pick<U>(p, s, rep_sk, rep_st);
+            smp->select(p * f, s, f, seed ^ 0x5eed, z.sk, z.st);
+            if (f > 1) smp->sel->template pick<U>(p, s, 1, rep_sk, rep_st);
         } else {
             e.internal_splitters(z, seed);
         }
@@ -727,7 +727,7 @@ template <int DT, bool KV> struct DroSort {
         c.check();
         if (ts32) ts32->run(0xd0d0);
         else ts64->run(0xd0d0);
-        launch(c, k_pick_splitters<U>, cdiv(p, 256), 256, 0, t_pack, t_key, t_tag, p, s, sk, st);
+        launch(c, k_pick_splitters<U>, cdiv(p, 256), 256, 0, t_pack, t_key, t_tag, p, s, 1u, sk, st);
         c.check();
         c.mark(1);
         // a13: split every sorted sequence by binary search; bucket starts and run offsets
@@ -817,7 +817,7 @@ template <int DT, bool KV> struct DistSort {
         c.check();
         // the coarse-bucket counters are zeroed here too: this call may run on a fresh process
         OVS_CK(cudaMemsetAsync(smp->sel->gcnt, 0, 8 * SEL_GMAX, c.st));
-        smp->select(p, s, seed ^ 0x5eed, z.sk, z.st);
+        smp->select(p, s, 1, seed ^ 0x5eed, z.sk, z.st);
         e.B.k[0] = keys; e.B.v[0] = vals;
         e.B.k[1] = send_k; e.B.v[1] = send_v; e.B.i[1] = send_i;
         e.B.i[0] = nullptr;

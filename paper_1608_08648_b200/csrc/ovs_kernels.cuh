@@ -575,12 +575,13 @@ __global__ void __launch_bounds__(1024) k_sel_scatter(const u64* tk, const u32* 
 
 // a4: S[q] = T[(q+1)s - 1] (reading Q4); also the p-1 report arrays
 template <class U>
-__global__ void k_pick_splitters(const u64* t_pack, const u64* t_key, const u32* t_tag, u32 P, u32 s,
+// (f > 1: the refined splitters floor((q+1)s/f) - 1 of RosSort, a superset of the contract's)
+__global__ void k_pick_splitters(const u64* t_pack, const u64* t_key, const u32* t_tag, u32 P, u32 s, u32 f,
                                  U* sk, u32* st) {
     PDL_PROLOGUE();
     u32 q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q + 1 >= P) return;
-    u64 r = (u64)(q + 1) * s - 1;
+    u64 r = (u64)(q + 1) * s / f - 1;
     if (sizeof(U) == 4) {
         u64 v = t_pack[r];
         sk[q] = (U)(v >> 32);

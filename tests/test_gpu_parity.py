@@ -71,6 +71,8 @@ EDGE = [
     ("i32_few", 1_000_003, 1000, 16), ("f64_normal", 200_000, 64, 32), ("f64_uniform", 1_000_003, 7, 64),
     ("u32_u31", 100_000, 1, 1), ("f64_normal", 300_000, 1, 1), ("u32", 3_000_017, 4096, 64), ("u32_u31", 65_536, 2, 1),
     ("u32", 2_000_000, 2, 1_000_000),
+    # refinement of oversized contract buckets with s not a multiple of the refinement factor
+    ("u32", 1_500_000, 8, 37), ("f64_uniform", 2_000_000, 16, 51), ("i32_few", 3_000_000, 32, 129),
 ]
 
 

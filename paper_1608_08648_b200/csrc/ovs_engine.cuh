@@ -13,6 +13,8 @@
 #include <stdexcept>
 #include <string>
 #include <vector>
+#include <mutex>
+#include <unordered_map>
 
 namespace ovs {
 
@@ -77,6 +79,25 @@ struct Ctx {
 };
 
 static inline u32 cdiv(u64 a, u64 b) { return (u32)((a + b - 1) / b); }
+
+// Dynamic shared memory limit of a kernel, raised once per process to the most the kernel can
+// use (the device's opt-in limit minus its static shared memory), so no launch pays for
+// cudaFuncSetAttribute again; `need` is checked against it.
+template <class... KA>
+static void smem_limit(void (*k)(KA...), size_t need, const DevInfo& di) {
+    static std::mutex mu;
+    static std::unordered_map<const void*, size_t> lim;
+    std::lock_guard<std::mutex> g(mu);
+    auto it = lim.find((const void*)k);
+    if (it == lim.end()) {
+        cudaFuncAttributes fa;
+        OVS_CK(cudaFuncGetAttributes(&fa, (const void*)k));
+        const size_t mx = (size_t)di.smem_optin - fa.sharedSizeBytes;
+        OVS_CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx));
+        it = lim.emplace((const void*)k, mx).first;
+    }
+    if (need > it->second) throw CudaFail("kernel shared memory " + std::to_string(need) + " > limit " + std::to_string(it->second));
+}
 
 // Kernel launch with programmatic dependent launch (PDL, cudaLaunchAttributeProgrammatic-
 // StreamSerialization): every kernel lets its successor be scheduled as soon as all of its own
@@ -245,7 +266,7 @@ template <int DT, bool KV> struct Engine {
         const u32 si = std::max<u32>(1, std::min<u32>(32, 8192 / z.P));
         const u32 N = pow2_at_least(z.P * si);
         const size_t sm = (sizeof(U) + 4) * (size_t)N;
-        OVS_CK(cudaFuncSetAttribute(k_internal_sample<DT, KV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        smem_limit(k_internal_sample<DT, KV>, sm, c.di);
         launch(c, k_internal_sample<DT, KV>, 1, 1024, sm, B, n, z.P, si, N, seed, z.sk, z.st);
         c.check();
     }
@@ -254,7 +275,7 @@ template <int DT, bool KV> struct Engine {
     void level0(Level0& z, Lists& l, u64* counts_out) {
         if (c.dry) return;
         const size_t sm_cls = std::max<size_t>(sizeof(U) * std::max<u32>(z.P, 1), 16);
-        OVS_CK(cudaFuncSetAttribute(k_build_cls0<U>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_cls));
+        smem_limit(k_build_cls0<U>, sm_cls, c.di);
         launch(c, k_build_cls0<U>, std::max<u32>(1, std::min<u32>(z.L / 1024 + 1, 16)), 1024, sm_cls, 
             z.sk, z.P, z.L, z.log2L, z.lut, z.seg, n, z.nchunk);
         c.check();
@@ -265,7 +286,7 @@ template <int DT, bool KV> struct Engine {
         const size_t sm_h = cls_smem_bytes<U>(z.P, z.L) + 4 * (size_t)z.P;
         const u32 hsplit = 2;  // two 1024-thread CTAs per chunk
         OVS_CK(cudaMemsetAsync(z.hist, 0, sizeof(u32) * (size_t)z.nchunk * z.P, c.st));
-        OVS_CK(cudaFuncSetAttribute(k_hist<DT, KV, true, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_h));
+        smem_limit(k_hist<DT, KV, true, 1024>, sm_h, c.di);
         launch(c, k_hist<DT, KV, true, 1024>, z.nchunk * hsplit, 1024, sm_h, B, z.chunks, z.nchunks, z.seg, z.sk, z.st,
                                                                            z.lut, z.P, z.L, z.hist, hsplit, tag_base,
                                                                            use_wc(z.P) ? z.bid : nullptr);
@@ -280,14 +301,14 @@ template <int DT, bool KV> struct Engine {
             constexpr int IT = WC_ITEMS * 4 / (int)sizeof(U);  // u32: WC_ITEMS keys per thread
             const size_t sm_w = wc_smem_bytes<U>(z.P);
             auto kw = k_scatter_wc<DT, WC_NT, IT, true>;
-            OVS_CK(cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_w));
+            smem_limit(kw, sm_w, c.di);
             launch(c, kw, z.nchunk, WC_NT, sm_w, B, z.chunks, z.nchunks, z.seg, z.P, z.hist, z.tot, z.bid);
             c.check();
         } else {
             constexpr int IT = PartItems<U, KV>::v;
             const size_t sm_s = scatter_smem(z.P, z.L);
             auto ks = k_scatter<DT, KV, true, PT_NT, IT>;
-            OVS_CK(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_s));
+            smem_limit(ks, sm_s, c.di);
             launch(c, ks, z.nchunk, PT_NT, sm_s, B, z.chunks, z.nchunks, z.seg, z.sk, z.st, z.lut, z.P, z.L, z.hist,
                                                 z.tot, tag_base);
             c.check();
@@ -307,8 +328,8 @@ template <int DT, bool KV> struct Engine {
         if (c.dry) return;
         if (!okeys) { okeys = B.k[0]; ovals = KV ? B.v[0] : nullptr; }
         const size_t sm = bucket_smem<U, KV>(cap);
-        OVS_CK(cudaFuncSetAttribute(k_bucket_sort<DT, KV, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        OVS_CK(cudaFuncSetAttribute(k_bucket_sort<DT, KV, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        smem_limit(k_bucket_sort<DT, KV, false>, sm, c.di);
+        smem_limit(k_bucket_sort<DT, KV, true>, sm, c.di);
         fill_u32(c, l.nwl, 0, 2);
         launch(c, k_bucket_sort<DT, KV, false>, l.grid, BS_NT, sm, l.fit, l.nfit, l.ticket, B, okeys, ovals, oidx, out_raw,
                                                           cap, l.stack, seed, c.status, ixbits, l.wl, l.nwl, l.wl_cap);
@@ -350,7 +371,7 @@ template <int DT, bool KV> struct Level1 {
         if (c.dry) return;
         const u32 part = (u32)(e.cap * 6ull / 10);
         const size_t sm0 = setup_smem();
-        OVS_CK(cudaFuncSetAttribute(k_l1_setup<DT, KV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm0));
+        smem_limit(k_l1_setup<DT, KV>, sm0, c.di);
         launch(c, k_l1_setup<DT, KV>, maxseg, 1024, sm0, e.B, list, nlist, part, PS, LS, 10u, sk, st, lut, segs, nsegs,
                seed, CH);
         c.check();
@@ -358,7 +379,7 @@ template <int DT, bool KV> struct Level1 {
         c.check();
         OVS_CK(cudaMemsetAsync(hist, 0, sizeof(u32) * (size_t)maxchunk * PS, c.st));
         const size_t sm_h = cls_smem_bytes<U>(PS, LS) + 4 * (size_t)PS;
-        OVS_CK(cudaFuncSetAttribute(k_hist<DT, KV, false, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_h));
+        smem_limit(k_hist<DT, KV, false, 1024>, sm_h, c.di);
         launch(c, k_hist<DT, KV, false, 1024>, std::min<u32>(maxchunk, 4 * (u32)c.di.sms), 1024, sm_h, e.B, chunks,
                nsegs + 1, segs, sk, st, lut, PS, LS, hist, 1u, 0u, bid);
         c.check();
@@ -371,14 +392,14 @@ template <int DT, bool KV> struct Level1 {
             constexpr int IT = WC_ITEMS * 4 / (int)sizeof(U);
             const size_t sm_w = wc_smem_bytes<U>(PS);
             auto kw = k_scatter_wc<DT, WC_NT, IT, false>;
-            OVS_CK(cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_w));
+            smem_limit(kw, sm_w, c.di);
             launch(c, kw, std::min<u32>(maxchunk, (u32)c.di.sms), WC_NT, sm_w, e.B, chunks, nsegs + 1, segs, PS, hist, tot,
                    (const u16*)bid);
         } else {
             constexpr int IT = PartItems<U, KV>::v;
             const size_t sm_s = Engine<DT, KV>::scatter_smem(PS, LS);
             auto ks = k_scatter<DT, KV, false, PT_NT, IT>;
-            OVS_CK(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_s));
+            smem_limit(ks, sm_s, c.di);
             launch(c, ks, std::min<u32>(maxchunk, 2 * (u32)c.di.sms), PT_NT, sm_s, e.B, chunks, nsegs + 1, segs, sk, st,
                    lut, PS, LS, hist, tot, 0u);
         }

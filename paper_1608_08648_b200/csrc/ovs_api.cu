@@ -14,9 +14,9 @@ using namespace ovs;
 // ------------------------------------------------------------------ C ABI
 static Out plan_dispatch(Ctx& c, void* keys, u32* vals, size_t n, int dtype, const ovs_params* prm) {
     const bool kv = vals != nullptr || (c.dry && keys == (void*)1);
-    if (dtype == OVS_U32) return plan_u32(c, keys, vals, n, prm, kv);
-    if (dtype == OVS_I32) return plan_i32(c, keys, vals, n, prm, kv);
-    return plan_f64(c, keys, vals, n, prm, kv);
+    if (dtype == OVS_U32) return kv ? plan_u32_v(c, keys, vals, n, prm) : plan_u32_k(c, keys, vals, n, prm);
+    if (dtype == OVS_I32) return kv ? plan_i32_v(c, keys, vals, n, prm) : plan_i32_k(c, keys, vals, n, prm);
+    return kv ? plan_f64_v(c, keys, vals, n, prm) : plan_f64_k(c, keys, vals, n, prm);
 }
 
 static int sort_impl(void* d_keys, uint32_t* d_vals, bool kv, size_t n, int dtype, const ovs_params* prm, void* d_ws,
@@ -170,9 +170,9 @@ static int dist_validate(uint64_t n_local, uint64_t n_global, int dtype, const o
 }
 
 static size_t dist_dispatch(Ctx& c, int step, int dtype, bool kv, const ovs_params* prm, const DistArgs& a) {
-    if (dtype == OVS_U32) return dist_u32(c, step, prm, a, kv);
-    if (dtype == OVS_I32) return dist_i32(c, step, prm, a, kv);
-    return dist_f64(c, step, prm, a, kv);
+    if (dtype == OVS_U32) return kv ? dist_u32_v(c, step, prm, a) : dist_u32_k(c, step, prm, a);
+    if (dtype == OVS_I32) return kv ? dist_i32_v(c, step, prm, a) : dist_i32_k(c, step, prm, a);
+    return kv ? dist_f64_v(c, step, prm, a) : dist_f64_k(c, step, prm, a);
 }
 
 static int dist_call(int step, int dtype, bool kv, const ovs_params* prm, DistArgs a, void* d_ws, size_t ws_bytes,

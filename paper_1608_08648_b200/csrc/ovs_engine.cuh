@@ -918,14 +918,20 @@ size_t dist_run(Ctx& c, int step, const ovs_params* prm, const DistArgs& a) {
     }
     return c.off + 256;
 }
-size_t dist_u32(Ctx& c, int step, const ovs_params* prm, const DistArgs& a, bool kv);
-size_t dist_i32(Ctx& c, int step, const ovs_params* prm, const DistArgs& a, bool kv);
-size_t dist_f64(Ctx& c, int step, const ovs_params* prm, const DistArgs& a, bool kv);
+size_t dist_u32_k(Ctx& c, int step, const ovs_params* prm, const DistArgs& a);
+size_t dist_u32_v(Ctx& c, int step, const ovs_params* prm, const DistArgs& a);
+size_t dist_i32_k(Ctx& c, int step, const ovs_params* prm, const DistArgs& a);
+size_t dist_i32_v(Ctx& c, int step, const ovs_params* prm, const DistArgs& a);
+size_t dist_f64_k(Ctx& c, int step, const ovs_params* prm, const DistArgs& a);
+size_t dist_f64_v(Ctx& c, int step, const ovs_params* prm, const DistArgs& a);
 
-// per-dtype entry points (ovs_u32.cu, ovs_i32.cu, ovs_f64.cu)
-Out plan_u32(Ctx& c, void* keys, u32* vals, size_t n, const ovs_params* prm, bool kv);
-Out plan_i32(Ctx& c, void* keys, u32* vals, size_t n, const ovs_params* prm, bool kv);
-Out plan_f64(Ctx& c, void* keys, u32* vals, size_t n, const ovs_params* prm, bool kv);
+// per-(dtype, keys/pairs) entry points (ovs_<dtype>_<k|v>.cu)
+Out plan_u32_k(Ctx& c, void* keys, u32* vals, size_t n, const ovs_params* prm);
+Out plan_u32_v(Ctx& c, void* keys, u32* vals, size_t n, const ovs_params* prm);
+Out plan_i32_k(Ctx& c, void* keys, u32* vals, size_t n, const ovs_params* prm);
+Out plan_i32_v(Ctx& c, void* keys, u32* vals, size_t n, const ovs_params* prm);
+Out plan_f64_k(Ctx& c, void* keys, u32* vals, size_t n, const ovs_params* prm);
+Out plan_f64_v(Ctx& c, void* keys, u32* vals, size_t n, const ovs_params* prm);
 int validate(size_t n, int dtype, const ovs_params* prm);
 DevInfo dev_info();
 extern thread_local std::string g_err;

@@ -1,0 +1,25 @@
+// ovs_f64_k.cu — instantiation of the sort engine for f64 (IEEE total order) keys, keys only (one
+// translation unit per (dtype, keys/pairs) so the build runs in parallel).
+#include "ovs_engine.cuh"
+
+namespace ovs {
+Out plan_f64_k(Ctx& c, void* keys, u32* vals, size_t n, const ovs_params* prm) {
+    return plan_or_run<DT_F64, false>(c, keys, vals, n, prm);
+}
+size_t dist_f64_k(Ctx& c, int step, const ovs_params* prm, const DistArgs& a) {
+    return dist_run<DT_F64, false>(c, step, prm, a);
+}
+}  // namespace ovs
+
+#ifdef OVS_BS_PROF  // experiments only: bucket-sorter phase cycles of this translation unit's kernels
+extern "C" int ovs_debug_bsprof_f64_k(unsigned long long* out, int reset) {
+    unsigned long long v[16];
+    if (cudaMemcpyFromSymbol(v, ovs::g_bsprof, sizeof(v)) != cudaSuccess) return 1;
+    for (int i = 0; i < 16; ++i) out[i] += v[i];
+    if (reset) {
+        unsigned long long z[16] = {0};
+        cudaMemcpyToSymbol(ovs::g_bsprof, z, sizeof(z));
+    }
+    return 0;
+}
+#endif

@@ -6,7 +6,7 @@ NAME=$1; FLAGS=$2
 D=/root/repo/tools/variants/$NAME; mkdir -p $D
 C=${SRC:-/root/repo/paper_1608_08648_b200/csrc}
 ARCH="-gencode arch=compute_100a,code=sm_100a"
-for f in ovs_api ovs_u32 ovs_i32 ovs_f64; do
+for f in ovs_api ovs_u32_k ovs_u32_v ovs_i32_k ovs_i32_v ovs_f64_k ovs_f64_v; do
   nvcc -O3 -std=c++17 $ARCH -lineinfo -Xcompiler -fPIC -I/root/repo/include $FLAGS -c -o $D/$f.o $C/$f.cu &
 done
 wait

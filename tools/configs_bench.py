@@ -45,9 +45,9 @@ for name, dist, dseed, n, method, p, s, kv, bpk in CASES:
 
 import ctypes
 L = ovs.lib()
-if hasattr(L, "ovs_debug_bsprof_u32"):
+if hasattr(L, "ovs_debug_bsprof_u32_k"):
     arr = (ctypes.c_ulonglong * 16)()
-    for dt in ("u32", "i32", "f64"):
+    for dt in ("u32_k", "u32_v", "i32_k", "i32_v", "f64_k", "f64_v"):
         getattr(L, "ovs_debug_bsprof_" + dt)(arr, 1)
     names = ["resplit-push", "loose", "setup", "hist", "scan", "scatter", "net8", "net16+warp", "huge", "write", "rs-sample", "rs-count", "rs-scatter"]
     tot = arr[15] or 1

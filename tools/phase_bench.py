@@ -39,10 +39,10 @@ for path in libs:
 import ctypes
 for path in libs:
     L = ctypes.CDLL(path or ovs.LIB_PATH)
-    if not hasattr(L, "ovs_debug_bsprof_u32"):
+    if not hasattr(L, "ovs_debug_bsprof_u32_k"):
         continue
     arr = (ctypes.c_ulonglong * 16)()
-    for dt in ("u32", "i32", "f64"):
+    for dt in ("u32_k", "u32_v", "i32_k", "i32_v", "f64_k", "f64_v"):
         getattr(L, "ovs_debug_bsprof_" + dt)(arr, 1)
     srt = ovs.Sorter(n, torch.uint32, False, "ros", p, s, 1) if False else None
     names = ["resplit-push", "loose", "setup", "hist", "scan", "scatter", "net8", "net16+warp", "huge", "write", "rs-sample", "rs-count", "rs-scatter"]

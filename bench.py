@@ -30,6 +30,7 @@ sys.path.insert(0, ROOT)
 WORKLOAD = dict(workload="C5/metric: 2^27 uint32 keys per GPU, uniform on [0,2^32) (data seed 51), "
                          "ROS p=4096 s=64 (sample seed 1)",
                 n=1 << 27, dist="u32", data_seed=51, method="ros", p=4096, s=64, seed=1)
+METRIC = "sort throughput (BASELINE.json: Gkeys/s for 2^27 uint32 keys per B200)"
 # algorithmic HBM bytes per key of each timed phase, u32 keys
 PHASE_BYTES = {"classify_hist": 4, "scatter": 8, "bucket_sort": 8}
 
@@ -123,7 +124,7 @@ def run_reference(args):
     sec = sum(ts) / len(ts)
     v = n_s / sec / 1e9
     sample = f"first {n_s} keys of the workload, ROS p={p_s} s={WORKLOAD['s']} (n/p kept), 1 thread"
-    line = {"impl": "reference", "metric": "sort throughput", "value": v, "unit": "Gkeys/s", "n_gpus": args.gpus,
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "Gkeys/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
             "config": {"workload": WORKLOAD["workload"], "global_batch": n_s, "seq_len": None,
@@ -187,7 +188,7 @@ def run_dist(args, x, src, work, dev, rank, world, local):
     te = torch.tensor([statistics.mean(e2e)], device=dev, dtype=torch.float64)
     dist.all_reduce(te, op=dist.ReduceOp.MAX)
     if rank == 0:
-        line = {"metric": "sort throughput (BASELINE.json: Gkeys/s for 2^27 uint32 keys per B200)",
+        line = {"metric": METRIC,
                 "value": value, "unit": "Gkeys/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
                 "dtype": "u32", "data": "synthetic (ovs_inputs, seeded)",
@@ -347,7 +348,7 @@ def main():
                "sample": f"{n_c} keys of the workload, ROS p={p_c} s={s}, one run, {dt:.1f} s"}
 
     if rank == 0:
-        line = {"metric": "sort throughput (BASELINE.json: Gkeys/s for 2^27 uint32 keys per B200)",
+        line = {"metric": METRIC,
                 "value": value, "unit": "Gkeys/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
                 "dtype": "u32", "data": "synthetic (ovs_inputs, seeded)",

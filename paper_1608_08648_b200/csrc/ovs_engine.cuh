@@ -459,6 +459,7 @@ template <bool TAG> struct Selector {
     const u32* tt = nullptr;
     u64* csk = nullptr; u32* cst = nullptr; uint8_t* cb = nullptr;
     u32* gcnt = nullptr; u32* gcur = nullptr;  // zeroed by the owner before run()
+    u32 stride = 1;  // coarse subsample: T[i] (1, T in random order) or random positions (0)
     Selector(Ctx& c, u32 m_, const u64* tk_, const u32* tt_, u32* gcnt_, u32* gcur_)
         : e(c), m(m_), tk(tk_), tt(tt_), gcnt(gcnt_), gcur(gcur_) {
         u32 g = 1;
@@ -481,9 +482,9 @@ template <bool TAG> struct Selector {
         Ctx& c = e.c;
         if (c.dry) return;
         const u32 grid = cdiv(m, SEL_PER);
-        launch(c, k_sel_count<TAG>, grid, 1024, 0, tk, tt, m, G, csk, cst, cb, gcnt);
+        launch(c, k_sel_count<TAG>, grid, 1024, 0, tk, tt, m, G, stride, csk, cst, cb, gcnt);
         c.check();
-        launch(c, k_sel_scatter<TAG>, grid, 1024, 0, tk, tt, m, G, cb, gcnt, gcur, csk, e.B.k[0], e.B.v[0], e.B.i[0],
+        launch(c, k_sel_scatter<TAG>, grid, 1024, 0, tk, tt, m, G, cb, gcnt, gcur, csk, e.B.k[1], e.B.v[1], e.B.i[1],
                                                     l.fit, l.nfit);
         c.check();
         e.bucket_sort(l, seed);
@@ -695,6 +696,8 @@ template <int DT, bool KV> struct DroSort {
         counts = c.take<u64>(p);
         sk = c.take<U>(p);
         st = c.take<u32>(p);
+        // (the sample of sorted runs is sorted by the generic internal sort; the ROS coarse-bucket
+        // selector measured slower here: its buckets of ~n/(128 r p) records overflow the chip)
         if (sizeof(U) == 4) {
             t_pack = c.take<u64>(ns);
             ts32 = new InternalSort<false>(c, ns, t_pack, nullptr);

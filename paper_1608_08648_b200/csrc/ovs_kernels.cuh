@@ -477,7 +477,7 @@ __device__ __forceinline__ u32 coarse_of(const u64* ck, const u32* ct, u32 nc, u
 }
 
 template <bool TAG>
-__global__ void __launch_bounds__(1024) k_sel_count(const u64* tk, const u32* tt, u32 m, u32 G, u64* csk, u32* cst,
+__global__ void __launch_bounds__(1024) k_sel_count(const u64* tk, const u32* tt, u32 m, u32 G, u32 stride, u64* csk, u32* cst,
                                                     uint8_t* cb, u32* gcnt) {
     PDL_PROLOGUE();
     __shared__ u64 qk[SEL_Q];
@@ -488,8 +488,11 @@ __global__ void __launch_bounds__(1024) k_sel_count(const u64* tk, const u32* tt
         u32 N = 1;
         while (N < Q) N <<= 1;
         for (u32 i = threadIdx.x; i < N; i += blockDim.x) {
-            qk[i] = i < Q ? tk[i] : ~0ull;
-            qt[i] = i < Q ? (TAG ? tt[i] : 0u) : 0xffffffffu;
+            // records i (stride 1: T in random order, ROS) or at random positions (stride 0: T made
+            // of sorted runs, DRO's regular samples, where fixed offsets would be biased)
+            const u64 r = stride ? (u64)i * stride : __umul64hi(rng_H(0x5e1ec7ull, 90, i), (u64)m);
+            qk[i] = i < Q ? tk[r] : ~0ull;
+            qt[i] = i < Q ? (TAG ? tt[r] : 0u) : 0xffffffffu;
         }
         __syncthreads();
         cta_bitonic_kt<u64>(qk, qt, N);
@@ -562,7 +565,7 @@ __global__ void __launch_bounds__(1024) k_sel_scatter(const u64* tk, const u32* 
             const u32 len = st[g + 1] - st[g];
             if (len == 0) continue;
             Bucket b;
-            b.beg = st[g]; b.len = len; b.buf = 0;
+            b.beg = st[g]; b.len = len; b.buf = 1;  // sorted into buffer 0 (not in place: windows allowed)
             b.level = (g == 0 || g + 1 == G) ? BK_LOOSE : 0u;
             b.lo = g ? csk[g - 1] : 0ull;
             b.hi = g + 1 < G ? csk[g] : ~0ull;

@@ -1,6 +1,6 @@
 #!/bin/bash
 # build an experimental variant of libovs.so: tools/build_variant.sh <name> "<nvcc -D flags>"
-# -> tools/variants/libovs_<name>.so (u32 translation unit + api only; enough for the metric sort)
+# -> tools/vso/libovs_<name>.so (u32 translation unit + api only; enough for the metric sort)
 set -e
 NAME=$1; FLAGS=$2
 D=/root/repo/tools/variants/$NAME; mkdir -p $D
@@ -10,6 +10,6 @@ for f in ovs_api ovs_u32_k ovs_u32_v ovs_i32_k ovs_i32_v ovs_f64_k ovs_f64_v; do
   nvcc -O3 -std=c++17 $ARCH -lineinfo -Xcompiler -fPIC -I/root/repo/include $FLAGS -c -o $D/$f.o $C/$f.cu &
 done
 wait
-nvcc $ARCH -shared -o /root/repo/tools/variants/libovs_$NAME.so $D/*.o
+mkdir -p /root/repo/tools/vso; nvcc $ARCH -shared -o /root/repo/tools/vso/libovs_$NAME.so $D/*.o
 rm -rf $D
 echo built libovs_$NAME.so

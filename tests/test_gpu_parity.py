@@ -209,6 +209,18 @@ def test_dro_level1(ovs, orc, dist, n, p, r, kv):
     check(ref, out, vout, rep, p)
 
 
+@pytest.mark.parametrize("method,dist,n,p,s", [("dro", "u16key", 400_003, 8, 3), ("ros", "u32_few4", 600_000, 16, 8),
+                                               ("ros", "f64_normal", 500_000, 8, 8), ("dro", "i32_gauss", 700_000, 4, 5)])
+def test_pairs_windows(ovs, orc, method, dist, n, p, s):
+    """Key-value buckets of 1.1-4x the on-chip capacity (no refinement possible with these s):
+    the windowed bucket sorter (k_bucket_sort<..., WIN>) with values and indices."""
+    x = ovs_inputs.keys(dist, n, seed=17)
+    v = ovs_inputs.index_values(n)
+    ref = orc.ros_sort(x, p, s, 3, vals=v) if method == "ros" else orc.dro_sort(x, p, s, vals=v)
+    out, vout, rep = gpu_sort(ovs, x, method, p, s, 3, v)
+    check(ref, out, vout, rep, p)
+
+
 def test_dro_closed_forms(ovs):
     """Sorted input: counts = m_j; reverse: m_{p-1-j}; constant: m_j (tags order equal keys)."""
     n, p, r = 1_000_003, 64, 3

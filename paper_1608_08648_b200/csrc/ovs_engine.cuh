@@ -276,16 +276,12 @@ template <int DT, bool KV> struct Engine {
         if (c.dry) return;
         const size_t sm_cls = std::max<size_t>(sizeof(U) * std::max<u32>(z.P, 1), 16);
         smem_limit(k_build_cls0<U>, sm_cls, c.di);
-        launch(c, k_build_cls0<U>, std::max<u32>(1, std::min<u32>(z.L / 1024 + 1, 16)), 1024, sm_cls, 
-            z.sk, z.P, z.L, z.log2L, z.lut, z.seg, n, z.nchunk);
+        launch(c, k_build_cls0<U>, std::max<u32>(16, std::min<u32>(z.L / 1024 + 1, 64)), 1024, sm_cls,
+            z.sk, z.P, z.L, z.log2L, z.lut, z.seg, n, z.nchunk, z.chunk, z.chunks, z.nchunks, l.nfit, z.hist,
+            z.nchunk * z.P);
         c.check();
-        launch(c, k_make_chunks0, cdiv(z.nchunk, 256), 256, 0, z.chunks, z.nchunk, n, z.chunk);
-        c.check();
-        set_pair(z.nchunks, z.nchunk, 1);  // device counts: chunks, segments
-        fill_u32(c, l.nfit, 0, 2);
         const size_t sm_h = cls_smem_bytes<U>(z.P, z.L) + 4 * (size_t)z.P;
         const u32 hsplit = 2;  // two 1024-thread CTAs per chunk
-        OVS_CK(cudaMemsetAsync(z.hist, 0, sizeof(u32) * (size_t)z.nchunk * z.P, c.st));
         smem_limit(k_hist<DT, KV, true, 1024>, sm_h, c.di);
         launch(c, k_hist<DT, KV, true, 1024>, z.nchunk * hsplit, 1024, sm_h, B, z.chunks, z.nchunks, z.seg, z.sk, z.st,
                                                                            z.lut, z.P, z.L, z.hist, hsplit, tag_base,
@@ -316,10 +312,6 @@ template <int DT, bool KV> struct Engine {
         if (mark_phases) c.mark(3);
     }
 
-    void set_pair(u32* p, u32 a, u32 b) {
-        launch(c, k_set2, 1, 1, 0, p, a, b);
-        c.check();
-    }
 
     // sorts every bucket of the list into okeys (+ ovals, + oidx) at the bucket's position;
     // out_raw applies the codec's inverse (the caller's dtype) on the way out

@@ -621,9 +621,26 @@ __device__ u32 count_less_key(const U* sk, u32 nsp, U thr) {
 // internal sort of a whole array): LUT entries in parallel over CTAs, splitter keys staged in
 // shared memory; CTA 0 writes the segment header.
 template <class U>
+// Also the rest of level 0's setup (one launch instead of five): the chunk list, the device
+// counts (chunks, segments), the zeroed bucket-list counters and the zeroed histogram rows.
 __global__ void __launch_bounds__(1024) k_build_cls0(const U* sk, u32 P, u32 L, u32 log2L, u32* lut, Seg* seg, u32 n,
-                                                     u32 nchunk) {
+                                                     u32 nchunk, u32 chunk, Chunk* chunks, u32* ncounts, u32* nfit,
+                                                     u32* hist, u32 hist_words) {
     PDL_PROLOGUE();
+    {
+        const u32 gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
+        for (u32 c = gt; c < nchunk; c += gs) {
+            Chunk x;
+            x.beg = c * chunk;
+            x.end = min(n, (c + 1) * chunk);
+            x.seg = 0; x.pad = 0;
+            chunks[c] = x;
+        }
+        uint4* h4 = (uint4*)hist;  // hist_words is a multiple of 4 (carved 256-byte aligned)
+        for (u32 i = gt; i < hist_words / 4; i += gs) h4[i] = make_uint4(0, 0, 0, 0);
+        for (u32 i = (hist_words / 4) * 4 + gt; i < hist_words; i += gs) hist[i] = 0;
+        if (gt == 0) { ncounts[0] = nchunk; ncounts[1] = 1; nfit[0] = 0; nfit[1] = 0; }
+    }
     extern __shared__ __align__(16) char smem[];
     U* s = (U*)smem;
     for (u32 i = threadIdx.x; i + 1 < P; i += blockDim.x) s[i] = sk[i];
@@ -656,16 +673,6 @@ __global__ void __launch_bounds__(1024) k_build_cls0(const U* sk, u32 P, u32 L, 
     }
 }
 
-__global__ void k_make_chunks0(Chunk* ch, u32 nchunk, u32 n, u32 chunk) {
-    PDL_PROLOGUE();
-    u32 c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= nchunk) return;
-    Chunk x;
-    x.beg = c * chunk;
-    x.end = min(n, (c + 1) * chunk);
-    x.seg = 0; x.pad = 0;
-    ch[c] = x;
-}
 
 // ------------------------------------------------------------------ partition: classifier loader
 __host__ __device__ constexpr size_t a16(size_t x) { return (x + 15) & ~(size_t)15; }
@@ -2600,8 +2607,6 @@ __global__ void k_fill_u32(u32* p, u32 v, u32 n) {
     if (i < n) p[i] = v;
 }
 
-__global__ void k_set2(u32* p, u32 a, u32 b) {
-    PDL_PROLOGUE(); p[0] = a; p[1] = b; }
 
 __global__ void k_iota(u32* p, u32 n) {
     PDL_PROLOGUE();

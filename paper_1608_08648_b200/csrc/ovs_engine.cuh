@@ -150,6 +150,9 @@ template <class U, bool KV> static size_t bucket_smem(u32 cap) {
 #endif
 // write-combining scatter: WC_NT threads x WC_ITEMS (u32) keys per sub-tile
 constexpr int WC_NT = OVS_WC_NT, WC_ITEMS = 8192 / OVS_WC_NT;
+#ifndef OVS_SEL_PER_BUCKET
+#define OVS_SEL_PER_BUCKET 2048u
+#endif
 // partition tile shape: 512 threads x ITEMS per sub-tile
 constexpr int PT_NT = 512;
 template <class U, bool KV> struct PartItems { static constexpr int v = (sizeof(U) == 4 && !KV) ? 16 : 8; };
@@ -455,7 +458,7 @@ template <bool TAG> struct Selector {
     Selector(Ctx& c, u32 m_, const u64* tk_, const u32* tt_, u32* gcnt_, u32* gcur_)
         : e(c), m(m_), tk(tk_), tt(tt_), gcnt(gcnt_), gcur(gcur_) {
         u32 g = 1;
-        while (g * 2 <= m / 2048 && g * 2 <= SEL_GMAX) g *= 2;
+        while (g * 2 <= m / OVS_SEL_PER_BUCKET && g * 2 <= SEL_GMAX) g *= 2;
         G = g;
         e.n = m;
         e.cap = bucket_cap<u64, TAG>(c.di);

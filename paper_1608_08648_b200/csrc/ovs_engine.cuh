@@ -99,11 +99,9 @@ static void smem_limit(void (*k)(KA...), size_t need, const DevInfo& di) {
     if (need > it->second) throw CudaFail("kernel shared memory " + std::to_string(need) + " > limit " + std::to_string(it->second));
 }
 
-// Kernel launch with programmatic dependent launch (PDL, cudaLaunchAttributeProgrammatic-
-// StreamSerialization): every kernel lets its successor be scheduled as soon as all of its own
-// CTAs have started (griddepcontrol.launch_dependents) and waits for its predecessor's results
-// (griddepcontrol.wait) before touching memory, so the launch latency of the ~16 kernels of a
-// sort overlaps the tail of the previous kernel instead of adding to it.
+// Kernel launch (cudaLaunchKernelEx).  With -DOVS_PDL=1 it sets programmatic dependent launch
+// (cudaLaunchAttributeProgrammaticStreamSerialization): every kernel starts with PDL_PROLOGUE, so
+// its successor may be scheduled while it drains; off by default (no measured gain).
 template <class... KA, class... AA>
 static void launch(Ctx& c, void (*k)(KA...), dim3 grid, dim3 block, size_t smem, AA&&... args) {
     cudaLaunchConfig_t cfg = {};
@@ -198,7 +196,7 @@ template <int DT, bool KV> struct Engine {
         U* sk = nullptr; u32* st = nullptr; u32* lut = nullptr;
         Seg* seg = nullptr; Chunk* chunks = nullptr; u32* nchunks = nullptr;
         u32* hist = nullptr; u32* tot = nullptr; u32* nseg = nullptr;
-        u16* bid = nullptr;  // keys-only: bucket ids from the histogram pass (OVS_WC_IDS)
+        u16* bid = nullptr;  // keys only: every key's bucket, from the histogram pass (scatter input)
     };
     struct Lists {
         Bucket* fit = nullptr; u32* nfit = nullptr; u32* ticket = nullptr; u32 fit_cap = 0;

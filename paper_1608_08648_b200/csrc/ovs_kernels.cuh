@@ -1131,11 +1131,15 @@ __global__ void __launch_bounds__(NT, 1) k_scatter_wc(Bufs<typename Codec<DT>::U
         const Seg sg = segs[ch.seg];
         const u32 P = sg.P;
         const U* src = B.k[LEVEL0 ? 0 : sg.src];
-        U* dst = B.k[LEVEL0 ? 1 : 1 - sg.src];
+        // positions are counted from an aligned base (the output array may be the caller's, not
+        // 32-byte aligned): position x is dst[x] with dst = the array - al
+        U* const dst0 = B.k[LEVEL0 ? 1 : 1 - sg.src];
+        const u32 al = (u32)(((uintptr_t)dst0 / sizeof(U)) & (SV - 1));
+        U* dst = dst0 - al;
         const u32* hrow = hist + (size_t)c * PS;
         const u32* bst = tot_pool + (size_t)ch.seg * (PS + 1);
         for (u32 b = threadIdx.x; b < P; b += NT) {
-            const u32 r = sg.beg + bst[b] + hrow[b];
+            const u32 r = sg.beg + bst[b] + hrow[b] + al;
             q[b] = r;
             sb[b] = r;  // sector r & ~(SV-1), first valid slot r & (SV-1)
         }

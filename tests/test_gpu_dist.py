@@ -45,6 +45,45 @@ def test_virtual_ranks_kv_and_dtypes(orc, dist_name, G):
     np.testing.assert_array_equal(counts, ref.counts)
 
 
+def _random_dist_cases():
+    rng = np.random.default_rng(4242)
+    out = []
+    for i in range(12):
+        G = int(rng.choice([2, 3, 4, 8]))
+        dist_name = ["u32", "i32_few", "f64_uniform", "u16key", "u32_const"][i % 5]
+        sizes = [int(rng.integers(0, 400_000)) for _ in range(G)]
+        kv = bool(rng.integers(2))
+        p = G * int(rng.choice([1, 4, 16, 64, 256]))
+        s = int(rng.choice([2, 8, 33]))
+        while p > G and p * s - 1 > sum(sizes):
+            p //= 2
+            p = max(G, p // G * G)
+        out.append((i, G, dist_name, sizes, kv, p, s))
+    return out
+
+
+@pytest.mark.parametrize("i,G,dist_name,sizes,kv,p,s", _random_dist_cases())
+def test_virtual_ranks_random(orc, i, G, dist_name, sizes, kv, p, s):
+    """Seeded random world sizes, unequal (also empty) shards, dtypes, key-value or not."""
+    from paper_1608_08648_b200.dist import dist_sort_virtual
+    n = sum(sizes)
+    if p < 2 or p * s - 1 > n:
+        pytest.skip("sample larger than the input")
+    x = ovs_inputs.keys(dist_name, n, seed=30 + i)
+    offs = np.concatenate([[0], np.cumsum(sizes)])
+    xs = [x[offs[r]:offs[r + 1]] for r in range(G)]
+    v = ovs_inputs.index_values(n) if kv else None
+    vs = [v[offs[r]:offs[r + 1]] for r in range(G)] if kv else None
+    out, vout, counts = dist_sort_virtual([torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in xs],
+                                          [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in vs] if kv else None,
+                                          p, s, 9)
+    ref = orc.ros_sort(x, p, s, 9, vals=v)
+    np.testing.assert_array_equal(out.cpu().numpy(), ref.keys)
+    if kv:
+        np.testing.assert_array_equal(vout.cpu().numpy(), ref.vals)
+    np.testing.assert_array_equal(counts, ref.counts)
+
+
 def test_nccl_world1(orc):
     import torch.distributed as dist
     from paper_1608_08648_b200.dist import dist_sort

@@ -765,8 +765,17 @@ template <int DT, bool KV> struct DroSort {
         launch(c, k_dro_gather<U, KV>, cdiv((u64)p * p * 32, 256), 256, 0, B, n, p, bound, cnt, tot);
         c.check();
         c.mark(3);
-        if (big) sort_big(l2, 0x5e9u, B.k[0], KV ? B.v[0] : nullptr, nullptr, true);
-        else e.bucket_sort(l2, 0x5e9u);
+        if (big) {
+            sort_big(l2, 0x5e9u, B.k[0], KV ? B.v[0] : nullptr, nullptr, true);
+        } else if (n / p > e.cap) {
+            // buckets mostly over the on-chip capacity: sorted out of place into the free buffer 1
+            // (so they can be sorted in windows instead of re-split by their CTA), then copied back
+            e.bucket_sort(l2, 0x5e9u, B.k[1], KV ? B.v[1] : nullptr, nullptr, true);
+            OVS_CK(cudaMemcpyAsync(B.k[0], B.k[1], n * sizeof(U), cudaMemcpyDeviceToDevice, c.st));
+            if (KV) OVS_CK(cudaMemcpyAsync(B.v[0], B.v[1], n * sizeof(u32), cudaMemcpyDeviceToDevice, c.st));
+        } else {
+            e.bucket_sort(l2, 0x5e9u);
+        }
         c.mark(4);
     }
 };

@@ -329,21 +329,19 @@ __device__ void block_scan_small(u32* a, u32 cnt, u32* red) {
 }
 
 // ------------------------------------------------------------------ CTA bitonic sort of (key, tag)
-// N a power of two, records in shared memory; ascending by (key, tag).
+// N a power of two, records in shared memory; ascending by (key, tag).  Every thread step is one
+// comparator (x, x + j): t's bits below j stay, the bits above move up one place.
 template <class U>
 __device__ void cta_bitonic_kt(U* tk, u32* tt, u32 N) {
     for (u32 kk = 2; kk <= N; kk <<= 1) {
         for (u32 j = kk >> 1; j > 0; j >>= 1) {
-            for (u32 t = threadIdx.x; t < N; t += blockDim.x) {
-                const u32 o = t ^ j;
-                if (o > t) {
-                    const bool asc = (t & kk) == 0;
-                    const bool gt = tk[t] > tk[o] || (tk[t] == tk[o] && tt[t] > tt[o]);
-                    if (gt == asc) {
-                        U a = tk[t]; tk[t] = tk[o]; tk[o] = a;
-                        u32 b = tt[t]; tt[t] = tt[o]; tt[o] = b;
-                    }
-                }
+            for (u32 t = threadIdx.x; t < N / 2; t += blockDim.x) {
+                const u32 x = ((t & ~(j - 1)) << 1) | (t & (j - 1)), y = x | j;
+                const bool asc = (x & kk) == 0;
+                const U a = tk[x], b = tk[y];
+                const u32 ta = tt[x], tb = tt[y];
+                const bool gt = a > b || (a == b && ta > tb);
+                if (gt == asc) { tk[x] = b; tk[y] = a; tt[x] = tb; tt[y] = ta; }
             }
             __syncthreads();
         }

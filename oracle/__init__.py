@@ -107,8 +107,8 @@ def _run(fn, keys, vals, n, p, s, extra):
     vals = None if vals is None else np.ascontiguousarray(vals, dtype=np.uint32)
     out = np.empty_like(keys)
     outv = None if vals is None else np.empty_like(vals)
-    sk = np.empty(max(p - 1, 0), dtype=keys.dtype)
-    st = np.empty(max(p - 1, 0), dtype=np.uint64)
+    sk = np.zeros(max(p - 1, 0), dtype=keys.dtype)  # n = 0: no splitters drawn, reported as 0
+    st = np.zeros(max(p - 1, 0), dtype=np.uint64)
     cnt = np.zeros(max(p, 1), dtype=np.uint64)
     rc = fn(DTYPES[keys.dtype], _ptr(keys), _ptr(vals), n, p, s, *extra, _ptr(out), _ptr(outv), _ptr(sk), _ptr(st),
             _ptr(cnt))

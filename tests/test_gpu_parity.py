@@ -197,6 +197,22 @@ def test_dro_pairs_stable_edge_matrix(ovs, orc, dist, n, p, r):
     dro_case(ovs, orc, ovs_inputs.keys(dist, n, seed=3), p, r, kv=True)
 
 
+@pytest.mark.parametrize("dist", ["u32", "i32_gauss", "f64_normal"])
+@pytest.mark.parametrize("method", ["ros", "dro"])
+@pytest.mark.parametrize("kv", [False, True])
+def test_empty_input(ovs, orc, dist, method, kv):
+    """n = 0: nothing to sort; the oracle's report is p zero counts (and the call must succeed)."""
+    x = ovs_inputs.keys(dist, 0, seed=1)
+    v = ovs_inputs.index_values(0) if kv else None
+    ref = orc.ros_sort(x, 4, 2, 1, vals=v) if method == "ros" else orc.dro_sort(x, 4, 2, vals=v)
+    xt = torch.from_numpy(x).cuda()
+    srt = ovs.Sorter(0, xt.dtype, kv, method, 4, 2, 1)
+    rep = srt(xt, torch.from_numpy(v).cuda(), report=True) if kv else srt(xt, report=True)
+    torch.cuda.synchronize()
+    assert rep.device_status == 0 and xt.numel() == 0
+    np.testing.assert_array_equal(rep.counts, ref.counts)  # p zero counts; no splitters are drawn
+
+
 @pytest.mark.parametrize("dist,n,p,r,kv", [("u32", 2_000_003, 8, 2, False), ("i32_few", 1_600_000, 4, 3, False),
                                            ("u16key", 600_001, 4, 2, True), ("f64_normal", 900_000, 4, 2, False)])
 def test_dro_level1(ovs, orc, dist, n, p, r, kv):

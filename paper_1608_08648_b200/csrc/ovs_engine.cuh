@@ -51,6 +51,10 @@ inline DevInfo dev_info_impl() {
     return d;
 }
 
+#ifndef OVS_INT_SAMPLES
+#define OVS_INT_SAMPLES 4096
+#endif
+
 // ------------------------------------------------------------------ workspace carving
 // The same code path sizes the workspace (dry run) and hands out pointers (real run).
 struct Ctx {
@@ -263,8 +267,9 @@ template <int DT, bool KV> struct Engine {
     // internal splitters for level 0 (P-1 of them) from a one-CTA sorted random sample
     void internal_splitters(Level0& z, u64 seed) {
         if (c.dry || z.P <= 1) return;
-        // 32 samples per internal splitter, sorted by one CTA (a power-of-two bitonic network)
-        const u32 si = std::max<u32>(1, std::min<u32>(32, 8192 / z.P));
+        // up to 32 samples per internal splitter, at most OVS_INT_SAMPLES in all, sorted by one CTA
+        // (a power-of-two bitonic network)
+        const u32 si = std::max<u32>(1, std::min<u32>(32, OVS_INT_SAMPLES / z.P));
         const u32 N = pow2_at_least(z.P * si);
         const size_t sm = (sizeof(U) + 4) * (size_t)N;
         smem_limit(k_internal_sample<DT, KV>, sm, c.di);

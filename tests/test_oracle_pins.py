@@ -310,3 +310,14 @@ def test_dro_worked_positions(orc):
     e = orc.dro_sample_positions(d["n"], d["p"], d["r"], 0, padded=True)
     s = d["p"] * d["r"]
     assert e.tolist() == [min((j + 1) * d["x"], 1000) - 1 for j in range(s - 1)] + [999]
+
+
+def test_empty_input_reading_q26(orc):
+    """DESIGN.md Q26: n = 0 sorts nothing; all p counts are 0 and the (undrawn) splitters are reported as 0."""
+    for dt in (np.uint32, np.int32, np.float64):
+        x = np.empty(0, dt)
+        for res in (orc.ros_sort(x, 4, 2, 1), orc.dro_sort(x, 4, 2),
+                    orc.ros_sort(x, 4, 2, 1, vals=np.empty(0, np.uint32))):
+            assert len(res.keys) == 0
+            assert res.counts.tolist() == [0, 0, 0, 0]
+            assert not np.any(res.split_keys) and not np.any(res.split_tags)

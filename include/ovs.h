@@ -23,7 +23,8 @@
  *     enqueued on it and the call returns after enqueue (it is CUDA-graph capturable) unless
  *     `rep` is non-NULL, in which case it synchronises `stream` and fills the report.
  *   - Parameters are validated before any launch: a failing call does no work.
- *   - Preconditions: f64 inputs contain no NaN and no -0.0 (BASELINE.json north_star); n < 2^32.
+ *   - Preconditions: f64 inputs contain no NaN and no -0.0 (BASELINE.json north_star);
+ *     n < 2^32 - 33 (positions are 32-bit, counted from a 32-byte-aligned base).
  *   - Determinism: the same input bytes and parameters give bit-identical output, splitters
  *     and bucket counts (the oracle's, see oracle/ovs_oracle.cpp).
  */
@@ -39,14 +40,15 @@ extern "C" {
 
 typedef enum {
     OVS_OK = 0,
-    OVS_EINVAL = 1,      /* p == 0, NULL pointer with n > 0, n >= 2^32, bad method/flags     */
+    OVS_EINVAL = 1,      /* p == 0, NULL pointer with n > 0, n >= 2^32-33, bad method/flags  */
     OVS_EDTYPE = 2,      /* unsupported dtype                                                   */
     OVS_ESAMPLE = 3,     /* ROS: s == 0 or p*s-1 > n ("ps-1 <= n");
                             DRO: r == 0 or r*p > floor(n/p) (distinct positions) */
     OVS_EWORKSPACE = 4,  /* ws_bytes < ovs_workspace_bytes(...)                                  */
     OVS_ECUDA = 5,       /* a CUDA runtime error; see ovs_last_error()                           */
     OVS_ECAPACITY = 7,   /* distributed: output larger than out_capacity                         */
-    OVS_EINTERNAL = 8    /* a device-side check failed (reported only when rep != NULL)          */
+    OVS_EINTERNAL = 8    /* a device-side check failed: returned by a call with rep != NULL, and
+                            by ovs_device_status() for calls without a report (graph replays)          */
 } ovs_status;
 
 typedef enum { OVS_U32 = 0, OVS_I32 = 1, OVS_F64 = 2 } ovs_dtype;
@@ -70,8 +72,13 @@ typedef struct {          /* optional, caller-owned HOST memory; each array poin
     uint64_t* splitter_tags;  /* p-1 tags: ROS original index; DRO position in the sorted X_k
                                  array (start_k + t)  (reading Q6)           */
     uint64_t* bucket_counts;  /* p bucket sizes |Y_j|                                           */
-    float phase_ms[8];        /* sample, sample_sort, classify_hist, scatter, bucket_sort,
-                                 resplit, exchange, total  (CUDA events on `stream`)            */
+    float phase_ms[8];        /* CUDA events on `stream` between the phase boundaries of
+                                 ovs_set_phase_events: [0] sample (a1-a2; DRO: a9 sequence
+                                 sorts), [1] sample sort + splitters (a3-a4; DRO a10-a12),
+                                 [2] classify + histogram + scans (a5-a6; DRO a13), [3] scatter
+                                 (a7; DRO a14 gather), [4] bucket sort (a8; DRO a14 sorts),
+                                 [5] 0 (re-splits run inside the bucket sorter), [6] exchange
+                                 (distributed calls; 0 here), [7] total                          */
     uint32_t max_bucket;      /* max_j |Y_j|                                                    */
     uint32_t kernel_launches; /* kernels this call enqueued                                     */
     uint32_t device_status;   /* 0, or a device-side failure bit set                            */
@@ -142,10 +149,23 @@ int ovs_auto_params(size_t n, int dtype, int with_values, int method, ovs_params
 
 /* Profiling hook (thread-local): subsequent sort calls on this thread record events[k]
  * (cudaEvent_t passed as void*) on their stream at phase boundary k, without synchronising:
- *   0 start, 1 after the sample + splitters (a1-a4), 2 after classify + histogram + scans
- *   (a5-a6), 3 after the scatter (a7), 4 after the bucket sort (a8) = end.
+ *   0 start, 1 after the sample draw + gather (a1-a2), 2 after the sample sort + splitters
+ *   (a3-a4), 3 after classify + histogram + scans (a5-a6), 4 after the scatter (a7), 5 after
+ *   the bucket sort (a8) = end.  DRO: 1 after the sequence sorts (a9), 2 after a10-a12, 3 after
+ *   the split (a13), 4 after the bucket gather, 5 end.
  * count = 0 disables.  NULL entries are skipped.  The caller owns the events. */
 void ovs_set_phase_events(void* const* events, int count);
+
+/* Device-side status without a report.  The first 8 bytes of a workspace hold two status words:
+ * word 0 = the failure bits of the last call (zeroed when a call starts), word 1 = the sticky OR
+ * of every call's bits since the last reset (so a CUDA-graph replay loop can be checked once).
+ * Bits: 1 fewer than ps-1 distinct sample draws; 2 a bucket over the on-chip capacity reached the
+ * sorter; 4 a work list overflowed (output possibly not sorted).  ovs_device_status synchronises
+ * `stream`, writes the sticky word to *status (may be NULL) and, if reset != 0, clears it
+ * (enqueued on `stream`).  Returns OVS_OK when the sticky word is 0, else OVS_EINTERNAL (message
+ * in ovs_last_error()), OVS_ECUDA on a CUDA error.  A fresh workspace's sticky word is whatever
+ * the memory held: zero the first 8 bytes, or call ovs_device_status(..., reset=1) once, before use. */
+int ovs_device_status(const void* d_ws, void* stream, uint32_t* status, int reset);
 
 /* Thread-local message of the last failure on this thread ("" if none). */
 const char* ovs_last_error(void);

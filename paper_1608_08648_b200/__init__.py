@@ -65,6 +65,8 @@ def lib() -> ctypes.CDLL:
         L.ovs_set_phase_events.argtypes = [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int]
         L.ovs_auto_params.restype = i32
         L.ovs_auto_params.argtypes = [sz, i32, i32, i32, ctypes.POINTER(Params)]
+        L.ovs_device_status.restype = i32
+        L.ovs_device_status.argtypes = [vp, vp, ctypes.POINTER(ctypes.c_uint32), i32]
         L.ovs_last_error.restype = ctypes.c_char_p
         L.ovs_version.restype = ctypes.c_char_p
         _lib = L
@@ -75,13 +77,13 @@ def version() -> str:
     return lib().ovs_version().decode()
 
 
-PHASES = ("sample", "classify_hist", "scatter", "bucket_sort")
+PHASES = ("sample", "sample_sort", "classify_hist", "scatter", "bucket_sort")
 
 
 def set_phase_events(events) -> None:
     """Record torch.cuda.Event objects (enable_timing=True) at the phase boundaries of every
-    following sort call on this thread: 0 start, 1 sample done, 2 histogram done, 3 scatter
-    done, 4 bucket sort done.  Pass None / [] to disable."""
+    following sort call on this thread: 0 start, 1 sample drawn, 2 splitters, 3 histogram done,
+    4 scatter done, 5 bucket sort done (6 events, PHASES between them).  None / [] disables."""
     events = list(events or [])
     for e in events:
         if e.cuda_event == 0:  # torch creates the event lazily
@@ -141,6 +143,7 @@ class Sorter:
         if n > 0 and nb == 0:
             self._raise(OVS_EINVAL)
         self.ws = torch.empty(max(nb, 1), dtype=torch.uint8, device=device or "cuda")
+        self.ws[:16].zero_()  # the status words (include/ovs.h ovs_device_status): sticky bits start clear
         self.ws_bytes = nb
 
     def _raise(self, rc):
@@ -149,7 +152,27 @@ class Sorter:
     def __call__(self, keys, vals=None, stream=None, report: bool = False):
         import torch
         assert keys.is_cuda and keys.is_contiguous() and keys.numel() == self.n
-        st = ctypes.c_void_p(stream.cuda_stream if stream is not None else torch.cuda.current_stream().cuda_stream)
+        assert keys.device == self.ws.device, "keys and the workspace must be on the same device"
+        with torch.cuda.device(keys.device):
+            return self._call(keys, vals, stream, report)
+
+    def status(self, stream=None, reset: bool = True) -> int:
+        """ovs_device_status: synchronise the stream and return the sticky device-status bits of every
+        sort run on this workspace since the last reset (0 = no device-side check failed)."""
+        import torch
+        with torch.cuda.device(self.ws.device):
+            st = ctypes.c_void_p(stream.cuda_stream if stream is not None
+                                 else torch.cuda.current_stream(self.ws.device).cuda_stream)
+            out = ctypes.c_uint32(0)
+            rc = lib().ovs_device_status(self.ws.data_ptr(), st, ctypes.byref(out), 1 if reset else 0)
+            if rc not in (OVS_OK, OVS_EINTERNAL):
+                self._raise(rc)
+            return int(out.value)
+
+    def _call(self, keys, vals, stream, report):
+        import torch
+        st = ctypes.c_void_p(stream.cuda_stream if stream is not None
+                             else torch.cuda.current_stream(keys.device).cuda_stream)
         rep = None
         p = self.prm.p
         kbuf = tbuf = cbuf = None

@@ -48,23 +48,28 @@ static int sort_impl(void* d_keys, uint32_t* d_vals, bool kv, size_t n, int dtyp
         c.dry = false;
         c.ws = (char*)d_ws;
         c.status = c.take<u32>(4);
-        cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+        // the report's phase events: boundaries 0..5 of Ctx::mark (include/ovs.h)
+        struct Evs {
+            cudaEvent_t e[OVS_NMARKS] = {};
+            ~Evs() { for (auto x : e) if (x) cudaEventDestroy(x); }
+        } ev;
         if (rep) {
-            OVS_CK(cudaEventCreate(&ev0));
-            OVS_CK(cudaEventCreate(&ev1));
-            OVS_CK(cudaEventRecord(ev0, c.st));
+            for (auto& x : ev.e) OVS_CK(cudaEventCreate(&x));
+            c.rep_marks = ev.e;
         }
-        OVS_CK(cudaMemsetAsync(c.status, 0, 16, c.st));
+        OVS_CK(cudaMemsetAsync(c.status, 0, 4, c.st));  // this call's bits (status[1] is sticky)
         Out o = plan_dispatch(c, d_keys, kv ? d_vals : nullptr, n, dtype, prm);
         if (rep) {
-            OVS_CK(cudaEventRecord(ev1, c.st));
             OVS_CK(cudaStreamSynchronize(c.st));
-            float ms = 0;
-            cudaEventElapsedTime(&ms, ev0, ev1);
             std::memset(rep->phase_ms, 0, sizeof(rep->phase_ms));
-            rep->phase_ms[7] = ms;
-            cudaEventDestroy(ev0);
-            cudaEventDestroy(ev1);
+            for (u32 k = 0; k + 1 < OVS_NMARKS; ++k) {
+                float ms = 0;
+                OVS_CK(cudaEventElapsedTime(&ms, ev.e[k], ev.e[k + 1]));
+                rep->phase_ms[k] = ms;  // sample, sample_sort, classify_hist, scatter, bucket_sort
+            }
+            float tot = 0;
+            OVS_CK(cudaEventElapsedTime(&tot, ev.e[0], ev.e[OVS_NMARKS - 1]));
+            rep->phase_ms[7] = tot;
             u32 stv = 0;
             OVS_CK(cudaMemcpy(&stv, c.status, 4, cudaMemcpyDeviceToHost));
             rep->device_status = stv;
@@ -111,6 +116,9 @@ static int sort_impl(void* d_keys, uint32_t* d_vals, bool kv, size_t n, int dtyp
         return e.code;
     } catch (const std::exception& e) {
         g_err = e.what();
+        return OVS_ECUDA;
+    } catch (...) {
+        g_err = "unknown exception";
         return OVS_ECUDA;
     }
 }
@@ -165,7 +173,6 @@ static int dist_validate(uint64_t n_local, uint64_t n_global, int dtype, const o
     if (prm->p < 2 || prm->p % (uint32_t)world != 0) return OVS_EINVAL;  // "p ... a multiple of m"
     if (n_global >= 0xffffffffull || n_local > n_global) return OVS_EINVAL;
     if (prm->s == 0 || (uint64_t)prm->p * prm->s - 1 > n_global) return OVS_ESAMPLE;
-    if (ros_draws(n_global, (uint64_t)prm->p * prm->s - 1) == 0) return OVS_ESAMPLE;
     return OVS_OK;
 }
 
@@ -201,6 +208,12 @@ static int dist_call(int step, int dtype, bool kv, const ovs_params* prm, DistAr
     } catch (const StatusFail& e) {
         g_err = e.msg;
         return e.code;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return OVS_ECUDA;
+    } catch (...) {
+        g_err = "unknown exception";
+        return OVS_ECUDA;
     }
 }
 
@@ -257,6 +270,27 @@ int ovs_dist_finish(const void* d_recv_keys, const uint32_t* d_recv_vals, const 
     a.C = d_all_counts; a.out_k = d_out_keys; a.out_v = d_out_vals;
     if (rank < 0 || rank >= world) return OVS_EINVAL;
     return dist_call(2, dtype, d_recv_vals != nullptr, prm, a, d_ws, ws_bytes, stream);
+}
+
+int ovs_device_status(const void* d_ws, void* stream, uint32_t* status, int reset) {
+    g_err.clear();
+    if (!d_ws) { g_err = "NULL workspace"; return OVS_EINVAL; }
+    try {
+        u32 w[2] = {0, 0};
+        const cudaStream_t st = (cudaStream_t)stream;
+        OVS_CK(cudaMemcpyAsync(w, d_ws, 8, cudaMemcpyDeviceToHost, st));
+        OVS_CK(cudaStreamSynchronize(st));
+        if (reset) OVS_CK(cudaMemsetAsync((char*)d_ws + 4, 0, 4, st));
+        if (status) *status = w[1];
+        if (w[1] != 0) {
+            g_err = "device-side check failed (sticky status bits " + std::to_string(w[1]) + ")";
+            return OVS_EINTERNAL;
+        }
+        return OVS_OK;
+    } catch (const CudaFail& e) {
+        g_err = e.what();
+        return OVS_ECUDA;
+    }
 }
 
 const char* ovs_last_error(void) { return g_err.c_str(); }

@@ -51,6 +51,8 @@ inline DevInfo dev_info_impl() {
     return d;
 }
 
+constexpr u32 OVS_NMARKS = 6;
+
 #ifndef OVS_INT_SAMPLES
 #define OVS_INT_SAMPLES 4096
 #endif
@@ -66,8 +68,13 @@ struct Ctx {
     DevInfo di;
     u32* status = nullptr;
     const std::vector<cudaEvent_t>* marks = nullptr;  // ovs_set_phase_events
+    cudaEvent_t* rep_marks = nullptr;                  // the report's phase events (OVS_NMARKS)
+    // phase boundary k (include/ovs.h, ovs_set_phase_events): 0 start, 1 sample drawn, 2 splitters,
+    // 3 classify + histogram + scans, 4 scatter, 5 bucket sort (end)
     void mark(u32 k) {
-        if (!dry && marks && k < marks->size() && (*marks)[k]) OVS_CK(cudaEventRecord((*marks)[k], st));
+        if (dry) return;
+        if (marks && k < marks->size() && (*marks)[k]) OVS_CK(cudaEventRecord((*marks)[k], st));
+        if (rep_marks && k < OVS_NMARKS) OVS_CK(cudaEventRecord(rep_marks[k], st));
     }
     template <class T> T* take(size_t count) {
         off = (off + 255) & ~(size_t)255;
@@ -84,21 +91,32 @@ struct Ctx {
 
 static inline u32 cdiv(u64 a, u64 b) { return (u32)((a + b - 1) / b); }
 
-// Dynamic shared memory limit of a kernel, raised once per process to the most the kernel can
-// use (the device's opt-in limit minus its static shared memory), so no launch pays for
-// cudaFuncSetAttribute again; `need` is checked against it.
+// Dynamic shared memory limit of a kernel, raised once per (device, kernel) to the most the
+// kernel can use (the device's opt-in limit minus its static shared memory), so no launch pays
+// for cudaFuncSetAttribute again; `need` is checked against it.  The attribute is per device, so
+// the cache is keyed by the current device too.
+struct SmemKey {
+    int dev;
+    const void* k;
+    bool operator==(const SmemKey& o) const { return dev == o.dev && k == o.k; }
+};
+struct SmemKeyHash {
+    size_t operator()(const SmemKey& x) const { return std::hash<const void*>()(x.k) ^ ((size_t)x.dev * 0x9e3779b97f4a7c15ull); }
+};
 template <class... KA>
 static void smem_limit(void (*k)(KA...), size_t need, const DevInfo& di) {
     static std::mutex mu;
-    static std::unordered_map<const void*, size_t> lim;
+    static std::unordered_map<SmemKey, size_t, SmemKeyHash> lim;
+    int dev = 0;
+    OVS_CK(cudaGetDevice(&dev));
     std::lock_guard<std::mutex> g(mu);
-    auto it = lim.find((const void*)k);
+    auto it = lim.find(SmemKey{dev, (const void*)k});
     if (it == lim.end()) {
         cudaFuncAttributes fa;
         OVS_CK(cudaFuncGetAttributes(&fa, (const void*)k));
         const size_t mx = (size_t)di.smem_optin - fa.sharedSizeBytes;
         OVS_CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx));
-        it = lim.emplace((const void*)k, mx).first;
+        it = lim.emplace(SmemKey{dev, (const void*)k}, mx).first;
     }
     if (need > it->second) throw CudaFail("kernel shared memory " + std::to_string(need) + " > limit " + std::to_string(it->second));
 }
@@ -168,14 +186,13 @@ static void fill_u32(Ctx& c, u32* p, u32 v, u32 n) {
 // Number of candidate draws for the ROS sample (reading Q1: the first ps-1 distinct values of
 // the counter stream): the expected number of draws to collect m distinct indices out of n
 // (coupon collector, E = n(H_n - H_{n-m})) plus 10 standard deviations and 64; a shortfall
-// (never observed) is caught on the device (ST_SAMPLE_SHORT).  0 = too many draws.
-inline u32 ros_draws(u64 n, u64 m) {
+// (probability below 1e-20, never observed) is caught on the device (ST_SAMPLE_SHORT).
+inline u64 ros_draws(u64 n, u64 m) {
     const double N = (double)n, a = (double)(n - m) + 0.5, b = N + 0.5;
     const double E = N * std::log(b / a);
     const double var = std::max(0.0, N * N * (1.0 / a - 1.0 / b) - E);
     const double M = std::ceil(E + 10.0 * std::sqrt(var) + 64.0);
-    if (M > (double)(1u << 26)) return 0;
-    return (u32)std::max<double>(M, (double)m);
+    return (u64)std::max<double>(M, (double)m);  // < 2^37 for n < 2^32: inside the 2^40 stream
 }
 
 // ------------------------------------------------------------------ the sort engine
@@ -298,7 +315,7 @@ template <int DT, bool KV> struct Engine {
         launch(c, k_segscan<U>, 1, 1024, 0, z.seg, z.nseg, z.P, z.tot, z.sk, 0, cap, l.fit, l.nfit, l.fit_cap, nullptr,
                                           nullptr, 0, counts_out, c.status);
         c.check();
-        if (mark_phases) c.mark(2);
+        if (mark_phases) c.mark(3);
         if (use_wc(z.P)) {
             constexpr int IT = WC_ITEMS * 4 / (int)sizeof(U);  // u32: WC_ITEMS keys per thread
             const size_t sm_w = wc_smem_bytes<U>(z.P);
@@ -315,7 +332,7 @@ template <int DT, bool KV> struct Engine {
                                                 z.tot, tag_base);
             c.check();
         }
-        if (mark_phases) c.mark(3);
+        if (mark_phases) c.mark(4);
     }
 
 
@@ -504,30 +521,68 @@ template <int DT, bool DIST> struct RosSampler {
     typedef typename Codec<DT>::U U;
     static constexpr bool TAG = sizeof(U) == 8;
     Ctx& c;
-    u64 n;
-    u32 m, M, lg, nb;
+    u64 n, Mfull;
+    u32 m, M = 0, lg = 0, nb = 0;
     u64* zero = nullptr; u32* bits = nullptr; u32* bcnt = nullptr;
     u64* tk = nullptr; u32* tt = nullptr;
     Selector<TAG>* sel = nullptr;
+    // direct-address form (k_ros_draw_direct ...): when the draws outnumber the indices or the
+    // hash set would be too large (samples that are a large fraction of n, up to ps-1 = n)
+    bool direct = false;
+    u64* minj = nullptr; RSel* rsel = nullptr; u32* ghist = nullptr; u32* dbcnt = nullptr;
+    u32 dnb = 0, Lr = 0;
     RosSampler(Ctx& ctx, u64 n_, u32 p, u32 s) : c(ctx), n(n_) {
         m = p * s - 1;
-        M = ros_draws(n, m);
-        lg = ilog2(pow2_at_least(std::max<u32>(1024, M + M / 2)));
-        nb = cdiv(M, TK_NT);
-        zero = c.take<u64>(((size_t)1 << lg) + SEL_GMAX);
-        bits = c.take<u32>((size_t)nb * (TK_NT / 32));
-        bcnt = c.take<u32>(nb);
+        Mfull = ros_draws(n, m);
+        direct = Mfull > (1ull << 26) || Mfull > n;
+        u32* gcnt = nullptr;
+        if (!direct) {
+            M = (u32)Mfull;
+            lg = ilog2(pow2_at_least(std::max<u32>(1024, M + M / 2)));
+            nb = cdiv(M, TK_NT);
+            zero = c.take<u64>(((size_t)1 << lg) + SEL_GMAX);
+            bits = c.take<u32>((size_t)nb * (TK_NT / 32));
+            bcnt = c.take<u32>(nb);
+            gcnt = zero ? (u32*)(zero + ((size_t)1 << lg)) : nullptr;
+        } else {
+            zero = c.take<u64>(SEL_GMAX);
+            gcnt = zero ? (u32*)zero : nullptr;
+            minj = c.take<u64>(n);
+            rsel = c.take<RSel>(1);
+            ghist = c.take<u32>(RS_BINS);
+            dnb = (u32)((n + DT_NT * DT_PER - 1) / (DT_NT * DT_PER));
+            dbcnt = c.take<u32>(dnb + 1);
+            u32 L = 1;
+            while (L < 64 && (Mfull - 1) >> L) ++L;  // bits of the largest draw number
+            Lr = (L + RS_BITS - 1) / RS_BITS * RS_BITS;
+        }
         tk = c.take<u64>(m);
         tt = TAG ? c.take<u32>(m) : nullptr;
-        u32* gcnt = zero ? (u32*)(zero + ((size_t)1 << lg)) : nullptr;
         sel = new Selector<TAG>(c, m, tk, tt, gcnt, gcnt ? gcnt + SEL_GMAX : nullptr);
+        if (direct) sel->stride = 0;  // T in index order: coarse splitters from random positions
     }
     ~RosSampler() { delete sel; }
-    size_t zero_bytes() const { return 8 * (((size_t)1 << lg) + SEL_GMAX); }
-    // the hash set of the draws and the first-draw masks
+    size_t zero_bytes() const { return 8 * ((direct ? 0 : ((size_t)1 << lg)) + SEL_GMAX); }
+    // the hash set of the draws and the first-draw masks (direct: the table and j*)
     void draw(u64 seed) {
         if (c.dry) return;
         OVS_CK(cudaMemsetAsync(zero, 0, zero_bytes(), c.st));
+        if (direct) {
+            OVS_CK(cudaMemsetAsync(minj, 0xff, 8 * (size_t)n, c.st));
+            const u64 g = std::min<u64>((Mfull + 255) / 256, (u64)c.di.sms * 16);
+            launch(c, k_ros_draw_direct, (u32)g, 256, 0, minj, Mfull, n, seed);
+            c.check();
+            launch(c, k_rsel_init, 1, 1024, 0, rsel, (u64)(m - 1), ghist);
+            c.check();
+            const u32 hg = std::min<u32>(cdiv(n, 1024 * 8), (u32)c.di.sms * 2);
+            for (int sh = (int)Lr - (int)RS_BITS; sh >= 0; sh -= (int)RS_BITS) {
+                launch(c, k_rsel_hist, std::max<u32>(hg, 1), 1024, 0, (const u64*)minj, n, (const RSel*)rsel, (u32)sh, ghist);
+                c.check();
+                launch(c, k_rsel_pick, 1, 1024, 0, rsel, (u32)sh, ghist, c.status, sh == 0 ? 1u : 0u);
+                c.check();
+            }
+            return;
+        }
         launch(c, k_ros_draw, cdiv(M, 256), 256, 0, zero, lg, M, n, seed);
         c.check();
         launch(c, k_ros_first, nb, TK_NT, 0, zero, lg, M, n, seed, bits, bcnt);
@@ -536,6 +591,16 @@ template <int DT, bool DIST> struct RosSampler {
     // records of the members of I (DIST: of the shard [offset, offset + nl), into rec)
     void take(u64 seed, const U* x, u64 offset, u32 nl, u64* rec) {
         if (c.dry) return;
+        if (direct) {
+            launch(c, k_direct_count, dnb, DT_NT, 0, (const u64*)minj, n, (const RSel*)rsel, dbcnt);
+            c.check();
+            launch(c, k_direct_scan, 1, 1024, 0, dbcnt, dnb, m, c.status);
+            c.check();
+            launch(c, k_direct_take<DT, DIST>, dnb, DT_NT, 0, (const u64*)minj, n, (const RSel*)rsel,
+                   (const u32*)dbcnt, x, offset, nl, DIST ? rec : tk, tt);
+            c.check();
+            return;
+        }
         launch(c, k_ros_take<DT, DIST>, nb, TK_NT, 0, bits, bcnt, M, n, seed, m, x, offset, nl, DIST ? rec : tk, tt,
                                                       c.status);
         c.check();
@@ -606,13 +671,15 @@ template <int DT, bool KV> struct RosSort {
             // a1+a2: ps-1 distinct random indices and their records T = [(x[i], i)]
             smp->draw(seed);
             smp->take(seed, e.B.k[0], 0, n, nullptr);
+            c.mark(1);
             // a3+a4: sort T by (key, i); S[q] = T[(q+1)s - 1] (refined: every (s/f)-th)
             smp->select(p * f, s, f, seed ^ 0x5eed, z.sk, z.st);
             if (f > 1) smp->sel->template pick<U>(p, s, 1, rep_sk, rep_st);
         } else {
             e.internal_splitters(z, seed);
+            c.mark(1);
         }
-        c.mark(1);
+        c.mark(2);
         // a5-a7: classify, histogram, scan, scatter;  a8: bucket sort
         e.level0(z, l, p > 1 ? (f > 1 ? int_counts : counts) : nullptr);
         if (f > 1) {
@@ -620,7 +687,7 @@ template <int DT, bool KV> struct RosSort {
             c.check();
         }
         e.bucket_sort(l, seed);
-        c.mark(4);
+        c.mark(5);
     }
 };
 
@@ -629,14 +696,15 @@ inline int validate_impl(size_t n, int dtype, const ovs_params* prm) {
     if (!prm) return OVS_EINVAL;
     if (dtype != OVS_U32 && dtype != OVS_I32 && dtype != OVS_F64) return OVS_EDTYPE;
     if (prm->p == 0) return OVS_EINVAL;
-    if (n >= 0xffffffffull) return OVS_EINVAL;
+    // positions are u32 counted from a 32-byte-aligned base (the write-combining scatter adds up
+    // to 7 slots): n + 32 must stay below 2^32
+    if (n >= 0xffffffffull - 32) return OVS_EINVAL;
     if (prm->method != OVS_ROS && prm->method != OVS_DRO) return OVS_EINVAL;
     if (prm->flags & ~OVS_DRO_PADDED_POSITIONS) return OVS_EINVAL;
     if (n == 0 || prm->p == 1) return OVS_OK;
     if (prm->method == OVS_ROS) {
         if (prm->s == 0) return OVS_ESAMPLE;
         if ((uint64_t)prm->p * prm->s - 1 > n) return OVS_ESAMPLE;
-        if (ros_draws(n, (uint64_t)prm->p * prm->s - 1) == 0) return OVS_ESAMPLE;
     } else {
         if (prm->s == 0) return OVS_ESAMPLE;
         if ((uint64_t)prm->s * prm->p > n / prm->p) return OVS_ESAMPLE;
@@ -743,6 +811,7 @@ template <int DT, bool KV> struct DroSort {
         } else {
             e.bucket_sort(l1, 0x5e9u, B.k[1], KV ? B.v[1] : nullptr, KV ? B.i[1] : nullptr, false);
         }
+        c.mark(1);
         // a10-a12: regular sample, sample sort, splitters
         launch(c, k_dro_sample<U>, cdiv((u64)ns, 256), 256, 0, B.k[1], n, p, s, flags & OVS_DRO_PADDED_POSITIONS,
                                                              t_pack, t_key, t_tag);
@@ -751,7 +820,7 @@ template <int DT, bool KV> struct DroSort {
         else ts64->run(0xd0d0);
         launch(c, k_pick_splitters<U>, cdiv(p, 256), 256, 0, t_pack, t_key, t_tag, p, s, 1u, sk, st);
         c.check();
-        c.mark(1);
+        c.mark(2);
         // a13: split every sorted sequence by binary search; bucket starts and run offsets
         launch(c, k_dro_bounds<U>, cdiv((u64)p * (p + 1), 256), 256, 0, B.k[1], n, p, sk, st, bound);
         c.check();
@@ -765,11 +834,11 @@ template <int DT, bool KV> struct DroSort {
         launch(c, k_segscan<U>, 1, 1024, 0, seg, nseg, p, tot, sk, 0, e.cap, l2.fit, l2.nfit, l2.fit_cap, nullptr,
                                           nullptr, 0, counts, c.status);
         c.check();
-        c.mark(2);
+        c.mark(3);
         // a14: gather the runs X_{k,j} of every bucket (k order) into buffer 0, sort each bucket
         launch(c, k_dro_gather<U, KV>, cdiv((u64)p * p * 32, 256), 256, 0, B, n, p, bound, cnt, tot);
         c.check();
-        c.mark(3);
+        c.mark(4);
         if (big) {
             sort_big(l2, 0x5e9u, B.k[0], KV ? B.v[0] : nullptr, nullptr, true);
         } else if (n / p > e.cap) {
@@ -781,7 +850,7 @@ template <int DT, bool KV> struct DroSort {
         } else {
             e.bucket_sort(l2, 0x5e9u);
         }
-        c.mark(4);
+        c.mark(5);
     }
 };
 
@@ -814,7 +883,7 @@ template <int DT, bool KV> struct DistSort {
         f.cap = e.cap;
         f.ixbits = bits_for(ng);
         m = p * s - 1;
-        M = ros_draws(ng, m);
+        M = (u32)std::min<u64>(ros_draws(ng, m), 0xffffffffull);
         words = sizeof(U) == 4 ? 1 : 2;
         counts64 = c.take<u64>(p);
         smp = new RosSampler<DT, true>(c, ng, p, s);

@@ -71,6 +71,12 @@ enum : u32 {
     ST_BUCKET_OVER = 2u,    // a bucket larger than the on-chip capacity reached the sorter
     ST_LIST_OVER = 4u,      // a work list overflowed its capacity
 };
+// status[0]: bits of the current call (zeroed when the call starts); status[1]: sticky bits of
+// every call since the caller last reset them (ovs_device_status), so graph replays are checkable
+__device__ __forceinline__ void st_set(u32* status, u32 bit) {
+    atomicOr(status, bit);
+    atomicOr(status + 1, bit);
+}
 
 // ------------------------------------------------------------------ counter-based RNG
 // H(seed, stream, j) = SplitMix64 output number stream*2^40 + j (reading Q1).
@@ -356,7 +362,7 @@ __device__ void cta_bitonic_kt(U* tk, u32* tt, u32 N) {
 // I; the records T[rank] = (x[c], c) are written in draw order, a uniformly random order that
 // the coarse level of the sample sort relies on (T's order is not part of any result).
 __device__ __forceinline__ u32 ht_slot(u64 c, u32 lg) { return (u32)((c * 0x9e3779b97f4a7c15ull) >> (64 - lg)); }
-__device__ __forceinline__ u64 ros_draw_c(u64 seed, u32 j, u64 n) { return __umul64hi(rng_H(seed, 1, j), n); }
+__device__ __forceinline__ u64 ros_draw_c(u64 seed, u64 j, u64 n) { return __umul64hi(rng_H(seed, 1, j), n); }
 
 __global__ void k_ros_draw(u64* tab, u32 lg, u32 M, u64 n, u64 seed) {
     PDL_PROLOGUE();
@@ -437,7 +443,7 @@ __global__ void __launch_bounds__(TK_NT) k_ros_take(const u32* bits, const u32* 
             if (lane >= o) x2 += y;
         }
         wpre[lane] = b + x2 - w;  // exclusive prefix of warp `lane` in the whole draw order
-        if (blockIdx.x + 1 == gridDim.x && lane == 31 && b + x2 < m) atomicOr(status, ST_SAMPLE_SHORT);
+        if (blockIdx.x + 1 == gridDim.x && lane == 31 && b + x2 < m) st_set(status, ST_SAMPLE_SHORT);
     }
     __syncthreads();
     if (!((mask >> lane) & 1u)) return;
@@ -455,6 +461,157 @@ __global__ void __launch_bounds__(TK_NT) k_ros_take(const u32* bits, const u32* 
         tk[rank] = (u64)k;
         tt[rank] = (u32)c;
     }
+}
+
+// ------------------------------------------------------------------ a1+a2: direct-address form
+// For samples that are a large fraction of n (ps-1 up to n; the draws then number up to
+// n(ln n + 1)), the set of draws is a direct-address table over the n indices: minj[c] = the
+// smallest draw number j with c_j = c (atomicMin; empty = ~0).  I = the m indices with the m
+// smallest minj, i.e. {c : minj[c] <= j*} where j* is the m-th smallest minj (radix select over
+// the table); the records are written in index order (the sample sort then draws its coarse
+// splitters at random positions, Selector::stride = 0).  Same set as the hash-set form.
+__global__ void k_ros_draw_direct(u64* minj, u64 M, u64 n, u64 seed) {
+    PDL_PROLOGUE();
+    const u64 stride = (u64)gridDim.x * blockDim.x;
+    for (u64 j = (u64)blockIdx.x * blockDim.x + threadIdx.x; j < M; j += stride)
+        atomicMin((unsigned long long*)(minj + ros_draw_c(seed, j, n)), (unsigned long long)j);
+}
+
+// radix select of j*: sel = {prefix, rank remaining, shift}; pass k histograms digit
+// (minj >> sh) & (RS_BINS-1) of the entries whose bits above sh+RS_BITS equal the prefix
+constexpr u32 RS_BITS = 13, RS_BINS = 1u << RS_BITS;
+struct RSel { u64 prefix; u64 rank; u32 hibits; u32 found; };  // hibits: bits fixed so far (from the top)
+__global__ void __launch_bounds__(1024) k_rsel_hist(const u64* minj, u64 n, const RSel* sel, u32 sh, u32* ghist) {
+    PDL_PROLOGUE();
+    __shared__ u32 h[RS_BINS];
+    for (u32 i = threadIdx.x; i < RS_BINS; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    const RSel sv = *sel;
+    const u32 top = sh + RS_BITS;  // entries must match the prefix in bits [top, 64)
+    for (u64 c = (u64)blockIdx.x * blockDim.x + threadIdx.x; c < n; c += (u64)gridDim.x * blockDim.x) {
+        const u64 v = minj[c];
+        if (v == ~0ull) continue;
+        if (top < 64 && (v >> top) != (sv.prefix >> top)) continue;
+        atomicAdd(&h[(u32)(v >> sh) & (RS_BINS - 1)], 1u);
+    }
+    __syncthreads();
+    for (u32 i = threadIdx.x; i < RS_BINS; i += blockDim.x)
+        if (h[i]) atomicAdd(&ghist[i], h[i]);
+}
+__global__ void k_rsel_init(RSel* sel, u64 rank, u32* ghist) {
+    PDL_PROLOGUE();
+    if (threadIdx.x == 0) {
+        RSel v;
+        v.prefix = 0; v.rank = rank; v.hibits = 0; v.found = 0;
+        *sel = v;
+    }
+    for (u32 i = threadIdx.x; i < RS_BINS; i += blockDim.x) ghist[i] = 0;
+}
+// one CTA: the digit holding rank sel.rank (0-based) -> prefix; zeroes ghist for the next pass
+__global__ void __launch_bounds__(1024) k_rsel_pick(RSel* sel, u32 sh, u32* ghist, u32* status, u32 last) {
+    PDL_PROLOGUE();
+    __shared__ u32 red[33];
+    __shared__ u32 s_d;
+    __shared__ u64 s_before;
+    // per thread 16 consecutive bins; exclusive scan of the thread sums
+    const u32 per = RS_BINS / 1024;
+    u32 loc[RS_BINS / 1024], sum = 0;
+#pragma unroll
+    for (u32 q = 0; q < per; ++q) { loc[q] = ghist[threadIdx.x * per + q]; sum += loc[q]; }
+    u32 tot = 0;
+    const u32 ex = block_exclusive_scan<1024>(sum, red, &tot);
+    if (threadIdx.x == 0) { s_d = 0xffffffffu; s_before = 0; }
+    __syncthreads();
+    const u64 r = sel->rank;
+    if ((u64)ex <= r && r < (u64)ex + sum) {
+        u32 run = ex;
+        for (u32 q = 0; q < per; ++q) {
+            if (r < (u64)run + loc[q]) { s_d = threadIdx.x * per + q; s_before = run; break; }
+            run += loc[q];
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (u32 q = 0; q < per; ++q) ghist[threadIdx.x * per + q] = 0;
+    if (threadIdx.x == 0) {
+        RSel sv = *sel;
+        if (s_d == 0xffffffffu) {  // fewer than rank+1 entries: not enough distinct draws
+            st_set(status, ST_SAMPLE_SHORT);
+            sv.found = 0;
+            sv.prefix = 0;
+        } else {
+            const u64 mask = (sh + RS_BITS >= 64) ? ~0ull : ((1ull << (sh + RS_BITS)) - 1);
+            sv.prefix = (sv.prefix & ~mask) | ((u64)s_d << sh);
+            sv.rank = r - s_before;
+            sv.found = last;
+        }
+        *sel = sv;
+    }
+}
+
+constexpr u32 DT_NT = 1024, DT_PER = 8;  // compaction: 8192 table entries per block
+// per block of DT_NT*DT_PER entries: the number of members (minj <= j*)
+__global__ void __launch_bounds__(DT_NT) k_direct_count(const u64* minj, u64 n, const RSel* sel, u32* bcnt) {
+    PDL_PROLOGUE();
+    __shared__ u32 red[33];
+    const u64 js = sel->found ? sel->prefix : 0ull;
+    const bool any = sel->found != 0;
+    u32 cnt = 0;
+    const u64 b0 = (u64)blockIdx.x * DT_NT * DT_PER;
+#pragma unroll
+    for (u32 q = 0; q < DT_PER; ++q) {
+        const u64 c = b0 + q * DT_NT + threadIdx.x;
+        if (any && c < n && minj[c] <= js) ++cnt;
+    }
+    u32 tot = 0;
+    block_exclusive_scan<DT_NT>(cnt, red, &tot);
+    if (threadIdx.x == 0) bcnt[blockIdx.x] = tot;
+}
+// records of the members in index order; DIST: only the shard [offset, offset + nl) writes
+template <int DT, bool DIST>
+__global__ void __launch_bounds__(DT_NT) k_direct_take(const u64* minj, u64 n, const RSel* sel, const u32* bscan,
+                                                        const typename Codec<DT>::U* x, u64 offset, u32 nl, u64* tk,
+                                                        u32* tt) {
+    PDL_PROLOGUE();
+    typedef typename Codec<DT>::U U;
+    __shared__ u32 red[33];
+    const u64 js = sel->found ? sel->prefix : 0ull;
+    const bool any = sel->found != 0;
+    const u64 b0 = (u64)blockIdx.x * DT_NT * DT_PER;
+    bool mem[DT_PER];
+    u32 cnt = 0;
+#pragma unroll
+    for (u32 q = 0; q < DT_PER; ++q) {
+        // thread t owns the consecutive entries b0 + t*DT_PER + q (index order inside the block)
+        const u64 c = b0 + (u64)threadIdx.x * DT_PER + q;
+        mem[q] = any && c < n && minj[c] <= js;
+        cnt += mem[q] ? 1u : 0u;
+    }
+    u32 rank = bscan[blockIdx.x] + block_exclusive_scan<DT_NT>(cnt, red, nullptr);
+#pragma unroll
+    for (u32 q = 0; q < DT_PER; ++q) {
+        if (!mem[q]) continue;
+        const u64 c = b0 + (u64)threadIdx.x * DT_PER + q;
+        const u32 rk = rank++;
+        if (DIST && (c < offset || c >= offset + nl)) continue;
+        const U k = Codec<DT>::ord(x[c - offset]);
+        if (sizeof(U) == 4) {
+            tk[rk] = ((u64)k << 32) | c;
+        } else if (DIST) {
+            tk[2 * (u64)rk] = (u64)k;
+            tk[2 * (u64)rk + 1] = c;
+        } else {
+            tk[rk] = (u64)k;
+            tt[rk] = (u32)c;
+        }
+    }
+}
+// exclusive scan of the block counts (one CTA); a shortfall of members sets ST_SAMPLE_SHORT
+__global__ void __launch_bounds__(1024) k_direct_scan(u32* bcnt, u32 nb, u32 m, u32* status) {
+    PDL_PROLOGUE();
+    __shared__ u32 red[33];
+    block_scan_array<1024>(bcnt, nb, red);
+    if (threadIdx.x == 0 && bcnt[nb] != m) st_set(status, ST_SAMPLE_SHORT);
 }
 
 // ------------------------------------------------------------------ a3: sample sort (coarse level)
@@ -948,8 +1105,8 @@ __global__ void __launch_bounds__(1024) k_segscan(const Seg* segs, const u32* ns
                 bk.level = level | (((b == 0 || b + 1 == sg.P) && sg.loose) ? BK_LOOSE : 0u);
                 bk.lo = (b == 0) ? sg.lo : (u64)sk[b - 1];
                 bk.hi = (b + 1 == sg.P) ? sg.hi : (u64)sk[b];
-                if (isfit) { if (of < fit_cap) fit[of] = bk; else atomicOr(status, ST_LIST_OVER); }
-                else { if (ob < big_cap) big[ob] = bk; else atomicOr(status, ST_LIST_OVER); }
+                if (isfit) { if (of < fit_cap) fit[of] = bk; else st_set(status, ST_LIST_OVER); }
+                else { if (ob < big_cap) big[ob] = bk; else st_set(status, ST_LIST_OVER); }
             }
         }
         __syncthreads();
@@ -1738,7 +1895,7 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                 // sorted on chip in windows by the second launch (k_bucket_sort<..., true>)
                 if (threadIdx.x == 0) {
                     const u32 w = atomicAdd(nwlist, 1u);
-                    if (w < wcap) wlist[w] = bk; else atomicOr(status, ST_LIST_OVER);
+                    if (w < wcap) wlist[w] = bk; else st_set(status, ST_LIST_OVER);
                 }
                 __syncthreads();
                 continue;
@@ -1896,7 +2053,7 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                     for (int b = (int)P - 1; b >= 0; --b) {
                         const u32 len = sp_cnt[b + 1] - sp_cnt[b];
                         if (len == 0) continue;
-                        if (sp >= BS_STACK) { atomicOr(status, ST_LIST_OVER); break; }
+                        if (sp >= BS_STACK) { st_set(status, ST_LIST_OVER); break; }
                         Bucket nb;
                         nb.beg = bk.beg + sp_cnt[b]; nb.len = len; nb.buf = db;
                         const bool edge = (b == 0 || b + 1 == (int)P);
@@ -2055,7 +2212,7 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                     else if (lane == 0) {
                         const u32 h = atomicAdd(&s_nhuge, 1u);
                         if (h < BS_HUGEMAX) s_huge[h] = g;
-                        else atomicOr(status, ST_LIST_OVER);
+                        else st_set(status, ST_LIST_OVER);
                     }
                 }
                 __syncthreads();
@@ -2192,7 +2349,7 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                         if (threadIdx.x == 0) {
                             Bucket fb = bk;
                             fb.level |= BK_FORCE;
-                            if (s_sp < BS_STACK) stk[s_sp++] = fb; else atomicOr(status, ST_LIST_OVER);
+                            if (s_sp < BS_STACK) stk[s_sp++] = fb; else st_set(status, ST_LIST_OVER);
                         }
                         __syncthreads();
                         continue;
@@ -2316,7 +2473,7 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                         else if (lane == 0) {
                             const u32 h = atomicAdd(&s_nhuge, 1u);
                             if (h < BS_HUGEMAX) s_huge[h] = g;
-                            else atomicOr(status, ST_LIST_OVER);
+                            else st_set(status, ST_LIST_OVER);
                         }
                     }
                     __syncthreads();
@@ -2566,7 +2723,7 @@ __global__ void __launch_bounds__(1024) k_dist_plan(const u32* C /*world x p*/, 
             for (u32 b = b0; b < b1; ++b) o += C[(u64)s * p + b];
         }
         *nlist = 0;
-        if (bstart[nb] > cap_items) atomicOr(status, ST_LIST_OVER);
+        if (bstart[nb] > cap_items) st_set(status, ST_LIST_OVER);
     }
     __syncthreads();
     for (u32 b = threadIdx.x; b < nb; b += 1024) {

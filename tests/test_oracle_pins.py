@@ -253,7 +253,48 @@ def test_lemma1_bound_random_instances(orc):
             s = r * p
             xx = -(-(-(-n // p)) // s)
             assert mx <= s * xx + p * xx - xx
+            assert mx <= orc.tight_bound(n, p, r)
         done += 1
+
+
+def _dro_brute_counts(x, p, r):
+    """Algorithm 1's split re-derived in plain Python from the paper (independent of the
+    oracle): baseline split (Q8), stable sort of every X_k, balanced regular sample of s = rp
+    segment ends with tags start_k + position (Q6, Q9), T sorted by (key, tag),
+    S[q] = T[(q+1)rp - 1], counts by a linear scan in (key, tag) order."""
+    n, s = len(x), r * p
+    tags = _dro_tags(x, p)
+    T = []
+    start = 0
+    for m in _baseline_sizes(n, p):
+        xs = sorted(x[start:start + m])
+        q, rho = m // s, m % s
+        for j in range(s):
+            e = (j + 1) * q + min(j + 1, rho) - 1
+            T.append((xs[e], start + e))
+        start += m
+    T.sort()
+    S = [T[(q + 1) * r * p - 1] for q in range(p - 1)]
+    return _brute_counts(list(x), S, p, tags)
+
+
+def test_tight_bound_attained_reading_q10(orc):
+    """The tight form s*x + (p-1)(x-1) of Lemma 1's count (reading Q10; proof at P:430-476) is
+    never exceeded (test_lemma1_bound_random_instances) and is attained exactly on hill-climbed
+    inputs (tests/golden/dro_tight_instances.json, written by tools/gen_tight_instance.py): their
+    largest bucket, re-derived by brute force from Algorithm 1, equals oracle.tight_bound, so a
+    formula one too large or too small fails here or there."""
+    d = gold("dro_tight_instances.json")
+    assert len(d["instances"]) >= 5
+    for inst in d["instances"]:
+        n, p, r = inst["n"], inst["p"], inst["r"]
+        x = [int(v) for v in inst["keys"]]
+        assert len(x) == n
+        mx = max(_dro_brute_counts(x, p, r))
+        assert mx == inst["max_bucket"] == inst["tight_bound"] == orc.tight_bound(n, p, r)
+        assert mx <= orc.lemma1_bound(n, p, r)
+        res = orc.dro_sort(np.array(x, dtype=np.int32), p, r)
+        assert int(res.counts.max()) == mx
 
 
 def test_dro_parameter_errors(orc):

@@ -272,14 +272,18 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
+    sorter.status(reset=True)  # clear the sticky device-status word before the timed replays
     for k in range(args.steps):
         work.copy_(src)
         evs[k][0].record(stream)
         replay()
         evs[k][4].record(stream)
     torch.cuda.synchronize(dev)
+    # every timed replay ran its device-side checks (work lists, sample size) without a failure
+    dev_status = sorter.status(reset=True)
+    assert dev_status == 0, f"device status {dev_status} after the timed replays"
     # phase split of the same sort (eager launches with the library's phase events)
-    pevs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    pevs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(args.steps)]
     for k in range(args.steps):
         work.copy_(src)
         ovs.set_phase_events(pevs[k])
@@ -289,7 +293,7 @@ def main():
     if world > 1:
         dist.barrier()
     step_ms = [evs[k][0].elapsed_time(evs[k][4]) for k in range(args.steps)]
-    ph_names = ["sample", "classify_hist", "scatter", "bucket_sort"]
+    ph_names = list(ovs.PHASES)  # sample, sample_sort, classify_hist, scatter, bucket_sort
     phase_ms = {nm: statistics.mean(pevs[k][i].elapsed_time(pevs[k][i + 1]) for k in range(args.steps))
                 for i, nm in enumerate(ph_names)}
     tot_ms = sum(step_ms)
@@ -364,6 +368,7 @@ def main():
                 "e2e": {"value": e2e_v, "unit": "Gkeys/s", "h2d_bytes_per_step": int(n * 4),
                         "d2h_bytes_per_step": int(n * 4), "ms_per_step": e2e_ms},
                 "gpu_launches": launches_per_step * args.steps, "launches_per_step": launches_per_step,
+                "device_status": dev_status,
                 "clocks": clocks}
         print(json.dumps(line), flush=True)
     if world > 1:

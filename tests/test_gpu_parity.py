@@ -262,3 +262,73 @@ def test_c4_full(ovs, orc):
     original index), DRO p=512, r=ceil(log2 n)=27; checks stability element by element."""
     c = ovs_inputs.CONFIGS["C4"]
     dro_case(ovs, orc, ovs_inputs.keys("u16key", c["n"], seed=41), c["p"], c["s"], kv=True)
+
+
+# ---------------------------------------------------------------- samples that are a large fraction of n
+@pytest.mark.parametrize("dist,n,p,s,kv", [
+    ("u32", 1_000_000, 64, 12_000, False),      # ps-1 = 0.77 n: the direct-address sample table
+    ("i32_few", 300_000, 16, 18_750, True),     # ps-1 = n - 1
+    ("f64_normal", 200_000, 40, 5_000, False),  # ps-1 = n - 1, 64-bit keys
+    ("u32_u31", 1_048_575, 64, 16_384, False),  # ps-1 = n exactly
+    ("u32", 2_000_000, 1000, 1_000, False),     # ps-1 = n/2 - 1 (hash-set form)
+])
+def test_ros_large_sample_fraction(ovs, orc, dist, n, p, s, kv):
+    """ps-1 up to n is valid (SURVEY.md §8(b): ps >= n/2 allowed, Claim 1's precondition only);
+    the GPU takes the same first ps-1 distinct draws as the oracle (reading Q1)."""
+    ros_case(ovs, orc, dist, n, p, s, seed=9, kv=kv)
+
+
+def _closed_form_exhaustive(x, p, s):
+    """ps-1 = n: T is the whole input, splitter q is the element of rank (q+1)s in (key, index)
+    order and the counts are [s, ..., s, s-1] (closed form)."""
+    order = np.argsort(x, kind="stable")
+    idx = order[np.arange(1, p) * s - 1]
+    return x[idx], idx.astype(np.uint64), np.array([s] * (p - 1) + [s - 1], dtype=np.uint64)
+
+
+@pytest.mark.slow
+def test_ros_sample_equals_input_full_size(ovs):
+    """n = 2^27 u32 with ps-1 = n (p = 1539, s = 87211, ps = 2^27 + 1): ~2.6e9 draws through the
+    direct-address table; splitters and counts equal the closed form, output sorted."""
+    n, p, s = 1 << 27, 1539, 87211
+    assert p * s - 1 == n
+    x = ovs_inputs.keys("u32", n, seed=51)
+    out, _, rep = gpu_sort(ovs, x, "ros", p, s, 5)
+    assert rep.device_status == 0
+    sk, st, cnt = _closed_form_exhaustive(x, p, s)
+    np.testing.assert_array_equal(rep.splitter_keys, sk)
+    np.testing.assert_array_equal(rep.splitter_tags, st)
+    np.testing.assert_array_equal(rep.counts, cnt)
+    np.testing.assert_array_equal(out, np.sort(x))
+
+
+@pytest.mark.slow
+def test_ros_half_sample_full_size(ovs, orc):
+    """n = 2^27 u32 with ps-1 = n/2 (p = 4096, s = 16384): ~9.3e7 draws (beyond the round-1
+    2^26-draw cap); splitters, counts and output equal the oracle's."""
+    n, p, s = 1 << 27, 4096, 16384
+    x = ovs_inputs.keys("u32", n, seed=51)
+    ref = orc.ros_sort(x, p, s, 5)
+    out, _, rep = gpu_sort(ovs, x, "ros", p, s, 5)
+    check(ref, out, None, rep, p)
+
+
+def test_sticky_status_after_graph_replays(ovs):
+    """ovs_device_status: the sticky status word after CUDA-graph replays (no report) is 0, and
+    the per-phase report events are filled (phase_ms[0..4] and the total)."""
+    n = 3_000_017
+    x = torch.from_numpy(ovs_inputs.keys("u32", n, seed=3)).cuda()
+    w = x.clone()
+    srt = ovs.Sorter(n, torch.uint32, False, "ros", 1024, 64, 1)
+    replay = srt.graph(w)
+    for _ in range(3):
+        w.copy_(x)
+        replay()
+    assert srt.status() == 0
+    h = w.cpu().numpy()
+    assert bool(np.all(h[1:] >= h[:-1]))
+    w.copy_(x)
+    rep = srt(w, report=True)
+    assert rep.device_status == 0
+    assert all(v >= 0 for v in rep.phase_ms[:5]) and rep.phase_ms[7] > 0
+    assert abs(sum(rep.phase_ms[:5]) - rep.phase_ms[7]) < 0.05 * rep.phase_ms[7] + 0.01

@@ -27,14 +27,14 @@ for name, dist, dseed, n, method, p, s, kv, bpk in CASES:
         wk.copy_(x)
         if kv:
             wv.copy_(v)
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
         ovs.set_phase_events(ev)
         srt(wk, wv) if kv else srt(wk)
         ovs.set_phase_events(None)
-        ev[4].synchronize()
+        ev[5].synchronize()
         if r >= 2:
-            ms.append(ev[0].elapsed_time(ev[4]))
-            ph.append([ev[i].elapsed_time(ev[i + 1]) for i in range(4)])
+            ms.append(ev[0].elapsed_time(ev[5]))
+            ph.append([ev[i].elapsed_time(ev[i + 1]) for i in range(5)])
     t = statistics.median(ms)
     phases = {nm: round(statistics.median(q[i] for q in ph), 3) for i, nm in enumerate(ovs.PHASES)}
     print(json.dumps({"config": name, "n": n, "dtype": str(x.dtype).replace("torch.", ""), "method": method, "p": p,

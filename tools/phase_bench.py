@@ -21,7 +21,7 @@ for path in libs:
     torch.cuda.synchronize()
     h = w[:: 1 << 12].cpu().numpy()
     ok = bool(np.all(np.diff(w.cpu().numpy().astype(np.int64)) >= 0))
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(10)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(10)]
     for k in range(13):
         w.copy_(x)
         if k >= 3:
@@ -29,8 +29,8 @@ for path in libs:
         srt(w)
     ovs.set_phase_events(None)
     torch.cuda.synchronize()
-    ph = [statistics.median(e[i].elapsed_time(e[i + 1]) for e in evs) for i in range(4)]
-    tot = statistics.median(e[0].elapsed_time(e[4]) for e in evs)
+    ph = [statistics.median(e[i].elapsed_time(e[i + 1]) for e in evs) for i in range(5)]
+    tot = statistics.median(e[0].elapsed_time(e[5]) for e in evs)
     print(f"{path or 'libovs.so'}: sorted={ok} total {tot:.3f} ms ({n / tot / 1e6:.1f} Gkeys/s)  "
           + "  ".join(f"{nm} {v:.3f}" for nm, v in zip(ovs.PHASES, ph)), flush=True)
     del srt

@@ -135,56 +135,59 @@ def run_reference(args):
 
 
 def run_dist(args, x, src, work, dev, rank, world, local):
-    """N > 1: weak scaling, 2^27 keys per GPU; the distributed ROS sort (sample all-reduce,
-    count all-gather, all-to-all-v over NVLink, local sort); device time, max over ranks."""
+    """N > 1: weak scaling, 2^27 keys per GPU; the library's distributed ROS sort (ovs_dist_sort_keys:
+    sample records and count rows stored into every rank's NCCL window, the scatter storing every
+    key straight into its owner's window over NVLink, LSA barriers, local bucket sort).  Device
+    time per step with CUDA events, max over ranks."""
     import torch
     import torch.distributed as dist
-    from paper_1608_08648_b200.dist import CudaBackend, dist_sort
+    from paper_1608_08648_b200.dist import DistSorter
     n = args.n
-    p = args.p // world * world  # 4096 buckets at every N: the write-combining scatter's range
+    p = args.p // world * world  # 4096 buckets at every N (the write-combining scatter's range)
     s, seed = args.s, WORKLOAD["seed"]
-    be = CudaBackend(n, n * world, torch.uint32, False, p, s, seed, world, 2 * n, dev)
-    res = dist_sort(src, None, p, s, seed, backend=be)
+    ds = DistSorter(n, torch.uint32, False, p, s, seed, device=dev)
+    res = ds(src, report=True)
     host = res.keys.cpu().numpy()
     assert bool(np.all(host[1:] >= host[:-1]))
+    nvlink = torch.tensor([float(res.exchange_bytes)], device=dev, dtype=torch.float64)
+    dist.all_reduce(nvlink, op=dist.ReduceOp.SUM)
     for _ in range(args.warmup):
-        dist_sort(src, None, p, s, seed, backend=be)
+        ds(src)
     torch.cuda.synchronize(dev)
     sampler = ClockSampler(local)
     sampler.start()
     ms = []
-    sent = 0
     for _ in range(args.steps):
         dist.barrier()
         torch.cuda.synchronize(dev)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        r = dist_sort(src, None, p, s, seed, backend=be)
+        ds(src)
         b.record()
         b.synchronize()
         ms.append(a.elapsed_time(b))
-        sent += r.exchange_bytes
-    clocks = sampler.stop()
     t = torch.tensor([sum(ms)], device=dev, dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_per_step = float(t.item()) / args.steps
-    nv = torch.tensor([sent / args.steps], device=dev, dtype=torch.float64)
-    dist.all_reduce(nv, op=dist.ReduceOp.SUM)
     value = n * world / (ms_per_step * 1e-3) / 1e9
     # end to end: pinned host shard -> device -> distributed sort -> host slice
     hx = torch.from_numpy(x).pin_memory()
-    e2e = []
+    hout = torch.empty(ds.out_cap, dtype=torch.uint32).pin_memory()
+    e2e, d2h = [], 0
     for k in range(args.e2e_steps + 1):
         dist.barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         work.copy_(hx, non_blocking=True)
-        r = dist_sort(work, None, p, s, seed, backend=be)
-        out_h = r.keys.to("cpu")
+        r = ds(work)
+        nk = r.keys.numel()
+        hout[:nk].copy_(r.keys, non_blocking=True)
         b.record()
         b.synchronize()
+        d2h = nk * 4
         if k > 0:
             e2e.append(a.elapsed_time(b))
+    clocks = sampler.stop()
     te = torch.tensor([statistics.mean(e2e)], device=dev, dtype=torch.float64)
     dist.all_reduce(te, op=dist.ReduceOp.MAX)
     if rank == 0:
@@ -194,15 +197,21 @@ def run_dist(args, x, src, work, dev, rank, world, local):
                 "dtype": "u32", "data": "synthetic (ovs_inputs, seeded)",
                 "config": {"workload": f"C5: 2^27 uint32 keys per GPU x {world}, uniform on [0,2^32) (data seed 51), "
                                        f"ROS p={p} s={s}", "global_batch": n * world, "seq_len": None,
-                           "parallelism": f"dp{world}: sample all-reduce, count all-gather, all-to-all-v (NCCL)",
+                           "parallelism": f"dp{world}: ovs_dist_sort_keys (NCCL symmetric window; sample, counts "
+                                          f"and items stored into peer windows over NVLink; LSA barriers)",
                            "n_per_gpu": n, "p": p, "s": s,
                            "l2": "input 512 MiB per GPU > 126 MB L2"},
-                "nvlink_bytes_per_step": float(nv.item()),
+                "nvlink_bytes_per_step": float(nvlink.item()),
                 "roofline": None, "cpu_baseline": None,
                 "e2e": {"value": n * world / (float(te.item()) * 1e-3) / 1e9, "unit": "Gkeys/s",
-                        "h2d_bytes_per_step": int(n * 4 * world), "d2h_bytes_per_step": int(n * 4 * world)},
-                "gpu_launches": None, "clocks": clocks}
+                        "h2d_bytes_per_step": int(n * 4), "d2h_bytes_per_step": int(d2h),
+                        "note": "per rank; value = all ranks' keys / max-over-ranks time"},
+                "gpu_launches": res.kernel_launches * args.steps, "launches_per_step": res.kernel_launches,
+                "phases_ms_rank0": dict(zip(["sample+records", "sample_sort", "hist+counts", "fused_scatter",
+                                              "bucket_sort"], res.phase_ms[:5])),
+                "clocks": clocks}
         print(json.dumps(line), flush=True)
+    ds.close()
     dist.destroy_process_group()
 
 
@@ -219,6 +228,7 @@ def main():
     ap.add_argument("--cpu-n", type=int, default=1 << 26, help="keys of the cpu_baseline oracle run")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--force-dist", action="store_true", help="run the distributed path even at N=1 (tests)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -232,8 +242,13 @@ def main():
     rank, world, local = dist_info()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    if world > 1 or args.force_dist:
         import torch.distributed as dist
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=dev)
     n, p, s, seed = args.n, args.p, args.s, WORKLOAD["seed"]
 
@@ -241,7 +256,7 @@ def main():
     src = torch.from_numpy(x).to(dev)
     work = torch.empty_like(src)
     stream = torch.cuda.current_stream(dev)
-    if world > 1:
+    if world > 1 or args.force_dist:
         run_dist(args, x, src, work, dev, rank, world, local)
         return
     sorter = ovs.Sorter(n, torch.uint32, False, "ros", p, s, seed, device=dev)

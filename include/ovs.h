@@ -46,7 +46,9 @@ typedef enum {
                             DRO: r == 0 or r*p > floor(n/p) (distinct positions) */
     OVS_EWORKSPACE = 4,  /* ws_bytes < ovs_workspace_bytes(...)                                  */
     OVS_ECUDA = 5,       /* a CUDA runtime error; see ovs_last_error()                           */
-    OVS_ECAPACITY = 7,   /* distributed: output larger than out_capacity                         */
+    OVS_ENCCL = 6,       /* an NCCL failure (distributed calls); see ovs_last_error()            */
+    OVS_ECAPACITY = 7,   /* distributed: some rank's received items exceed its out_capacity or the
+                            window (*n_out = this rank's requirement; every rank returns it)      */
     OVS_EINTERNAL = 8    /* a device-side check failed: returned by a call with rep != NULL, and
                             by ovs_device_status() for calls without a report (graph replays)          */
 } ovs_status;
@@ -83,6 +85,8 @@ typedef struct {          /* optional, caller-owned HOST memory; each array poin
     uint32_t kernel_launches; /* kernels this call enqueued                                     */
     uint32_t device_status;   /* 0, or a device-side failure bit set                            */
     uint32_t reserved;
+    uint64_t exchange_bytes;  /* distributed calls: bytes this rank stored into other ranks'
+                                 windows (sample records, count rows, items); 0 otherwise        */
 } ovs_report;
 
 /* Bytes of workspace ovs_sort_keys / ovs_sort_pairs_stable need for these arguments
@@ -101,42 +105,73 @@ int ovs_sort_pairs_stable(void* d_keys, uint32_t* d_vals, size_t n, int dtype, c
                           size_t ws_bytes, void* stream, ovs_report* rep);
 
 /* ---------------------------------------------------------------------------------------
- * Multi-GPU building blocks (ROS).  One process per GPU; rank r holds the contiguous shard
- * [offset, offset + n_local) of a global array of n_global keys (ranks in index order).  The
- * caller runs the NCCL collectives between the three calls (paper_1608_08648_b200/dist.py
- * does it with torch.distributed), the way the paper's multi-core method splits the work
- * (PAPER.md:656-681): each GPU samples its shard, the sample is assembled everywhere, every
- * GPU classifies its keys against the same splitters, buckets are exchanged (bucket j goes to
- * rank floor(j*world/p); p must be a multiple of world), and each GPU sorts
- * the buckets it received.  Tags are global indices, so rank r's output is exactly the
- * [sum_{j<j0} n_j, sum_{j<j1} n_j) slice of the single-GPU sort of the concatenated input.
- *   1. ovs_dist_sample: d_sample (ovs_dist_sample_words u64 words, device) receives this
- *      shard's records of the global sample, zero elsewhere -> caller: all-reduce SUM.
- *   2. ovs_dist_partition: splitters from the assembled sample, local bucket counts d_counts
- *      (p u32, device) and the local keys (order-preserving bits; + values and global indices
- *      for key-value sorts) in bucket order in d_send_* (n_local items each) -> caller:
- *      all-gather of the counts (world x p, rank-major) and an all-to-all-v of the send buffers
- *      (to rank d: its buckets, in bucket order; from rank s: concatenated in rank order).
- *   3. ovs_dist_finish: the received items (<= recv_capacity) are gathered bucket by bucket
- *      (source-rank order) and sorted into d_out_keys (+ d_out_vals), raw dtype.
- * The three calls must use the same workspace and the same (n_local, n_global, dtype,
- * with_values, params, world, recv_capacity).  Errors: OVS_EINVAL also for DRO, p % world,
- * rank out of range; device-side overflow of recv_capacity sets a status bit (the caller
- * can size recv_capacity from the all-gathered counts before calling finish). */
-size_t ovs_dist_workspace_bytes(size_t n_local, uint64_t n_global, int dtype, int with_values, const ovs_params* prm,
-                                int world, size_t recv_capacity);
-size_t ovs_dist_sample_words(uint64_t n_global, int dtype, const ovs_params* prm);
-int ovs_dist_sample(const void* d_keys, size_t n_local, uint64_t offset, uint64_t n_global, int dtype, int with_values,
-                    const ovs_params* prm, int world, size_t recv_capacity, uint64_t* d_sample, void* d_ws,
-                    size_t ws_bytes, void* stream);
-int ovs_dist_partition(const void* d_keys, const uint32_t* d_vals, size_t n_local, uint64_t offset, uint64_t n_global,
-                       int dtype, const ovs_params* prm, int world, size_t recv_capacity, const uint64_t* d_sample,
-                       void* d_send_keys, uint32_t* d_send_vals, uint32_t* d_send_idx, uint32_t* d_counts, void* d_ws,
-                       size_t ws_bytes, void* stream);
-int ovs_dist_finish(const void* d_recv_keys, const uint32_t* d_recv_vals, const uint32_t* d_recv_idx, size_t n_local,
-                    uint64_t n_global, int dtype, const ovs_params* prm, int world, int rank, size_t recv_capacity,
-                    const uint32_t* d_all_counts, void* d_out_keys, uint32_t* d_out_vals, void* d_ws, size_t ws_bytes,
-                    void* stream);
+ * Multi-GPU (ROS): one process per GPU of one NVLink/NVSwitch node, one
+ * call per rank.  Rank r holds the contiguous shard [offset_r, offset_r + n_local_r) of a global
+ * array of n_global keys (ranks in index order; the library all-gathers the sizes).  The work is
+ * split the way the paper's multi-core method splits it: every GPU draws the
+ * same global sample index set (reading Q1 over n_global) and contributes the records of its
+ * shard, every GPU computes the same splitters, classifies its keys (tags = global indices, so
+ * the tie rule is the single-process one) and stores them straight into the owner's
+ * receive window over NVLink (bucket j lives on rank floor(j*world/p); p must be a multiple of
+ * world), and every GPU sorts the buckets it owns.  Rank r's output is exactly the
+ * slice [sum_{j<j0} n_j, sum_{j<j1} n_j) of the single-GPU sort of the concatenated input, with
+ * the same splitters and bucket counts.
+ *
+ * The communicator owns an NCCL communicator (torch's NCCL 2.28) and a symmetric NCCL window
+ * (ncclMemAlloc + ncclCommWindowRegister) that holds the sample records, the count matrix and
+ * the received items; kernels store into the other ranks' windows through their NVLink mappings
+ * (ncclGetLsaPointer) and the phases are separated by NCCL device-API LSA barriers.  These calls
+ * make the communicator's device current on the calling thread. */
+typedef struct ovs_comm ovs_comm;
+
+/* ncclGetUniqueId into out[128] (call on one rank, broadcast the bytes to the others). */
+int ovs_comm_unique_id(void* out);
+/* Collective: create the communicator of `world` ranks on CUDA device `device`, with a window of
+ * at least window_bytes (OVS_ENCCL if NCCL fails or not every rank is NVLink load/store reachable). */
+int ovs_comm_create(ovs_comm** out, const void* nccl_unique_id, int rank, int world, int device, size_t window_bytes);
+/* Collective: grow the window to the largest window_bytes any rank asks for (no-op if large enough). */
+int ovs_comm_reserve(ovs_comm* c, size_t window_bytes, void* stream);
+int ovs_comm_destroy(ovs_comm* c);
+size_t ovs_comm_window_bytes(const ovs_comm* c);
+/* Window bytes that let a rank receive n_recv items (sample records and count matrix included). */
+size_t ovs_dist_window_bytes(size_t n_recv, int dtype, int with_values, const ovs_params* prm, int world);
+/* Collective (all-gathers the shard sizes; synchronises `stream`): workspace bytes this rank
+ * needs for ovs_dist_sort_* with these arguments; 0 on invalid arguments. */
+size_t ovs_dist_workspace_bytes(ovs_comm* c, size_t n_local, int dtype, int with_values, const ovs_params* prm,
+                                size_t out_capacity, void* stream);
+/* Collective distributed sort.  d_in (n_local keys, device, not modified); d_out receives this
+ * rank's sorted slice (*n_out items, raw dtype; out_capacity items available).  Synchronises
+ * `stream` twice (the shard-size all-gather; the count matrix read-back, which decides capacity
+ * and the exchange plan) and returns with the exchange and the local sort enqueued.  Errors are
+ * decided from all-gathered data, so every rank returns the same code: OVS_EINVAL (p not a
+ * multiple of world, DRO, flags, n_global >= 2^32-33), OVS_ESAMPLE (p*s-1 > n_global),
+ * OVS_EWORKSPACE (some rank's ws_bytes too small), OVS_ECAPACITY (some rank receives more items
+ * than its out_capacity or the window holds: *n_out = this rank's requirement; grow and call
+ * again), OVS_ENCCL, OVS_ECUDA.  rep (optional, host): the global splitters and bucket counts,
+ * phase_ms ([0] sample + record exchange, [1] sample sort, [2] classify + histogram + count
+ * exchange and read-back, [3] = [6] fused scatter/exchange, [4] local bucket sort, [7] total). */
+int ovs_dist_sort_keys(ovs_comm* c, const void* d_in, size_t n_local, int dtype, const ovs_params* prm, void* d_out,
+                       size_t out_capacity, size_t* n_out, void* d_ws, size_t ws_bytes, void* stream, ovs_report* rep);
+/* Stable key-value variant: uint32 values ride with their keys; equal keys keep their global
+ * input order. */
+int ovs_dist_sort_pairs_stable(ovs_comm* c, const void* d_keys, const uint32_t* d_vals, size_t n_local, int dtype,
+                               const ovs_params* prm, void* d_out_keys, uint32_t* d_out_vals, size_t out_capacity,
+                               size_t* n_out, void* d_ws, size_t ws_bytes, void* stream, ovs_report* rep);
+/* Host-only: the exchange plan of `rank` from the all-gathered count matrix counts[world][p]:
+ * dst_off[p] = where this rank's run of bucket b starts inside its owner's receive region (owner
+ * floor(b*world/p); runs of one bucket in source-rank order), recv[world] = items every rank
+ * receives.  (The plan ovs_dist_sort_* computes; exported for the multi-process CPU tests.) */
+int ovs_dist_plan(const uint32_t* counts, int world, uint32_t p, int rank, uint32_t* dst_off, uint64_t* recv);
+/* Test support: `world` ranks emulated on ONE GPU by one call (the same phases and kernels; the
+ * fused scatter stores into the other emulated ranks' windows d_win[r] of win_bytes each; every
+ * phase runs rank after rank, so no kernel waits on another).  Arrays of length world. */
+int ovs_dist_sort_virtual(int world, const void* const* d_keys, const uint32_t* const* d_vals, const size_t* n_local,
+                          int dtype, const ovs_params* prm, void* const* d_out_keys, uint32_t* const* d_out_vals,
+                          const size_t* out_capacity, size_t* n_out, void* const* d_ws, const size_t* ws_bytes,
+                          void* const* d_win, size_t win_bytes, void* stream, uint64_t* counts, void* split_keys,
+                          uint64_t* split_tags);
+size_t ovs_dist_virtual_workspace_bytes(int world, const size_t* n_local, int dtype, int with_values,
+                                        const ovs_params* prm, const size_t* out_capacity, size_t win_bytes);
 
 /* Parameters for which the buckets of n keys fit one SM's shared memory in one level (SURVEY.md
  * §8(f) f4; the paper leaves p to the user and takes s = lg^2 n).  ROS: p = the

@@ -34,7 +34,8 @@ class Report(ctypes.Structure):
     _fields_ = [("splitter_keys", ctypes.c_void_p), ("splitter_tags", ctypes.c_void_p),
                 ("bucket_counts", ctypes.c_void_p), ("phase_ms", ctypes.c_float * 8),
                 ("max_bucket", ctypes.c_uint32), ("kernel_launches", ctypes.c_uint32),
-                ("device_status", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
+                ("device_status", ctypes.c_uint32), ("reserved", ctypes.c_uint32),
+                ("exchange_bytes", ctypes.c_uint64)]
 
 
 class OvsError(RuntimeError):

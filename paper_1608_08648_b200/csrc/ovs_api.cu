@@ -34,7 +34,7 @@ static int sort_impl(void* d_keys, uint32_t* d_vals, bool kv, size_t n, int dtyp
             if (rep) {
                 std::memset(rep->phase_ms, 0, sizeof(rep->phase_ms));
                 if (rep->bucket_counts) for (u32 j = 0; j < prm->p; ++j) rep->bucket_counts[j] = 0;
-                rep->max_bucket = 0; rep->kernel_launches = 0; rep->device_status = 0;
+                rep->max_bucket = 0; rep->kernel_launches = 0; rep->device_status = 0; rep->exchange_bytes = 0;
             }
             return OVS_OK;
         }
@@ -74,6 +74,7 @@ static int sort_impl(void* d_keys, uint32_t* d_vals, bool kv, size_t n, int dtyp
             OVS_CK(cudaMemcpy(&stv, c.status, 4, cudaMemcpyDeviceToHost));
             rep->device_status = stv;
             rep->kernel_launches = c.launches;
+            rep->exchange_bytes = 0;
             const u32 p = prm->p;
             std::vector<u64> cnt(p, 0);
             if (p > 1) OVS_CK(cudaMemcpy(cnt.data(), o.counts, 8 * (size_t)p, cudaMemcpyDeviceToHost));
@@ -163,113 +164,6 @@ int ovs_sort_keys(void* d_keys, size_t n, int dtype, const ovs_params* prm, void
 int ovs_sort_pairs_stable(void* d_keys, uint32_t* d_vals, size_t n, int dtype, const ovs_params* prm, void* d_ws,
                           size_t ws_bytes, void* stream, ovs_report* rep) {
     return sort_impl(d_keys, d_vals, true, n, dtype, prm, d_ws, ws_bytes, stream, rep);
-}
-
-// ------------------------------------------------------------------ multi-GPU building blocks
-static int dist_validate(uint64_t n_local, uint64_t n_global, int dtype, const ovs_params* prm, int world) {
-    if (!prm || world < 1) return OVS_EINVAL;
-    if (dtype != OVS_U32 && dtype != OVS_I32 && dtype != OVS_F64) return OVS_EDTYPE;
-    if (prm->method != OVS_ROS) return OVS_EINVAL;               // DRO: single GPU in this revision
-    if (prm->p < 2 || prm->p % (uint32_t)world != 0) return OVS_EINVAL;  // "p ... a multiple of m"
-    if (n_global >= 0xffffffffull || n_local > n_global) return OVS_EINVAL;
-    if (prm->s == 0 || (uint64_t)prm->p * prm->s - 1 > n_global) return OVS_ESAMPLE;
-    return OVS_OK;
-}
-
-static size_t dist_dispatch(Ctx& c, int step, int dtype, bool kv, const ovs_params* prm, const DistArgs& a) {
-    if (dtype == OVS_U32) return kv ? dist_u32_v(c, step, prm, a) : dist_u32_k(c, step, prm, a);
-    if (dtype == OVS_I32) return kv ? dist_i32_v(c, step, prm, a) : dist_i32_k(c, step, prm, a);
-    return kv ? dist_f64_v(c, step, prm, a) : dist_f64_k(c, step, prm, a);
-}
-
-static int dist_call(int step, int dtype, bool kv, const ovs_params* prm, DistArgs a, void* d_ws, size_t ws_bytes,
-                     void* stream) {
-    g_err.clear();
-    int v = dist_validate(a.n_local, a.n_global, dtype, prm, (int)a.world);
-    if (v != OVS_OK) { g_err = "invalid arguments"; return v; }
-    try {
-        Ctx d;
-        d.di = dev_info();
-        d.dry = true;
-        d.take<u32>(4);
-        const size_t need = dist_dispatch(d, step, dtype, kv, prm, a);
-        if (ws_bytes < need || !d_ws) { g_err = "workspace too small"; return OVS_EWORKSPACE; }
-        Ctx c;
-        c.di = d.di;
-        c.dry = false;
-        c.ws = (char*)d_ws;
-        c.st = (cudaStream_t)stream;
-        c.status = c.take<u32>(4);
-        dist_dispatch(c, step, dtype, kv, prm, a);
-        return OVS_OK;
-    } catch (const CudaFail& e) {
-        g_err = e.what();
-        return OVS_ECUDA;
-    } catch (const StatusFail& e) {
-        g_err = e.msg;
-        return e.code;
-    } catch (const std::exception& e) {
-        g_err = e.what();
-        return OVS_ECUDA;
-    } catch (...) {
-        g_err = "unknown exception";
-        return OVS_ECUDA;
-    }
-}
-
-size_t ovs_dist_workspace_bytes(size_t n_local, uint64_t n_global, int dtype, int with_values, const ovs_params* prm,
-                                int world, size_t recv_capacity) {
-    if (dist_validate(n_local, n_global, dtype, prm, world) != OVS_OK || recv_capacity >= 0xffffffffull) return 0;
-    try {
-        Ctx d;
-        d.di = dev_info();
-        d.dry = true;
-        d.take<u32>(4);
-        DistArgs a{};
-        a.n_local = n_local; a.n_global = n_global; a.world = (u32)world; a.recv_cap = (u32)recv_capacity;
-        return dist_dispatch(d, 0, dtype, with_values != 0, prm, a);
-    } catch (...) {
-        return 0;
-    }
-}
-
-size_t ovs_dist_sample_words(uint64_t n_global, int dtype, const ovs_params* prm) {
-    if (!prm || prm->p < 2 || prm->s == 0) return 0;
-    return ((size_t)prm->p * prm->s - 1) * (dtype == OVS_F64 ? 2 : 1);
-}
-
-int ovs_dist_sample(const void* d_keys, size_t n_local, uint64_t offset, uint64_t n_global, int dtype, int with_values,
-                    const ovs_params* prm, int world, size_t recv_capacity, uint64_t* d_sample, void* d_ws,
-                    size_t ws_bytes, void* stream) {
-    DistArgs a{};
-    a.keys = d_keys; a.n_local = n_local; a.offset = offset; a.n_global = n_global; a.world = (u32)world;
-    a.recv_cap = (u32)recv_capacity; a.rec = d_sample;
-    if (offset + n_local > n_global) return OVS_EINVAL;
-    return dist_call(0, dtype, with_values != 0, prm, a, d_ws, ws_bytes, stream);
-}
-
-int ovs_dist_partition(const void* d_keys, const uint32_t* d_vals, size_t n_local, uint64_t offset, uint64_t n_global,
-                       int dtype, const ovs_params* prm, int world, size_t recv_capacity, const uint64_t* d_sample,
-                       void* d_send_keys, uint32_t* d_send_vals, uint32_t* d_send_idx, uint32_t* d_counts, void* d_ws,
-                       size_t ws_bytes, void* stream) {
-    DistArgs a{};
-    a.keys = d_keys; a.vals = d_vals; a.n_local = n_local; a.offset = offset; a.n_global = n_global;
-    a.world = (u32)world; a.recv_cap = (u32)recv_capacity; a.rec = (u64*)d_sample;
-    a.send_k = d_send_keys; a.send_v = d_send_vals; a.send_i = d_send_idx; a.counts = d_counts;
-    if (offset + n_local > n_global) return OVS_EINVAL;
-    return dist_call(1, dtype, d_vals != nullptr, prm, a, d_ws, ws_bytes, stream);
-}
-
-int ovs_dist_finish(const void* d_recv_keys, const uint32_t* d_recv_vals, const uint32_t* d_recv_idx, size_t n_local,
-                    uint64_t n_global, int dtype, const ovs_params* prm, int world, int rank, size_t recv_capacity,
-                    const uint32_t* d_all_counts, void* d_out_keys, uint32_t* d_out_vals, void* d_ws, size_t ws_bytes,
-                    void* stream) {
-    DistArgs a{};
-    a.n_local = n_local; a.n_global = n_global; a.world = (u32)world; a.rank = (u32)rank;
-    a.recv_cap = (u32)recv_capacity; a.recv_k = d_recv_keys; a.recv_v = d_recv_vals; a.recv_i = d_recv_idx;
-    a.C = d_all_counts; a.out_k = d_out_keys; a.out_v = d_out_vals;
-    if (rank < 0 || rank >= world) return OVS_EINVAL;
-    return dist_call(2, dtype, d_recv_vals != nullptr, prm, a, d_ws, ws_bytes, stream);
 }
 
 int ovs_device_status(const void* d_ws, void* stream, uint32_t* status, int reset) {

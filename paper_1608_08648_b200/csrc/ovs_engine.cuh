@@ -15,6 +15,7 @@
 #include <vector>
 #include <mutex>
 #include <unordered_map>
+#include <memory>
 
 namespace ovs {
 
@@ -295,7 +296,7 @@ template <int DT, bool KV> struct Engine {
     }
 
     // level 0: classifier build, histogram, scans, scatter buffer 0 -> buffer 1
-    void level0(Level0& z, Lists& l, u64* counts_out) {
+    void level0_hist(Level0& z, Lists& l, u64* counts_out) {
         if (c.dry) return;
         const size_t sm_cls = std::max<size_t>(sizeof(U) * std::max<u32>(z.P, 1), 16);
         smem_limit(k_build_cls0<U>, sm_cls, c.di);
@@ -316,20 +317,32 @@ template <int DT, bool KV> struct Engine {
                                           nullptr, 0, counts_out, c.status);
         c.check();
         if (mark_phases) c.mark(3);
+    }
+    void level0(Level0& z, Lists& l, u64* counts_out) {
+        level0_hist(z, l, counts_out);
+        level0_scatter(z);
+    }
+    // a7: buffer 0 -> buffer 1 at the scanned positions; DIST: straight into the owners' windows
+    // (dst_off[b]: this rank's run of bucket b in its owner's receive region)
+    template <bool DIST = false>
+    void level0_scatter(Level0& z, const u32* dst_off = nullptr, PeerOut pk = PeerOut{nullptr, 0, 1},
+                        size_t off_v = 0, size_t off_i = 0) {
+        if (c.dry) return;
         if (use_wc(z.P)) {
             constexpr int IT = WC_ITEMS * 4 / (int)sizeof(U);  // u32: WC_ITEMS keys per thread
             const size_t sm_w = wc_smem_bytes<U>(z.P);
-            auto kw = k_scatter_wc<DT, WC_NT, IT, true>;
+            auto kw = k_scatter_wc<DT, WC_NT, IT, true, DIST>;
             smem_limit(kw, sm_w, c.di);
-            launch(c, kw, z.nchunk, WC_NT, sm_w, B, z.chunks, z.nchunks, z.seg, z.P, z.hist, z.tot, z.bid);
+            launch(c, kw, z.nchunk, WC_NT, sm_w, B, z.chunks, z.nchunks, z.seg, z.P, z.hist, z.tot, (const u16*)z.bid,
+                   dst_off, pk);
             c.check();
         } else {
             constexpr int IT = PartItems<U, KV>::v;
             const size_t sm_s = scatter_smem(z.P, z.L);
-            auto ks = k_scatter<DT, KV, true, PT_NT, IT>;
+            auto ks = k_scatter<DT, KV, true, PT_NT, IT, DIST>;
             smem_limit(ks, sm_s, c.di);
             launch(c, ks, z.nchunk, PT_NT, sm_s, B, z.chunks, z.nchunks, z.seg, z.sk, z.st, z.lut, z.P, z.L, z.hist,
-                                                z.tot, tag_base);
+                                                z.tot, tag_base, dst_off, pk, off_v, off_i);
             c.check();
         }
         if (mark_phases) c.mark(4);
@@ -409,14 +422,14 @@ template <int DT, bool KV> struct Level1 {
             auto kw = k_scatter_wc<DT, WC_NT, IT, false>;
             smem_limit(kw, sm_w, c.di);
             launch(c, kw, std::min<u32>(maxchunk, (u32)c.di.sms), WC_NT, sm_w, e.B, chunks, nsegs + 1, segs, PS, hist, tot,
-                   (const u16*)bid);
+                   (const u16*)bid, (const u32*)nullptr, PeerOut{nullptr, 0, 1});
         } else {
             constexpr int IT = PartItems<U, KV>::v;
             const size_t sm_s = Engine<DT, KV>::scatter_smem(PS, LS);
             auto ks = k_scatter<DT, KV, false, PT_NT, IT>;
             smem_limit(ks, sm_s, c.di);
             launch(c, ks, std::min<u32>(maxchunk, 2 * (u32)c.di.sms), PT_NT, sm_s, e.B, chunks, nsegs + 1, segs, sk, st,
-                   lut, PS, LS, hist, tot, 0u);
+                   lut, PS, LS, hist, tot, 0u, (const u32*)nullptr, PeerOut{nullptr, 0, 1}, (size_t)0, (size_t)0);
         }
         c.check();
     }
@@ -589,7 +602,7 @@ template <int DT, bool DIST> struct RosSampler {
         c.check();
     }
     // records of the members of I (DIST: of the shard [offset, offset + nl), into rec)
-    void take(u64 seed, const U* x, u64 offset, u32 nl, u64* rec) {
+    void take(u64 seed, const U* x, u64 offset, u32 nl, PeerOut po = PeerOut{nullptr, 0, 1}) {
         if (c.dry) return;
         if (direct) {
             launch(c, k_direct_count, dnb, DT_NT, 0, (const u64*)minj, n, (const RSel*)rsel, dbcnt);
@@ -597,12 +610,11 @@ template <int DT, bool DIST> struct RosSampler {
             launch(c, k_direct_scan, 1, 1024, 0, dbcnt, dnb, m, c.status);
             c.check();
             launch(c, k_direct_take<DT, DIST>, dnb, DT_NT, 0, (const u64*)minj, n, (const RSel*)rsel,
-                   (const u32*)dbcnt, x, offset, nl, DIST ? rec : tk, tt);
+                   (const u32*)dbcnt, x, offset, nl, tk, tt, po);
             c.check();
             return;
         }
-        launch(c, k_ros_take<DT, DIST>, nb, TK_NT, 0, bits, bcnt, M, n, seed, m, x, offset, nl, DIST ? rec : tk, tt,
-                                                      c.status);
+        launch(c, k_ros_take<DT, DIST>, nb, TK_NT, 0, bits, bcnt, M, n, seed, m, x, offset, nl, tk, tt, c.status, po);
         c.check();
     }
     void select(u32 P, u32 s, u32 f, u64 seed, U* sk, u32* st) { sel->template run<U>(P, s, f, seed, sk, st); }
@@ -670,7 +682,7 @@ template <int DT, bool KV> struct RosSort {
         if (p > 1) {
             // a1+a2: ps-1 distinct random indices and their records T = [(x[i], i)]
             smp->draw(seed);
-            smp->take(seed, e.B.k[0], 0, n, nullptr);
+            smp->take(seed, e.B.k[0], 0, n);
             c.mark(1);
             // a3+a4: sort T by (key, i); S[q] = T[(q+1)s - 1] (refined: every (s/f)-th)
             smp->select(p * f, s, f, seed ^ 0x5eed, z.sk, z.st);
@@ -710,6 +722,13 @@ inline int validate_impl(size_t n, int dtype, const ovs_params* prm) {
         if ((uint64_t)prm->s * prm->p > n / prm->p) return OVS_ESAMPLE;
     }
     return OVS_OK;
+}
+
+// ordered bits -> the caller's dtype on the host (the report's splitter keys)
+template <int DT> inline typename Codec<DT>::U host_raw(typename Codec<DT>::U o) {
+    if constexpr (DT == DT_I32) return (typename Codec<DT>::U)(o ^ 0x80000000u);
+    else if constexpr (DT == DT_F64) return (typename Codec<DT>::U)((o >> 63) ? (o & 0x7fffffffffffffffull) : ~o);
+    else return o;
 }
 
 struct Out {
@@ -854,100 +873,191 @@ template <int DT, bool KV> struct DroSort {
     }
 };
 
-// ------------------------------------------------------------------ multi-GPU building blocks
-// One process per GPU; the caller moves bytes between the steps with NCCL collectives
-// (paper_1608_08648_b200/dist.py does it with torch.distributed).  The layout of the
-// workspace depends only on (n_local, n_global, dtype, kv, params, world, recv_capacity), so
-// the three calls share it (splitters written by partition are read by finish).
-template <int DT, bool KV> struct DistSort {
+// ------------------------------------------------------------------ multi-GPU
+// One rank's distributed ROS sort, in phases that ovs_dist.cu runs with barriers between them
+// (the paper's multi-core split, with GPUs in place of cores):
+//   sample   every rank draws the same global index set over n_global keys (a1) and stores the
+//            records of its own shard into slot `rank` of EVERY rank's window (NVLink stores)
+//   select   records -> sample sort -> splitters (a3-a4, identical on every rank)
+//   count    classify + histogram of the local shard (a5-a6, tags = global indices); the bucket
+//            counts -> row `rank` of the count matrix in every rank's window
+//   scatter  (after the host plan) every key straight into its owner's window (a7 fused with the
+//            exchange: bucket j lives on rank floor(j*world/p), p a multiple of world)
+//   finish   the owned buckets (runs in source-rank order, so the order of equal keys is the
+//            global index order) are sorted from the window into the caller's output (a8)
+// Window layout (every rank the same; byte offsets): the sample records, the count matrix, then
+// the received keys (+ values + original indices).
+struct WinLayout {
+    size_t rec = 0, C = 0, rk = 0, rv = 0, ri = 0, end = 0;
+    u64 cap = 0;  // received items that fit
+};
+inline WinLayout win_layout(size_t win_bytes, u64 m, u32 kb, bool kv, u32 world, u32 p) {
+    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    WinLayout L;
+    size_t o = 0;
+    L.rec = o; o = al(o + 8 * (size_t)m * (kb == 8 ? 2 : 1));
+    L.C = o; o = al(o + 4 * (size_t)world * p);
+    const size_t per = kb + (kv ? 8 : 0);
+    const size_t rem = win_bytes > o + 3 * 256 ? win_bytes - o - 3 * 256 : 0;
+    L.cap = std::min<u64>(rem / per, 0xffffffffull - 64);
+    L.rk = o; o = al(o + kb * L.cap);
+    L.rv = o; o = kv ? al(o + 4 * L.cap) : o;
+    L.ri = o; o = kv ? al(o + 4 * L.cap) : o;
+    L.end = o;
+    return L;
+}
+// the host part of the exchange plan (also exported as ovs_dist_plan for the CPU tests):
+// dst_off[b] = where this rank's run of bucket b starts inside owner(b)'s receive region,
+// desc = (begin, length, global id) of every non-empty owned bucket, recv[r] = items rank r gets
+struct DistPlanHost {
+    std::vector<u32> dst_off, desc;
+    std::vector<u64> recv;
+};
+inline void dist_plan_host(const u32* C, u32 world, u32 p, u32 rank, DistPlanHost& P) {
+    P.dst_off.assign(p, 0);
+    P.desc.clear();
+    P.recv.assign(world, 0);
+    std::vector<u64> tot(p, 0);
+    for (u32 g = 0; g < world; ++g)
+        for (u32 b = 0; b < p; ++b) tot[b] += C[(size_t)g * p + b];
+    for (u32 d = 0; d < world; ++d) {
+        const u32 b0 = (u32)((u64)d * p / world), b1 = (u32)((u64)(d + 1) * p / world);
+        u64 run = 0;
+        for (u32 b = b0; b < b1; ++b) {
+            u64 before = 0;
+            for (u32 g = 0; g < rank; ++g) before += C[(size_t)g * p + b];
+            P.dst_off[b] = (u32)(run + before);
+            if (d == rank && tot[b] > 0) { P.desc.push_back((u32)run); P.desc.push_back((u32)tot[b]); P.desc.push_back(b); }
+            run += tot[b];
+        }
+        P.recv[d] = run;
+    }
+}
+
+struct DistCfg {
+    const void* keys; const u32* vals; u64 n_local, n_global, offset;
+    u32 p, s, world, rank; u64 seed;
+    u64 out_cap;  // output items (d_out) the caller provides
+    WinLayout W;
+    void* out_k; u32* out_v;
+};
+
+struct DistRun {
+    virtual ~DistRun() {}
+    virtual void sample(char* const* d_peer) = 0;            // records -> every window
+    virtual void select(const char* win) = 0;                // this rank's window
+    virtual void count(char* const* d_peer) = 0;             // counts -> every window
+    virtual void scatter(char* const* d_peer, const DistPlanHost& P, u32* h_stage) = 0;
+    virtual void finish(const char* win, u32 n_owned) = 0;   // owned buckets -> out
+    virtual void splitters(void* h_keys, uint64_t* h_tags) = 0;  // raw dtype (after select)
+    virtual size_t ws() const = 0;
+};
+
+template <int DT, bool KV> struct DistSort : DistRun {
     typedef typename Codec<DT>::U U;
     Ctx& c;
-    Engine<DT, KV> e;   // local partition: buffer 0 = local shard, buffer 1 = send buffers
-    Engine<DT, KV> f;   // finish: buffer 0 = output, buffer 1 = scratch
+    DistCfg g;
+    Engine<DT, KV> e;   // local partition: buffer 0 = the local shard (read only)
+    Engine<DT, KV> f;   // receive side: buffer 1 = the window's received items, buffer 0 = the output
     typename Engine<DT, KV>::Level0 z;
-    typename Engine<DT, KV>::Lists l, lf;
-    u32 nl, p, s, world, m, M, words, recv_cap;
-    u64 ng, offset = 0, seed;
+    typename Engine<DT, KV>::Lists l, lf, lb;
+    u32 m = 0;
     u64* counts64 = nullptr;
-    RosSampler<DT, true>* smp = nullptr;  // a1-a4 over the global index set
-    u32* bstart = nullptr; u32* srcoff = nullptr;
-    Level1<DT, KV>* l1x = nullptr;  // owned buckets far over capacity
-    typename Engine<DT, KV>::Lists lb;
+    u32* dst_off = nullptr;   // p (device)
+    u32* desc = nullptr;      // 3p (device)
+    RosSampler<DT, true>* smp = nullptr;
+    Level1<DT, KV>* l1x = nullptr;
 
-    DistSort(Ctx& ctx, u32 n_local, u64 n_global, u32 p_, u32 s_, u64 seed_, u32 world_, u32 recv_capacity)
-        : c(ctx), e(ctx), f(ctx), nl(n_local), p(p_), s(s_), world(world_), recv_cap(recv_capacity), ng(n_global),
-          seed(seed_) {
+    DistSort(Ctx& ctx, const DistCfg& cfg) : c(ctx), g(cfg), e(ctx), f(ctx) {
+        const u32 nl = (u32)g.n_local, p = g.p;
+        m = p * g.s - 1;
         e.n = nl;
         e.cap = bucket_cap<U, KV>(c.di);
-        f.n = recv_cap;
-        f.cap = e.cap;
-        f.ixbits = bits_for(ng);
-        m = p * s - 1;
-        M = (u32)std::min<u64>(ros_draws(ng, m), 0xffffffffull);
-        words = sizeof(U) == 4 ? 1 : 2;
+        e.tag_base = (u32)g.offset;
+        e.B.k[0] = (U*)g.keys;  // read only: the fused scatter writes to the windows
+        e.B.v[0] = (u32*)g.vals;
+        e.B.k[1] = nullptr; e.B.v[1] = nullptr; e.B.i[0] = nullptr; e.B.i[1] = nullptr;
         counts64 = c.take<u64>(p);
-        smp = new RosSampler<DT, true>(c, ng, p, s);
+        dst_off = c.take<u32>(p);
+        desc = c.take<u32>(3 * (size_t)p);
+        smp = new RosSampler<DT, true>(c, g.n_global, p, g.s);
         e.carve_level0(z, p);
         e.carve_lists(l, p);
-        // finish side
-        f.B.k[1] = c.take<U>(recv_cap);
-        f.B.v[1] = KV ? c.take<u32>(recv_cap) : nullptr;
-        f.B.i[0] = KV ? c.take<u32>(recv_cap) : nullptr;
-        f.B.i[1] = KV ? c.take<u32>(recv_cap) : nullptr;
-        bstart = c.take<u32>(p + 2);
-        srcoff = c.take<u32>(world + 1);
+        // receive side: items in the window (buffer 1), output in buffer 0
+        const u32 oc = (u32)std::min<u64>(g.out_cap, 0xffffffffull - 64);
+        f.n = oc;
+        f.cap = e.cap;
+        f.ixbits = bits_for(g.n_global);
+        f.B.k[0] = (U*)g.out_k;
+        f.B.v[0] = g.out_v;
+        f.B.k[1] = nullptr; f.B.v[1] = nullptr; f.B.i[1] = nullptr;
+        f.B.i[0] = KV ? c.take<u32>(oc) : nullptr;  // level-1 scratch of the original indices
         f.carve_lists(lf, p);
-        if (ng / p > BS_WMAX * f.cap) {
-            l1x = new Level1<DT, KV>(f, p / world + 1);
-            f.carve_lists(lb, (p / world + 1) * Level1<DT, KV>::PS);
+        if (g.n_global / p > BS_WMAX * f.cap) {
+            l1x = new Level1<DT, KV>(f, p / g.world + 1);
+            f.carve_lists(lb, (p / g.world + 1) * Level1<DT, KV>::PS);
         }
     }
     ~DistSort() { delete smp; delete l1x; }
+    size_t ws() const override { return c.off + 256; }
 
-    void sample(const U* keys, u64* rec) {
+    void sample(char* const* d_peer) override {
         if (c.dry) return;
-        OVS_CK(cudaMemsetAsync(rec, 0, sizeof(u64) * (size_t)m * words, c.st));
-        smp->draw(seed);
-        smp->take(seed, keys, offset, nl, rec);
+        smp->draw(g.seed);
+        smp->take(g.seed, (const U*)g.keys, g.offset, (u32)g.n_local, PeerOut{d_peer, g.W.rec, g.world});
     }
-
-    void partition(U* keys, u32* vals, const u64* rec, U* send_k, u32* send_v, u32* send_i, u32* counts) {
+    void select(const char* win) override {
         if (c.dry) return;
-        launch(c, k_dist_unpack, cdiv(m, 256), 256, 0, rec, m, words, smp->tk, smp->tk, smp->tt);
+        const u32 words = sizeof(U) == 4 ? 1 : 2;
+        launch(c, k_dist_unpack, cdiv(m, 256), 256, 0, (const u64*)(win + g.W.rec), m, words, smp->tk, smp->tk, smp->tt);
         c.check();
-        // the coarse-bucket counters are zeroed here too: this call may run on a fresh process
         OVS_CK(cudaMemsetAsync(smp->sel->gcnt, 0, 8 * SEL_GMAX, c.st));
-        smp->select(p, s, 1, seed ^ 0x5eed, z.sk, z.st);
-        e.B.k[0] = keys; e.B.v[0] = vals;
-        e.B.k[1] = send_k; e.B.v[1] = send_v; e.B.i[1] = send_i;
-        e.B.i[0] = nullptr;
-        e.tag_base = (u32)offset;
-        e.level0(z, l, counts64);
-        launch(c, k_u64_to_u32, cdiv(p, 256), 256, 0, counts64, counts, p);
+        smp->select(g.p, g.s, 1, g.seed ^ 0x5eed, z.sk, z.st);
+    }
+    void count(char* const* d_peer) override {
+        if (c.dry) return;
+        e.level0_hist(z, l, counts64);
+        launch(c, k_put_counts, cdiv(g.p * g.world, 256), 256, 0, (const u64*)counts64, g.p, g.rank,
+               PeerOut{d_peer, g.W.C, g.world});
         c.check();
     }
-
-    void finish(const U* rk, const u32* rv, const u32* ri, const u32* C, u32 rnk, U* out_k, u32* out_v) {
+    void scatter(char* const* d_peer, const DistPlanHost& P, u32* h_stage) override {
         if (c.dry) return;
-        launch(c, k_dist_plan<U>, 1, 1024, 0, C, world, p, rnk, z.sk, bstart, srcoff, lf.fit, lf.nfit, recv_cap, c.status,
-               1u);
-        c.check();
-        const u32 nb = (u32)((u64)(rnk + 1) * p / world) - (u32)((u64)rnk * p / world);
-        f.B.k[0] = out_k;
-        f.B.v[0] = out_v;
-        // the owned buckets are assembled in the scratch buffer 1 and sorted into the output
-        // (buffer 0): a bucket does not live in the output array, so oversized ones can be
-        // sorted in windows; buckets far over capacity go through level 1 first
-        launch(c, k_dist_gather<U, KV>, cdiv((u64)world * nb * 32, 256), 256, 0,
-            rk, rv, ri, f.B.k[1], f.B.v[1], f.B.i[1], C, world, p, rnk, bstart, srcoff);
+        // the plan: dst_off (p) and the owned-bucket descriptors, staged in pinned host memory
+        std::memcpy(h_stage, P.dst_off.data(), 4 * (size_t)g.p);
+        if (!P.desc.empty()) std::memcpy(h_stage + g.p, P.desc.data(), 4 * P.desc.size());
+        OVS_CK(cudaMemcpyAsync(dst_off, h_stage, 4 * (size_t)g.p, cudaMemcpyHostToDevice, c.st));
+        if (!P.desc.empty())
+            OVS_CK(cudaMemcpyAsync(desc, h_stage + g.p, 4 * P.desc.size(), cudaMemcpyHostToDevice, c.st));
+        e.template level0_scatter<true>(z, dst_off, PeerOut{d_peer, g.W.rk, g.world}, g.W.rv, g.W.ri);
+    }
+    void finish(const char* win, u32 n_owned) override {
+        if (c.dry) return;
+        f.B.k[1] = (U*)(win + g.W.rk);
+        f.B.v[1] = KV ? (u32*)(win + g.W.rv) : nullptr;
+        f.B.i[1] = KV ? (u32*)(win + g.W.ri) : nullptr;
+        launch(c, k_dist_list<U>, std::max<u32>(1, cdiv(n_owned, 256)), 256, 0, (const u32*)desc, n_owned,
+               (const U*)z.sk, g.p, lf.fit, lf.nfit, 1u);
         c.check();
         fill_u32(c, lf.ticket, 0, 1);
         if (l1x) {
             fill_u32(c, lb.nfit, 0, 2);
-            l1x->run(lf.fit, lf.nfit, lb, seed ^ 0xf2);
-            f.bucket_sort(lb, seed ^ 0xf1);
+            l1x->run(lf.fit, lf.nfit, lb, g.seed ^ 0xf2);
+            f.bucket_sort(lb, g.seed ^ 0xf1);
         } else {
-            f.bucket_sort(lf, seed ^ 0xf1);
+            f.bucket_sort(lf, g.seed ^ 0xf1);
+        }
+    }
+    void splitters(void* h_keys, uint64_t* h_tags) override {
+        if (c.dry || g.p < 2) return;
+        std::vector<U> kb(g.p - 1);
+        std::vector<u32> tb(g.p - 1);
+        OVS_CK(cudaMemcpyAsync(kb.data(), z.sk, sizeof(U) * (g.p - 1), cudaMemcpyDeviceToHost, c.st));
+        OVS_CK(cudaMemcpyAsync(tb.data(), z.st, 4 * (size_t)(g.p - 1), cudaMemcpyDeviceToHost, c.st));
+        OVS_CK(cudaStreamSynchronize(c.st));
+        for (u32 q = 0; q + 1 < g.p; ++q) {
+            if (h_keys) ((U*)h_keys)[q] = host_raw<DT>(kb[q]);
+            if (h_tags) h_tags[q] = tb[q];
         }
     }
 };
@@ -978,31 +1088,14 @@ Out plan_or_run(Ctx& c, void* keys, u32* vals, size_t n, const ovs_params* prm) 
 }
 
 
-// multi-GPU entry (step 0 sample, 1 partition, 2 finish)
-struct DistArgs {
-    const void* keys; const u32* vals; u64 n_local, n_global, offset; u32 world, rank, recv_cap;
-    u64* rec; void* send_k; u32* send_v; u32* send_i; u32* counts;
-    const void* recv_k; const u32* recv_v; const u32* recv_i; const u32* C; void* out_k; u32* out_v;
-};
-template <int DT, bool KV>
-size_t dist_run(Ctx& c, int step, const ovs_params* prm, const DistArgs& a) {
-    typedef typename Codec<DT>::U U;
-    DistSort<DT, KV> d(c, (u32)a.n_local, a.n_global, prm->p, prm->s, prm->seed, a.world, a.recv_cap);
-    d.offset = a.offset;
-    if (prm->p > d.e.max_p_one_level()) throw StatusFail{OVS_EINVAL, "p too large for the one-level classifier"};
-    if (!c.dry) {
-        if (step == 0) d.sample((const U*)a.keys, a.rec);
-        else if (step == 1) d.partition((U*)a.keys, (u32*)a.vals, a.rec, (U*)a.send_k, a.send_v, a.send_i, a.counts);
-        else d.finish((const U*)a.recv_k, a.recv_v, a.recv_i, a.C, a.rank, (U*)a.out_k, a.out_v);
-    }
-    return c.off + 256;
-}
-size_t dist_u32_k(Ctx& c, int step, const ovs_params* prm, const DistArgs& a);
-size_t dist_u32_v(Ctx& c, int step, const ovs_params* prm, const DistArgs& a);
-size_t dist_i32_k(Ctx& c, int step, const ovs_params* prm, const DistArgs& a);
-size_t dist_i32_v(Ctx& c, int step, const ovs_params* prm, const DistArgs& a);
-size_t dist_f64_k(Ctx& c, int step, const ovs_params* prm, const DistArgs& a);
-size_t dist_f64_v(Ctx& c, int step, const ovs_params* prm, const DistArgs& a);
+// multi-GPU: one rank's distributed sort object (per (dtype, keys/pairs) translation unit)
+template <int DT, bool KV> DistRun* make_dist(Ctx& c, const DistCfg& cfg) { return new DistSort<DT, KV>(c, cfg); }
+DistRun* dist_u32_k(Ctx& c, const DistCfg& cfg);
+DistRun* dist_u32_v(Ctx& c, const DistCfg& cfg);
+DistRun* dist_i32_k(Ctx& c, const DistCfg& cfg);
+DistRun* dist_i32_v(Ctx& c, const DistCfg& cfg);
+DistRun* dist_f64_k(Ctx& c, const DistCfg& cfg);
+DistRun* dist_f64_v(Ctx& c, const DistCfg& cfg);
 
 // per-(dtype, keys/pairs) entry points (ovs_<dtype>_<k|v>.cu)
 Out plan_u32_k(Ctx& c, void* keys, u32* vals, size_t n, const ovs_params* prm);

@@ -112,6 +112,25 @@ template <class U> struct Bufs {
     u32* i[2];
 };
 
+// Multi-GPU: every rank's receive window as addressable from this GPU (NVLink peer mappings of
+// the NCCL symmetric window: peers[d] = window base of rank d), and an offset into it
+struct PeerOut {
+    char* const* peers;  // device array [world]
+    size_t off;          // byte offset of the region inside every window
+    u32 world;
+};
+
+// DIST sample records: record rk of the global sample goes to slot rk of every rank's window
+// (32-bit keys: one word ord key << 32 | global index; 64-bit keys: key word, index word)
+template <bool WIDE>
+__device__ __forceinline__ void put_rec(const PeerOut& po, u32 rk, u64 kw, u64 c) {
+    for (u32 d = 0; d < po.world; ++d) {
+        u64* r = (u64*)(po.peers[d] + po.off);
+        if (!WIDE) r[rk] = (kw << 32) | c;
+        else { r[2 * (u64)rk] = kw; r[2 * (u64)rk + 1] = c; }
+    }
+}
+
 // Bucket.level flags: lo/hi are not tight bounds; the items are the caller's raw keys (codec
 // not applied yet, value/index arrays not built yet: index = position)
 enum : u32 { BK_LOOSE = 0x80000000u, BK_RAW = 0x40000000u, BK_FORCE = 0x20000000u /* re-split it */ };
@@ -420,7 +439,7 @@ __global__ void __launch_bounds__(TK_NT) k_ros_first(const u64* tab, u32 lg, u32
 template <int DT, bool DIST>
 __global__ void __launch_bounds__(TK_NT) k_ros_take(const u32* bits, const u32* bcnt, u32 M, u64 n, u64 seed, u32 m,
                                                      const typename Codec<DT>::U* x, u64 offset, u32 nl, u64* tk, u32* tt,
-                                                     u32* status) {
+                                                     u32* status, PeerOut po) {
     PDL_PROLOGUE();
     typedef typename Codec<DT>::U U;
     __shared__ u32 red[TK_NT / 32], wpre[TK_NT / 32];
@@ -452,11 +471,10 @@ __global__ void __launch_bounds__(TK_NT) k_ros_take(const u32* bits, const u32* 
     const u64 c = ros_draw_c(seed, j, n);
     if (DIST && (c < offset || c >= offset + nl)) return;
     const U k = Codec<DT>::ord(x[c - offset]);
-    if (sizeof(U) == 4) {
+    if (DIST) {
+        put_rec<sizeof(U) == 8>(po, rank, (u64)k, c);
+    } else if (sizeof(U) == 4) {
         tk[rank] = ((u64)k << 32) | c;
-    } else if (DIST) {
-        tk[2 * (u64)rank] = (u64)k;
-        tk[2 * (u64)rank + 1] = c;
     } else {
         tk[rank] = (u64)k;
         tt[rank] = (u32)c;
@@ -571,7 +589,7 @@ __global__ void __launch_bounds__(DT_NT) k_direct_count(const u64* minj, u64 n, 
 template <int DT, bool DIST>
 __global__ void __launch_bounds__(DT_NT) k_direct_take(const u64* minj, u64 n, const RSel* sel, const u32* bscan,
                                                         const typename Codec<DT>::U* x, u64 offset, u32 nl, u64* tk,
-                                                        u32* tt) {
+                                                        u32* tt, PeerOut po) {
     PDL_PROLOGUE();
     typedef typename Codec<DT>::U U;
     __shared__ u32 red[33];
@@ -595,11 +613,10 @@ __global__ void __launch_bounds__(DT_NT) k_direct_take(const u64* minj, u64 n, c
         const u32 rk = rank++;
         if (DIST && (c < offset || c >= offset + nl)) continue;
         const U k = Codec<DT>::ord(x[c - offset]);
-        if (sizeof(U) == 4) {
+        if (DIST) {
+            put_rec<sizeof(U) == 8>(po, rk, (u64)k, c);
+        } else if (sizeof(U) == 4) {
             tk[rk] = ((u64)k << 32) | c;
-        } else if (DIST) {
-            tk[2 * (u64)rk] = (u64)k;
-            tk[2 * (u64)rk + 1] = c;
         } else {
             tk[rk] = (u64)k;
             tt[rk] = (u32)c;
@@ -1124,11 +1141,15 @@ __host__ __device__ constexpr size_t scatter_smem_bytes(u32 PS, u32 LS) {
            3 * a16(4 * ((size_t)PS + 1));
 }
 
-template <int DT, bool KV, bool LEVEL0, int NT, int ITEMS>
+// DIST (multi-GPU f1, key-value sorts): bucket b's items go to its owner's window (keys at
+// po.off, values at off_v, original indices at off_i) at dst_off[b] + the chunk's offset.
+template <int DT, bool KV, bool LEVEL0, int NT, int ITEMS, bool DIST = false>
 __global__ void __launch_bounds__(NT) k_scatter(Bufs<typename Codec<DT>::U> B, const Chunk* chunks, const u32* nchunks,
                                                 const Seg* segs, const typename Codec<DT>::U* sk_pool,
                                                 const u32* st_pool, const u32* lut_pool, u32 PS, u32 LS,
-                                                const u32* hist, const u32* tot_pool, u32 tag_base) {
+                                                const u32* hist, const u32* tot_pool, u32 tag_base,
+                                                const u32* dst_off = nullptr, PeerOut po = PeerOut{nullptr, 0, 1},
+                                                size_t off_v = 0, size_t off_i = 0) {
     PDL_PROLOGUE();
     typedef typename Codec<DT>::U U;
     constexpr int TS = NT * ITEMS;
@@ -1153,7 +1174,7 @@ __global__ void __launch_bounds__(NT) k_scatter(Bufs<typename Codec<DT>::U> B, c
         const u32 P = sg.P;
         const u32* hrow = hist + (size_t)c * PS;
         const u32* bst = tot_pool + (size_t)ch.seg * (PS + 1);
-        for (u32 b = threadIdx.x; b < P; b += NT) cur[b] = sg.beg + bst[b] + hrow[b];
+        for (u32 b = threadIdx.x; b < P; b += NT) cur[b] = DIST ? dst_off[b] + hrow[b] : sg.beg + bst[b] + hrow[b];
         const u32 srcb = LEVEL0 ? 0 : sg.src, dstb = 1 - srcb;
         const U* src = B.k[srcb];
         const u32* vsrc = KV ? B.v[srcb] : nullptr;
@@ -1231,13 +1252,21 @@ __global__ void __launch_bounds__(NT) k_scatter(Bufs<typename Codec<DT>::U> B, c
             }
             __syncthreads();
             for (u32 o = threadIdx.x; o < nt; o += NT) {
-                const u32 d = dbase[stb[o]] + o;
-                dst[d] = stk[o];
-                if (KV) { vdst[d] = stv[o]; idst[d] = sti[o]; }
+                const u32 bb = stb[o];
+                const u32 d = dbase[bb] + o;
+                if constexpr (DIST) {
+                    char* const w = po.peers[(bb * po.world) / P];
+                    ((U*)(w + po.off))[d] = stk[o];
+                    if (KV) { ((u32*)(w + off_v))[d] = stv[o]; ((u32*)(w + off_i))[d] = sti[o]; }
+                } else {
+                    dst[d] = stk[o];
+                    if (KV) { vdst[d] = stv[o]; idst[d] = sti[o]; }
+                }
             }
             __syncthreads();
         }
     }
+    if (DIST) __threadfence_system();
 }
 
 // ------------------------------------------------------------------ a7: write-combining scatter
@@ -1265,10 +1294,14 @@ template <class U> __host__ __device__ constexpr size_t wc_smem_bytes(u32 PS) {
 
 // LEVEL0: the caller's raw keys in buffer 0 -> buffer 1; otherwise ordered keys of every chunk's
 // segment source buffer -> the other buffer (level 1)
-template <int DT, int NT, int ITEMS, bool LEVEL0>
+// DIST (multi-GPU): bucket b's keys go straight to its owner rank
+// floor(b*world/P)'s receive window over NVLink (po.peers[owner] + po.off), at dst_off[b] (this
+// rank's run of b inside the owner's region, ovs_dist.cu) + the chunk's offset in the run.
+template <int DT, int NT, int ITEMS, bool LEVEL0, bool DIST = false>
 __global__ void __launch_bounds__(NT, 1) k_scatter_wc(Bufs<typename Codec<DT>::U> B, const Chunk* chunks,
                                                        const u32* nchunks, const Seg* segs, u32 PS, const u32* hist,
-                                                       const u32* tot_pool, const u16* bid) {
+                                                       const u32* tot_pool, const u16* bid, const u32* dst_off = nullptr,
+                                                       PeerOut po = PeerOut{nullptr, 0, 1}) {
     PDL_PROLOGUE();
     typedef typename Codec<DT>::U U;
     constexpr u32 SV = 32 / sizeof(U);  // keys per 32-byte sector
@@ -1288,13 +1321,18 @@ __global__ void __launch_bounds__(NT, 1) k_scatter_wc(Bufs<typename Codec<DT>::U
         const U* src = B.k[LEVEL0 ? 0 : sg.src];
         // positions are counted from an aligned base (the output array may be the caller's, not
         // 32-byte aligned): position x is dst[x] with dst = the array - al
-        U* const dst0 = B.k[LEVEL0 ? 1 : 1 - sg.src];
-        const u32 al = (u32)(((uintptr_t)dst0 / sizeof(U)) & (SV - 1));
+        U* const dst0 = DIST ? nullptr : B.k[LEVEL0 ? 1 : 1 - sg.src];
+        const u32 al = DIST ? 0u : (u32)(((uintptr_t)dst0 / sizeof(U)) & (SV - 1));
         U* dst = dst0 - al;
+        // destination array of bucket b (DIST: the owner's window, 256-byte aligned)
+        auto dst_of = [&](u32 b) -> U* {
+            if constexpr (DIST) return (U*)(po.peers[(b * po.world) / P] + po.off);
+            else return dst;
+        };
         const u32* hrow = hist + (size_t)c * PS;
         const u32* bst = tot_pool + (size_t)ch.seg * (PS + 1);
         for (u32 b = threadIdx.x; b < P; b += NT) {
-            const u32 r = sg.beg + bst[b] + hrow[b] + al;
+            const u32 r = DIST ? dst_off[b] + hrow[b] : sg.beg + bst[b] + hrow[b] + al;
             q[b] = r;
             sb[b] = r;  // sector r & ~(SV-1), first valid slot r & (SV-1)
         }
@@ -1380,17 +1418,18 @@ __global__ void __launch_bounds__(NT, 1) k_scatter_wc(Bufs<typename Codec<DT>::U
                 if (lead & (1u << j)) {
                     const u32 sv = sb[b], s0 = sv & ~(SV - 1), front = sv & (SV - 1);
                     const U* wb = wc + (size_t)b * SV;
+                    U* const db = dst_of(b);
                     if (front == 0) {
                         const uint4* w4 = (const uint4*)wb;
-                        uint4* g4 = (uint4*)(dst + s0);
+                        uint4* g4 = (uint4*)(db + s0);
                         g4[0] = w4[0];
                         g4[1] = w4[1];
                     } else {
-                        for (u32 x = front; x < SV; ++x) dst[s0 + x] = wb[x];
+                        for (u32 x = front; x < SV; ++x) db[s0 + x] = wb[x];
                     }
                     sb[b] = qf[j] & ~(SV - 1);
                 } else if ((vmask & ~inmask) & (1u << j)) {
-                    if (pos[j] < (qf[j] & ~(SV - 1))) dst[pos[j]] = k[j];
+                    if (pos[j] < (qf[j] & ~(SV - 1))) dst_of(b)[pos[j]] = k[j];
                     else tail |= 1u << j;
                 }
             }
@@ -1408,10 +1447,13 @@ __global__ void __launch_bounds__(NT, 1) k_scatter_wc(Bufs<typename Codec<DT>::U
         // the chunk's last, incomplete sectors (and runs inside one sector)
         for (u32 b = threadIdx.x; b < P; b += NT) {
             const u32 qe = q[b], sv = sb[b], s0 = sv & ~(SV - 1), front = sv & (SV - 1);
-            for (u32 x = front; s0 + x < qe; ++x) dst[s0 + x] = wc[(size_t)b * SV + x];
+            U* const db = dst_of(b);
+            for (u32 x = front; s0 + x < qe; ++x) db[s0 + x] = wc[(size_t)b * SV + x];
         }
         __syncthreads();
     }
+    // the peers read these stores after the next barrier (ovs_dist.cu): make them visible system-wide
+    if (DIST) __threadfence_system();
 }
 
 // ------------------------------------------------------------------ bulk async copies (TMA)
@@ -2695,71 +2737,33 @@ __global__ void k_dist_unpack(const u64* rec, u32 m, u32 words, u64* t_pack, u64
     else { t_key[t] = rec[2 * (u64)t]; t_tag[t] = (u32)rec[2 * (u64)t + 1]; }
 }
 
-__global__ void k_u64_to_u32(const u64* a, u32* b, u32 n) {
+// this rank's bucket counts -> row `rank` of the count matrix C (world x p u32) in every rank's
+// window (the count all-gather as NVLink stores)
+__global__ void k_put_counts(const u64* counts, u32 p, u32 rank, PeerOut po) {
     PDL_PROLOGUE();
-    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) b[i] = (u32)a[i];
+    const u32 t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= p * po.world) return;
+    const u32 d = t / p, b = t % p;
+    ((u32*)(po.peers[d] + po.off))[(size_t)rank * p + b] = (u32)counts[b];
+    __threadfence_system();
 }
 
-// owned buckets [b0, b1) of rank `rank`: totals, bucket starts, source offsets; one CTA
+// the received (owned) buckets as a work list: desc[3j..3j+2] = (begin in the receive region,
+// length, global bucket id) from the host plan; bounds from the splitters around the bucket
 template <class U>
-__global__ void __launch_bounds__(1024) k_dist_plan(const u32* C /*world x p*/, u32 world, u32 p, u32 rank, const U* sk,
-                                                    u32* bstart /*nb+1*/, u32* srcoff /*world*/, Bucket* list, u32* nlist,
-                                                    u32 cap_items, u32* status, u32 buf) {
+__global__ void k_dist_list(const u32* desc, u32 nb, const U* sk, u32 p, Bucket* list, u32* nlist, u32 buf) {
     PDL_PROLOGUE();
-    __shared__ u32 red[33];
-    const u32 b0 = (u32)((u64)rank * p / world), b1 = (u32)((u64)(rank + 1) * p / world), nb = b1 - b0;
-    for (u32 b = threadIdx.x; b < nb; b += 1024) {
-        u32 t = 0;
-        for (u32 s = 0; s < world; ++s) t += C[(u64)s * p + b0 + b];
-        bstart[b] = t;
-    }
-    __syncthreads();
-    block_scan_array<1024>(bstart, nb, red);  // bstart[nb] = items received
-    if (threadIdx.x == 0) {
-        u32 o = 0;
-        for (u32 s = 0; s < world; ++s) {
-            srcoff[s] = o;
-            for (u32 b = b0; b < b1; ++b) o += C[(u64)s * p + b];
-        }
-        *nlist = 0;
-        if (bstart[nb] > cap_items) st_set(status, ST_LIST_OVER);
-    }
-    __syncthreads();
-    for (u32 b = threadIdx.x; b < nb; b += 1024) {
-        const u32 len = bstart[b + 1] - bstart[b];
-        if (len == 0) continue;
-        const u32 q = atomicAdd(nlist, 1u);
-        Bucket bk;
-        bk.beg = bstart[b]; bk.len = len; bk.buf = buf;
-        const u32 g = b0 + b;  // global bucket id
-        const bool lo_open = (g == 0), hi_open = (g + 1 == p);
-        bk.level = (lo_open || hi_open) ? BK_LOOSE : 0u;
-        bk.lo = lo_open ? 0 : (u64)sk[g - 1];
-        bk.hi = hi_open ? (u64)umax_of<U>() : (u64)sk[g];
-        list[q] = bk;
-    }
-}
-
-// run (s, b): source s's items of owned bucket b -> output bucket b at offset sum_{s'<s} C[s'][b]
-template <class U, bool KV>
-__global__ void k_dist_gather(const U* rk, const u32* rv, const u32* ri, U* ok, u32* ov, u32* oi, const u32* C, u32 world,
-                              u32 p, u32 rank, const u32* bstart, const u32* srcoff) {
-    PDL_PROLOGUE();
-    const u32 b0 = (u32)((u64)rank * p / world), b1 = (u32)((u64)(rank + 1) * p / world), nb = b1 - b0;
-    const u64 w = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const u32 lane = threadIdx.x & 31;
-    if (w >= (u64)world * nb) return;
-    const u32 s = (u32)(w / nb), b = (u32)(w % nb);
-    u32 a = srcoff[s];
-    for (u32 q = b0; q < b0 + b; ++q) a += C[(u64)s * p + q];
-    u32 d = bstart[b];
-    for (u32 q = 0; q < s; ++q) d += C[(u64)q * p + b0 + b];
-    const u32 len = C[(u64)s * p + b0 + b];
-    for (u32 t = lane; t < len; t += 32) {
-        ok[d + t] = rk[a + t];
-        if (KV) { ov[d + t] = rv[a + t]; oi[d + t] = ri[a + t]; }
-    }
+    const u32 j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j == 0) { nlist[0] = nb; nlist[1] = 0; }
+    if (j >= nb) return;
+    Bucket bk;
+    bk.beg = desc[3 * j]; bk.len = desc[3 * j + 1]; bk.buf = buf;
+    const u32 g = desc[3 * j + 2];
+    const bool lo_open = g == 0, hi_open = g + 1 == p;
+    bk.level = (lo_open || hi_open) ? BK_LOOSE : 0u;
+    bk.lo = lo_open ? 0 : (u64)sk[g - 1];
+    bk.hi = hi_open ? (u64)umax_of<U>() : (u64)sk[g];
+    list[j] = bk;
 }
 
 __global__ void k_fill_u32(u32* p, u32 v, u32 n) {

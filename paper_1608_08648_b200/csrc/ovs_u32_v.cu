@@ -6,9 +6,7 @@ namespace ovs {
 Out plan_u32_v(Ctx& c, void* keys, u32* vals, size_t n, const ovs_params* prm) {
     return plan_or_run<DT_U32, true>(c, keys, vals, n, prm);
 }
-size_t dist_u32_v(Ctx& c, int step, const ovs_params* prm, const DistArgs& a) {
-    return dist_run<DT_U32, true>(c, step, prm, a);
-}
+DistRun* dist_u32_v(Ctx& c, const DistCfg& cfg) { return make_dist<DT_U32, true>(c, cfg); }
 }  // namespace ovs
 
 #ifdef OVS_BS_PROF  // experiments only: bucket-sorter phase cycles of this translation unit's kernels

@@ -1,16 +1,13 @@
-"""Multi-GPU sort (ROS): one process per GPU, NCCL collectives through torch.distributed.
+"""Multi-GPU sort (ROS) through the library's communicator (include/ovs.h, ovs_comm_* and
+ovs_dist_*): argument marshalling only.
 
-The work is split the way the paper's multi-core method splits it (SURVEY.md
-§8(e)): every GPU samples its shard, the sample is assembled on every GPU (all-reduce), every
-GPU classifies its keys against the same splitters and scatters them into destination order
-(kernels), the bucket counts are all-gathered, the buckets are exchanged (all-to-all-v over
-NVLink/NVSwitch), and every GPU sorts the buckets it received (kernels).  Bucket j lives on
-rank floor(j*world/p) (p must be a multiple of world).  Rank r's output is
-exactly its slice of the single-GPU sort of the rank-ordered concatenation of the shards.
-
-Only argument marshalling and the collectives live here; every compute step runs in the
-library's kernels (include/ovs.h, ovs_dist_*).  `Backend` is the seam the CPU gloo tests use
-to exercise this host logic without a GPU.
+One process per GPU.  The library owns the NCCL communicator and its symmetric window; every
+step, including the exchange (the scatter stores each key straight into its owner's window over
+NVLink) and the barriers between the phases, runs inside libovs.  Python only
+hands the NCCL unique id from rank 0 to the others (torch.distributed broadcast) and allocates
+the tensors.  Rank r's output is exactly its slice of the single-GPU sort of the rank-ordered
+concatenation of the shards (bucket j lives on rank floor(j*world/p), p a
+multiple of world).
 """
 from __future__ import annotations
 
@@ -19,26 +16,41 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from . import (OVS_F64, OVS_I32, OVS_OK, OVS_U32, OvsError, lib, params)
+from . import (OVS_ECAPACITY, OVS_F64, OVS_I32, OVS_OK, OVS_U32, OvsError, Params, Report, _NP, lib, params)
 
 
 def _ensure_sigs():
     L = lib()
     if getattr(L, "_dist_sigs", False):
         return L
-    vp, sz, i32, u64 = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_uint64
-    from . import Params
+    vp, sz, i32, u32 = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_uint32
     P = ctypes.POINTER(Params)
+    L.ovs_comm_unique_id.restype = i32
+    L.ovs_comm_unique_id.argtypes = [vp]
+    L.ovs_comm_create.restype = i32
+    L.ovs_comm_create.argtypes = [ctypes.POINTER(vp), vp, i32, i32, i32, sz]
+    L.ovs_comm_reserve.restype = i32
+    L.ovs_comm_reserve.argtypes = [vp, sz, vp]
+    L.ovs_comm_destroy.restype = i32
+    L.ovs_comm_destroy.argtypes = [vp]
+    L.ovs_comm_window_bytes.restype = sz
+    L.ovs_comm_window_bytes.argtypes = [vp]
+    L.ovs_dist_window_bytes.restype = sz
+    L.ovs_dist_window_bytes.argtypes = [sz, i32, i32, P, i32]
     L.ovs_dist_workspace_bytes.restype = sz
-    L.ovs_dist_workspace_bytes.argtypes = [sz, u64, i32, i32, P, i32, sz]
-    L.ovs_dist_sample_words.restype = sz
-    L.ovs_dist_sample_words.argtypes = [u64, i32, P]
-    L.ovs_dist_sample.restype = i32
-    L.ovs_dist_sample.argtypes = [vp, sz, u64, u64, i32, i32, P, i32, sz, vp, vp, sz, vp]
-    L.ovs_dist_partition.restype = i32
-    L.ovs_dist_partition.argtypes = [vp, vp, sz, u64, u64, i32, P, i32, sz, vp, vp, vp, vp, vp, vp, sz, vp]
-    L.ovs_dist_finish.restype = i32
-    L.ovs_dist_finish.argtypes = [vp, vp, vp, sz, u64, i32, P, i32, i32, sz, vp, vp, vp, vp, sz, vp]
+    L.ovs_dist_workspace_bytes.argtypes = [vp, sz, i32, i32, P, sz, vp]
+    L.ovs_dist_sort_keys.restype = i32
+    L.ovs_dist_sort_keys.argtypes = [vp, vp, sz, i32, P, vp, sz, ctypes.POINTER(sz), vp, sz, vp,
+                                     ctypes.POINTER(Report)]
+    L.ovs_dist_sort_pairs_stable.restype = i32
+    L.ovs_dist_sort_pairs_stable.argtypes = [vp, vp, vp, sz, i32, P, vp, vp, sz, ctypes.POINTER(sz), vp, sz, vp,
+                                             ctypes.POINTER(Report)]
+    L.ovs_dist_plan.restype = i32
+    L.ovs_dist_plan.argtypes = [vp, i32, u32, i32, vp, vp]
+    L.ovs_dist_sort_virtual.restype = i32
+    L.ovs_dist_sort_virtual.argtypes = [i32, vp, vp, vp, i32, P, vp, vp, vp, vp, vp, vp, vp, sz, vp, vp, vp, vp]
+    L.ovs_dist_virtual_workspace_bytes.restype = sz
+    L.ovs_dist_virtual_workspace_bytes.argtypes = [i32, vp, i32, i32, P, vp, sz]
     L._dist_sigs = True
     return L
 
@@ -46,47 +58,78 @@ def _ensure_sigs():
 def _dtcode(dt):
     import torch
     m = {torch.uint32: OVS_U32, torch.int32: OVS_I32, torch.float64: OVS_F64}
+    if dt not in m:
+        raise OvsError(2, f"unsupported dtype {dt}")
     return m[dt]
 
 
-def _ptr(t):
-    return None if t is None else t.data_ptr()
-
-
 def owned(world: int, p: int, r: int):
-    """Buckets [b0, b1) owned by rank r."""
+    """Buckets [b0, b1) owned by rank r (bucket j on rank floor(j*world/p))."""
     return (r * p) // world, ((r + 1) * p) // world
 
 
 def exchange_plan(C: np.ndarray, world: int, p: int, rank: int):
-    """Split sizes of the all-to-all from the all-gathered count matrix C (world x p):
-    send_split[d] = this rank's items of d's buckets; recv_split[s] = s's items of ours."""
-    send = [int(C[rank, slice(*owned(world, p, d))].sum()) for d in range(world)]
-    recv = [int(C[s, slice(*owned(world, p, rank))].sum()) for s in range(world)]
-    return send, recv
+    """ovs_dist_plan (the library's host plan): dst_off[b] = where `rank`'s run of bucket b starts
+    inside its owner's receive region; recv[r] = items rank r receives.  C = world x p counts."""
+    L = _ensure_sigs()
+    C = np.ascontiguousarray(C, dtype=np.uint32)
+    dst = np.zeros(p, dtype=np.uint32)
+    recv = np.zeros(world, dtype=np.uint64)
+    rc = L.ovs_dist_plan(C.ctypes.data, world, p, rank, dst.ctypes.data, recv.ctypes.data)
+    if rc != OVS_OK:
+        raise OvsError(rc, "ovs_dist_plan")
+    return dst, recv
 
 
-class CudaBackend:
-    """The product backend: the three C-ABI steps on CUDA tensors."""
+@dataclass
+class DistResult:
+    keys: object            # this rank's sorted slice (torch tensor, n_out items)
+    vals: object            # values (key-value sorts) or None
+    counts: np.ndarray      # the p global bucket counts (report) or None
+    n_before: int           # keys on lower ranks (this slice's global offset), or -1 without report
+    splitter_keys: np.ndarray
+    splitter_tags: np.ndarray
+    exchange_bytes: int     # bytes this rank stored into other ranks' windows (report) or -1
+    phase_ms: list
+    kernel_launches: int = -1  # kernels the call enqueued (report)
 
-    def __init__(self, n_local, n_global, dtype, kv, p, s, seed, world, recv_capacity, device):
+
+class DistSorter:
+    """One rank's handle: the library communicator (NCCL + symmetric window), the workspace and
+    the output buffers, sized for shards of n_local keys; collective like NCCL (every rank of
+    `group` constructs it and calls it the same number of times)."""
+
+    def __init__(self, n_local: int, dtype, with_values: bool = False, p: int = 1024, s: int = 64, seed: int = 1,
+                 group=None, device=None, out_capacity: int | None = None, window_bytes: int | None = None):
         import torch
+        import torch.distributed as dist
         self.L = _ensure_sigs()
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.dtype, self.dt, self.kv = dtype, _dtcode(dtype), with_values
         self.prm = params("ros", p, s, seed)
-        self.dt = _dtcode(dtype)
-        self.dtype, self.kv, self.world, self.device = dtype, kv, world, device
-        self.n_local, self.n_global = n_local, n_global
         self.p = p
-        self.cap = max(int(recv_capacity), 1)
-        nb = self._ws_bytes(self.cap)
-        if nb == 0:
-            raise OvsError(1, self.L.ovs_last_error().decode() or "invalid distributed arguments")
-        self.ws = torch.empty(nb, dtype=torch.uint8, device=device)
-        self.words = int(self.L.ovs_dist_sample_words(n_global, self.dt, ctypes.byref(self.prm)))
-
-    def _ws_bytes(self, cap):
-        return int(self.L.ovs_dist_workspace_bytes(self.n_local, self.n_global, self.dt, 1 if self.kv else 0,
-                                                   ctypes.byref(self.prm), self.world, cap))
+        self.n_local = n_local
+        # the NCCL unique id: rank 0 draws it, the process group broadcasts the 128 bytes
+        idb = np.zeros(128, dtype=np.uint8)
+        if self.rank == 0:
+            self._check(self.L.ovs_comm_unique_id(idb.ctypes.data))
+        backend = dist.get_backend(group)
+        t = torch.from_numpy(idb)
+        if backend == "nccl":
+            t = t.to(self.device)
+        dist.broadcast(t, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+        idb = t.cpu().numpy().copy()
+        self.out_cap = int(out_capacity or (n_local + n_local // 4 + 4096))
+        win = int(window_bytes or self.L.ovs_dist_window_bytes(self.out_cap, self.dt, int(with_values),
+                                                               ctypes.byref(self.prm), self.world))
+        self.comm = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            self._check(self.L.ovs_comm_create(ctypes.byref(self.comm), idb.ctypes.data, self.rank, self.world,
+                                               self.device.index, win))
+        self._alloc()
 
     def _check(self, rc):
         if rc != OVS_OK:
@@ -96,150 +139,140 @@ class CudaBackend:
         import torch
         return ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
 
-    def sample(self, keys, offset):
+    def _alloc(self):
         import torch
-        rec = torch.empty(self.words, dtype=torch.int64, device=self.device)
-        self._check(self.L.ovs_dist_sample(keys.data_ptr(), self.n_local, offset, self.n_global, self.dt,
-                                           1 if self.kv else 0, ctypes.byref(self.prm), self.world, self.cap,
-                                           rec.data_ptr(), self.ws.data_ptr(), self.ws.numel(), self._stream()))
-        return rec
+        with torch.cuda.device(self.device):
+            nb = int(self.L.ovs_dist_workspace_bytes(self.comm, self.n_local, self.dt, int(self.kv),
+                                                     ctypes.byref(self.prm), self.out_cap, self._stream()))
+            if nb == 0:
+                raise OvsError(1, self.L.ovs_last_error().decode() or "invalid distributed arguments")
+            self.ws = torch.empty(nb, dtype=torch.uint8, device=self.device)
+            self.ws[:16].zero_()
+            self.out_k = torch.empty(self.out_cap, dtype=self.dtype, device=self.device)
+            self.out_v = torch.empty(self.out_cap, dtype=torch.uint32, device=self.device) if self.kv else None
 
-    def partition(self, keys, vals, offset, rec):
+    def window_bytes(self) -> int:
+        return int(self.L.ovs_comm_window_bytes(self.comm))
+
+    def __call__(self, keys, vals=None, report: bool = False) -> DistResult:
         import torch
-        sk = torch.empty_like(keys)
-        sv = torch.empty_like(vals) if self.kv else None
-        si = torch.empty(self.n_local, dtype=torch.uint32, device=self.device) if self.kv else None
-        counts = torch.empty(self.p, dtype=torch.int32, device=self.device)
-        self._check(self.L.ovs_dist_partition(keys.data_ptr(), _ptr(vals), self.n_local, offset, self.n_global,
-                                              self.dt, ctypes.byref(self.prm), self.world, self.cap, rec.data_ptr(),
-                                              sk.data_ptr(), _ptr(sv), _ptr(si), counts.data_ptr(),
-                                              self.ws.data_ptr(), self.ws.numel(), self._stream()))
-        return sk, sv, si, counts
+        assert keys.is_cuda and keys.is_contiguous() and keys.numel() == self.n_local and keys.dtype == self.dtype
+        with torch.cuda.device(self.device):
+            for _ in range(3):
+                rc, res = self._call(keys, vals, report)
+                if rc != OVS_ECAPACITY:
+                    self._check(rc)
+                    return res
+                # every rank got OVS_ECAPACITY (decided from the all-gathered counts): grow the
+                # output and the (symmetric, collective) window, then call again
+                need = int(self._n_out.value)
+                self.out_cap = max(self.out_cap, need + need // 8 + 4096)
+                win = int(self.L.ovs_dist_window_bytes(self.out_cap, self.dt, int(self.kv), ctypes.byref(self.prm),
+                                                       self.world))
+                self._check(self.L.ovs_comm_reserve(self.comm, win, self._stream()))
+                self._alloc()
+            self._check(rc)
 
-    def reserve(self, n_recv):
-        """Grow recv_capacity: the workspace prefix (sample, splitters) keeps its layout."""
-        import torch
-        if n_recv <= self.cap:
-            return
-        nb = self._ws_bytes(n_recv)
-        ws = torch.empty(nb, dtype=torch.uint8, device=self.device)
-        ws[: self.ws.numel()].copy_(self.ws)
-        self.ws, self.cap = ws, n_recv
+    def _call(self, keys, vals, report):
+        p = self.p
+        rep = None
+        kbuf = np.zeros(p - 1, dtype=_NP[self.dt])
+        tbuf = np.zeros(p - 1, dtype=np.uint64)
+        cbuf = np.zeros(p, dtype=np.uint64)
+        if report:
+            rep = Report(kbuf.ctypes.data, tbuf.ctypes.data, cbuf.ctypes.data)
+        rp = ctypes.byref(rep) if rep is not None else None
+        self._n_out = ctypes.c_size_t(0)
+        if self.kv:
+            assert vals is not None and vals.dtype.itemsize == 4 and vals.numel() == self.n_local
+            rc = self.L.ovs_dist_sort_pairs_stable(self.comm, keys.data_ptr(), vals.data_ptr(), self.n_local, self.dt,
+                                                   ctypes.byref(self.prm), self.out_k.data_ptr(),
+                                                   self.out_v.data_ptr(), self.out_cap, ctypes.byref(self._n_out),
+                                                   self.ws.data_ptr(), self.ws.numel(), self._stream(), rp)
+        else:
+            rc = self.L.ovs_dist_sort_keys(self.comm, keys.data_ptr(), self.n_local, self.dt, ctypes.byref(self.prm),
+                                           self.out_k.data_ptr(), self.out_cap, ctypes.byref(self._n_out),
+                                           self.ws.data_ptr(), self.ws.numel(), self._stream(), rp)
+        if rc != OVS_OK:
+            return rc, None
+        n = int(self._n_out.value)
+        n_before, xbytes, phases, counts = -1, -1, [], None
+        if report:
+            counts = cbuf
+            b0, b1 = owned(self.world, p, self.rank)
+            n_before = int(cbuf[:b0].sum())
+            phases = list(rep.phase_ms)
+            xbytes = int(rep.exchange_bytes)
+        res = DistResult(self.out_k[:n], self.out_v[:n] if self.kv else None, counts, n_before, kbuf, tbuf, xbytes,
+                         phases, int(rep.kernel_launches) if report else -1)
+        return rc, res
 
-    def finish(self, rk, rv, ri, C, rank, n_recv):
-        import torch
-        ok = torch.empty(n_recv, dtype=self.dtype, device=self.device)
-        ov = torch.empty(n_recv, dtype=torch.uint32, device=self.device) if self.kv else None
-        self._check(self.L.ovs_dist_finish(rk.data_ptr(), _ptr(rv), _ptr(ri), self.n_local, self.n_global, self.dt,
-                                           ctypes.byref(self.prm), self.world, rank, self.cap, C.data_ptr(),
-                                           ok.data_ptr(), _ptr(ov), self.ws.data_ptr(), self.ws.numel(),
-                                           self._stream()))
-        return ok, ov
+    def close(self):
+        if getattr(self, "comm", None) and self.comm.value:
+            self.L.ovs_comm_destroy(self.comm)
+            self.comm = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
-@dataclass
-class DistResult:
-    keys: object            # this rank's sorted slice (torch tensor)
-    vals: object            # values (key-value sorts) or None
-    counts: np.ndarray      # the p global bucket counts
-    n_before: int           # number of keys on lower ranks (this slice's global offset)
-    exchange_bytes: int     # bytes this rank sent to other ranks
-
-
-def _as_comm(t):
-    """Bit-identical view with a dtype every backend's collectives accept."""
+def dist_sort_virtual(shards, vals=None, p: int = 1024, s: int = 64, seed: int = 1, win_items=None):
+    """G ranks emulated on ONE GPU by one library call (ovs_dist_sort_virtual: the same phases
+    and kernels, the fused scatter storing into the other emulated ranks' windows, phases run
+    rank after rank so no kernel waits on another).  Returns (concatenated output, values,
+    global counts, splitter keys, splitter tags, per-rank output sizes)."""
     import torch
-    if t is None:
-        return None
-    if t.dtype == torch.uint32:
-        return t.view(torch.int32)
-    return t
-
-
-def dist_sort(keys, vals=None, p: int = 1024, s: int = 64, seed: int = 1, group=None, backend=None,
-              recv_capacity=None) -> DistResult:
-    """Sort the rank-ordered concatenation of every rank's `keys` (and `vals`) across the
-    process group; returns this rank's slice.  Collective: every rank must call it."""
-    import torch
-    import torch.distributed as dist
-    world = dist.get_world_size(group)
-    rank = dist.get_rank(group)
-    dev = keys.device
-    kv = vals is not None
-    n_local = keys.numel()
-    # shard sizes -> global offsets (ranks in index order)
-    sizes = torch.zeros(world, dtype=torch.int64, device=dev)
-    mine = torch.tensor([n_local], dtype=torch.int64, device=dev)
-    dist.all_gather_into_tensor(sizes, mine, group=group)
-    sizes_h = sizes.cpu().tolist()
-    offset, n_global = int(sum(sizes_h[:rank])), int(sum(sizes_h))
-    if backend is None:
-        backend = CudaBackend(n_local, n_global, keys.dtype, kv, p, s, seed, world,
-                              recv_capacity or max(2 * n_local, 1024), dev)
-    # 1. sample: this shard's records of the global sample; all-reduce assembles T
-    rec = backend.sample(keys, offset)
-    dist.all_reduce(rec, op=dist.ReduceOp.SUM, group=group)
-    # 2. splitters, local counts, destination-ordered send buffers
-    sk, sv, si, counts = backend.partition(keys, vals, offset, rec)
-    C = torch.empty(world * p, dtype=torch.int32, device=dev)
-    dist.all_gather_into_tensor(C, counts, group=group)
-    Ch = C.view(world, p).cpu().numpy().astype(np.int64)
-    send, recv = exchange_plan(Ch, world, p, rank)
-    n_recv = int(sum(recv))
-    # 3. all-to-all-v of the buckets
-    rk = torch.empty(n_recv, dtype=keys.dtype, device=dev)
-    dist.all_to_all_single(_as_comm(rk), _as_comm(sk), recv, send, group=group)
-    rv = ri = None
-    if kv:
-        rv = torch.empty(n_recv, dtype=torch.uint32, device=dev)
-        ri = torch.empty(n_recv, dtype=torch.uint32, device=dev)
-        dist.all_to_all_single(_as_comm(rv), _as_comm(sv), recv, send, group=group)
-        dist.all_to_all_single(_as_comm(ri), _as_comm(si), recv, send, group=group)
-    # 4. gather every owned bucket's runs (source order) and sort them
-    backend.reserve(n_recv)
-    ok, ov = backend.finish(rk, rv, ri, C, rank, n_recv)
-    counts_g = Ch.sum(axis=0)
-    b0, _ = owned(world, p, rank)
-    item = keys.element_size() + (8 if kv else 0)
-    sent_out = sum(send) - send[rank]
-    return DistResult(ok, ov, counts_g, int(counts_g[:b0].sum()), int(sent_out * item))
-
-
-def dist_sort_virtual(shards, vals=None, p: int = 1024, s: int = 64, seed: int = 1):
-    """The same three steps for G shards held by ONE process on one GPU (the collectives are
-    emulated with device copies, one rank after the other; no kernel waits on another).
-    Used to test the multi-rank kernels on a single GPU.  Returns the concatenated output,
-    values and the global counts."""
-    import torch
+    L = _ensure_sigs()
     world = len(shards)
     kv = vals is not None
     dev = shards[0].device
-    sizes = [int(x.numel()) for x in shards]
-    n_global = sum(sizes)
-    offs = [sum(sizes[:r]) for r in range(world)]
-    bes = [CudaBackend(sizes[r], n_global, shards[0].dtype, kv, p, s, seed, world, max(2 * sizes[r], 1024), dev)
-           for r in range(world)]
-    recs = [bes[r].sample(shards[r], offs[r]) for r in range(world)]
-    rec = torch.stack(recs).sum(0)
-    parts = [bes[r].partition(shards[r], vals[r] if kv else None, offs[r], rec.clone()) for r in range(world)]
-    C = torch.cat([pp[3] for pp in parts])
-    Ch = C.view(world, p).cpu().numpy().astype(np.int64)
-    outs, vouts = [], []
-    for r in range(world):
-        pieces_k, pieces_v, pieces_i = [], [], []
-        for src in range(world):
-            send, _ = exchange_plan(Ch, world, p, src)
-            a = sum(send[:r])
-            pieces_k.append(parts[src][0][a:a + send[r]])
-            if kv:
-                pieces_v.append(parts[src][1][a:a + send[r]])
-                pieces_i.append(parts[src][2][a:a + send[r]])
-        rk = torch.cat(pieces_k)
-        rv = torch.cat(pieces_v) if kv else None
-        ri = torch.cat(pieces_i) if kv else None
-        bes[r].reserve(rk.numel())
-        ok, ov = bes[r].finish(rk, rv, ri, C, r, rk.numel())
-        outs.append(ok)
-        vouts.append(ov)
+    dt = _dtcode(shards[0].dtype)
+    prm = params("ros", p, s, seed)
+    n_local = np.array([int(x.numel()) for x in shards], dtype=np.uint64)
+    n_global = int(n_local.sum())
+    cap = int(win_items or (n_global // world + n_global // (2 * world) + 8192))
+    for _ in range(3):
+        res = _virtual_call(L, shards, vals, dt, prm, n_local, cap, world, kv, dev, p)
+        if isinstance(res, tuple):
+            return res
+        cap = max(cap, res + res // 8 + 4096)  # OVS_ECAPACITY: the largest requirement
+    raise OvsError(OVS_ECAPACITY, "dist_sort_virtual: capacity")
+
+
+def _virtual_call(L, shards, vals, dt, prm, n_local, cap, world, kv, dev, p):
+    import torch
+    out_cap = np.full(world, cap, dtype=np.uint64)
+    win_bytes = int(L.ovs_dist_window_bytes(cap, dt, int(kv), ctypes.byref(prm), world))
+    wsb = int(L.ovs_dist_virtual_workspace_bytes(world, n_local.ctypes.data, dt, int(kv), ctypes.byref(prm),
+                                                 out_cap.ctypes.data, win_bytes))
+    if wsb == 0:
+        raise OvsError(1, "invalid virtual distributed arguments")
+    wins = [torch.empty(win_bytes, dtype=torch.uint8, device=dev) for _ in range(world)]
+    wss = [torch.zeros(wsb, dtype=torch.uint8, device=dev) for _ in range(world)]
+    outs = [torch.empty(cap, dtype=shards[0].dtype, device=dev) for _ in range(world)]
+    vouts = [torch.empty(cap, dtype=torch.uint32, device=dev) for _ in range(world)] if kv else None
+
+    def arr(ts):
+        return (ctypes.c_void_p * world)(*[t.data_ptr() for t in ts])
+
+    n_out = np.zeros(world, dtype=np.uint64)
+    ws_bytes = np.full(world, wsb, dtype=np.uint64)
+    counts = np.zeros(p, dtype=np.uint64)
+    sk = np.zeros(p - 1, dtype=_NP[dt])
+    st = np.zeros(p - 1, dtype=np.uint64)
+    rc = L.ovs_dist_sort_virtual(world, arr(shards), arr(vals) if kv else None, n_local.ctypes.data, dt,
+                                 ctypes.byref(prm), arr(outs), arr(vouts) if kv else None, out_cap.ctypes.data,
+                                 n_out.ctypes.data, arr(wss), ws_bytes.ctypes.data, arr(wins), win_bytes,
+                                 ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream), counts.ctypes.data,
+                                 sk.ctypes.data, st.ctypes.data)
+    if rc == OVS_ECAPACITY:
+        return int(n_out.max())
+    if rc != OVS_OK:
+        raise OvsError(rc, L.ovs_last_error().decode())
     torch.cuda.synchronize(dev)
-    return torch.cat(outs), (torch.cat(vouts) if kv else None), Ch.sum(axis=0)
+    out = torch.cat([outs[r][:int(n_out[r])] for r in range(world)])
+    vout = torch.cat([vouts[r][:int(n_out[r])] for r in range(world)]) if kv else None
+    return out, vout, counts, sk, st, n_out

@@ -19,7 +19,8 @@ def test_library_exports_every_declared_symbol():
     import paper_1608_08648_b200 as ovs
     L = ovs.lib()
     names = header_functions()
-    assert {"ovs_sort_keys", "ovs_sort_pairs_stable", "ovs_workspace_bytes", "ovs_last_error"} <= set(names)
+    assert {"ovs_sort_keys", "ovs_sort_pairs_stable", "ovs_workspace_bytes", "ovs_last_error", "ovs_device_status",
+            "ovs_comm_create", "ovs_comm_destroy", "ovs_dist_sort_keys", "ovs_dist_sort_pairs_stable"} <= set(names)
     for nm in names:
         assert hasattr(L, nm), nm
     assert ovs.version().startswith("ovs")
@@ -93,3 +94,14 @@ def test_auto_params():
     big = ovs.auto_params(1 << 27, torch.uint32)
     assert big.p == 4096 and big.s == 64          # the metric's configuration
     assert ovs.auto_params(1 << 27, torch.float64).p < 1 << 27
+
+
+def test_dist_plan_validation():
+    """ovs_dist_plan (host only): p must be a multiple of world, rank in range."""
+    import numpy as np
+    from paper_1608_08648_b200.dist import exchange_plan
+    C = np.ones((2, 6), dtype=np.uint32)
+    dst, recv = exchange_plan(C, 2, 6, 1)
+    assert dst.tolist() == [1, 3, 5, 1, 3, 5] and recv.tolist() == [6, 6]
+    with pytest.raises(Exception):
+        exchange_plan(np.ones((2, 5), dtype=np.uint32), 2, 5, 0)

@@ -1,9 +1,14 @@
-"""The multi-GPU host logic (paper_1608_08648_b200/dist.py) with world_size 2 and 3 over gloo
-on CPU: shard offsets, the all-reduce that assembles the global sample, the all-gather of the
-count matrix, the all-to-all split sizes, bucket ownership (p a multiple of world,
-PAPER.md:669-670) and the per-rank output slices.  The device steps are replaced by a CPU test
-backend implementing the same contract from the oracle's pieces; the result must equal the
-single-process oracle on the rank-ordered concatenation (splitters, counts, output)."""
+"""The multi-GPU exchange protocol with world_size 2 and 3 over gloo on CPU (no GPU needed).
+
+Each process is one rank holding a ragged shard.  It computes what the library's device steps
+compute (the global sample, the splitters and its bucket counts, here from the oracle's sample
+index set and a plain lexicographic classification: test infrastructure), all-gathers the count
+matrix, and takes the exchange plan from the LIBRARY's host code (ovs_dist_plan, the function
+ovs_dist_sort_* runs).  Every rank then sends each key to its owner (bucket j on rank
+floor(j*world/p)) at the position the plan gives (all_to_all over gloo, in place
+of the NVLink stores), the owner checks that the runs of all senders tile its receive region
+exactly, sorts every owned bucket by (key, global index), and the concatenation over ranks must
+equal the single-process oracle (output, values, counts, splitters)."""
 import os
 import socket
 
@@ -16,57 +21,6 @@ import torch.multiprocessing as mp
 import ovs_inputs
 
 
-class CpuBackend:
-    """Test double of dist.CudaBackend on CPU tensors (test infrastructure)."""
-
-    def __init__(self, n_local, n_global, p, s, seed, kv):
-        import oracle
-        self.orc = oracle
-        self.n_local, self.n_global, self.p, self.s, self.seed, self.kv = n_local, n_global, p, s, seed, kv
-
-    def sample(self, keys, offset):
-        I, _ = self.orc.ros_sample_indices(self.n_global, self.p, self.s, self.seed)
-        I = np.sort(I.astype(np.int64))
-        rec = torch.zeros(2 * len(I), dtype=torch.int64)
-        x = keys.numpy()
-        for t, gi in enumerate(I):
-            if offset <= gi < offset + self.n_local:
-                rec[2 * t] = int(np.float64(x[gi - offset]).view(np.int64)) if x.dtype == np.float64 else int(x[gi - offset])
-                rec[2 * t + 1] = int(gi)
-        return rec
-
-    def partition(self, keys, vals, offset, rec):
-        x = keys.numpy()
-        r = rec.numpy().reshape(-1, 2)
-        tk = r[:, 0].view(np.float64) if x.dtype == np.float64 else r[:, 0]
-        order = np.lexsort((r[:, 1], tk))
-        T = [(tk[i], int(r[i, 1])) for i in order]
-        self.S = [T[(q + 1) * self.s - 1] for q in range(self.p - 1)]
-        gi = offset + np.arange(len(x))
-        sk = np.array([k for k, _ in self.S]) if self.S else np.zeros(0)
-        st = np.array([t for _, t in self.S], dtype=np.int64)
-        # bucket = #{q : S[q] <lex (x, gi)}
-        b = np.searchsorted(sk, x, side="left")
-        hi = np.searchsorted(sk, x, side="right")
-        for i in range(len(x)):
-            b[i] += int(np.sum(st[b[i]:hi[i]] < gi[i]))
-        o = np.argsort(b, kind="stable")
-        counts = np.bincount(b, minlength=self.p).astype(np.int32)
-        sv = torch.from_numpy(vals.numpy()[o].copy()) if vals is not None else None
-        si = torch.from_numpy(gi[o].astype(np.uint32)) if self.kv else None
-        return torch.from_numpy(x[o].copy()), sv, si, torch.from_numpy(counts)
-
-    def reserve(self, n):
-        pass
-
-    def finish(self, rk, rv, ri, C, rank, n_recv):
-        k = rk.numpy()
-        if self.kv:
-            o = np.lexsort((ri.numpy(), k))
-            return torch.from_numpy(k[o].copy()), torch.from_numpy(rv.numpy()[o].copy())
-        return torch.from_numpy(np.sort(k)), None
-
-
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -75,25 +29,86 @@ def _free_port():
     return port
 
 
+def _classify(x, gidx, sk, st):
+    """bucket = #{q : (sk[q], st[q]) <lex (x, gidx)} (reading Q5), vectorised."""
+    b = np.searchsorted(sk, x, side="left")
+    hi = np.searchsorted(sk, x, side="right")
+    for i in np.nonzero(hi > b)[0]:
+        b[i] += int(np.sum(st[b[i]:hi[i]] < gidx[i]))
+    return b
+
+
 def _worker(rank, world, port, dist_name, n_per, p, s, kv, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    from paper_1608_08648_b200.dist import dist_sort
-    n_local = n_per + rank  # ragged shards
-    start = sum(n_per + r for r in range(rank))
+    import oracle
+    from paper_1608_08648_b200.dist import exchange_plan, owned
+    sizes = [n_per + r for r in range(world)]  # ragged shards
+    start = sum(sizes[:rank])
+    n_local, n_global = sizes[rank], sum(sizes)
     x = ovs_inputs.keys(dist_name, n_local, seed=7, start=start, world=world, rank=rank)
     v = ovs_inputs.index_values(n_local, start) if kv else None
-    n_global = sum(n_per + r for r in range(world))
-    be = CpuBackend(n_local, n_global, p, s, 3, kv)
-    res = dist_sort(torch.from_numpy(x), torch.from_numpy(v) if kv else None, p, s, 3, backend=be)
-    q.put((rank, res.keys.numpy(), None if res.vals is None else res.vals.numpy(), res.counts, res.n_before,
-           [be.S[i] for i in range(len(be.S))]))
+    gidx = start + np.arange(n_local, dtype=np.int64)
+    # the global sample (same on every rank) and this shard's records, assembled by all-gather
+    I, _ = oracle.ros_sample_indices(n_global, p, s, 3)
+    I = I.astype(np.int64)
+    mine = (I >= start) & (I < start + n_local)
+    rec = np.zeros((len(I), 2), dtype=np.float64 if x.dtype == np.float64 else np.int64)
+    rec[mine, 0] = x[I[mine] - start]
+    rec[mine, 1] = I[mine]
+    got = [torch.zeros_like(torch.from_numpy(rec)) for _ in range(world)]
+    dist.all_gather(got, torch.from_numpy(rec))
+    T = sum(g.numpy() for g in got)  # every slot filled by exactly one rank
+    order = np.lexsort((T[:, 1], T[:, 0]))
+    S = T[order][np.arange(1, p) * s - 1]
+    sk, st = S[:, 0].astype(x.dtype), S[:, 1].astype(np.int64)
+    b = _classify(x, gidx, sk, st)
+    counts = np.bincount(b, minlength=p).astype(np.uint32)
+    allc = [torch.zeros(p, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(allc, torch.from_numpy(counts.astype(np.int64)))
+    C = np.stack([c.numpy() for c in allc]).astype(np.uint32)
+    dst_off, recv = exchange_plan(C, world, p, rank)  # the library's host plan
+    # positions inside the owners' receive regions: dst_off[b] + rank of the key in this rank's run
+    o = np.argsort(b, kind="stable")
+    run_start = np.concatenate([[0], np.cumsum(counts)[:-1]]).astype(np.int64)
+    pos = np.empty(n_local, dtype=np.int64)
+    pos[o] = dst_off[b[o]].astype(np.int64) + (np.arange(n_local) - run_start[b[o]])
+    owner = (b.astype(np.int64) * world) // p
+    send, recv_sizes = [], [int(C[r, slice(*owned(world, p, rank))].sum()) for r in range(world)]
+    payload = [np.stack([pos[owner == d], gidx[owner == d], (v[owner == d] if kv else np.zeros(int((owner == d).sum()))).astype(np.int64),
+                         x[owner == d].view(np.int64) if x.dtype == np.float64 else x[owner == d].astype(np.int64)], 1)
+               for d in range(world)]
+    send = torch.from_numpy(np.concatenate(payload).astype(np.int64)) if n_local else torch.zeros((0, 4), dtype=torch.int64)
+    out = torch.zeros((sum(recv_sizes), 4), dtype=torch.int64)
+    dist.all_to_all_single(out, send, recv_sizes, [len(pp) for pp in payload])
+    R = out.numpy()
+    n_out = int(recv[rank])
+    assert n_out == len(R)
+    hit = np.zeros(n_out, dtype=np.int64)
+    np.add.at(hit, R[:, 0], 1)
+    assert np.all(hit == 1), "the senders' runs must tile the receive region exactly"
+    region = np.empty_like(R)
+    region[R[:, 0]] = R
+    keys = region[:, 3].view(np.float64) if x.dtype == np.float64 else region[:, 3].astype(x.dtype)
+    # every owned bucket (contiguous in the region) sorted by (key, global index)
+    b0, b1 = owned(world, p, rank)
+    tot = C.sum(axis=0).astype(np.int64)
+    ok, ov = [], []
+    at = 0
+    for j in range(b0, b1):
+        seg = slice(at, at + int(tot[j]))
+        oo = np.lexsort((region[seg, 1], keys[seg]))
+        ok.append(keys[seg][oo])
+        ov.append(region[seg, 2][oo])
+        at += int(tot[j])
+    q.put((rank, np.concatenate(ok) if ok else keys[:0], np.concatenate(ov).astype(np.uint32) if ov else None,
+           C.sum(axis=0), sk, st))
     dist.destroy_process_group()
 
 
 @pytest.mark.parametrize("world,dist_name,kv", [(2, "u32_u31", False), (2, "u32_few4", True), (3, "i32_gauss", False),
-                                                (2, "f64_normal", True)])
-def test_dist_host_logic_matches_oracle(orc, world, dist_name, kv):
+                                                (2, "f64_normal", True), (3, "u32_staggered", False)])
+def test_dist_exchange_protocol_matches_oracle(orc, world, dist_name, kv):
     n_per, p, s = 2000, 6 * world, 8
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -101,11 +116,10 @@ def test_dist_host_logic_matches_oracle(orc, world, dist_name, kv):
     procs = [ctx.Process(target=_worker, args=(r, world, port, dist_name, n_per, p, s, kv, q)) for r in range(world)]
     for pr in procs:
         pr.start()
-    got = sorted([q.get(timeout=120) for _ in range(world)], key=lambda t: t[0])
+    got = sorted([q.get(timeout=180) for _ in range(world)], key=lambda t: t[0])
     for pr in procs:
         pr.join(timeout=60)
         assert pr.exitcode == 0
-    # the single-process oracle on the concatenation
     xs, vs = [], []
     start = 0
     for r in range(world):
@@ -113,22 +127,27 @@ def test_dist_host_logic_matches_oracle(orc, world, dist_name, kv):
         xs.append(ovs_inputs.keys(dist_name, n_local, seed=7, start=start, world=world, rank=r))
         vs.append(ovs_inputs.index_values(n_local, start))
         start += n_local
-    x = np.concatenate(xs)
-    ref = orc.ros_sort(x, p, s, 3, vals=np.concatenate(vs) if kv else None)
+    ref = orc.ros_sort(np.concatenate(xs), p, s, 3, vals=np.concatenate(vs) if kv else None)
     np.testing.assert_array_equal(np.concatenate([g[1] for g in got]), ref.keys)
     if kv:
         np.testing.assert_array_equal(np.concatenate([g[2] for g in got]), ref.vals)
     for g in got:
         np.testing.assert_array_equal(g[3], ref.counts)
-        assert [t for _, t in g[5]] == ref.split_tags.tolist()
-    assert got[0][4] == 0 and got[-1][4] + len(got[-1][1]) == len(x)
+        np.testing.assert_array_equal(g[4], ref.split_keys)
+        np.testing.assert_array_equal(g[5], ref.split_tags)
 
 
-def test_exchange_plan_ownership():
+def test_exchange_plan_closed_form():
+    """ovs_dist_plan against its definition on a hand-checkable matrix (4 ranks, 8 buckets)."""
     from paper_1608_08648_b200.dist import exchange_plan, owned
     world, p = 4, 8
-    C = np.arange(world * p).reshape(world, p)
+    C = np.arange(1, world * p + 1, dtype=np.uint32).reshape(world, p)
     assert [owned(world, p, r) for r in range(world)] == [(0, 2), (2, 4), (4, 6), (6, 8)]
-    send, recv = exchange_plan(C, world, p, 1)
-    assert send == [C[1, 0:2].sum(), C[1, 2:4].sum(), C[1, 4:6].sum(), C[1, 6:8].sum()]
-    assert recv == [C[s, 2:4].sum() for s in range(world)]
+    tot = C.sum(axis=0)
+    for rank in range(world):
+        dst, recv = exchange_plan(C, world, p, rank)
+        for b in range(p):
+            d = b * world // p
+            b0 = owned(world, p, d)[0]
+            assert dst[b] == tot[b0:b].sum() + C[:rank, b].sum()
+        assert recv.tolist() == [int(tot[slice(*owned(world, p, d))].sum()) for d in range(world)]

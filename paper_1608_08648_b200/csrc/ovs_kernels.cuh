@@ -183,8 +183,7 @@ __device__ __forceinline__ u32 classify(const ClsView<U>& c, U k, u32 tag) {
     return lo;
 }
 
-// Batched form for N keys held in registers: the table lookups for all N first (N independent
-// shared loads in flight), the 16-bit position test, then a search loop only for the keys left.
+#ifdef OVS_CLS_OLD  // round-1 form (A/B experiments): lookups first, then the position test per key
 template <class U, int N, class TagF>
 __device__ __forceinline__ void classify_n(const ClsView<U>& c, const U (&k)[N], TagF&& tag, u32 (&b)[N]) {
     if (c.P <= 1) {
@@ -201,7 +200,7 @@ __device__ __forceinline__ void classify_n(const ClsView<U>& c, const U (&k)[N],
         e[j] = (below || above) ? 0u : c.lut[(u32)d];
         b[j] = below ? 0u : above ? c.P - 1 : (e[j] & 0x1fffu);
     }
-    u32 left = 0;  // keys that still need splitter comparisons
+    u32 left = 0;
 #pragma unroll
     for (int j = 0; j < N; ++j) {
         const u32 cnt = (e[j] >> 13) & 7u;
@@ -229,6 +228,49 @@ __device__ __forceinline__ void classify_n(const ClsView<U>& c, const U (&k)[N],
         }
     }
 }
+#else
+// Batched form for N keys held in registers, branch-free on the common path: entry d of the table
+// (d clamped to L; lut[L] is the sentinel entry "bucket P-1, no splitter") gives b = lo + (kf > sf),
+// exact whenever the entry holds no splitter (sf = 0xffff there, so kf > sf never holds) or one
+// splitter whose 16-bit position differs from the key's.  The keys left (two or more splitters in
+// the entry, or kf == sf) take the binary search among the entry's splitters, from lo.
+template <class U, int N, class TagF>
+__device__ __forceinline__ void classify_n(const ClsView<U>& c, const U (&k)[N], TagF&& tag, u32 (&b)[N]) {
+    if (c.P <= 1) {
+#pragma unroll
+        for (int j = 0; j < N; ++j) b[j] = 0;
+        return;
+    }
+    u32 e[N], left = 0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+        const U x = (U)(k[j] - c.base);
+        const bool below = k[j] < c.base;
+        const U d = min((U)(x >> c.shift), (U)c.L);
+        e[j] = c.lut[(u32)d];
+        const u32 kf = cls_kfrac<U>(c, x), sf = e[j] >> 16;
+        b[j] = below ? 0u : (e[j] & 0x1fffu) + (kf > sf ? 1u : 0u);
+        const bool ex = !below && (((e[j] >> 13) & 7u) >= 2u || kf == sf);
+        left |= (ex ? 1u : 0u) << j;
+    }
+    if (__any_sync(0xffffffffu, left != 0)) {
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            if (!((left >> j) & 1u)) continue;
+            b[j] = e[j] & 0x1fffu;
+            u32 cnt = (e[j] >> 13) & 7u;
+            if (cnt == 7) cnt = (c.lut[(u32)((U)(k[j] - c.base) >> c.shift) + 1] & 0x1fffu) - b[j];
+            while (cnt > 0) {
+                const u32 half = cnt >> 1, mid = b[j] + half;
+                const U s = c.sk[mid];
+                const bool less = (s < k[j]) || (s == k[j] && c.st[mid] < tag(j));
+                if (less) { b[j] = mid + 1; cnt -= half + 1; } else { cnt = half; }
+            }
+        }
+    }
+}
+
+#endif
 
 // ------------------------------------------------------------------ block helpers
 template <int NT>
@@ -831,18 +873,18 @@ __global__ void __launch_bounds__(1024) k_build_cls0(const U* sk, u32 P, u32 L, 
             u32 a = ((U)e > lim) ? (P - 1) : count_less_key<U>(s, P - 1, (U)(base + ((U)e << shift)));
             u32 b = ((U)(e + 1) > lim) ? (P - 1) : count_less_key<U>(s, P - 1, (U)(base + ((U)(e + 1) << shift)));
             // position of the first splitter key inside the entry (16-bit resolution)
-            const u32 fr = b > a ? cls_frac<U>((U)(s[a] - base) & (((U)1 << shift) - 1), shift) : 0u;
+            const u32 fr = b > a ? cls_frac<U>((U)(s[a] - base) & (((U)1 << shift) - 1), shift) : 0xffffu;
             lut[e] = a | (min(b - a, 7u) << 13) | (fr << 16);
         }
-        if (blockIdx.x == 0 && threadIdx.x == 0) lut[L] = P - 1;
+        if (blockIdx.x == 0 && threadIdx.x == 0) lut[L] = (P - 1) | (0xffffu << 16);  // keys past the table
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         Seg g;
-        g.lo = (u64)umax_of<U>();  // min/max reduced by the histogram pass
-        g.hi = 0;
+        g.lo = 0;  // loose: the edge buckets' key bounds are found by the bucket sorter
+        g.hi = (u64)umax_of<U>();
         g.base = (u64)base;
         g.beg = 0; g.len = n; g.P = P; g.shift = shift; g.L = L; g.chunk0 = 0; g.nchunk = nchunk; g.src = 0;
-        g.loose = 0; g.pad = 0;
+        g.loose = 1; g.pad = 0;
         *seg = g;
     }
 }
@@ -948,14 +990,12 @@ __global__ void __launch_bounds__(NT, OVS_HIST_MINB) k_hist(Bufs<typename Codec<
         const u32 pend = (part + 1 == split) ? ch.end : ch.beg + (u32)(((u64)len * (part + 1) / split) & ~15ull);
         const U* src = B.k[LEVEL0 ? 0 : sg.src];
         const u32* isrc = (KV && !LEVEL0) ? B.i[sg.src] : nullptr;
-        U mn = umax_of<U>(), mx = 0;
         auto tag_at = [&](u32 o) -> u32 { return (KV && !LEVEL0) ? isrc[pbeg + o] : (LEVEL0 ? tag_base : 0u) + pbeg + o; };
         auto body = [&](U kr, u32 o) {
             const U k = LEVEL0 ? Codec<DT>::ord(kr) : kr;
             const u32 b = classify<U>(cls, k, tag_at(o));
             atomicAdd(&h[b], 1u);
             if (bid) bid[pbeg + o] = (u16)b;
-            if (LEVEL0) { mn = min(mn, k); mx = max(mx, k); }
         };
         // misaligned head and the tail one key at a time, the body in batches of UNR vectors
         constexpr u32 V = 16 / sizeof(U);
@@ -996,10 +1036,7 @@ __global__ void __launch_bounds__(NT, OVS_HIST_MINB) k_hist(Bufs<typename Codec<
             }, bb);
 #pragma unroll
             for (int j = 0; j < NB; ++j) {
-                if (vm & (1u << j)) {
-                    atomicAdd(&h[bb[j]], 1u);
-                    if (LEVEL0) { mn = min(mn, kk[j]); mx = max(mx, kk[j]); }
-                }
+                if (vm & (1u << j)) atomicAdd(&h[bb[j]], 1u);
             }
             if (bid) {
                 // the V ids of a vector as one 2V-byte store
@@ -1029,14 +1066,6 @@ __global__ void __launch_bounds__(NT, OVS_HIST_MINB) k_hist(Bufs<typename Codec<
         } else {
             for (u32 b = threadIdx.x; b < sg.P; b += NT)
                 if (h[b]) atomicAdd(&row[b], h[b]);
-        }
-        if (LEVEL0) {
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) { mn = min(mn, shfl_xor_any(mn, o)); mx = max(mx, shfl_xor_any(mx, o)); }
-            if ((threadIdx.x & 31) == 0 && pend > pbeg) {
-                atomicMin((unsigned long long*)&segs[0].lo, (unsigned long long)mn);
-                atomicMax((unsigned long long*)&segs[0].hi, (unsigned long long)mx);
-            }
         }
         __syncthreads();
     }
@@ -1554,11 +1583,11 @@ __global__ void __launch_bounds__(1024) k_l1_setup(Bufs<typename Codec<DT>::U> B
     for (u32 e = threadIdx.x; e < L; e += blockDim.x) {
         const u32 a = ((U)e > lim) ? (P - 1) : count_less_key<U>(tk, P - 1, (U)(base + ((U)e << shift)));
         const u32 b = ((U)(e + 1) > lim) ? (P - 1) : count_less_key<U>(tk, P - 1, (U)(base + ((U)(e + 1) << shift)));
-        const u32 fr = b > a ? cls_frac<U>((U)(tk[a] - base) & (((U)1 << shift) - 1), shift) : 0u;
+        const u32 fr = b > a ? cls_frac<U>((U)(tk[a] - base) & (((U)1 << shift) - 1), shift) : 0xffffu;
         lut[e] = a | (min(b - a, 7u) << 13) | (fr << 16);
     }
     if (threadIdx.x == 0) {
-        lut[L] = P - 1;
+        lut[L] = (P - 1) | (0xffffu << 16);
         Seg sg;
         sg.lo = bk.lo; sg.hi = bk.hi; sg.base = (u64)base;
         sg.beg = bk.beg; sg.len = len; sg.P = P; sg.shift = shift; sg.L = L;
@@ -1665,6 +1694,9 @@ __global__ void __launch_bounds__(1024) k_internal_sample(Bufs<typename Codec<DT
 #define OVS_BS_NT 512
 #endif
 constexpr int BS_NT = OVS_BS_NT;
+#ifndef OVS_BS_WIN16  // 32-bit keys only: swizzled items + 16-key window networks (0: round-1 path)
+#define OVS_BS_WIN16 1
+#endif
 constexpr u32 BS_WARPMAX = BS_NT >= 1024 ? 256 : 512;  // largest group a warp sorts in registers
 #ifdef OVS_BS_PROF  // phase profile of the bucket sorter (experiments only): CTA-0-thread cycles per phase
 __device__ unsigned long long g_bsprof[16];
@@ -1837,8 +1869,77 @@ template <class U> __device__ __forceinline__ u32 lower_bound_kt(const U* sk, co
     return lo;
 }
 
+// ---- 32-bit keys-only buckets: the item array is swizzled at 16-byte
+// granularity (chunk c of 4 keys lives at chunk c ^ ((c >> 2) & 7)), so that the 16-key windows
+// below (4 chunks per thread, consecutive threads on consecutive windows) and the sequential
+// write-out both touch 8 distinct 16-byte bank groups per quarter warp (no bank conflicts).
+__device__ __forceinline__ u32 sw16(u32 P) { return P ^ (((P >> 4) & 7u) << 2); }
+__device__ __forceinline__ void cexu(u32& a, u32& b) {
+    const u32 lo = min(a, b);
+    b = max(a, b);
+    a = lo;
+}
+// Batcher odd-even merge sort of 16 (63 comparators) and the merge of two sorted 8s (25)
+__device__ __forceinline__ void sort8u(u32* a) {
+    cexu(a[0], a[1]); cexu(a[2], a[3]); cexu(a[4], a[5]); cexu(a[6], a[7]);
+    cexu(a[0], a[2]); cexu(a[1], a[3]); cexu(a[4], a[6]); cexu(a[5], a[7]);
+    cexu(a[1], a[2]); cexu(a[5], a[6]);
+    cexu(a[0], a[4]); cexu(a[1], a[5]); cexu(a[2], a[6]); cexu(a[3], a[7]);
+    cexu(a[2], a[4]); cexu(a[3], a[5]);
+    cexu(a[1], a[2]); cexu(a[3], a[4]); cexu(a[5], a[6]);
+}
+__device__ __forceinline__ void merge16u(u32 (&a)[16]) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) cexu(a[i], a[i + 8]);
+    cexu(a[4], a[8]); cexu(a[5], a[9]); cexu(a[6], a[10]); cexu(a[7], a[11]);
+    cexu(a[2], a[4]); cexu(a[3], a[5]); cexu(a[6], a[8]); cexu(a[7], a[9]); cexu(a[10], a[12]); cexu(a[11], a[13]);
+    cexu(a[1], a[2]); cexu(a[3], a[4]); cexu(a[5], a[6]); cexu(a[7], a[8]); cexu(a[9], a[10]); cexu(a[11], a[12]);
+    cexu(a[13], a[14]);
+}
+__device__ __forceinline__ void sort16u(u32 (&a)[16]) {
+    sort8u(a);
+    sort8u(a + 8);
+    merge16u(a);
+}
+// load / store the 16 keys of a window that starts at physical chunk c0 (4 chunks)
+__device__ __forceinline__ void win_ld(const u32* kb, u32 c0, u32 (&e)[16]) {
+    const uint4* k4 = (const uint4*)kb;
+#pragma unroll
+    for (u32 j = 0; j < 4; ++j) {
+        const u32 c = c0 + j;
+        const uint4 v = k4[c ^ ((c >> 2) & 7u)];
+        e[4 * j] = v.x; e[4 * j + 1] = v.y; e[4 * j + 2] = v.z; e[4 * j + 3] = v.w;
+    }
+}
+__device__ __forceinline__ void win_st(u32* kb, u32 c0, const u32 (&e)[16]) {
+    uint4* k4 = (uint4*)kb;
+#pragma unroll
+    for (u32 j = 0; j < 4; ++j) {
+        const u32 c = c0 + j;
+        k4[c ^ ((c >> 2) & 7u)] = make_uint4(e[4 * j], e[4 * j + 1], e[4 * j + 2], e[4 * j + 3]);
+    }
+}
+// a group of len <= 32*R swizzled keys (logical start gs, alignment offset al) sorted by one warp
+template <int R>
+__device__ __forceinline__ void warp_sort_sw(u32* kb, u32 al, u32 gs, u32 len) {
+    typedef Elem<u32, false> E;
+    const int lane = threadIdx.x & 31;
+    E a[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const u32 e = r * 32 + lane;
+        a[r].k = e < len ? kb[sw16(gs + e + al)] : 0xffffffffu;
+    }
+    warp_bitonic<E, R>(a);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const u32 e = r * 32 + lane;
+        if (e < len) kb[sw16(gs + e + al)] = a[r].k;
+    }
+}
+
 template <class U, bool KV> __host__ __device__ constexpr size_t bucket_smem_fixed() {
-    return 4 * ((size_t)BS_NGMAX + 4) + 16;  // group counters + alignment slack of the items
+    return 4 * ((size_t)BS_NGMAX + 4) + 96;  // group counters + slack of the items (alignment, window tails)
 }
 template <class U, bool KV> __host__ __device__ constexpr size_t bucket_item_bytes() {
     return sizeof(U) + (KV ? 8 : 0);
@@ -1873,7 +1974,7 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
     {
         char* sp = smem;
         S.cnt = (u32*)sp; sp += 4 * ((size_t)BS_NGMAX + 4);
-        S.k = (U*)sp; sp += sizeof(U) * (size_t)cap + 16;
+        S.k = (U*)sp; sp += sizeof(U) * (size_t)cap + 96;
         if (KV) { S.i = (u32*)sp; sp += 4 * (size_t)cap; S.v = (u32*)sp; sp += 4 * (size_t)cap; }
     }
     Bucket* stk = stack_pool + (size_t)blockIdx.x * BS_STACK;
@@ -2170,146 +2271,287 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                 BS_PROBE(3)
                 block_scan_small<BS_NT>(Sa.cnt, ng, red);  // cnt[g] = start of group g
                 BS_PROBE(4)
-                // 2. scatter into shared memory by digit; afterwards cnt[g] = end of group g
-                for_items<U, BS_NT, OVS_BS_UNR>(src, bk.beg, m, [&](U kr, u32 o) {
-                    const U k = K(kr);
-                    u32 ix = 0, vv = 0;
-                    if (KV) { ix = IX(bk.beg + o); vv = vsrc[bk.beg + o]; }
-                    const u32 pos = atomicAdd(&Sa.cnt[digit(k, ix)], 1u);
-                    Sa.k[pos] = k;
-                    if (KV) { Sa.i[pos] = ix; Sa.v[pos] = vv; }
-                });
-                __syncthreads();
-                BS_PROBE(5)
-                // 3. one thread per group of <= 8: Batcher network in registers; larger groups are
-                // appended (warp-aggregated) to a list for 3b
-                // (OVS_NET8_X: groups per thread per iteration, their loads and networks interleaved)
-                for (u32 g0 = 0; need_sort && g0 < ng; g0 += BS_NT * OVS_NET8_X) {
-                    u32 gs[OVS_NET8_X], len[OVS_NET8_X];
-                    E a[OVS_NET8_X][8];
-    #pragma unroll
-                    for (int x = 0; x < OVS_NET8_X; ++x) {
-                        const u32 g = g0 + x * BS_NT + threadIdx.x;
-                        gs[x] = 0; len[x] = 0;
-                        if (g < ng) { gs[x] = g ? Sa.cnt[g - 1] : 0u; len[x] = Sa.cnt[g] - gs[x]; }
-                    }
-    #pragma unroll
-                    for (int x = 0; x < OVS_NET8_X; ++x) {
-                        const u32 lx = (len[x] > 1 && len[x] <= 8) ? len[x] : 0u;
-    #pragma unroll
-                        for (u32 q = 0; q < 8; ++q) a[x][q] = q < lx ? sm_get<U, KV>(Sa, gs[x] + q) : E::inf();
-                    }
-    #pragma unroll
-                    for (int x = 0; x < OVS_NET8_X; ++x) network8(a[x]);
-    #pragma unroll
-                    for (int x = 0; x < OVS_NET8_X; ++x) {
-                        const u32 lx = (len[x] > 1 && len[x] <= 8) ? len[x] : 0u;
-    #pragma unroll
-                        for (u32 q = 0; q < 8; ++q)
-                            if (q < lx) sm_put<U, KV>(Sa, gs[x] + q, a[x][q]);
-                    }
-    #pragma unroll
-                    for (int x = 0; x < OVS_NET8_X; ++x) {
-                        const u32 g = g0 + x * BS_NT + threadIdx.x;
-                        const u32 mb = __ballot_sync(0xffffffffu, len[x] > 8);
-                        if (mb) {
-                            u32 base = 0;
-                            if (lane == 0) base = atomicAdd(&s_nbig, __popc(mb));
-                            base = __shfl_sync(0xffffffffu, base, 0) + __popc(mb & ((1u << lane) - 1));
-                            if (len[x] > 8) {
-                                if (base < BS_BIGMAX) s_big[base] = g;
-                                else atomicOr(&s_over, 1u);
+                if constexpr (!KV && sizeof(U) == 4 && OVS_BS_WIN16) {
+                    // ---- 32-bit keys only: swizzled item array, windowed networks
+                    u32* const kb = (u32*)S.k;  // 16-byte aligned; logical item x at kb[sw16(x + al)]
+                    const u32 al = (u32)(((uintptr_t)(okeys + bk.beg)) / sizeof(U)) & 3u;
+                    // 2. scatter into shared memory by digit; afterwards cnt[g] = end of group g
+                    for_items<U, BS_NT, OVS_BS_UNR>(src, bk.beg, m, [&](U kr, u32) {
+                        const u32 k = (u32)K(kr);
+                        const u32 pos = atomicAdd(&S.cnt[digit((U)k, 0u)], 1u);
+                        kb[sw16(pos + al)] = k;
+                    });
+                    __syncthreads();
+                    BS_PROBE(5)
+                    if (need_sort) {
+                        // groups of >= 10 keys are listed; every shorter group lies inside one window
+                        // of 16 consecutive keys starting at a multiple of 8 (pass A: starts 16w,
+                        // pass B: 16w + 8), and sorting a window by key never breaks the digit order
+                        for (u32 g0 = 0; g0 < ng; g0 += BS_NT) {
+                            const u32 g = g0 + threadIdx.x;
+                            u32 len = 0;
+                            if (g < ng) len = S.cnt[g] - (g ? S.cnt[g - 1] : 0u);
+                            const u32 mb = __ballot_sync(0xffffffffu, len >= 10);
+                            if (mb) {
+                                u32 base = 0;
+                                if (lane == 0) base = atomicAdd(&s_nbig, __popc(mb));
+                                base = __shfl_sync(0xffffffffu, base, 0) + __popc(mb & ((1u << lane) - 1));
+                                if (len >= 10) {
+                                    if (base < BS_BIGMAX) s_big[base] = g;
+                                    else atomicOr(&s_over, 1u);
+                                }
+                            }
+                        }
+                        // pass A: physical windows [16w, 16w + 16); slots outside [al, al + m) get the
+                        // minimum / maximum key, so they stay in place
+                        const u32 nw = (al + m + 15) >> 4;
+                        for (u32 w = threadIdx.x; w < nw; w += BS_NT) {
+                            u32 e[16];
+                            win_ld(kb, 4 * w, e);
+#pragma unroll
+                            for (u32 i = 0; i < 16; ++i) {
+                                const u32 P = 16 * w + i;
+                                if (P < al) e[i] = 0u;
+                                else if (P >= al + m) e[i] = 0xffffffffu;
+                            }
+                            sort16u(e);
+                            win_st(kb, 4 * w, e);
+                        }
+                        __syncthreads();
+                        // pass B: windows [16w + 8, 16w + 24) = two sorted halves: one merge
+                        for (u32 w = threadIdx.x; w + 1 < nw; w += BS_NT) {
+                            u32 e[16];
+                            win_ld(kb, 4 * w + 2, e);
+                            merge16u(e);
+                            win_st(kb, 4 * w + 2, e);
+                        }
+                        __syncthreads();
+                        BS_PROBE(6)
+                        const u32 nlisted = min(s_nbig, (u32)BS_BIGMAX);
+                        const bool rescan = s_over != 0;  // list overflow (pathological skew): scan all groups
+                        const u32 nwork = rescan ? ng : nlisted;
+                        // listed groups of 10..16: one thread each
+                        for (u32 q = threadIdx.x; q < nwork; q += BS_NT) {
+                            const u32 g = rescan ? q : s_big[q];
+                            const u32 gs = g ? S.cnt[g - 1] : 0u, len = S.cnt[g] - gs;
+                            if (len < 10 || len > 16) continue;
+                            u32 e[16];
+#pragma unroll
+                            for (u32 t = 0; t < 16; ++t) e[t] = t < len ? kb[sw16(gs + t + al)] : 0xffffffffu;
+                            sort16u(e);
+#pragma unroll
+                            for (u32 t = 0; t < 16; ++t)
+                                if (t < len) kb[sw16(gs + t + al)] = e[t];
+                        }
+                        // 17..512: one warp each (register bitonic); larger: the CTA
+                        for (u32 q = wid; q < nwork; q += BS_NT / 32) {
+                            const u32 g = rescan ? q : s_big[q];
+                            const u32 gs = g ? S.cnt[g - 1] : 0u, len = S.cnt[g] - gs;
+                            if (len <= 16) continue;
+                            if (len <= 32) warp_sort_sw<1>(kb, al, gs, len);
+                            else if (len <= 64) warp_sort_sw<2>(kb, al, gs, len);
+                            else if (len <= 128) warp_sort_sw<4>(kb, al, gs, len);
+                            else if (len <= 256) warp_sort_sw<8>(kb, al, gs, len);
+                            else if (len <= 512 && BS_WARPMAX >= 512) warp_sort_sw<BS_WARPMAX / 32>(kb, al, gs, len);
+                            else if (lane == 0) {
+                                const u32 h = atomicAdd(&s_nhuge, 1u);
+                                if (h < BS_HUGEMAX) s_huge[h] = g;
+                                else st_set(status, ST_LIST_OVER);
+                            }
+                        }
+                        __syncthreads();
+                        BS_PROBE(7)
+                        const u32 nhuge = min(s_nhuge, (u32)BS_HUGEMAX);
+                        for (u32 q = 0; q < nhuge; ++q) {
+                            const u32 g = s_huge[q];
+                            const u32 gs = g ? S.cnt[g - 1] : 0u, len = S.cnt[g] - gs;
+                            u32 N = 1;
+                            while (N < len) N <<= 1;
+                            auto cx = [&](u32 x, u32 y) {
+                                const u32 px = sw16(gs + x + al), py = sw16(gs + y + al);
+                                const u32 u = kb[px], v = kb[py];
+                                if (v < u) { kb[px] = v; kb[py] = u; }
+                            };
+                            for (u32 kk = 2; kk <= N; kk <<= 1) {
+                                const u32 hk = kk >> 1;
+                                for (u32 t = threadIdx.x; t < N / 2; t += BS_NT) {
+                                    const u32 blk = t / hk, off = t % hk;
+                                    const u32 x = blk * kk + off, y = blk * kk + kk - 1 - off;
+                                    if (y < len) cx(x, y);
+                                }
+                                __syncthreads();
+                                for (u32 j = kk >> 2; j > 0; j >>= 1) {
+                                    for (u32 t = threadIdx.x; t < N / 2; t += BS_NT) {
+                                        const u32 x = (t / j) * 2 * j + (t % j), y = x + j;
+                                        if (y < len) cx(x, y);
+                                    }
+                                    __syncthreads();
+                                }
                             }
                         }
                     }
-                }
-                __syncthreads();
-                BS_PROBE(6)
-                // 3b. listed groups of 9..16: one thread each (63-comparator network)
-                const u32 nlisted = min(s_nbig, (u32)BS_BIGMAX);
-                const bool rescan = s_over != 0;  // list overflow (pathological skew): scan all groups
-                const u32 nwork = rescan ? ng : nlisted;
-                for (u32 q = threadIdx.x; q < nwork; q += BS_NT) {
-                    const u32 g = rescan ? q : s_big[q];
-                    const u32 gs = g ? Sa.cnt[g - 1] : 0u, len = Sa.cnt[g] - gs;
-                    if (len <= 8 || len > 16) continue;
-                    E a[16];
-    #pragma unroll
-                    for (u32 t = 0; t < 16; ++t) a[t] = t < len ? sm_get<U, KV>(Sa, gs + t) : E::inf();
-                    network16(a);
-    #pragma unroll
-                    for (u32 t = 0; t < 16; ++t)
-                        if (t < len) sm_put<U, KV>(Sa, gs + t, a[t]);
-                }
-                // 3c'. groups of 17..512: one warp each (register bitonic); over 512: the CTA
-                for (u32 q = wid; q < nwork; q += BS_NT / 32) {
-                    const u32 g = rescan ? q : s_big[q];
-                    const u32 gs = g ? Sa.cnt[g - 1] : 0u, len = Sa.cnt[g] - gs;
-                    if (len <= 16) continue;
-                    if (len <= 32) warp_sort_group<U, KV, 1>(Sa, gs, len);
-                    else if (len <= 64) warp_sort_group<U, KV, 2>(Sa, gs, len);
-                    else if (len <= 128) warp_sort_group<U, KV, 4>(Sa, gs, len);
-                    else if (len <= 256) warp_sort_group<U, KV, 8>(Sa, gs, len);
-                    else if (len <= 512 && BS_WARPMAX >= 512) warp_sort_group<U, KV, BS_WARPMAX / 32>(Sa, gs, len);
-                    else if (lane == 0) {
-                        const u32 h = atomicAdd(&s_nhuge, 1u);
-                        if (h < BS_HUGEMAX) s_huge[h] = g;
-                        else st_set(status, ST_LIST_OVER);
-                    }
-                }
-                __syncthreads();
-                BS_PROBE(7)
-                // 3c. groups over BS_WARPMAX: in-place bitonic network in shared memory, all comparators
-                // ascending (the first step of each merge compares i with its mirror), so virtual
-                // +inf padding beyond len never moves and len need not be a power of two
-                const u32 nhuge = min(s_nhuge, (u32)BS_HUGEMAX);
-                for (u32 q = 0; q < nhuge; ++q) {
-                    const u32 g = s_huge[q];
-                    const u32 gs = g ? Sa.cnt[g - 1] : 0u, len = Sa.cnt[g] - gs;
-                    u32 N = 1;
-                    while (N < len) N <<= 1;
-                    for (u32 kk = 2; kk <= N; kk <<= 1) {
-                        const u32 hk = kk >> 1;
-                        for (u32 t = threadIdx.x; t < N / 2; t += BS_NT) {
-                            const u32 blk = t / hk, off = t % hk;
-                            const u32 x = blk * kk + off, y = blk * kk + kk - 1 - off;
-                            if (y < len) smem_cex<U, KV>(Sa, gs + x, gs + y);
+                    __syncthreads();
+                    BS_PROBE(8)
+                    // 4. write the sorted bucket: swizzled 16-byte shared loads, 16-byte global stores
+                    {
+                        U* out = okeys + bk.beg;
+                        const u32 head = al ? min(m, 4u - al) : 0u;
+                        auto R = [&](u32 x) -> u32 { return out_raw ? (u32)Codec<DT>::raw((U)x) : x; };
+                        if (threadIdx.x < head) out[threadIdx.x] = (U)R(kb[sw16(threadIdx.x + al)]);
+                        const u32 nv = (m - head) / 4;
+                        uint4* o4 = (uint4*)(out + head);
+                        const uint4* k4 = (const uint4*)kb;
+                        const u32 c0 = (head + al) >> 2;
+                        for (u32 v = threadIdx.x; v < nv; v += BS_NT) {
+                            const u32 c = c0 + v;
+                            uint4 r = k4[c ^ ((c >> 2) & 7u)];
+                            r.x = R(r.x); r.y = R(r.y); r.z = R(r.z); r.w = R(r.w);
+                            o4[v] = r;
                         }
-                        __syncthreads();
-                        for (u32 j = kk >> 2; j > 0; j >>= 1) {
+                        for (u32 o = head + nv * 4 + threadIdx.x; o < m; o += BS_NT) out[o] = (U)R(kb[sw16(o + al)]);
+                    }
+                } else {
+                    // 2. scatter into shared memory by digit; afterwards cnt[g] = end of group g
+                    for_items<U, BS_NT, OVS_BS_UNR>(src, bk.beg, m, [&](U kr, u32 o) {
+                        const U k = K(kr);
+                        u32 ix = 0, vv = 0;
+                        if (KV) { ix = IX(bk.beg + o); vv = vsrc[bk.beg + o]; }
+                        const u32 pos = atomicAdd(&Sa.cnt[digit(k, ix)], 1u);
+                        Sa.k[pos] = k;
+                        if (KV) { Sa.i[pos] = ix; Sa.v[pos] = vv; }
+                    });
+                    __syncthreads();
+                    BS_PROBE(5)
+                    // 3. one thread per group of <= 8: Batcher network in registers; larger groups are
+                    // appended (warp-aggregated) to a list for 3b
+                    // (OVS_NET8_X: groups per thread per iteration, their loads and networks interleaved)
+                    for (u32 g0 = 0; need_sort && g0 < ng; g0 += BS_NT * OVS_NET8_X) {
+                        u32 gs[OVS_NET8_X], len[OVS_NET8_X];
+                        E a[OVS_NET8_X][8];
+        #pragma unroll
+                        for (int x = 0; x < OVS_NET8_X; ++x) {
+                            const u32 g = g0 + x * BS_NT + threadIdx.x;
+                            gs[x] = 0; len[x] = 0;
+                            if (g < ng) { gs[x] = g ? Sa.cnt[g - 1] : 0u; len[x] = Sa.cnt[g] - gs[x]; }
+                        }
+        #pragma unroll
+                        for (int x = 0; x < OVS_NET8_X; ++x) {
+                            const u32 lx = (len[x] > 1 && len[x] <= 8) ? len[x] : 0u;
+        #pragma unroll
+                            for (u32 q = 0; q < 8; ++q) a[x][q] = q < lx ? sm_get<U, KV>(Sa, gs[x] + q) : E::inf();
+                        }
+        #pragma unroll
+                        for (int x = 0; x < OVS_NET8_X; ++x) network8(a[x]);
+        #pragma unroll
+                        for (int x = 0; x < OVS_NET8_X; ++x) {
+                            const u32 lx = (len[x] > 1 && len[x] <= 8) ? len[x] : 0u;
+        #pragma unroll
+                            for (u32 q = 0; q < 8; ++q)
+                                if (q < lx) sm_put<U, KV>(Sa, gs[x] + q, a[x][q]);
+                        }
+        #pragma unroll
+                        for (int x = 0; x < OVS_NET8_X; ++x) {
+                            const u32 g = g0 + x * BS_NT + threadIdx.x;
+                            const u32 mb = __ballot_sync(0xffffffffu, len[x] > 8);
+                            if (mb) {
+                                u32 base = 0;
+                                if (lane == 0) base = atomicAdd(&s_nbig, __popc(mb));
+                                base = __shfl_sync(0xffffffffu, base, 0) + __popc(mb & ((1u << lane) - 1));
+                                if (len[x] > 8) {
+                                    if (base < BS_BIGMAX) s_big[base] = g;
+                                    else atomicOr(&s_over, 1u);
+                                }
+                            }
+                        }
+                    }
+                    __syncthreads();
+                    BS_PROBE(6)
+                    // 3b. listed groups of 9..16: one thread each (63-comparator network)
+                    const u32 nlisted = min(s_nbig, (u32)BS_BIGMAX);
+                    const bool rescan = s_over != 0;  // list overflow (pathological skew): scan all groups
+                    const u32 nwork = rescan ? ng : nlisted;
+                    for (u32 q = threadIdx.x; q < nwork; q += BS_NT) {
+                        const u32 g = rescan ? q : s_big[q];
+                        const u32 gs = g ? Sa.cnt[g - 1] : 0u, len = Sa.cnt[g] - gs;
+                        if (len <= 8 || len > 16) continue;
+                        E a[16];
+        #pragma unroll
+                        for (u32 t = 0; t < 16; ++t) a[t] = t < len ? sm_get<U, KV>(Sa, gs + t) : E::inf();
+                        network16(a);
+        #pragma unroll
+                        for (u32 t = 0; t < 16; ++t)
+                            if (t < len) sm_put<U, KV>(Sa, gs + t, a[t]);
+                    }
+                    // 3c'. groups of 17..512: one warp each (register bitonic); over 512: the CTA
+                    for (u32 q = wid; q < nwork; q += BS_NT / 32) {
+                        const u32 g = rescan ? q : s_big[q];
+                        const u32 gs = g ? Sa.cnt[g - 1] : 0u, len = Sa.cnt[g] - gs;
+                        if (len <= 16) continue;
+                        if (len <= 32) warp_sort_group<U, KV, 1>(Sa, gs, len);
+                        else if (len <= 64) warp_sort_group<U, KV, 2>(Sa, gs, len);
+                        else if (len <= 128) warp_sort_group<U, KV, 4>(Sa, gs, len);
+                        else if (len <= 256) warp_sort_group<U, KV, 8>(Sa, gs, len);
+                        else if (len <= 512 && BS_WARPMAX >= 512) warp_sort_group<U, KV, BS_WARPMAX / 32>(Sa, gs, len);
+                        else if (lane == 0) {
+                            const u32 h = atomicAdd(&s_nhuge, 1u);
+                            if (h < BS_HUGEMAX) s_huge[h] = g;
+                            else st_set(status, ST_LIST_OVER);
+                        }
+                    }
+                    __syncthreads();
+                    BS_PROBE(7)
+                    // 3c. groups over BS_WARPMAX: in-place bitonic network in shared memory, all comparators
+                    // ascending (the first step of each merge compares i with its mirror), so virtual
+                    // +inf padding beyond len never moves and len need not be a power of two
+                    const u32 nhuge = min(s_nhuge, (u32)BS_HUGEMAX);
+                    for (u32 q = 0; q < nhuge; ++q) {
+                        const u32 g = s_huge[q];
+                        const u32 gs = g ? Sa.cnt[g - 1] : 0u, len = Sa.cnt[g] - gs;
+                        u32 N = 1;
+                        while (N < len) N <<= 1;
+                        for (u32 kk = 2; kk <= N; kk <<= 1) {
+                            const u32 hk = kk >> 1;
                             for (u32 t = threadIdx.x; t < N / 2; t += BS_NT) {
-                                const u32 x = (t / j) * 2 * j + (t % j), y = x + j;
+                                const u32 blk = t / hk, off = t % hk;
+                                const u32 x = blk * kk + off, y = blk * kk + kk - 1 - off;
                                 if (y < len) smem_cex<U, KV>(Sa, gs + x, gs + y);
                             }
                             __syncthreads();
+                            for (u32 j = kk >> 2; j > 0; j >>= 1) {
+                                for (u32 t = threadIdx.x; t < N / 2; t += BS_NT) {
+                                    const u32 x = (t / j) * 2 * j + (t % j), y = x + j;
+                                    if (y < len) smem_cex<U, KV>(Sa, gs + x, gs + y);
+                                }
+                                __syncthreads();
+                            }
                         }
                     }
-                }
-                __syncthreads();
-                BS_PROBE(8)
-                // 4. write the sorted bucket (16-byte stores where the output is aligned)
-                {
-                    constexpr u32 V = 16 / sizeof(U);
-                    U* out = okeys + bk.beg;
-                    const u32 mis = (u32)(((uintptr_t)out) & 15u) / (u32)sizeof(U);
-                    const u32 head = mis ? min(m, V - mis) : 0u;
-                    auto R = [&](U x) -> U { return out_raw ? Codec<DT>::raw(x) : x; };
-                    if (threadIdx.x < head) out[threadIdx.x] = R(Sa.k[threadIdx.x]);
-                    const u32 nv = (m - head) / V;
-                    uint4* o4 = (uint4*)(out + head);
-                    const uint4* s4 = (const uint4*)(Sa.k + head);
-                    for (u32 v = threadIdx.x; v < nv; v += BS_NT) {
-                        uint4 r = s4[v];
-                        U* e = (U*)&r;
-    #pragma unroll
-                        for (u32 q = 0; q < V; ++q) e[q] = R(e[q]);
-                        o4[v] = r;
-                    }
-                    for (u32 o = head + nv * V + threadIdx.x; o < m; o += BS_NT) out[o] = R(Sa.k[o]);
-                    if (KV) {
-                        for (u32 o = threadIdx.x; o < m; o += BS_NT) ovals[bk.beg + o] = Sa.v[o];
-                        if (oidx)
-                            for (u32 o = threadIdx.x; o < m; o += BS_NT) oidx[bk.beg + o] = Sa.i[o];
+                    __syncthreads();
+                    BS_PROBE(8)
+                    // 4. write the sorted bucket (16-byte stores where the output is aligned)
+                    {
+                        constexpr u32 V = 16 / sizeof(U);
+                        U* out = okeys + bk.beg;
+                        const u32 mis = (u32)(((uintptr_t)out) & 15u) / (u32)sizeof(U);
+                        const u32 head = mis ? min(m, V - mis) : 0u;
+                        auto R = [&](U x) -> U { return out_raw ? Codec<DT>::raw(x) : x; };
+                        if (threadIdx.x < head) out[threadIdx.x] = R(Sa.k[threadIdx.x]);
+                        const u32 nv = (m - head) / V;
+                        uint4* o4 = (uint4*)(out + head);
+                        const uint4* s4 = (const uint4*)(Sa.k + head);
+                        for (u32 v = threadIdx.x; v < nv; v += BS_NT) {
+                            uint4 r = s4[v];
+                            U* e = (U*)&r;
+        #pragma unroll
+                            for (u32 q = 0; q < V; ++q) e[q] = R(e[q]);
+                            o4[v] = r;
+                        }
+                        for (u32 o = head + nv * V + threadIdx.x; o < m; o += BS_NT) out[o] = R(Sa.k[o]);
+                        if (KV) {
+                            for (u32 o = threadIdx.x; o < m; o += BS_NT) ovals[bk.beg + o] = Sa.v[o];
+                            if (oidx)
+                                for (u32 o = threadIdx.x; o < m; o += BS_NT) oidx[bk.beg + o] = Sa.i[o];
+                        }
                     }
                 }
                 __syncthreads();

@@ -31,6 +31,9 @@ typedef uint16_t u16;
 #ifndef OVS_PDL
 #define OVS_PDL 0
 #endif
+#ifndef OVS_WC_BFLUSH  // write-combining scatter: completed sectors flushed per bucket (0: per key)
+#define OVS_WC_BFLUSH 1
+#endif
 #define PDL_PROLOGUE() asm volatile("griddepcontrol.launch_dependents;\n\tgriddepcontrol.wait;" ::: "memory")
 
 // ------------------------------------------------------------------ key codecs
@@ -1413,6 +1416,73 @@ __global__ void __launch_bounds__(NT, 1) k_scatter_wc(Bufs<typename Codec<DT>::U
                 for (u32 j = 0; j < ITEMS; ++j)
                     if (((j / V) * NT + threadIdx.x) * V + (j % V) < nt) vmask |= 1u << j;
             }
+#if OVS_WC_BFLUSH
+            // P1: a position per key; keys inside their bucket's current sector are parked in it,
+            // the others (rare: a bucket whose sector fills up within this sub-tile) are marked
+            u32 pos[ITEMS], sv[ITEMS], out = 0;
+#pragma unroll
+            for (u32 j = 0; j < ITEMS; ++j) {
+                const u32 b = (id[j / 2] >> (16 * (j & 1))) & 0xffffu;
+                if (LEVEL0) k[j] = Codec<DT>::ord(k[j]);
+                if (vmask & (1u << j)) pos[j] = atomicAdd(&q[b], 1u);
+            }
+#pragma unroll
+            for (u32 j = 0; j < ITEMS; ++j) sv[j] = sb[(id[j / 2] >> (16 * (j & 1))) & 0xffffu];
+#pragma unroll
+            for (u32 j = 0; j < ITEMS; ++j) {
+                const u32 b = (id[j / 2] >> (16 * (j & 1))) & 0xffffu;
+                const u32 d = pos[j] - (sv[j] & ~(SV - 1));
+                if (vmask & (1u << j)) {
+                    if (d < SV) wc[(size_t)b * SV + d] = k[j];
+                    else out |= 1u << j;
+                }
+            }
+            __syncthreads();
+            // P2: every bucket whose current sector is complete is flushed by the thread that owns
+            // the bucket (one check per bucket instead of per key); keys of complete sectors past it
+            // go straight out, keys of the new incomplete sector wait for P3
+            for (u32 b = threadIdx.x; b < P; b += NT) {
+                const u32 qe = q[b], sv0 = sb[b], s0 = sv0 & ~(SV - 1);
+                if (qe >= s0 + SV) {
+                    const u32 front = sv0 & (SV - 1);
+                    const U* wb = wc + (size_t)b * SV;
+                    U* const db = dst_of(b);
+                    if (front == 0) {
+                        const uint4* w4 = (const uint4*)wb;
+                        uint4* g4 = (uint4*)(db + s0);
+                        g4[0] = w4[0];
+                        g4[1] = w4[1];
+                    } else {
+                        for (u32 x = front; x < SV; ++x) db[s0 + x] = wb[x];
+                    }
+                    sb[b] = qe & ~(SV - 1);
+                }
+            }
+            u32 tail = 0;
+            if (__any_sync(0xffffffffu, out != 0)) {
+#pragma unroll
+                for (u32 j = 0; j < ITEMS; ++j) {
+                    if (out & (1u << j)) {
+                        const u32 b = (id[j / 2] >> (16 * (j & 1))) & 0xffffu;
+                        const u32 qf = q[b];
+                        if (pos[j] < (qf & ~(SV - 1))) dst_of(b)[pos[j]] = k[j];
+                        else tail |= 1u << j;
+                    }
+                }
+            }
+            __syncthreads();
+            // P3: keys of the new incomplete sector
+            if (__any_sync(0xffffffffu, tail != 0)) {
+#pragma unroll
+                for (u32 j = 0; j < ITEMS; ++j) {
+                    if (tail & (1u << j)) {
+                        const u32 b = (id[j / 2] >> (16 * (j & 1))) & 0xffffu;
+                        wc[(size_t)b * SV + (pos[j] & (SV - 1))] = k[j];
+                    }
+                }
+            }
+        }
+#else
             // P1: a position and the current sector per key; park it there if it is inside
             // (separate passes over the ITEMS keys: all atomics, then all sector loads, then the
             // stores, so ITEMS independent shared accesses are in flight instead of one chain)
@@ -1472,6 +1542,7 @@ __global__ void __launch_bounds__(NT, 1) k_scatter_wc(Bufs<typename Codec<DT>::U
                 }
             }
         }
+#endif
         __syncthreads();
         // the chunk's last, incomplete sectors (and runs inside one sector)
         for (u32 b = threadIdx.x; b < P; b += NT) {
@@ -1694,6 +1765,12 @@ __global__ void __launch_bounds__(1024) k_internal_sample(Bufs<typename Codec<DT
 #define OVS_BS_NT 512
 #endif
 constexpr int BS_NT = OVS_BS_NT;
+#ifndef OVS_BS_PF2  // prefetch two buckets ahead into L2
+#define OVS_BS_PF2 0
+#endif
+#ifndef OVS_BS_STCS  // streaming (evict-first) stores of the sorted output
+#define OVS_BS_STCS 0
+#endif
 #ifndef OVS_BS_WIN16  // 32-bit keys only: swizzled items + 16-key window networks (0: round-1 path)
 #define OVS_BS_WIN16 1
 #endif
@@ -1988,8 +2065,9 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
     // so no global round trip sits between two buckets.  The claimed bucket is kept in shared
     // memory; only resplit children go through the CTA's stack in global memory.
     __shared__ Bucket s_cur, s_nxt;
-    __shared__ u32 s_base;
+    __shared__ u32 s_base, s_first;
     if (threadIdx.x == 0) {
+        s_first = 1;
         s_work = atomicAdd(ticket, 1u);
         if (s_work < nl) s_cur = list[s_work];
         s_next = atomicAdd(ticket, 1u);
@@ -2000,15 +2078,18 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
         if (s_work >= nl) break;
         u32 t3 = 0xffffffffu;  // thread 0: the claim after the next one (consumed at the end)
         if (threadIdx.x == 0) {
-            if (s_next < nl) {
-                // the next bucket's keys into L2 with one bulk prefetch (16-byte aligned cover)
-                const Bucket nx = s_nxt;
+            // bucket keys into L2 with one bulk prefetch (16-byte aligned cover)
+            auto prefetch = [&](const Bucket& nx) {
                 const uintptr_t a0 = (uintptr_t)(B.k[nx.buf] + nx.beg) & ~(uintptr_t)15;
                 const uintptr_t a1 = ((uintptr_t)(B.k[nx.buf] + nx.beg + nx.len) + 15) & ~(uintptr_t)15;
                 if (a1 > a0)
                     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((u32)(a1 - a0)) : "memory");
-            }
+            };
+            // the next bucket (OVS_BS_PF2: already prefetched one bucket earlier, except the first)
+            if (s_next < nl && (!OVS_BS_PF2 || s_first)) prefetch(s_nxt);
             t3 = atomicAdd(ticket, 1u);
+            if (OVS_BS_PF2 && t3 < nl) prefetch(list[t3]);  // the bucket after it
+            s_first = 0;
             s_sp = 0;
             s_base = 1;
         }
@@ -2406,7 +2487,8 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                             const u32 c = c0 + v;
                             uint4 r = k4[c ^ ((c >> 2) & 7u)];
                             r.x = R(r.x); r.y = R(r.y); r.z = R(r.z); r.w = R(r.w);
-                            o4[v] = r;
+                            if (OVS_BS_STCS) __stcs(o4 + v, r);  // evict-first: keep the prefetched buckets in L2
+                            else o4[v] = r;
                         }
                         for (u32 o = head + nv * 4 + threadIdx.x; o < m; o += BS_NT) out[o] = (U)R(kb[sw16(o + al)]);
                     }

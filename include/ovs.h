@@ -59,6 +59,10 @@ typedef enum { OVS_ROS = 0, OVS_DRO = 1 } ovs_method;
 /* flags */
 #define OVS_DRO_PADDED_POSITIONS 1u /* DRO sample positions of the Lemma 1 proof's padding
                                         instead of balanced segments (Q9)   */
+#define OVS_DRO_MERGE 2u            /* DRO step 5 as the paper's p-way merge (Alg. 1 step 5,
+                                       PAPER.md:273-275): fine split by the regular sample, the
+                                       p sorted runs of every fine bucket merged on chip; the
+                                       default re-sorts every bucket (same output, see DESIGN) */
 
 typedef struct {
     uint32_t method; /* OVS_ROS or OVS_DRO                                                      */

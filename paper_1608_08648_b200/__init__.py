@@ -13,12 +13,13 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libovs.so")
+LIB_PATH = os.environ.get("OVS_LIB_PATH") or os.path.join(_HERE, "libovs.so")  # override: A/B experiments
 
 OVS_OK, OVS_EINVAL, OVS_EDTYPE, OVS_ESAMPLE, OVS_EWORKSPACE, OVS_ECUDA, OVS_ECAPACITY, OVS_EINTERNAL = 0, 1, 2, 3, 4, 5, 7, 8
 OVS_U32, OVS_I32, OVS_F64 = 0, 1, 2
 OVS_ROS, OVS_DRO = 0, 1
 OVS_DRO_PADDED_POSITIONS = 1
+OVS_DRO_MERGE = 2
 METHODS = {"ros": OVS_ROS, "dro": OVS_DRO}
 
 
@@ -101,8 +102,10 @@ def _dtype_code(dt) -> int:
     return m[dt]
 
 
-def params(method: str = "ros", p: int = 64, s: int = 32, seed: int = 1, padded: bool = False) -> Params:
-    return Params(METHODS[method], p, s, OVS_DRO_PADDED_POSITIONS if padded else 0, seed)
+def params(method: str = "ros", p: int = 64, s: int = 32, seed: int = 1, padded: bool = False,
+           merge: bool = False) -> Params:
+    flags = (OVS_DRO_PADDED_POSITIONS if padded else 0) | (OVS_DRO_MERGE if merge else 0)
+    return Params(METHODS[method], p, s, flags, seed)
 
 
 def auto_params(n: int, dtype, with_values: bool = False, method: str = "ros") -> Params:
@@ -134,9 +137,9 @@ class Sorter:
     """Holds a workspace tensor sized for (n, dtype, kv, params) and sorts tensors in place."""
 
     def __init__(self, n: int, dtype, with_values: bool = False, method: str = "ros", p: int = 64, s: int = 32,
-                 seed: int = 1, padded: bool = False, device=None):
+                 seed: int = 1, padded: bool = False, device=None, merge: bool = False):
         import torch
-        self.prm = params(method, p, s, seed, padded)
+        self.prm = params(method, p, s, seed, padded, merge)
         self.dt = _dtype_code(dtype)
         self.kv = with_values
         self.n = n

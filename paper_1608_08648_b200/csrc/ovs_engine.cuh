@@ -712,7 +712,7 @@ inline int validate_impl(size_t n, int dtype, const ovs_params* prm) {
     // to 7 slots): n + 32 must stay below 2^32
     if (n >= 0xffffffffull - 32) return OVS_EINVAL;
     if (prm->method != OVS_ROS && prm->method != OVS_DRO) return OVS_EINVAL;
-    if (prm->flags & ~OVS_DRO_PADDED_POSITIONS) return OVS_EINVAL;
+    if (prm->flags & ~(OVS_DRO_PADDED_POSITIONS | OVS_DRO_MERGE)) return OVS_EINVAL;
     if (n == 0 || prm->p == 1) return OVS_OK;
     if (prm->method == OVS_ROS) {
         if (prm->s == 0) return OVS_ESAMPLE;
@@ -764,9 +764,15 @@ template <int DT, bool KV> struct DroSort {
     bool big = false;
     Level1<DT, KV>* l1x = nullptr;
     typename Engine<DT, KV>::Lists lb;
+    // f2 (OVS_DRO_MERGE): step 5 as an on-chip p-way merge over P = p*f fine buckets
+    bool merge = false;  // OVS_DRO_MERGE flag (include/ovs.h)
+    u32 f = 1, P = 0, mcap = 0;
+    U* fsk = nullptr; u32* fst = nullptr; u64* fcounts = nullptr;
+    typename Engine<DT, KV>::Lists lfine, lbig;
 
     DroSort(Ctx& ctx, U* keys, u32* vals, u32 n_, u32 p_, u32 r_, u32 flags_)
         : c(ctx), e(ctx), n(n_), p(p_), r(r_), flags(flags_) {
+        merge = (flags & OVS_DRO_MERGE) != 0;
         e.n = n;
         e.ixbits = bits_for(n);
         e.cap = bucket_cap<U, KV>(c.di);
@@ -791,9 +797,29 @@ template <int DT, bool KV> struct DroSort {
             t_tag = c.take<u32>(ns);
             ts64 = new InternalSort<true>(c, ns, t_key, t_tag);
         }
-        bound = c.take<u32>((size_t)p * (p + 1));
-        cnt = c.take<u32>((size_t)p * p);
-        tot = c.take<u32>(p + 1);
+        if (merge) {
+            // merge capacity (items in shared memory, two buffers) and the refinement f: the
+            // smallest power of two whose worst-case fine bucket fits it, by the tight count of the
+            // Lemma 1 proof (reading Q10): ceil(s/f) sample segments of x keys plus x - 1 keys of
+            // every other sequence, x = ceil(ceil(n/p)/s)
+            const size_t item = merge_item_bytes<U, KV>();
+            const size_t fixed = merge_smem_bytes<U, KV>(0, p) + 2 * 16;
+            mcap = (u32)(((size_t)c.di.smem_optin - 1024 - fixed) / (2 * item)) & ~15u;
+            const u64 x = ((n + p - 1) / p + s - 1) / s;
+            auto worst = [&](u64 ff) { return ((s + ff - 1) / ff) * x + (u64)(p - 1) * (x > 0 ? x - 1 : 0); };
+            while (2 * f <= s && f < 4096 && worst(f) > mcap) f *= 2;  // f <= s: every fine splitter is a sample
+            P = p * f;
+            fsk = c.take<U>(P);
+            fst = c.take<u32>(P);
+            fcounts = c.take<u64>(P);
+            e.carve_lists(lfine, P);
+            e.carve_lists(lbig, P);
+        } else {
+            P = p;
+        }
+        bound = c.take<u32>((size_t)p * (P + 1));
+        cnt = c.take<u32>((size_t)p * P);
+        tot = c.take<u32>(P + 1);
         seg = c.take<Seg>(1);
         nseg = c.take<u32>(2);
         e.carve_lists(l1, p);
@@ -805,6 +831,40 @@ template <int DT, bool KV> struct DroSort {
         }
     }
     ~DroSort() { delete ts32; delete ts64; delete l1x; }
+
+    // f2: a13 against the P - 1 fine splitters, then a14 as an on-chip p-way merge per fine
+    // bucket (k_dro_merge); fine buckets over the merge capacity: gather + bucket sorter
+    void run_merge() {
+        Bufs<U>& B = e.B;
+        launch(c, k_dro_bounds<U>, cdiv((u64)p * (P + 1), 256), 256, 0, B.k[1], n, p, P, (const U*)fsk, (const u32*)fst,
+               bound);
+        c.check();
+        launch(c, k_dro_counts, cdiv((u64)p * P, 256), 256, 0, (const u32*)bound, p, P, cnt);
+        c.check();
+        launch(c, k_dro_seg<U>, 1, 1024, 0, B.k[1], n, p, P, (const U*)fsk, 0u, seg, nseg);
+        c.check();
+        launch(c, k_colscan, std::min<u32>(cdiv(P, 32), 4 * c.di.sms), 1024, 0, cnt, seg, nseg, P, tot);
+        c.check();
+        fill_u32(c, lfine.nfit, 0, 2);
+        fill_u32(c, lbig.nfit, 0, 2);
+        launch(c, k_segscan<U>, 1, 1024, 0, seg, nseg, P, tot, (const U*)fsk, 0u, mcap, lfine.fit, lfine.nfit,
+               lfine.fit_cap, lbig.fit, lbig.nfit, lbig.fit_cap, fcounts, c.status);
+        c.check();
+        launch(c, k_fold_counts, cdiv(p, 256), 256, 0, (const u64*)fcounts, f, p, counts);
+        c.check();
+        c.mark(3);
+        const size_t sm = merge_smem_bytes<U, KV>(mcap, p);
+        smem_limit(k_dro_merge<DT, KV>, sm, c.di);
+        launch(c, k_dro_merge<DT, KV>, (u32)c.di.sms, MG_NT, sm, B, n, p, P, (const u32*)bound, (const u32*)cnt,
+               (const u32*)tot, mcap);
+        c.check();
+        // fine buckets over the merge capacity (rare): gathered into place, then the bucket sorter
+        launch(c, k_dro_gather_big<U, KV>, 4 * (u32)c.di.sms, 256, 0, B, n, p, P, (const u32*)bound, (const u32*)cnt,
+               (const u32*)tot, (const Bucket*)lbig.fit, (const u32*)lbig.nfit);
+        c.check();
+        c.mark(4);
+        e.bucket_sort(lbig, 0x5e9u);
+    }
     // sort the buckets of list l (all far over capacity) through level 1
     void sort_big(typename Engine<DT, KV>::Lists& l, u64 seed, U* okeys, u32* ovals, u32* oidx, bool out_raw) {
         fill_u32(c, lb.nfit, 0, 2);
@@ -839,13 +899,22 @@ template <int DT, bool KV> struct DroSort {
         else ts64->run(0xd0d0);
         launch(c, k_pick_splitters<U>, cdiv(p, 256), 256, 0, t_pack, t_key, t_tag, p, s, 1u, sk, st);
         c.check();
+        if (merge) {
+            // fine splitters T[floor((i+1) s / f) - 1]: the contract's S[q] is fine splitter (q+1)f - 1
+            launch(c, k_pick_splitters<U>, cdiv(P, 256), 256, 0, t_pack, t_key, t_tag, P, s, f, fsk, fst);
+            c.check();
+            c.mark(2);
+            run_merge();
+            c.mark(5);
+            return;
+        }
         c.mark(2);
         // a13: split every sorted sequence by binary search; bucket starts and run offsets
-        launch(c, k_dro_bounds<U>, cdiv((u64)p * (p + 1), 256), 256, 0, B.k[1], n, p, sk, st, bound);
+        launch(c, k_dro_bounds<U>, cdiv((u64)p * (p + 1), 256), 256, 0, B.k[1], n, p, p, sk, st, bound);
         c.check();
-        launch(c, k_dro_counts, cdiv((u64)p * p, 256), 256, 0, bound, p, cnt);
+        launch(c, k_dro_counts, cdiv((u64)p * p, 256), 256, 0, bound, p, p, cnt);
         c.check();
-        launch(c, k_dro_seg<U>, 1, 1024, 0, B.k[1], n, p, sk, 0, seg, nseg);
+        launch(c, k_dro_seg<U>, 1, 1024, 0, B.k[1], n, p, p, sk, 0, seg, nseg);
         c.check();
         launch(c, k_colscan, std::min<u32>(cdiv(p, 32), 4 * c.di.sms), 1024, 0, cnt, seg, nseg, p, tot);
         c.check();

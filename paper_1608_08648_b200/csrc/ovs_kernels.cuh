@@ -2965,17 +2965,18 @@ __global__ void k_dro_sample(const U* xs, u32 n, u32 p, u32 s, u32 padded, u64* 
 
 // a13: bound[k][j+1] = #{t : (X_k[t], start_k + t) <=lex S[j]} by binary search of splitter j
 // into the sorted X_k; count matrix cnt[k][j] = bound[k][j+1]-bound[k][j]
+// (P buckets: P - 1 splitters; P = p for the contract split, p*f for the fine split of f2)
 template <class U>
-__global__ void k_dro_bounds(const U* xs, u32 n, u32 p, const U* sk, const u32* st, u32* bound) {
+__global__ void k_dro_bounds(const U* xs, u32 n, u32 p, u32 P, const U* sk, const u32* st, u32* bound) {
     PDL_PROLOGUE();
     const u64 id = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-    if (id >= (u64)p * (p + 1)) return;
-    const u32 k = (u32)(id / (p + 1)), j = (u32)(id % (p + 1));
+    if (id >= (u64)p * (P + 1)) return;
+    const u32 k = (u32)(id / (P + 1)), j = (u32)(id % (P + 1));
     const u32 q = n / p, rm = n % p;
     const u32 beg = k * q + min(k, rm), m = q + (k < rm ? 1u : 0u);
     u32 r;
     if (j == 0) r = 0;
-    else if (j == p) r = m;
+    else if (j == P) r = m;
     else {
         const U key = sk[j - 1];
         const u32 tag = st[j - 1];
@@ -2992,18 +2993,18 @@ __global__ void k_dro_bounds(const U* xs, u32 n, u32 p, const U* sk, const u32* 
     bound[id] = r;
 }
 
-__global__ void k_dro_counts(const u32* bound, u32 p, u32* cnt) {
+__global__ void k_dro_counts(const u32* bound, u32 p, u32 P, u32* cnt) {
     PDL_PROLOGUE();
     const u64 id = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-    if (id >= (u64)p * p) return;
-    const u32 k = (u32)(id / p), j = (u32)(id % p);
-    cnt[id] = bound[(u64)k * (p + 1) + j + 1] - bound[(u64)k * (p + 1) + j];
+    if (id >= (u64)p * P) return;
+    const u32 k = (u32)(id / P), j = (u32)(id % P);
+    cnt[id] = bound[(u64)k * (P + 1) + j + 1] - bound[(u64)k * (P + 1) + j];
 }
 
 // the single "segment" of the DRO split: p chunks (the sequences) x p buckets; key bounds of
 // the whole input from the sorted sequences' first and last keys
 template <class U>
-__global__ void k_dro_seg(const U* xs, u32 n, u32 p, const U* sk, u32 L, Seg* seg, u32* nseg) {
+__global__ void k_dro_seg(const U* xs, u32 n, u32 p, u32 P, const U* sk, u32 L, Seg* seg, u32* nseg) {
     PDL_PROLOGUE();
     __shared__ U smn[32], smx[32];
     const u32 q = n / p, rm = n % p;
@@ -3022,7 +3023,7 @@ __global__ void k_dro_seg(const U* xs, u32 n, u32 p, const U* sk, u32 L, Seg* se
         mn = min(mn, smn[0]); mx = max(mx, smx[0]);
         Seg g;
         g.lo = (u64)mn; g.hi = (u64)mx; g.base = 0;
-        g.beg = 0; g.len = n; g.P = p; g.shift = 0; g.L = L; g.chunk0 = 0; g.nchunk = p;
+        g.beg = 0; g.len = n; g.P = P; g.shift = 0; g.L = L; g.chunk0 = 0; g.nchunk = p;
         g.src = 1;  // buckets land in buffer 0
         g.loose = 0; g.pad = 0;
         *seg = g;
@@ -3046,6 +3047,138 @@ __global__ void k_dro_gather(Bufs<U> B, u32 n, u32 p, const u32* bound, const u3
     for (u32 t = a + lane; t < b; t += 32) {
         B.k[0][d + t - a] = B.k[1][beg + t];
         if (KV) { B.v[0][d + t - a] = B.v[1][beg + t]; B.i[0][d + t - a] = B.i[1][beg + t]; }
+    }
+}
+
+// ------------------------------------------------------------------ f2: a14 as a p-way merge
+// (Alg. 1 step 5: Y_j = the stable merge of the sorted runs X_{0,j} ..
+// X_{p-1,j}, ties to the lower k.)  The DRO split is refined with P = p*f fine splitters
+// taken from the same sorted regular sample (every rp/f-th record; every f-th one is a contract
+// splitter, so contract bucket q is fine buckets qf .. qf+f-1).  A fine bucket's p runs are
+// gathered in k order into shared memory straight from the sorted sequences (no copy pass) and
+// merged by a pairwise merge tree (log2 p levels; every thread merges E outputs after a
+// merge-path search on its diagonal, ties taken from the left run), then written once.  Fine
+// buckets over the on-chip capacity are listed and take the gather + bucket-sort route.
+constexpr int MG_NT = 512, MG_E = 8;
+template <class U, bool KV> __host__ __device__ constexpr size_t merge_item_bytes() { return sizeof(U) + (KV ? 4 : 0); }
+template <class U, bool KV> __host__ __device__ constexpr size_t merge_smem_bytes(u32 mcap, u32 p) {
+    return 2 * a16(merge_item_bytes<U, KV>() * (size_t)mcap) + a16(8 * ((size_t)p + 1)) + 64;
+}
+// fine bucket j' of P: runs k = 0..p-1 are X_k[bound[k][j'] .. bound[k][j'+1]) of the sorted
+// sequences (ordered keys in buffer 1), run offsets inside the bucket off[k*P + j'] (column scan),
+// bucket start tot[j'] (segment scan); output = buffer 0 (raw codec), values too
+template <int DT, bool KV>
+__global__ void __launch_bounds__(MG_NT, 1) k_dro_merge(Bufs<typename Codec<DT>::U> B, u32 n, u32 p, u32 P,
+                                                          const u32* bound, const u32* off, const u32* tot, u32 mcap) {
+    PDL_PROLOGUE();
+    typedef typename Codec<DT>::U U;
+    extern __shared__ __align__(16) char smem[];
+    U* ka = (U*)smem;
+    U* kb2 = (U*)(smem + a16(sizeof(U) * (size_t)mcap));
+    char* sp = smem + 2 * a16(sizeof(U) * (size_t)mcap);
+    u32* va = nullptr; u32* vb = nullptr;
+    if (KV) { va = (u32*)sp; sp += a16(4 * (size_t)mcap); vb = (u32*)sp; sp += a16(4 * (size_t)mcap); }
+    u32* R = (u32*)sp;  // run starts inside the bucket, R[p] = bucket length
+    u32* S = R + p + 1;  // run k's first item in the sorted sequences (buffer 1)
+    const u32 q = n / p, rm = n % p;
+    for (u32 j = blockIdx.x; j < P; j += gridDim.x) {
+        const u32 bs = tot[j], len = tot[j + 1] - bs;
+        if (len == 0 || len > mcap) continue;  // empty, or listed for the bucket sorter
+        for (u32 k = threadIdx.x; k < p; k += MG_NT) {
+            R[k] = off[(size_t)k * P + j];
+            S[k] = k * q + min(k, rm) + bound[(size_t)k * (P + 1) + j];
+        }
+        if (threadIdx.x == 0) R[p] = len;
+        __syncthreads();
+        // gather the runs (k order) straight from the sorted sequences: item e of the bucket is
+        // in run k = the last run starting at or before e (empty runs share a start; independent
+        // loads, many in flight)
+        for (u32 e = threadIdx.x; e < len; e += MG_NT) {
+            u32 lo = 0, cnt = p;
+            while (cnt > 1) {
+                const u32 half = cnt >> 1;
+                if (R[lo + half] <= e) { lo += half; cnt -= half; } else cnt = half;
+            }
+            const u32 src = S[lo] + (e - R[lo]);
+            ka[e] = B.k[1][src];
+            if (KV) va[e] = B.v[1][src];
+        }
+        __syncthreads();
+        U* sk = ka; U* dk = kb2;
+        u32* sv = va; u32* dv = vb;
+        for (u32 w = 1; w < p; w <<= 1) {
+            const u32 np = (p + 2 * w - 1) / (2 * w);  // pairs of sequences of w runs
+            for (u32 o0 = threadIdx.x * MG_E; o0 < len; o0 += MG_NT * MG_E) {
+                u32 o = o0;
+                const u32 oe = min(o0 + MG_E, len);
+                // pair holding output o: the last pair whose start R[2iw] <= o
+                u32 lo = 0, hi = np - 1;
+                while (lo < hi) {
+                    const u32 mid = (lo + hi + 1) >> 1;
+                    if (R[min(2 * mid * w, p)] <= o) lo = mid; else hi = mid - 1;
+                }
+                u32 pi = lo;
+                while (o < oe) {
+                    const u32 a0 = R[min(2 * pi * w, p)], a1 = R[min(2 * pi * w + w, p)], b1 = R[min(2 * pi * w + 2 * w, p)];
+                    const u32 la = a1 - a0, lb = b1 - a1, d = o - a0;
+                    // merge path: i outputs from the left run among the first d (ties: left first)
+                    u32 l2 = d > lb ? d - lb : 0u, h2 = min(d, la);
+                    while (l2 < h2) {
+                        const u32 mid = (l2 + h2) >> 1;
+                        if (sk[a0 + mid] <= sk[a1 + d - 1 - mid]) l2 = mid + 1; else h2 = mid;
+                    }
+                    u32 i = l2, jj = d - l2;
+                    const u32 stop = min(oe, b1);
+                    for (; o < stop; ++o) {
+                        const bool left = i < la && (jj >= lb || sk[a0 + i] <= sk[a1 + jj]);
+                        const u32 src = left ? a0 + i : a1 + jj;
+                        dk[o] = sk[src];
+                        if (KV) dv[o] = sv[src];
+                        if (left) ++i; else ++jj;
+                    }
+                    ++pi;
+                }
+            }
+            __syncthreads();
+            U* tk = sk; sk = dk; dk = tk;
+            u32* tv = sv; sv = dv; dv = tv;
+        }
+        // write the merged bucket (raw codec)
+        U* out = B.k[0] + bs;
+        for (u32 o = threadIdx.x; o < len; o += MG_NT) {
+            out[o] = Codec<DT>::raw(sk[o]);
+            if (KV) B.v[0][bs + o] = sv[o];
+        }
+        __syncthreads();
+    }
+}
+
+// fine buckets over the merge capacity (the segment scan's big list): gather their runs into
+// buffer 0 at the bucket position (keys, values, original indices) for the bucket sorter; the
+// fine bucket index is recovered from the bucket start (starts strictly increase)
+template <class U, bool KV>
+__global__ void k_dro_gather_big(Bufs<U> B, u32 n, u32 p, u32 P, const u32* bound, const u32* off, const u32* tot,
+                                 const Bucket* big, const u32* nbig) {
+    PDL_PROLOGUE();
+    const u32 lane = threadIdx.x & 31;
+    const u32 nb = *nbig;
+    for (u64 w = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < (u64)nb * p; w += ((u64)gridDim.x * blockDim.x) >> 5) {
+    const Bucket bk = big[w / p];
+    const u32 k = (u32)(w % p);
+    u32 lo = 0, hi = P;  // last j with tot[j] <= beg
+    while (lo < hi) {
+        const u32 mid = (lo + hi + 1) >> 1;
+        if (tot[mid] <= bk.beg) lo = mid; else hi = mid - 1;
+    }
+    const u32 j = lo;
+    const u32 q = n / p, rm = n % p;
+    const u32 beg = k * q + min(k, rm);
+    const u32 a = bound[(size_t)k * (P + 1) + j], b = bound[(size_t)k * (P + 1) + j + 1];
+    const u32 d = bk.beg + off[(size_t)k * P + j];
+    for (u32 t = a + lane; t < b; t += 32) {
+        B.k[0][d + t - a] = B.k[1][beg + t];
+        if (KV) { B.v[0][d + t - a] = B.v[1][beg + t]; B.i[0][d + t - a] = B.i[1][beg + t]; }
+    }
     }
 }
 

@@ -162,17 +162,17 @@ def test_c3_full(ovs, orc, dist, dseed):
 
 
 # ---------------------------------------------------------------- DRO (Algorithm 1, SqDet)
-def dro_case(ovs, orc, x, p, r, kv=False, padded=False):
+def dro_case(ovs, orc, x, p, r, kv=False, padded=False, merge=False):
     n = len(x)
     v = ovs_inputs.index_values(n) if kv else None
     ref = orc.dro_sort(x, p, r, vals=v, padded=padded)
     xt = torch.from_numpy(x).cuda()
     if kv:
         vt = torch.from_numpy(v).cuda()
-        rep = ovs.Sorter(n, xt.dtype, True, "dro", p, r, 0, padded)(xt, vt, report=True)
+        rep = ovs.Sorter(n, xt.dtype, True, "dro", p, r, 0, padded, merge=merge)(xt, vt, report=True)
     else:
         vt = None
-        rep = ovs.Sorter(n, xt.dtype, False, "dro", p, r, 0, padded)(xt, report=True)
+        rep = ovs.Sorter(n, xt.dtype, False, "dro", p, r, 0, padded, merge=merge)(xt, report=True)
     torch.cuda.synchronize()
     check(ref, xt.cpu().numpy(), None if vt is None else vt.cpu().numpy(), rep, p)
     # Lemma 1 on the GPU's own bucket counts
@@ -332,3 +332,31 @@ def test_sticky_status_after_graph_replays(ovs):
     assert rep.device_status == 0
     assert all(v >= 0 for v in rep.phase_ms[:5]) and rep.phase_ms[7] > 0
     assert abs(sum(rep.phase_ms[:5]) - rep.phase_ms[7]) < 0.05 * rep.phase_ms[7] + 0.01
+
+
+# ---------------------------------------------------------------- f2: DRO step 5 as a p-way merge
+@pytest.mark.parametrize("dist,n,p,r,kv", DRO_MERGE_CASES := [
+    ("u32_u31", 1000, 4, 1, False), ("i32_gauss", 100_003, 16, 3, False), ("u32_const", 65_536, 8, 4, True),
+    ("u32_few4", 200_000, 32, 5, True), ("f64_normal", 300_001, 64, 2, False), ("f64_uniform", 250_000, 16, 3, True),
+    ("i32_few", 1_000_000, 100, 24, False), ("u32", 3_000_000, 256, 8, False),
+    # fine buckets over the merge capacity (s small): gather + bucket sorter fallback
+    ("u32", 2_000_003, 8, 2, False), ("u16key", 600_001, 4, 2, True), ("i32_few", 1_600_000, 4, 3, False)])
+@pytest.mark.parametrize("padded", [False, True])
+def test_dro_merge_step5(ovs, orc, dist, n, p, r, kv, padded):
+    """OVS_DRO_MERGE: fine split by the regular sample, every fine bucket's p sorted runs merged
+    on chip (ties to the lower sequence): output, values (stability), splitters and the
+    contract counts (folded from the fine counts) equal the oracle's p-way merge."""
+    dro_case(ovs, orc, ovs_inputs.keys(dist, n, seed=n % 29), p, r, kv=kv, padded=padded, merge=True)
+
+
+@pytest.mark.parametrize("dist,dseed", [("i32_uniform", 21), ("i32_gauss", 22), ("i32_sorted", 23), ("i32_reverse", 24),
+                                        ("i32_few", 25)])
+def test_c2_full_merge(ovs, orc, dist, dseed):
+    c = ovs_inputs.CONFIGS["C2"]
+    dro_case(ovs, orc, ovs_inputs.keys(dist, c["n"], seed=dseed), c["p"], c["s"], merge=True)
+
+
+@pytest.mark.slow
+def test_c4_full_merge(ovs, orc):
+    c = ovs_inputs.CONFIGS["C4"]
+    dro_case(ovs, orc, ovs_inputs.keys("u16key", c["n"], seed=41), c["p"], c["s"], kv=True, merge=True)

@@ -1,6 +1,6 @@
 """Device time of one sort for each BASELINE.json configuration (C1-C4; C5 is bench.py):
 python tools/configs_bench.py [reps]   -> one JSON line per config (median of reps, after 2 warm-ups)"""
-import json, statistics, sys
+import json, os, statistics, sys
 sys.path.insert(0, ".")
 import torch
 import ovs_inputs
@@ -20,7 +20,8 @@ for name, dist, dseed, n, method, p, s, kv, bpk in CASES:
         continue
     x = torch.from_numpy(ovs_inputs.keys(dist, n, seed=dseed)).cuda()
     v = torch.from_numpy(ovs_inputs.index_values(n)).cuda() if kv else None
-    srt = ovs.Sorter(n, x.dtype, kv, method, p, s, 1)
+    merge = os.environ.get("OVS_BENCH_MERGE") == "1" and method == "dro"  # f2: DRO step 5 as a p-way merge
+    srt = ovs.Sorter(n, x.dtype, kv, method, p, s, 1, merge=merge)
     wk, wv = x.clone(), (v.clone() if kv else None)
     ms, ph = [], []
     for r in range(reps + 2):
@@ -37,7 +38,7 @@ for name, dist, dseed, n, method, p, s, kv, bpk in CASES:
             ph.append([ev[i].elapsed_time(ev[i + 1]) for i in range(5)])
     t = statistics.median(ms)
     phases = {nm: round(statistics.median(q[i] for q in ph), 3) for i, nm in enumerate(ovs.PHASES)}
-    print(json.dumps({"config": name, "n": n, "dtype": str(x.dtype).replace("torch.", ""), "method": method, "p": p,
+    print(json.dumps({"config": name + ("+merge" if merge else ""), "n": n, "dtype": str(x.dtype).replace("torch.", ""), "method": method, "p": p,
                       "s_or_r": s, "kv": kv, "ms": round(t, 4), "Gkeys_per_s": round(n / t / 1e6, 2),
                       "algorithmic_GBps": round(n * bpk / t / 1e6, 1), "phases_ms": phases}), flush=True)
     del srt, x, v, wk, wv

@@ -398,6 +398,43 @@ __device__ void block_scan_small(u32* a, u32 cnt, u32* red) {
     __syncthreads();
 }
 
+// block_scan_small that also appends every index whose count is >= T to list[] (warp-aggregated;
+// *over set when the list is full) - the 32-bit keys-only bucket sorter lists its large groups here
+template <int NT>
+__device__ void block_scan_small_list(u32* a, u32 cnt, u32* red, u32 T, u32* list, u32* nlist, u32 cap, u32* over) {
+    const u32 i0 = threadIdx.x * 16, r = (threadIdx.x >> 1) & 15;
+    const int lane = threadIdx.x & 31;
+    u32 v[16], s = 0, head = 0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const u32 e = (j + r) & 15;
+        v[j] = (i0 + e < cnt) ? a[i0 + e] : 0u;
+        s += v[j];
+        if (e < r) head += v[j];
+        const bool big = v[j] >= T;
+        const u32 mb = __ballot_sync(0xffffffffu, big);
+        if (mb) {
+            u32 base = 0;
+            if (lane == 0) base = atomicAdd(nlist, __popc(mb));
+            base = __shfl_sync(0xffffffffu, base, 0) + __popc(mb & ((1u << lane) - 1));
+            if (big) {
+                if (base < cap) list[base] = i0 + e;
+                else atomicOr(over, 1u);
+            }
+        }
+    }
+    const u32 base = block_exclusive_scan<NT>(s, red, nullptr);
+    u32 run = base + head;  // prefix of element r
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const u32 e = (j + r) & 15;
+        if (e == 0) run = base;
+        if (i0 + e < cnt) a[i0 + e] = run;
+        run += v[j];
+    }
+    __syncthreads();
+}
+
 // ------------------------------------------------------------------ CTA bitonic sort of (key, tag)
 // N a power of two, records in shared memory; ascending by (key, tag).  Every thread step is one
 // comparator (x, x + j): t's bits below j stay, the bits above move up one place.
@@ -676,6 +713,99 @@ __global__ void __launch_bounds__(1024) k_direct_scan(u32* bcnt, u32 nb, u32 m, 
     if (threadIdx.x == 0 && bcnt[nb] != m) st_set(status, ST_SAMPLE_SHORT);
 }
 
+// ------------------------------------------------------------------ register sorting networks
+template <class U> __device__ __forceinline__ U shfl_xor_any(U x, int o) {
+    if (sizeof(U) == 8) return (U)__shfl_xor_sync(0xffffffffu, (unsigned long long)x, o);
+    return (U)__shfl_xor_sync(0xffffffffu, (u32)x, o);
+}
+template <class U, bool KV> struct Elem;
+template <class U> struct Elem<U, false> {
+    U k;
+    __device__ __forceinline__ bool lt(const Elem& o) const { return k < o.k; }
+    __device__ __forceinline__ static Elem inf() { Elem e; e.k = umax_of<U>(); return e; }
+    __device__ __forceinline__ Elem shfl_xor(int m) const { Elem e; e.k = shfl_xor_any(k, m); return e; }
+};
+template <class U> struct Elem<U, true> {
+    U k; u32 i, v;
+    __device__ __forceinline__ bool lt(const Elem& o) const { return k < o.k || (k == o.k && i < o.i); }
+    __device__ __forceinline__ static Elem inf() { Elem e; e.k = umax_of<U>(); e.i = 0xffffffffu; e.v = 0; return e; }
+    __device__ __forceinline__ Elem shfl_xor(int m) const {
+        Elem e;
+        e.k = shfl_xor_any(k, m);
+        e.i = __shfl_xor_sync(0xffffffffu, i, m);
+        e.v = __shfl_xor_sync(0xffffffffu, v, m);
+        return e;
+    }
+};
+
+template <class E> __device__ __forceinline__ void cex(E& a, E& b) {
+    if (b.lt(a)) { E t = a; a = b; b = t; }
+}
+
+// Batcher's odd-even merge network for 8 inputs (19 comparators)
+template <class E> __device__ __forceinline__ void network8(E (&a)[8]) {
+    cex(a[0], a[1]); cex(a[2], a[3]); cex(a[4], a[5]); cex(a[6], a[7]);
+    cex(a[0], a[2]); cex(a[1], a[3]); cex(a[4], a[6]); cex(a[5], a[7]);
+    cex(a[1], a[2]); cex(a[5], a[6]);
+    cex(a[0], a[4]); cex(a[1], a[5]); cex(a[2], a[6]); cex(a[3], a[7]);
+    cex(a[2], a[4]); cex(a[3], a[5]);
+    cex(a[1], a[2]); cex(a[3], a[4]); cex(a[5], a[6]);
+}
+
+// Batcher's odd-even merge sort for 16 inputs: two 8-sorts (19 + 19 comparators) and the
+// odd-even merge of the halves (25 comparators), 63 in all
+template <class E> __device__ __forceinline__ void network16(E (&a)[16]) {
+    E* lo = a;
+    E* hi = a + 8;
+    E (&l8)[8] = *reinterpret_cast<E(*)[8]>(lo);
+    E (&h8)[8] = *reinterpret_cast<E(*)[8]>(hi);
+    network8(l8);
+    network8(h8);
+    // odd-even merge of a[0..8) and a[8..16)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) cex(a[i], a[i + 8]);
+    cex(a[4], a[8]); cex(a[5], a[9]); cex(a[6], a[10]); cex(a[7], a[11]);
+    cex(a[2], a[4]); cex(a[3], a[5]); cex(a[6], a[8]); cex(a[7], a[9]); cex(a[10], a[12]); cex(a[11], a[13]);
+    cex(a[1], a[2]); cex(a[3], a[4]); cex(a[5], a[6]); cex(a[7], a[8]); cex(a[9], a[10]); cex(a[11], a[12]);
+    cex(a[13], a[14]);
+}
+
+// bitonic sort of 32*R elements held as a[r] at lane: element index e = r*32 + lane
+template <class E, int R>
+__device__ __forceinline__ void warp_bitonic(E (&a)[R]) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int k = 2; k <= 32 * R; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j >= 32) {
+                const int jr = j >> 5;
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    if ((r & jr) == 0) {
+                        const int e = r * 32 + lane;
+                        const bool asc = (e & k) == 0;
+                        E x = a[r], y = a[r | jr];
+                        const bool sw = asc ? y.lt(x) : x.lt(y);
+                        if (sw) { a[r] = y; a[r | jr] = x; }
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int e = r * 32 + lane;
+                    const bool asc = (e & k) == 0;
+                    const bool lower = (lane & j) == 0;
+                    E o = a[r].shfl_xor(j);
+                    const bool keep_min = (lower == asc);
+                    const bool take = keep_min ? o.lt(a[r]) : a[r].lt(o);
+                    if (take) a[r] = o;
+                }
+            }
+        }
+    }
+}
+
 // ------------------------------------------------------------------ a3: sample sort (coarse level)
 // The m sample records (key word, tag) are sorted by (key, tag) in two steps: G coarse buckets,
 // then every coarse bucket by the bucket sorter.  Coarse splitter i = CS[(i+1)Q/G - 1], CS =
@@ -919,10 +1049,6 @@ template <class U> __host__ __device__ constexpr size_t cls_smem_bytes(u32 PS, u
     return a16(sizeof(U) * (size_t)PS) + a16(4 * (size_t)PS) + a16(4 * ((size_t)LS + 1));
 }
 
-template <class U> __device__ __forceinline__ U shfl_xor_any(U x, int o) {
-    if (sizeof(U) == 8) return (U)__shfl_xor_sync(0xffffffffu, (unsigned long long)x, o);
-    return (U)__shfl_xor_sync(0xffffffffu, (u32)x, o);
-}
 
 // ------------------------------------------------------------------ vectorised item loops
 // for_items(src, beg, m, f): calls f(key, o) for every o in [0, m) (any order) with 16-byte
@@ -1798,94 +1924,6 @@ constexpr u32 BS_SPMAX = 64;
 constexpr u32 BS_SI = 32;
 constexpr u32 BS_SSMAX = BS_SPMAX * BS_SI;
 
-template <class U, bool KV> struct Elem;
-template <class U> struct Elem<U, false> {
-    U k;
-    __device__ __forceinline__ bool lt(const Elem& o) const { return k < o.k; }
-    __device__ __forceinline__ static Elem inf() { Elem e; e.k = umax_of<U>(); return e; }
-    __device__ __forceinline__ Elem shfl_xor(int m) const { Elem e; e.k = shfl_xor_any(k, m); return e; }
-};
-template <class U> struct Elem<U, true> {
-    U k; u32 i, v;
-    __device__ __forceinline__ bool lt(const Elem& o) const { return k < o.k || (k == o.k && i < o.i); }
-    __device__ __forceinline__ static Elem inf() { Elem e; e.k = umax_of<U>(); e.i = 0xffffffffu; e.v = 0; return e; }
-    __device__ __forceinline__ Elem shfl_xor(int m) const {
-        Elem e;
-        e.k = shfl_xor_any(k, m);
-        e.i = __shfl_xor_sync(0xffffffffu, i, m);
-        e.v = __shfl_xor_sync(0xffffffffu, v, m);
-        return e;
-    }
-};
-
-template <class E> __device__ __forceinline__ void cex(E& a, E& b) {
-    if (b.lt(a)) { E t = a; a = b; b = t; }
-}
-
-// Batcher's odd-even merge network for 8 inputs (19 comparators)
-template <class E> __device__ __forceinline__ void network8(E (&a)[8]) {
-    cex(a[0], a[1]); cex(a[2], a[3]); cex(a[4], a[5]); cex(a[6], a[7]);
-    cex(a[0], a[2]); cex(a[1], a[3]); cex(a[4], a[6]); cex(a[5], a[7]);
-    cex(a[1], a[2]); cex(a[5], a[6]);
-    cex(a[0], a[4]); cex(a[1], a[5]); cex(a[2], a[6]); cex(a[3], a[7]);
-    cex(a[2], a[4]); cex(a[3], a[5]);
-    cex(a[1], a[2]); cex(a[3], a[4]); cex(a[5], a[6]);
-}
-
-// Batcher's odd-even merge sort for 16 inputs: two 8-sorts (19 + 19 comparators) and the
-// odd-even merge of the halves (25 comparators), 63 in all
-template <class E> __device__ __forceinline__ void network16(E (&a)[16]) {
-    E* lo = a;
-    E* hi = a + 8;
-    E (&l8)[8] = *reinterpret_cast<E(*)[8]>(lo);
-    E (&h8)[8] = *reinterpret_cast<E(*)[8]>(hi);
-    network8(l8);
-    network8(h8);
-    // odd-even merge of a[0..8) and a[8..16)
-#pragma unroll
-    for (int i = 0; i < 8; ++i) cex(a[i], a[i + 8]);
-    cex(a[4], a[8]); cex(a[5], a[9]); cex(a[6], a[10]); cex(a[7], a[11]);
-    cex(a[2], a[4]); cex(a[3], a[5]); cex(a[6], a[8]); cex(a[7], a[9]); cex(a[10], a[12]); cex(a[11], a[13]);
-    cex(a[1], a[2]); cex(a[3], a[4]); cex(a[5], a[6]); cex(a[7], a[8]); cex(a[9], a[10]); cex(a[11], a[12]);
-    cex(a[13], a[14]);
-}
-
-// bitonic sort of 32*R elements held as a[r] at lane: element index e = r*32 + lane
-template <class E, int R>
-__device__ __forceinline__ void warp_bitonic(E (&a)[R]) {
-    const int lane = threadIdx.x & 31;
-#pragma unroll
-    for (int k = 2; k <= 32 * R; k <<= 1) {
-#pragma unroll
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            if (j >= 32) {
-                const int jr = j >> 5;
-#pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    if ((r & jr) == 0) {
-                        const int e = r * 32 + lane;
-                        const bool asc = (e & k) == 0;
-                        E x = a[r], y = a[r | jr];
-                        const bool sw = asc ? y.lt(x) : x.lt(y);
-                        if (sw) { a[r] = y; a[r | jr] = x; }
-                    }
-                }
-            } else {
-#pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    const int e = r * 32 + lane;
-                    const bool asc = (e & k) == 0;
-                    const bool lower = (lane & j) == 0;
-                    E o = a[r].shfl_xor(j);
-                    const bool keep_min = (lower == asc);
-                    const bool take = keep_min ? o.lt(a[r]) : a[r].lt(o);
-                    if (take) a[r] = o;
-                }
-            }
-        }
-    }
-}
-
 template <class U, bool KV> struct BucketSmem {
     U* k; u32* i; u32* v; u32* cnt;
 };
@@ -2350,7 +2388,13 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                 });
                 __syncthreads();
                 BS_PROBE(3)
-                block_scan_small<BS_NT>(Sa.cnt, ng, red);  // cnt[g] = start of group g
+                if constexpr (!KV && sizeof(U) == 4 && OVS_BS_WIN16) {
+                    // (groups of >= 10 keys are listed here for the window networks below)
+                    block_scan_small_list<BS_NT>(Sa.cnt, ng, red, need_sort ? 10u : 0xffffffffu, s_big, &s_nbig,
+                                                 (u32)BS_BIGMAX, &s_over);
+                } else {
+                    block_scan_small<BS_NT>(Sa.cnt, ng, red);  // cnt[g] = start of group g
+                }
                 BS_PROBE(4)
                 if constexpr (!KV && sizeof(U) == 4 && OVS_BS_WIN16) {
                     // ---- 32-bit keys only: swizzled item array, windowed networks
@@ -2365,35 +2409,22 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                     __syncthreads();
                     BS_PROBE(5)
                     if (need_sort) {
-                        // groups of >= 10 keys are listed; every shorter group lies inside one window
-                        // of 16 consecutive keys starting at a multiple of 8 (pass A: starts 16w,
-                        // pass B: 16w + 8), and sorting a window by key never breaks the digit order
-                        for (u32 g0 = 0; g0 < ng; g0 += BS_NT) {
-                            const u32 g = g0 + threadIdx.x;
-                            u32 len = 0;
-                            if (g < ng) len = S.cnt[g] - (g ? S.cnt[g - 1] : 0u);
-                            const u32 mb = __ballot_sync(0xffffffffu, len >= 10);
-                            if (mb) {
-                                u32 base = 0;
-                                if (lane == 0) base = atomicAdd(&s_nbig, __popc(mb));
-                                base = __shfl_sync(0xffffffffu, base, 0) + __popc(mb & ((1u << lane) - 1));
-                                if (len >= 10) {
-                                    if (base < BS_BIGMAX) s_big[base] = g;
-                                    else atomicOr(&s_over, 1u);
-                                }
-                            }
-                        }
+                        // groups of >= 10 keys were listed by the scan; every shorter group lies inside
+                        // one window of 16 consecutive keys starting at a multiple of 8 (pass A: starts
+                        // 16w, pass B: 16w + 8), and sorting a window by key never breaks the digit order
                         // pass A: physical windows [16w, 16w + 16); slots outside [al, al + m) get the
                         // minimum / maximum key, so they stay in place
                         const u32 nw = (al + m + 15) >> 4;
                         for (u32 w = threadIdx.x; w < nw; w += BS_NT) {
                             u32 e[16];
                             win_ld(kb, 4 * w, e);
+                            if (16 * w < al || 16 * w + 16 > al + m) {  // the two edge windows only
 #pragma unroll
-                            for (u32 i = 0; i < 16; ++i) {
-                                const u32 P = 16 * w + i;
-                                if (P < al) e[i] = 0u;
-                                else if (P >= al + m) e[i] = 0xffffffffu;
+                                for (u32 i = 0; i < 16; ++i) {
+                                    const u32 P = 16 * w + i;
+                                    if (P < al) e[i] = 0u;
+                                    else if (P >= al + m) e[i] = 0xffffffffu;
+                                }
                             }
                             sort16u(e);
                             win_st(kb, 4 * w, e);

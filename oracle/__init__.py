@@ -18,7 +18,8 @@ _SRC = os.path.join(_HERE, "ovs_oracle.cpp")
 _LIB = os.path.join(_HERE, "libovs_oracle.so")
 
 OK, EINVAL, EDTYPE, ESAMPLE = 0, 1, 2, 3
-DTYPES = {np.dtype(np.uint32): 0, np.dtype(np.int32): 1, np.dtype(np.float64): 2}
+DTYPES = {np.dtype(np.uint32): 0, np.dtype(np.int32): 1, np.dtype(np.float64): 2,
+          np.dtype("V32"): 3}  # 32-byte strings in memcmp order (np.void, 32 bytes per key)
 DRO_PADDED_POSITIONS = 1
 
 

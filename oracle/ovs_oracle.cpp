@@ -29,7 +29,13 @@
 namespace {
 
 enum { OK = 0, EINVAL = 1, EDTYPE = 2, ESAMPLE = 3 };
-enum { DT_U32 = 0, DT_I32 = 1, DT_F64 = 2 };
+enum { DT_U32 = 0, DT_I32 = 1, DT_F64 = 2, DT_S32 = 3 };
+
+// 32-byte string keys in memcmp order: the paper's own workload, "keys ... random strings of
+// 32 bytes" compared as byte strings.  Every algorithm below is
+// written against operator< only, so the same code sorts them.
+struct S32 { unsigned char b[32]; };
+inline bool operator<(const S32& a, const S32& b) { return std::memcmp(a.b, b.b, 32) < 0; }
 enum { DRO_PADDED_POSITIONS = 1u };
 
 // ---- counter-based random stream (reading Q1) -------------------------------------------
@@ -337,6 +343,7 @@ int dispatch(int dtype, F&& f) {
         case DT_U32: return f((uint32_t*)nullptr);
         case DT_I32: return f((int32_t*)nullptr);
         case DT_F64: return f((double*)nullptr);
+        case DT_S32: return f((S32*)nullptr);
         default: return EDTYPE;
     }
 }

@@ -75,7 +75,20 @@ def keys(dist: str, n: int, seed: int, start: int = 0, world: int = 1, rank: int
       u32_const    all keys equal (42)
       u32_few4     u mod 4
       u32_staggered / u32_bucketsorted  C5 multi-GPU distributions (need world, rank)
+      s32          32-byte strings of uniform random bytes (the paper's workload):
+                   string i = the little-endian bytes of u_{4i} .. u_{4i+3}; numpy dtype V32
+      s32_prefix   s32 whose first 8 bytes take only 4 values (ties on the 8-byte prefix)
+      s32_few      8 distinct strings (u mod 8 picks one of 8 fixed s32 strings)
     """
+    if dist in ("s32", "s32_prefix", "s32_few"):
+        w = data_u64(seed, 4 * start, 4 * n).reshape(n, 4)
+        if dist == "s32_prefix":
+            w[:, 0] = w[:, 0] % np.uint64(4)
+        elif dist == "s32_few":
+            pick = w[:, 0] % np.uint64(8)
+            base = data_u64(seed + 1, 0, 32).reshape(8, 4)
+            w = base[pick.astype(np.int64)]
+        return np.ascontiguousarray(w).view("V32").reshape(n)
     if dist in ("i32_sorted", "i32_reverse") and start != 0:
         raise ValueError("sorted distributions are defined on the whole array only")
     u = None if dist in ("i32_gauss", "f64_normal") else data_u64(seed, start, n)

@@ -362,3 +362,32 @@ def test_empty_input_reading_q26(orc):
             assert len(res.keys) == 0
             assert res.counts.tolist() == [0, 0, 0, 0]
             assert not np.any(res.split_keys) and not np.any(res.split_tags)
+
+
+# ---------------------------------------------------------------- 32-byte string keys (f3)
+@pytest.mark.parametrize("dist", ["s32", "s32_prefix", "s32_few"])
+def test_strings_sorted_like_python_bytes(orc, dist):
+    """memcmp order of 32-byte keys = Python's bytes order (a library sort): the ROS,
+    literal SqRan and DRO outputs equal sorted(bytes)."""
+    n = 20_000
+    x = ovs_inputs.keys(dist, n, seed=11)
+    ref = sorted(bytes(v) for v in x)
+    for res in (orc.ros_sort(x, 16, 8, 2), orc.sqran_literal(x, 16, 8, 2), orc.dro_sort(x, 16, 3)):
+        assert [bytes(v) for v in res.keys] == ref
+        assert int(res.counts.sum()) == n
+    a, b = orc.ros_sort(x, 16, 8, 2), orc.sqran_literal(x, 16, 8, 2)
+    np.testing.assert_array_equal(a.split_tags, b.split_tags)
+    np.testing.assert_array_equal(a.counts, b.counts)
+
+
+@pytest.mark.parametrize("n,p,s", [(7, 2, 4), (8, 3, 3), (63, 4, 16)])
+def test_strings_exhaustive_sample_closed_form(orc, n, p, s):
+    """ps - 1 = n: T is every string, splitter q is the string of rank (q+1)s in (bytes, index)
+    order and the counts are [s, ..., s, s-1] (closed form)."""
+    x = ovs_inputs.keys("s32_few", n, seed=5)
+    res = orc.ros_sort(x, p, s, 3)
+    order = sorted(range(n), key=lambda i: (bytes(x[i]), i))
+    idx = [order[(q + 1) * s - 1] for q in range(p - 1)]
+    assert res.split_tags.tolist() == idx
+    assert [bytes(v) for v in res.split_keys] == [bytes(x[i]) for i in idx]
+    assert res.counts.tolist() == [s] * (p - 1) + [s - 1]

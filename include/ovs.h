@@ -53,7 +53,12 @@ typedef enum {
                             by ovs_device_status() for calls without a report (graph replays)          */
 } ovs_status;
 
-typedef enum { OVS_U32 = 0, OVS_I32 = 1, OVS_F64 = 2 } ovs_dtype;
+typedef enum {
+    OVS_U32 = 0, OVS_I32 = 1, OVS_F64 = 2,
+    OVS_S32 = 3  /* 32-byte string records in memcmp order (the paper's workload):
+                    d_keys holds n records of 32 bytes (16-byte aligned); ROS, ovs_sort_keys only
+                    (DRO or values: OVS_EDTYPE); the report's splitter keys are (p-1) records */
+} ovs_dtype;
 typedef enum { OVS_ROS = 0, OVS_DRO = 1 } ovs_method;
 
 /* flags */

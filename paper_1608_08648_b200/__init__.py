@@ -16,14 +16,14 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("OVS_LIB_PATH") or os.path.join(_HERE, "libovs.so")  # override: A/B experiments
 
 OVS_OK, OVS_EINVAL, OVS_EDTYPE, OVS_ESAMPLE, OVS_EWORKSPACE, OVS_ECUDA, OVS_ECAPACITY, OVS_EINTERNAL = 0, 1, 2, 3, 4, 5, 7, 8
-OVS_U32, OVS_I32, OVS_F64 = 0, 1, 2
+OVS_U32, OVS_I32, OVS_F64, OVS_S32 = 0, 1, 2, 3
 OVS_ROS, OVS_DRO = 0, 1
 OVS_DRO_PADDED_POSITIONS = 1
 OVS_DRO_MERGE = 2
 METHODS = {"ros": OVS_ROS, "dro": OVS_DRO}
 
 
-_NP = {OVS_U32: np.uint32, OVS_I32: np.int32, OVS_F64: np.float64}
+_NP = {OVS_U32: np.uint32, OVS_I32: np.int32, OVS_F64: np.float64, OVS_S32: np.dtype("V32")}
 
 
 class Params(ctypes.Structure):
@@ -95,7 +95,10 @@ def set_phase_events(events) -> None:
 
 
 def _dtype_code(dt) -> int:
+    """torch dtype -> ovs dtype; "s32" = 32-byte string records (a uint8 tensor of 32 n bytes)."""
     import torch
+    if dt == "s32":
+        return OVS_S32
     m = {torch.uint32: OVS_U32, torch.int32: OVS_I32, torch.float64: OVS_F64}
     if dt not in m:
         raise OvsError(OVS_EDTYPE, f"unsupported dtype {dt}")
@@ -155,7 +158,7 @@ class Sorter:
 
     def __call__(self, keys, vals=None, stream=None, report: bool = False):
         import torch
-        assert keys.is_cuda and keys.is_contiguous() and keys.numel() == self.n
+        assert keys.is_cuda and keys.is_contiguous() and keys.numel() == self.n * (32 if self.dt == OVS_S32 else 1)
         assert keys.device == self.ws.device, "keys and the workspace must be on the same device"
         with torch.cuda.device(keys.device):
             return self._call(keys, vals, stream, report)
@@ -175,6 +178,8 @@ class Sorter:
 
     def _call(self, keys, vals, stream, report):
         import torch
+        if self.dt == OVS_S32:
+            assert keys.dtype == torch.uint8 and keys.numel() == 32 * self.n, "s32: 32 n bytes of uint8"
         st = ctypes.c_void_p(stream.cuda_stream if stream is not None
                              else torch.cuda.current_stream(keys.device).cuda_stream)
         rep = None
@@ -228,3 +233,10 @@ def sort_pairs_stable(keys, vals, method: str = "ros", p: int = 64, s: int = 32,
                       padded: bool = False, report: bool = True):
     """Stable key-value sort (uint32 values) in place; returns the report."""
     return Sorter(keys.numel(), keys.dtype, True, method, p, s, seed, padded, keys.device)(keys, vals, report=report)
+
+
+def sort_strings32(recs, p: int = 64, s: int = 32, seed: int = 1, report: bool = True):
+    """Sort 32-byte string records (a CUDA uint8 tensor of 32 n bytes, memcmp order; the paper's
+    workload) in place with ROS; returns the report (splitter keys as V32)."""
+    n = recs.numel() // 32
+    return Sorter(n, "s32", False, "ros", p, s, seed, device=recs.device)(recs, report=report)

@@ -14,6 +14,10 @@ using namespace ovs;
 // ------------------------------------------------------------------ C ABI
 static Out plan_dispatch(Ctx& c, void* keys, u32* vals, size_t n, int dtype, const ovs_params* prm) {
     const bool kv = vals != nullptr || (c.dry && keys == (void*)1);
+    if (dtype == OVS_S32) {
+        if (kv) throw StatusFail{OVS_EDTYPE, "32-byte string keys: keys only"};
+        return plan_s32_k(c, keys, vals, n, prm);
+    }
     if (dtype == OVS_U32) return kv ? plan_u32_v(c, keys, vals, n, prm) : plan_u32_k(c, keys, vals, n, prm);
     if (dtype == OVS_I32) return kv ? plan_i32_v(c, keys, vals, n, prm) : plan_i32_k(c, keys, vals, n, prm);
     return kv ? plan_f64_v(c, keys, vals, n, prm) : plan_f64_k(c, keys, vals, n, prm);
@@ -54,7 +58,10 @@ static int sort_impl(void* d_keys, uint32_t* d_vals, bool kv, size_t n, int dtyp
             ~Evs() { for (auto x : e) if (x) cudaEventDestroy(x); }
         } ev;
         if (rep) {
-            for (auto& x : ev.e) OVS_CK(cudaEventCreate(&x));
+            for (auto& x : ev.e) {
+                OVS_CK(cudaEventCreate(&x));
+                OVS_CK(cudaEventRecord(x, c.st));  // a phase a path skips reads as 0 ms
+            }
             c.rep_marks = ev.e;
         }
         OVS_CK(cudaMemsetAsync(c.status, 0, 4, c.st));  // this call's bits (status[1] is sticky)
@@ -84,14 +91,14 @@ static int sort_impl(void* d_keys, uint32_t* d_vals, bool kv, size_t n, int dtyp
             rep->max_bucket = (u32)mx;
             if (rep->bucket_counts) std::memcpy(rep->bucket_counts, cnt.data(), 8 * (size_t)p);
             if (p > 1 && (rep->splitter_keys || rep->splitter_tags)) {
-                const size_t kb = dtype == OVS_F64 ? 8 : 4;
+                const size_t kb = dtype == OVS_S32 ? 32 : dtype == OVS_F64 ? 8 : 4;
                 std::vector<unsigned char> kbuf(kb * (p - 1));
                 std::vector<u32> tbuf(p - 1);
                 OVS_CK(cudaMemcpy(kbuf.data(), o.sk, kb * (p - 1), cudaMemcpyDeviceToHost));
                 OVS_CK(cudaMemcpy(tbuf.data(), o.st, 4 * (size_t)(p - 1), cudaMemcpyDeviceToHost));
                 if (rep->splitter_keys) {
                     // splitters are held as ordered bits: convert back to the raw dtype
-                    if (dtype == OVS_U32) std::memcpy(rep->splitter_keys, kbuf.data(), kbuf.size());
+                    if (dtype == OVS_U32 || dtype == OVS_S32) std::memcpy(rep->splitter_keys, kbuf.data(), kbuf.size());
                     else if (dtype == OVS_I32) {
                         u32* d = (u32*)rep->splitter_keys;
                         const u32* s = (const u32*)kbuf.data();

@@ -180,7 +180,10 @@ int dist_impl(ovs_comm* c, const void* keys, const u32* vals, bool kv, size_t n_
         cx.marks = &g_marks;
         Evs ev;
         if (rep) {
-            for (auto& x : ev.e) OVS_CK(cudaEventCreate(&x));
+            for (auto& x : ev.e) {
+                OVS_CK(cudaEventCreate(&x));
+                OVS_CK(cudaEventRecord(x, st));
+            }
             cx.rep_marks = ev.e;
         }
         cx.status = cx.take<u32>(4);

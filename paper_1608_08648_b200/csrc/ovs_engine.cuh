@@ -509,6 +509,13 @@ template <bool TAG> struct Selector {
     template <class U> void run(u32 P, u32 s, u32 f, u64 seed, U* sk, u32* st) {
         Ctx& c = e.c;
         if (c.dry) return;
+        sort(seed);
+        pick<U>(P, s, f, sk, st);
+    }
+    // the sorted records (key word e.B.k[0], tag e.B.v[0]) without picking splitters
+    void sort(u64 seed) {
+        Ctx& c = e.c;
+        if (c.dry) return;
         const u32 grid = cdiv(m, SEL_PER);
         launch(c, k_sel_count<TAG>, grid, 1024, 0, tk, tt, m, G, stride, csk, cst, cb, gcnt);
         c.check();
@@ -516,7 +523,6 @@ template <bool TAG> struct Selector {
                                                     l.fit, l.nfit);
         c.check();
         e.bucket_sort(l, seed);
-        pick<U>(P, s, f, sk, st);
     }
     // S[q] = T[(q+1)s - 1], q < P-1, from the sorted records
     template <class U> void pick(u32 P, u32 s, u32 f, U* sk, u32* st) {
@@ -703,10 +709,161 @@ template <int DT, bool KV> struct RosSort {
     }
 };
 
+// ------------------------------------------------------------------ f3: ROS on 32-byte strings
+// (the paper's workload).  Same contract as RosSort:
+// sample index set I (reading Q1), T sorted by (full key, index), S[q] = T[(q+1)s - 1], buckets by
+// the tagged lower bound, every bucket sorted, concatenated.  Keys only (equal strings are equal
+// bytes).  Refinement f as in RosSort keeps buckets on chip.
+struct RosSortS32 {
+    Ctx& c;
+    u32 n, p, s, f = 1, P0 = 1, L = 64, log2L = 6, nchunk = 1, chunk = 0, cap = 0;
+    u64 seed;
+    u64* recs = nullptr; u64* buf1 = nullptr;
+    u16* bid = nullptr; u32* gidx = nullptr;
+    u64* sk = nullptr; u32* st = nullptr; u32* lut = nullptr; Seg* seg = nullptr; Chunk* chunks = nullptr;
+    u32* nchunks = nullptr; u32* nseg = nullptr; u32* hist = nullptr; u32* tot = nullptr;
+    u64* sfull = nullptr;
+    u64* counts = nullptr; u64* int_counts = nullptr;
+    u64* rep_sk = nullptr; u32* rep_st = nullptr; u64* rep_raw = nullptr; u64* rep_full = nullptr;
+    u32* fixl = nullptr; u32* nfix = nullptr; u32 fix_cap = 0;
+    Bucket* fit = nullptr; u32* nfit = nullptr; u32 fit_cap = 0;
+    RosSampler<DT_S32, false>* smp = nullptr;
+
+    static u32 cap_s32(const DevInfo& di) {
+        return (u32)(((size_t)di.smem_optin - 2048) / 36) & ~31u;
+    }
+    u32 pc = 1;  // the contract's p (p == 1, a plain sort: an internal p keeps the buckets on chip)
+    RosSortS32(Ctx& ctx, void* keys, u32 n_, u32 p_, u32 s_, u64 seed_) : c(ctx), n(n_), p(p_), s(s_), seed(seed_) {
+        recs = (u64*)keys;
+        cap = cap_s32(c.di);
+        pc = p;
+        if (p == 1 && n > cap) {
+            p = std::min<u32>(4096, pow2_at_least(cdiv(n, cap * 6 / 10)));
+            s = 16;
+            while (p > 2 && (u64)p * s - 1 > n) p >>= 1;
+        }
+        buf1 = c.take<u64>(4 * (size_t)n);
+        bid = c.take<u16>(n);
+        gidx = c.take<u32>(n);
+        counts = c.take<u64>(std::max<u32>(p, 1));
+        if (p > 1) {
+            while (s / (2 * f) >= 8 && (u64)p * 2 * f <= 8192 && (u64)n * 10 > (u64)p * f * cap * 6) f *= 2;
+            P0 = p * f;
+        } else {
+            P0 = 1;
+        }
+        // classifier table: ~4 entries per splitter within the histogram kernel's shared memory
+        L = P0 > 1 ? std::min<u32>(16384, std::max<u32>(64, pow2_at_least(4 * P0))) : 1;
+        while (L > 64 && cls_smem_bytes<u64>(P0, L) + 4 * (size_t)P0 + 1024 > (size_t)c.di.smem_optin) L >>= 1;
+        log2L = ilog2(L);
+        chunk = std::max<u32>(4 * S32_NT, cdiv(cdiv(n, (u32)c.di.sms), 4 * S32_NT) * 4 * S32_NT);
+        nchunk = std::max<u32>(1, cdiv(n, chunk));
+        sk = c.take<u64>(std::max<u32>(P0, 1));
+        st = c.take<u32>(std::max<u32>(P0, 1));
+        lut = c.take<u32>(L + 1);
+        seg = c.take<Seg>(1);
+        chunks = c.take<Chunk>(nchunk);
+        nchunks = c.take<u32>(2);
+        nseg = nchunks + 1;
+        hist = c.take<u32>((size_t)nchunk * P0);
+        tot = c.take<u32>(P0 + 1);
+        sfull = c.take<u64>(4 * (size_t)std::max<u32>(P0, 1));
+        rep_sk = c.take<u64>(std::max<u32>(p, 1));
+        rep_st = c.take<u32>(std::max<u32>(p, 1));
+        rep_raw = c.take<u64>(4 * (size_t)std::max<u32>(p, 1));
+        rep_full = c.take<u64>(4 * (size_t)std::max<u32>(p, 1));
+        if (f > 1) int_counts = c.take<u64>(P0);
+        fit_cap = P0 + 64;
+        fit = c.take<Bucket>(fit_cap);
+        nfit = c.take<u32>(2);
+        if (p > 1) {
+            smp = new RosSampler<DT_S32, false>(c, n, p, s);
+            fix_cap = 4096;
+            fixl = c.take<u32>(2 * (size_t)fix_cap);
+            nfix = c.take<u32>(2);
+        }
+    }
+    ~RosSortS32() { delete smp; }
+
+    void run() {
+        if (c.dry) return;
+        c.mark(0);
+        if (p > 1) {
+            // a1+a2: the index set I and the records (prefix, index)
+            smp->draw(seed);
+            smp->take(seed, recs, 0, n);
+            c.mark(1);
+            // a3: sort by (prefix, index); runs of equal prefixes re-ordered by the full key
+            Selector<true>* sel = smp->sel;
+            sel->sort(seed ^ 0x5eed);
+            fill_u32(c, nfix, 0, 2);
+            launch(c, k_s32_fix, cdiv(smp->m, 256), 256, 0, (const u64*)sel->e.B.k[0], sel->e.B.v[0], smp->m,
+                   (const u64*)recs, fixl, nfix, fix_cap, c.status);
+            c.check();
+            launch(c, k_s32_fix_long, (u32)c.di.sms, 1024, 0, sel->e.B.v[0], (const u64*)recs, (const u32*)fixl,
+                   (const u32*)nfix);
+            c.check();
+            // a4: S[q] = T[(q+1)s - 1] (level 0 refined: every (s/f)-th record), their full keys
+            sel->template pick<u64>(P0, s, f, sk, st);
+            sel->template pick<u64>(p, s, 1, rep_sk, rep_st);
+            launch(c, k_s32_splitters, cdiv(P0, 256), 256, 0, (const u32*)st, P0 - 1, (const u64*)recs, sfull,
+                   (u64*)nullptr);
+            c.check();
+            launch(c, k_s32_splitters, cdiv(p, 256), 256, 0, (const u32*)rep_st, p - 1, (const u64*)recs, rep_full,
+                   rep_raw);
+            c.check();
+        } else {
+            c.mark(1);
+        }
+        c.mark(2);
+        // a5+a6: classify (prefix table + full-key ties), histogram, scans
+        const size_t sm_cls = std::max<size_t>(8 * (size_t)std::max<u32>(P0, 1), 16);
+        smem_limit(k_build_cls0<u64>, sm_cls, c.di);
+        launch(c, k_build_cls0<u64>, std::max<u32>(16, std::min<u32>(L / 1024 + 1, 64)), 1024, sm_cls, (const u64*)sk,
+               P0, L, log2L, lut, seg, n, nchunk, chunk, chunks, nchunks, nfit, hist, nchunk * P0);
+        c.check();
+        const size_t sm_h = cls_smem_bytes<u64>(P0, L) + 4 * (size_t)P0;
+        smem_limit(k_hist_s32, sm_h, c.di);
+        launch(c, k_hist_s32, nchunk, S32_NT, sm_h, (const u64*)recs, (const Chunk*)chunks, (const u32*)nchunks, seg,
+               (const u64*)sk, (const u32*)st, (const u32*)lut, P0, L, hist, (const u64*)sfull, bid);
+        c.check();
+        launch(c, k_colscan, std::min<u32>(cdiv(P0, 32), 4 * c.di.sms), 1024, 0, hist, (const Seg*)seg,
+               (const u32*)nseg, P0, tot);
+        c.check();
+        launch(c, k_segscan<u64>, 1, 1024, 0, (const Seg*)seg, (const u32*)nseg, P0, tot, (const u64*)sk, 0u,
+               0xffffffffu, fit, nfit, fit_cap, (Bucket*)nullptr, (u32*)nullptr, 0u,
+               p > 1 ? (f > 1 ? int_counts : counts) : (u64*)nullptr, c.status);
+        c.check();
+        c.mark(3);
+        // a7: whole records to their bucket positions (buffer 1)
+        const size_t sm_s = 4 * (size_t)P0 + 16;
+        smem_limit(k_scatter_s32, sm_s, c.di);
+        launch(c, k_scatter_s32, nchunk, S32_NT, sm_s, (const u64*)recs, buf1, (const Chunk*)chunks,
+               (const u32*)nchunks, (const Seg*)seg, P0, (const u32*)hist, (const u32*)tot, (const u16*)bid);
+        c.check();
+        c.mark(4);
+        // a8: every bucket sorted by the full key into the caller's array
+        const size_t sm_b = 36 * (size_t)cap + 64;
+        smem_limit(k_bucket_sort_s32, sm_b, c.di);
+        launch(c, k_bucket_sort_s32, (u32)c.di.sms, S32_BS_NT, sm_b, (const Bucket*)fit, (const u32*)nfit, nfit + 1,
+               (const u64*)buf1, recs, cap, gidx);
+        c.check();
+        if (pc == 1 && p > 1) {  // internal buckets of a plain sort: one count
+            launch(c, k_fold_counts, 1, 32, 0, (const u64*)(f > 1 ? int_counts : counts), P0, 1u, counts);
+            c.check();
+        } else if (p > 1 && f > 1) {
+            launch(c, k_fold_counts, cdiv(p, 256), 256, 0, (const u64*)int_counts, f, p, counts);
+            c.check();
+        }
+        c.mark(5);
+    }
+};
+
 // ------------------------------------------------------------------ parameter validation
 inline int validate_impl(size_t n, int dtype, const ovs_params* prm) {
     if (!prm) return OVS_EINVAL;
-    if (dtype != OVS_U32 && dtype != OVS_I32 && dtype != OVS_F64) return OVS_EDTYPE;
+    if (dtype != OVS_U32 && dtype != OVS_I32 && dtype != OVS_F64 && dtype != OVS_S32) return OVS_EDTYPE;
+    if (dtype == OVS_S32 && prm->method != OVS_ROS) return OVS_EDTYPE;  // strings: ROS (f3)
     if (prm->p == 0) return OVS_EINVAL;
     // positions are u32 counted from a 32-byte-aligned base (the write-combining scatter adds up
     // to 7 slots): n + 32 must stay below 2^32
@@ -1173,6 +1330,7 @@ Out plan_i32_k(Ctx& c, void* keys, u32* vals, size_t n, const ovs_params* prm);
 Out plan_i32_v(Ctx& c, void* keys, u32* vals, size_t n, const ovs_params* prm);
 Out plan_f64_k(Ctx& c, void* keys, u32* vals, size_t n, const ovs_params* prm);
 Out plan_f64_v(Ctx& c, void* keys, u32* vals, size_t n, const ovs_params* prm);
+Out plan_s32_k(Ctx& c, void* keys, u32* vals, size_t n, const ovs_params* prm);
 int validate(size_t n, int dtype, const ovs_params* prm);
 DevInfo dev_info();
 extern thread_local std::string g_err;

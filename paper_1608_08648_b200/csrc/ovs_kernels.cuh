@@ -39,7 +39,8 @@ typedef uint16_t u16;
 // ------------------------------------------------------------------ key codecs
 // Keys are compared as "ordered bits": an order-preserving map to unsigned integers
 // (native < on u32; sign flip on i32; IEEE total order on f64 without NaN / -0, reading Q18).
-enum { DT_U32 = 0, DT_I32 = 1, DT_F64 = 2, DT_U64 = 3 /* internal, identity */ };
+enum { DT_U32 = 0, DT_I32 = 1, DT_F64 = 2, DT_U64 = 3 /* internal, identity */,
+       DT_S32 = 4 /* 32-byte strings: the key word is the big-endian 8-byte prefix */ };
 
 template <int DT> struct Codec;
 template <> struct Codec<DT_U32> {
@@ -62,6 +63,24 @@ template <> struct Codec<DT_U64> {
     __device__ __forceinline__ static U ord(U b) { return b; }
     __device__ __forceinline__ static U raw(U o) { return o; }
 };
+
+template <> struct Codec<DT_S32> {
+    typedef u64 U;
+    __device__ __forceinline__ static U ord(U b) { return b; }
+    __device__ __forceinline__ static U raw(U o) { return o; }
+};
+// a 64-bit word of a string record as a big-endian number (memcmp order = integer order)
+__device__ __forceinline__ u64 bswap64(u64 x) {
+    const u32 lo = (u32)x, hi = (u32)(x >> 32);
+    return ((u64)__byte_perm(lo, 0, 0x0123) << 32) | __byte_perm(hi, 0, 0x0123);
+}
+// the key word of item i: the ordered key (x holds keys) or, for strings (x holds the 32-byte
+// records as 4 words each), the big-endian prefix
+template <int DT>
+__device__ __forceinline__ typename Codec<DT>::U load_key(const typename Codec<DT>::U* x, u64 i) {
+    if constexpr (DT == DT_S32) return bswap64(x[4 * i]);
+    else return Codec<DT>::ord(x[i]);
+}
 
 template <class U> __device__ __host__ __forceinline__ U umax_of() { return (U)~(U)0; }
 template <class U> __device__ __forceinline__ u32 bitlen(U x) {
@@ -552,7 +571,7 @@ __global__ void __launch_bounds__(TK_NT) k_ros_take(const u32* bits, const u32* 
     if (rank >= m) return;
     const u64 c = ros_draw_c(seed, j, n);
     if (DIST && (c < offset || c >= offset + nl)) return;
-    const U k = Codec<DT>::ord(x[c - offset]);
+    const U k = load_key<DT>(x, c - offset);
     if (DIST) {
         put_rec<sizeof(U) == 8>(po, rank, (u64)k, c);
     } else if (sizeof(U) == 4) {
@@ -694,7 +713,7 @@ __global__ void __launch_bounds__(DT_NT) k_direct_take(const u64* minj, u64 n, c
         const u64 c = b0 + (u64)threadIdx.x * DT_PER + q;
         const u32 rk = rank++;
         if (DIST && (c < offset || c >= offset + nl)) continue;
-        const U k = Codec<DT>::ord(x[c - offset]);
+        const U k = load_key<DT>(x, c - offset);
         if (DIST) {
             put_rec<sizeof(U) == 8>(po, rk, (u64)k, c);
         } else if (sizeof(U) == 4) {
@@ -3276,6 +3295,306 @@ __global__ void k_push_bucket(Bucket* list, u32* nlist, u32 len) {
     b.lo = 0; b.hi = (u64)umax_of<U>();
     list[0] = b;
     *nlist = 1;
+}
+
+// ------------------------------------------------------------------ f3: 32-byte string keys
+// The paper's own workload: keys are 32-byte strings in memcmp order.  A
+// record is 4 words; word w as a big-endian number (bswap64) makes memcmp order the
+// lexicographic order of (w0, w1, w2, w3).  The pipeline is ROS's: the sample index set and its
+// sort run on (prefix w0, index) records (equal-prefix runs of the sorted sample re-ordered by the
+// full key, k_s32_fix*), the classifier uses the prefix table and compares the full key on a prefix
+// tie (classify_s32), the scatter moves whole 32-byte records (one sector each), and every bucket is
+// sorted on chip by the full key (k_bucket_sort_s32).
+struct K32 { u64 w[4]; };  // big-endian words
+__device__ __forceinline__ K32 load_k32(const u64* recs, u64 i) {
+    const uint4* r = (const uint4*)(recs + 4 * i);
+    const uint4 a = r[0], b = r[1];
+    K32 k;
+    k.w[0] = bswap64(((u64)a.y << 32) | a.x);
+    k.w[1] = bswap64(((u64)a.w << 32) | a.z);
+    k.w[2] = bswap64(((u64)b.y << 32) | b.x);
+    k.w[3] = bswap64(((u64)b.w << 32) | b.z);
+    return k;
+}
+// (a, ta) <lex (b, tb) by the full key, then the tag (reading Q5)
+__device__ __forceinline__ bool k32_less(const K32& a, u32 ta, const K32& b, u32 tb) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+        if (a.w[q] != b.w[q]) return a.w[q] < b.w[q];
+    return ta < tb;
+}
+
+// equal-prefix runs of the sorted sample records (key word = prefix, tags = original indices):
+// runs of <= 32 re-ordered by (full key, tag) by one thread; longer runs listed for k_s32_fix_long
+__global__ void k_s32_fix(const u64* pk, u32* tags, u32 m, const u64* recs, u32* list, u32* nlist, u32 cap,
+                          u32* status) {
+    PDL_PROLOGUE();
+    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i + 1 >= m) return;
+    if (pk[i] != pk[i + 1] || (i > 0 && pk[i - 1] == pk[i])) return;  // not the start of a run
+    u32 L = 2;
+    while (i + L < m && pk[i + L] == pk[i]) ++L;
+    if (L > 32) {
+        const u32 q = atomicAdd(nlist, 1u);
+        if (q < cap) { list[2 * q] = i; list[2 * q + 1] = L; } else st_set(status, ST_LIST_OVER);
+        return;
+    }
+    for (u32 a = 1; a < L; ++a) {  // insertion sort of the tags by (full key, tag)
+        const u32 t = tags[i + a];
+        const K32 kt = load_k32(recs, t);
+        u32 b = a;
+        while (b > 0) {
+            const u32 u = tags[i + b - 1];
+            if (!k32_less(kt, t, load_k32(recs, u), u)) break;
+            tags[i + b] = u;
+            --b;
+        }
+        tags[i + b] = t;
+    }
+}
+// long runs: one CTA each, bitonic sort of the run's tags by (full key, tag) in place in global
+// memory (all comparators ascending, so the length need not be a power of two)
+__global__ void __launch_bounds__(1024) k_s32_fix_long(u32* tags, const u64* recs, const u32* list, const u32* nlist) {
+    PDL_PROLOGUE();
+    const u32 nl = *nlist;
+    for (u32 r = blockIdx.x; r < nl; r += gridDim.x) {
+        u32* t = tags + list[2 * r];
+        const u32 len = list[2 * r + 1];
+        u32 N = 1;
+        while (N < len) N <<= 1;
+        auto cx = [&](u32 x, u32 y) {
+            const u32 a = t[x], b = t[y];
+            if (k32_less(load_k32(recs, b), b, load_k32(recs, a), a)) { t[x] = b; t[y] = a; }
+        };
+        for (u32 kk = 2; kk <= N; kk <<= 1) {
+            const u32 hk = kk >> 1;
+            for (u32 q = threadIdx.x; q < N / 2; q += blockDim.x) {
+                const u32 blk = q / hk, off = q % hk;
+                const u32 x = blk * kk + off, y = blk * kk + kk - 1 - off;
+                if (y < len) cx(x, y);
+            }
+            __threadfence_block();
+            __syncthreads();
+            for (u32 j = kk >> 2; j > 0; j >>= 1) {
+                for (u32 q = threadIdx.x; q < N / 2; q += blockDim.x) {
+                    const u32 x = (q / j) * 2 * j + (q % j), y = x + j;
+                    if (y < len) cx(x, y);
+                }
+                __threadfence_block();
+                __syncthreads();
+            }
+        }
+    }
+}
+
+// full keys of the splitters (for the classifier's prefix ties and the report): rows of 4 words
+// (big-endian) + the raw 32-byte records
+__global__ void k_s32_splitters(const u32* st, u32 nsp, const u64* recs, u64* sfull, u64* sraw) {
+    PDL_PROLOGUE();
+    const u32 q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nsp) return;
+    const K32 k = load_k32(recs, st[q]);
+#pragma unroll
+    for (int w = 0; w < 4; ++w) sfull[4 * (size_t)q + w] = k.w[w];
+    if (sraw)
+#pragma unroll
+        for (int w = 0; w < 4; ++w) sraw[4 * (size_t)q + w] = recs[4 * (size_t)st[q] + w];
+}
+
+// bucket(key, tag) = #{q : S[q] <lex (key, tag)}: the prefix table narrows to the splitters with
+// an equal prefix (or none), the full key and the tag decide among those
+__device__ __forceinline__ u32 classify_s32(const ClsView<u64>& c, const u64* sfull, const K32& k, u32 tag) {
+    if (c.P <= 1) return 0;
+    const u64 pre = k.w[0];
+    u32 lo, cnt;
+    if (pre < c.base) return 0;
+    const u64 x = pre - c.base;
+    const u64 d = x >> c.shift;
+    if (d >= (u64)c.L) return c.P - 1;
+    const u32 e = c.lut[(u32)d];
+    lo = e & 0x1fffu;
+    cnt = (e >> 13) & 7u;
+    if (cnt == 7) cnt = (c.lut[(u32)d + 1] & 0x1fffu) - lo;
+    while (cnt > 0) {
+        const u32 half = cnt >> 1, mid = lo + half;
+        const u64 s = c.sk[mid];
+        bool less;
+        if (s != pre) less = s < pre;
+        else {
+            K32 sk;
+#pragma unroll
+            for (int w = 0; w < 4; ++w) sk.w[w] = sfull[4 * (size_t)mid + w];
+            less = k32_less(sk, c.st[mid], k, tag);
+        }
+        if (less) { lo = mid + 1; cnt -= half + 1; } else { cnt = half; }
+    }
+    return lo;
+}
+
+// a5+a6 for strings: per chunk histogram rows and every record's bucket id (u16)
+constexpr int S32_NT = 512;
+__global__ void __launch_bounds__(S32_NT) k_hist_s32(const u64* recs, const Chunk* chunks, const u32* nchunks,
+                                                     Seg* segs, const u64* sk_pool, const u32* st_pool,
+                                                     const u32* lut_pool, u32 PS, u32 LS, u32* hist, const u64* sfull,
+                                                     u16* bid) {
+    PDL_PROLOGUE();
+    extern __shared__ __align__(16) char smem[];
+    const u32 nc = *nchunks;
+    u32 loaded = 0xffffffffu;
+    for (u32 c = blockIdx.x; c < nc; c += gridDim.x) {
+        const Chunk ch = chunks[c];
+        const Seg sg = segs[ch.seg];
+        ClsView<u64> cls = load_cls<u64>(smem, sg, ch.seg, sk_pool, st_pool, lut_pool, PS, LS, loaded != ch.seg);
+        loaded = ch.seg;
+        u32* h = (u32*)(smem + cls_smem_bytes<u64>(PS, LS));
+        for (u32 i = threadIdx.x; i < sg.P; i += S32_NT) h[i] = 0;
+        __syncthreads();
+        for (u32 i0 = ch.beg; i0 < ch.end; i0 += 4 * S32_NT) {
+            K32 k[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const u32 i = i0 + u * S32_NT + threadIdx.x;
+                if (i < ch.end) k[u] = load_k32(recs, i);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const u32 i = i0 + u * S32_NT + threadIdx.x;
+                if (i < ch.end) {
+                    const u32 b = classify_s32(cls, sfull, k[u], i);
+                    atomicAdd(&h[b], 1u);
+                    bid[i] = (u16)b;
+                }
+            }
+        }
+        __syncthreads();
+        u32* row = hist + (size_t)c * PS;
+        for (u32 b = threadIdx.x; b < sg.P; b += S32_NT) row[b] = h[b];
+        __syncthreads();
+    }
+}
+
+// a7 for strings: every record (one 32-byte sector) stored at its bucket cursor
+__global__ void __launch_bounds__(S32_NT) k_scatter_s32(const u64* src, u64* dst, const Chunk* chunks,
+                                                        const u32* nchunks, const Seg* segs, u32 PS, const u32* hist,
+                                                        const u32* tot_pool, const u16* bid) {
+    PDL_PROLOGUE();
+    extern __shared__ __align__(16) char smem[];
+    u32* cur = (u32*)smem;
+    const u32 nc = *nchunks;
+    for (u32 c = blockIdx.x; c < nc; c += gridDim.x) {
+        const Chunk ch = chunks[c];
+        const Seg sg = segs[ch.seg];
+        const u32* hrow = hist + (size_t)c * PS;
+        const u32* bst = tot_pool + (size_t)ch.seg * (PS + 1);
+        for (u32 b = threadIdx.x; b < sg.P; b += S32_NT) cur[b] = sg.beg + bst[b] + hrow[b];
+        __syncthreads();
+        for (u32 i0 = ch.beg; i0 < ch.end; i0 += 4 * S32_NT) {
+            uint4 r[4][2];
+            u32 b[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const u32 i = i0 + u * S32_NT + threadIdx.x;
+                if (i < ch.end) {
+                    const uint4* s4 = (const uint4*)(src + 4 * (size_t)i);
+                    r[u][0] = s4[0]; r[u][1] = s4[1];
+                    b[u] = bid[i];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const u32 i = i0 + u * S32_NT + threadIdx.x;
+                if (i < ch.end) {
+                    const u32 pos = atomicAdd(&cur[b[u]], 1u);
+                    uint4* d4 = (uint4*)(dst + 4 * (size_t)pos);
+                    d4[0] = r[u][0]; d4[1] = r[u][1];
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// a8 for strings: persistent CTAs over the bucket list; a bucket of <= cap records is loaded into
+// shared memory as big-endian words and its index array sorted by the full key (bitonic network,
+// all comparators ascending: any length); larger buckets (outliers of the refined partition) are
+// sorted through an index array in global memory (idx) the same way, slower.  Output: buffer 0.
+constexpr int S32_BS_NT = 512;
+__global__ void __launch_bounds__(S32_BS_NT, 1) k_bucket_sort_s32(const Bucket* list, const u32* nlist, u32* ticket,
+                                                                  const u64* src, u64* dst, u32 cap, u32* gidx) {
+    PDL_PROLOGUE();
+    extern __shared__ __align__(16) char smem[];
+    u64* kw = (u64*)smem;                         // cap x 4 words (big-endian)
+    u32* ix = (u32*)(smem + 32 * (size_t)cap);    // cap indices
+    __shared__ u32 s_work;
+    const u32 nl = *nlist;
+    for (;;) {
+        if (threadIdx.x == 0) s_work = atomicAdd(ticket, 1u);
+        __syncthreads();
+        const u32 w = s_work;
+        __syncthreads();
+        if (w >= nl) break;
+        const Bucket bk = list[w];
+        const u32 m = bk.len;
+        const u64* s = src + 4 * (size_t)bk.beg;
+        u64* d = dst + 4 * (size_t)bk.beg;
+        const bool on_chip = m <= cap;
+        u32* id = on_chip ? ix : gidx + bk.beg;
+        auto key = [&](u32 r, int q) -> u64 { return on_chip ? kw[4 * (size_t)r + q] : bswap64(s[4 * (size_t)r + q]); };
+        for (u32 r = threadIdx.x; r < m; r += S32_BS_NT) {
+            if (on_chip) {
+                const uint4* s4 = (const uint4*)(s + 4 * (size_t)r);
+                const uint4 a = s4[0], b = s4[1];
+                kw[4 * (size_t)r + 0] = bswap64(((u64)a.y << 32) | a.x);
+                kw[4 * (size_t)r + 1] = bswap64(((u64)a.w << 32) | a.z);
+                kw[4 * (size_t)r + 2] = bswap64(((u64)b.y << 32) | b.x);
+                kw[4 * (size_t)r + 3] = bswap64(((u64)b.w << 32) | b.z);
+            }
+            id[r] = r;
+        }
+        __threadfence_block();
+        __syncthreads();
+        auto less = [&](u32 a, u32 b) -> bool {  // record a < record b (ties: keep either)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const u64 x = key(a, q), y = key(b, q);
+                if (x != y) return x < y;
+            }
+            return false;
+        };
+        u32 N = 1;
+        while (N < m) N <<= 1;
+        for (u32 kk = 2; kk <= N; kk <<= 1) {
+            const u32 hk = kk >> 1;
+            for (u32 t = threadIdx.x; t < N / 2; t += S32_BS_NT) {
+                const u32 blk = t / hk, off = t % hk;
+                const u32 x = blk * kk + off, y = blk * kk + kk - 1 - off;
+                if (y < m) {
+                    const u32 a = id[x], b = id[y];
+                    if (less(b, a)) { id[x] = b; id[y] = a; }
+                }
+            }
+            __threadfence_block();
+            __syncthreads();
+            for (u32 j = kk >> 2; j > 0; j >>= 1) {
+                for (u32 t = threadIdx.x; t < N / 2; t += S32_BS_NT) {
+                    const u32 x = (t / j) * 2 * j + (t % j), y = x + j;
+                    if (y < m) {
+                        const u32 a = id[x], b = id[y];
+                        if (less(b, a)) { id[x] = b; id[y] = a; }
+                    }
+                }
+                __threadfence_block();
+                __syncthreads();
+            }
+        }
+        // write out in sorted order (the raw records)
+        for (u32 r = threadIdx.x; r < m; r += S32_BS_NT) {
+            const uint4* s4 = (const uint4*)(s + 4 * (size_t)id[r]);
+            uint4* d4 = (uint4*)(d + 4 * (size_t)r);
+            d4[0] = s4[0]; d4[1] = s4[1];
+        }
+        __syncthreads();
+    }
 }
 
 }  // namespace

@@ -170,7 +170,10 @@ template <class U, bool KV> static size_t bucket_smem(u32 cap) {
 #define OVS_WC_NT 1024
 #endif
 // write-combining scatter: WC_NT threads x WC_ITEMS (u32) keys per sub-tile
-constexpr int WC_NT = OVS_WC_NT, WC_ITEMS = 8192 / OVS_WC_NT;
+#ifndef OVS_WC_TILE
+#define OVS_WC_TILE 8192
+#endif
+constexpr int WC_NT = OVS_WC_NT, WC_ITEMS = OVS_WC_TILE / OVS_WC_NT;
 #ifndef OVS_SEL_PER_BUCKET
 #define OVS_SEL_PER_BUCKET 2048u
 #endif

@@ -13,6 +13,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cuda_runtime.h>
+#include <type_traits>
 
 namespace ovs {
 // internal linkage: every translation unit gets its own copy of the kernels it launches
@@ -1161,39 +1162,37 @@ __global__ void __launch_bounds__(NT, OVS_HIST_MINB) k_hist(Bufs<typename Codec<
             const u32 idx = u * NT + threadIdx.x;
             nr[u] = idx < nv ? __ldcs(a4 + idx) : make_uint4(0, 0, 0, 0);
         }
+        u16* const bo = bid ? bid + pbeg + head : nullptr;
+        const bool bo_al = V == 4 && (((uintptr_t)bo) & 7u) == 0;  // the V ids of a vector as one 8-byte store
         for (u32 v0 = 0; v0 < nv; v0 += NT * UNR) {
-            U kk[NB];
-            u32 vm = 0;
+            // (full batches, all but the last, take the variant without per-vector bound tests)
+            auto batch = [&](auto full_t) {
+                constexpr bool FULL = decltype(full_t)::value;
+                U kk[NB];
 #pragma unroll
-            for (int u = 0; u < UNR; ++u) {
-                const u32 idx = v0 + u * NT + threadIdx.x;
-                const uint4 r = nr[u];
-                if (idx < nv) vm |= ((1u << V) - 1) << (u * V);
-                const U* e = (const U*)&r;
+                for (int u = 0; u < UNR; ++u) {
+                    const uint4 r = nr[u];
+                    const U* e = (const U*)&r;
 #pragma unroll
-                for (u32 x = 0; x < V; ++x) kk[u * V + x] = LEVEL0 ? Codec<DT>::ord(e[x]) : e[x];
-            }
+                    for (u32 x = 0; x < V; ++x) kk[u * V + x] = LEVEL0 ? Codec<DT>::ord(e[x]) : e[x];
+                }
 #pragma unroll
-            for (int u = 0; u < UNR; ++u) {
-                const u32 idx = v0 + NT * UNR + u * NT + threadIdx.x;
-                nr[u] = idx < nv ? __ldcs(a4 + idx) : make_uint4(0, 0, 0, 0);
-            }
-            u32 bb[NB];
-            classify_n<U, NB>(cls, kk, [&](int j) -> u32 {
-                return tag_at(head + (v0 + (j / V) * NT + threadIdx.x) * V + (j % V));
-            }, bb);
-#pragma unroll
-            for (int j = 0; j < NB; ++j) {
-                if (vm & (1u << j)) atomicAdd(&h[bb[j]], 1u);
-            }
-            if (bid) {
-                // the V ids of a vector as one 2V-byte store
-                u16* bo = bid + pbeg + head;
+                for (int u = 0; u < UNR; ++u) {
+                    const u32 idx = v0 + NT * UNR + u * NT + threadIdx.x;
+                    nr[u] = idx < nv ? __ldcs(a4 + idx) : make_uint4(0, 0, 0, 0);
+                }
+                u32 bb[NB];
+                classify_n<U, NB>(cls, kk, [&](int j) -> u32 {
+                    return tag_at(head + (v0 + (j / V) * NT + threadIdx.x) * V + (j % V));
+                }, bb);
 #pragma unroll
                 for (int u = 0; u < UNR; ++u) {
                     const u32 idx = v0 + u * NT + threadIdx.x;
-                    if (idx < nv) {
-                        if (V == 4 && (((uintptr_t)(bo + idx * V)) & 7u) == 0) {
+                    if (!FULL && idx >= nv) continue;
+#pragma unroll
+                    for (u32 x = 0; x < V; ++x) atomicAdd(&h[bb[u * V + x]], 1u);
+                    if (bo) {
+                        if (bo_al) {
                             uint2 w;
                             w.x = bb[u * V] | (bb[u * V + 1] << 16);
                             w.y = bb[u * V + 2 % V] | (bb[u * V + 3 % V] << 16);
@@ -1204,7 +1203,9 @@ __global__ void __launch_bounds__(NT, OVS_HIST_MINB) k_hist(Bufs<typename Codec<
                         }
                     }
                 }
-            }
+            };
+            if (v0 + NT * UNR <= nv) batch(std::true_type{});
+            else batch(std::false_type{});
         }
         for (u32 o = head + nv * V + threadIdx.x; o < m; o += NT) body(src[pbeg + o], o);
         __syncthreads();
@@ -1565,23 +1566,29 @@ __global__ void __launch_bounds__(NT, 1) k_scatter_wc(Bufs<typename Codec<DT>::U
             // P1: a position per key; keys inside their bucket's current sector are parked in it,
             // the others (rare: a bucket whose sector fills up within this sub-tile) are marked
             u32 pos[ITEMS], sv[ITEMS], out = 0;
+            // (full sub-tiles, all but a chunk's last, take the variant without per-item validity tests)
+            auto p1 = [&](auto full_t) {
+                constexpr bool FULL = decltype(full_t)::value;
 #pragma unroll
-            for (u32 j = 0; j < ITEMS; ++j) {
-                const u32 b = (id[j / 2] >> (16 * (j & 1))) & 0xffffu;
-                if (LEVEL0) k[j] = Codec<DT>::ord(k[j]);
-                if (vmask & (1u << j)) pos[j] = atomicAdd(&q[b], 1u);
-            }
-#pragma unroll
-            for (u32 j = 0; j < ITEMS; ++j) sv[j] = sb[(id[j / 2] >> (16 * (j & 1))) & 0xffffu];
-#pragma unroll
-            for (u32 j = 0; j < ITEMS; ++j) {
-                const u32 b = (id[j / 2] >> (16 * (j & 1))) & 0xffffu;
-                const u32 d = pos[j] - (sv[j] & ~(SV - 1));
-                if (vmask & (1u << j)) {
-                    if (d < SV) wc[(size_t)b * SV + d] = k[j];
-                    else out |= 1u << j;
+                for (u32 j = 0; j < ITEMS; ++j) {
+                    const u32 b = (id[j / 2] >> (16 * (j & 1))) & 0xffffu;
+                    if (LEVEL0) k[j] = Codec<DT>::ord(k[j]);
+                    if (FULL || (vmask & (1u << j))) pos[j] = atomicAdd(&q[b], 1u);
                 }
-            }
+#pragma unroll
+                for (u32 j = 0; j < ITEMS; ++j) sv[j] = sb[(id[j / 2] >> (16 * (j & 1))) & 0xffffu];
+#pragma unroll
+                for (u32 j = 0; j < ITEMS; ++j) {
+                    const u32 b = (id[j / 2] >> (16 * (j & 1))) & 0xffffu;
+                    const u32 d = pos[j] - (sv[j] & ~(SV - 1));
+                    if (FULL || (vmask & (1u << j))) {
+                        if (d < SV) wc[(size_t)b * SV + d] = k[j];
+                        else out |= 1u << j;
+                    }
+                }
+            };
+            if (nt == TS) p1(std::true_type{});
+            else p1(std::false_type{});
             __syncthreads();
             // P2: every bucket whose current sector is complete is flushed by the thread that owns
             // the bucket (one check per bucket instead of per key); keys of complete sectors past it

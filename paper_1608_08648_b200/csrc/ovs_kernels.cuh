@@ -826,6 +826,39 @@ __device__ __forceinline__ void warp_bitonic(E (&a)[R]) {
     }
 }
 
+// One element per thread (N == blockDim.x, a power of two >= 32): the comparators of distance
+// j < 32 exchange through warp shuffles (no block barrier); only j >= 32 goes through shared
+// memory.  55 barrier-separated steps of the plain network become 15 for N = 1024.
+template <class U>
+__device__ void cta_bitonic_1pt(U* tk, u32* tt, u32 N) {
+    const u32 e = threadIdx.x;
+    U k = tk[e];
+    u32 t = tt[e];
+    for (u32 kk = 2; kk <= N; kk <<= 1) {
+        for (u32 j = kk >> 1; j > 0; j >>= 1) {
+            U ok;
+            u32 ot;
+            if (j >= 32) {
+                __syncthreads();
+                tk[e] = k; tt[e] = t;
+                __syncthreads();
+                ok = tk[e ^ j]; ot = tt[e ^ j];
+            } else {
+                ok = shfl_xor_any(k, (int)j);
+                ot = __shfl_xor_sync(0xffffffffu, t, (int)j);
+            }
+            const bool asc = (e & kk) == 0, lower = (e & j) == 0;
+            const bool o_less = ok < k || (ok == k && ot < t);
+            // the lower slot of an ascending pair keeps the minimum, etc.
+            const bool take = (lower == asc) ? o_less : (!o_less && !(ok == k && ot == t));
+            if (take) { k = ok; t = ot; }
+        }
+    }
+    __syncthreads();
+    tk[e] = k; tt[e] = t;
+    __syncthreads();
+}
+
 // ------------------------------------------------------------------ a3: sample sort (coarse level)
 // The m sample records (key word, tag) are sorted by (key, tag) in two steps: G coarse buckets,
 // then every coarse bucket by the bucket sorter.  Coarse splitter i = CS[(i+1)Q/G - 1], CS =
@@ -864,7 +897,8 @@ __global__ void __launch_bounds__(1024) k_sel_count(const u64* tk, const u32* tt
             qt[i] = i < Q ? (TAG ? tt[r] : 0u) : 0xffffffffu;
         }
         __syncthreads();
-        cta_bitonic_kt<u64>(qk, qt, N);
+        if (N == blockDim.x) cta_bitonic_1pt<u64>(qk, qt, N);
+        else cta_bitonic_kt<u64>(qk, qt, N);
         // coarse splitters in place at the front (reads before writes: ranks are increasing)
         u64 ck = 0;
         u32 ct = 0;
@@ -1082,7 +1116,20 @@ __device__ __forceinline__ void for_items(const U* __restrict__ src, u32 beg, u3
     if (threadIdx.x < head) f(src[beg + threadIdx.x], threadIdx.x);
     const uint4* a = (const uint4*)(src + beg + head);
     const u32 nv = (m - head) / V;
-    for (u32 v0 = 0; v0 < nv; v0 += NT * UNR) {
+    u32 v0 = 0;
+    for (; v0 + NT * UNR <= nv; v0 += NT * UNR) {  // full batches: no bound tests
+        uint4 r[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) r[u] = STREAM ? __ldcs(a + v0 + u * NT + threadIdx.x) : a[v0 + u * NT + threadIdx.x];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const u32 idx = v0 + u * NT + threadIdx.x;
+            const U* e = (const U*)&r[u];
+#pragma unroll
+            for (u32 q = 0; q < V; ++q) f(e[q], head + idx * V + q);
+        }
+    }
+    if (v0 < nv) {
         uint4 r[UNR];
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {

@@ -178,7 +178,7 @@ int ovs_dist_sort_virtual(int world, const void* const* d_keys, const uint32_t* 
                           int dtype, const ovs_params* prm, void* const* d_out_keys, uint32_t* const* d_out_vals,
                           const size_t* out_capacity, size_t* n_out, void* const* d_ws, const size_t* ws_bytes,
                           void* const* d_win, size_t win_bytes, void* stream, uint64_t* counts, void* split_keys,
-                          uint64_t* split_tags);
+                          uint64_t* split_tags, float* rank_ms /* optional: each rank's device time */);
 size_t ovs_dist_virtual_workspace_bytes(int world, const size_t* n_local, int dtype, int with_values,
                                         const ovs_params* prm, const size_t* out_capacity, size_t win_bytes);
 

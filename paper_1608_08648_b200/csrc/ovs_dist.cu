@@ -437,7 +437,7 @@ int ovs_dist_sort_virtual(int world, const void* const* d_keys, const uint32_t* 
                           int dtype, const ovs_params* prm, void* const* d_out_keys, uint32_t* const* d_out_vals,
                           const size_t* out_capacity, size_t* n_out, void* const* d_ws, const size_t* ws_bytes,
                           void* const* d_win, size_t win_bytes, void* stream, uint64_t* counts, void* split_keys,
-                          uint64_t* split_tags) {
+                          uint64_t* split_tags, float* rank_ms) {
     g_err.clear();
     if (world < 1 || !d_keys || !n_local || !d_out_keys || !out_capacity || !n_out || !d_ws || !ws_bytes || !d_win)
         return fail(OVS_EINVAL, "NULL argument");
@@ -470,8 +470,28 @@ int ovs_dist_sort_virtual(int world, const void* const* d_keys, const uint32_t* 
             OVS_CK(cudaMemsetAsync(cx[r].status, 0, 4, st));
             off += n_local[r];
         }
-        for (int r = 0; r < world; ++r) runs[r]->sample(d_peer);
-        for (int r = 0; r < world; ++r) { runs[r]->select((const char*)d_win[r]); runs[r]->count(d_peer); }
+        // per-rank device time of every phase (rank_ms): events around each rank's launches
+        std::vector<cudaEvent_t> evs;
+        auto tick = [&]() -> cudaEvent_t {
+            if (!rank_ms) return nullptr;
+            cudaEvent_t e;
+            OVS_CK(cudaEventCreate(&e));
+            OVS_CK(cudaEventRecord(e, st));
+            evs.push_back(e);
+            return e;
+        };
+        std::vector<std::pair<cudaEvent_t, cudaEvent_t>> span[3];  // per phase group, per rank
+        for (int r = 0; r < world; ++r) {
+            cudaEvent_t a = tick();
+            runs[r]->sample(d_peer);
+            span[0].push_back({a, tick()});
+        }
+        for (int r = 0; r < world; ++r) {
+            cudaEvent_t a = tick();
+            runs[r]->select((const char*)d_win[r]);
+            runs[r]->count(d_peer);
+            span[1].push_back({a, tick()});
+        }
         std::vector<u32> C((size_t)world * p);
         OVS_CK(cudaMemcpyAsync(C.data(), (const char*)d_win[0] + W.C, 4 * C.size(), cudaMemcpyDeviceToHost, st));
         OVS_CK(cudaStreamSynchronize(st));
@@ -486,11 +506,21 @@ int ovs_dist_sort_virtual(int world, const void* const* d_keys, const uint32_t* 
                 cudaFree(d_peer);
                 return fail(OVS_ECAPACITY, "rank " + std::to_string(r) + " receives " + std::to_string(P[0].recv[r]));
             }
+        std::vector<std::vector<u32>> hsv(world);
         for (int r = 0; r < world; ++r) {
-            OVS_CK(cudaMallocHost(&hs[r], 4 * (4 * (size_t)p + 16)));
+            hsv[r].assign(4 * (size_t)p + 16, 0);
+            hs[r] = hsv[r].data();
+            cudaEvent_t a = tick();
             runs[r]->scatter(d_peer, P[r], hs[r]);
+            OVS_CK(cudaStreamSynchronize(st));  // pageable staging: keep it alive until the upload is done
+            span[2].push_back({a, tick()});
         }
-        for (int r = 0; r < world; ++r) runs[r]->finish((const char*)d_win[r], (u32)(P[r].desc.size() / 3));
+        std::vector<std::pair<cudaEvent_t, cudaEvent_t>> fin;
+        for (int r = 0; r < world; ++r) {
+            cudaEvent_t a = tick();
+            runs[r]->finish((const char*)d_win[r], (u32)(P[r].desc.size() / 3));
+            fin.push_back({a, tick()});
+        }
         if (counts)
             for (u32 b = 0; b < p; ++b) {
                 u64 t = 0;
@@ -504,7 +534,18 @@ int ovs_dist_sort_virtual(int world, const void* const* d_keys, const uint32_t* 
             u32 x = 0;
             OVS_CK(cudaMemcpy(&x, cx[r].status, 4, cudaMemcpyDeviceToHost));
             stv |= x;
-            cudaFreeHost(hs[r]);
+        }
+        if (rank_ms) {
+            for (int r = 0; r < world; ++r) {
+                float tot = 0, ms = 0;
+                for (int g = 0; g < 3; ++g) {
+                    OVS_CK(cudaEventElapsedTime(&ms, span[g][r].first, span[g][r].second));
+                    tot += ms;
+                }
+                OVS_CK(cudaEventElapsedTime(&ms, fin[r].first, fin[r].second));
+                rank_ms[r] = tot + ms;
+            }
+            for (auto e : evs) cudaEventDestroy(e);
         }
         cudaFree(d_peer);
         if (stv) return fail(OVS_EINTERNAL, "device-side check failed (status bits " + std::to_string(stv) + ")");

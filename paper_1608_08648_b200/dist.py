@@ -48,7 +48,7 @@ def _ensure_sigs():
     L.ovs_dist_plan.restype = i32
     L.ovs_dist_plan.argtypes = [vp, i32, u32, i32, vp, vp]
     L.ovs_dist_sort_virtual.restype = i32
-    L.ovs_dist_sort_virtual.argtypes = [i32, vp, vp, vp, i32, P, vp, vp, vp, vp, vp, vp, vp, sz, vp, vp, vp, vp]
+    L.ovs_dist_sort_virtual.argtypes = [i32, vp, vp, vp, i32, P, vp, vp, vp, vp, vp, vp, vp, sz, vp, vp, vp, vp, vp]
     L.ovs_dist_virtual_workspace_bytes.restype = sz
     L.ovs_dist_virtual_workspace_bytes.argtypes = [i32, vp, i32, i32, P, vp, sz]
     L._dist_sigs = True
@@ -259,6 +259,7 @@ def _virtual_call(L, shards, vals, dt, prm, n_local, cap, world, kv, dev, p):
         return (ctypes.c_void_p * world)(*[t.data_ptr() for t in ts])
 
     n_out = np.zeros(world, dtype=np.uint64)
+    rank_ms = np.zeros(world, dtype=np.float32)
     ws_bytes = np.full(world, wsb, dtype=np.uint64)
     counts = np.zeros(p, dtype=np.uint64)
     sk = np.zeros(p - 1, dtype=_NP[dt])
@@ -267,7 +268,7 @@ def _virtual_call(L, shards, vals, dt, prm, n_local, cap, world, kv, dev, p):
                                  ctypes.byref(prm), arr(outs), arr(vouts) if kv else None, out_cap.ctypes.data,
                                  n_out.ctypes.data, arr(wss), ws_bytes.ctypes.data, arr(wins), win_bytes,
                                  ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream), counts.ctypes.data,
-                                 sk.ctypes.data, st.ctypes.data)
+                                 sk.ctypes.data, st.ctypes.data, rank_ms.ctypes.data)
     if rc == OVS_ECAPACITY:
         return int(n_out.max())
     if rc != OVS_OK:
@@ -275,4 +276,5 @@ def _virtual_call(L, shards, vals, dt, prm, n_local, cap, world, kv, dev, p):
     torch.cuda.synchronize(dev)
     out = torch.cat([outs[r][:int(n_out[r])] for r in range(world)])
     vout = torch.cat([vouts[r][:int(n_out[r])] for r in range(world)]) if kv else None
+    dist_sort_virtual.last_rank_ms = rank_ms.tolist()  # each emulated rank's device time
     return out, vout, counts, sk, st, n_out

@@ -7,6 +7,8 @@
 #include <nccl.h>
 #include <nccl_device.h>
 
+#include <cstdlib>
+
 using namespace ovs;
 
 struct ovs_comm {
@@ -544,6 +546,12 @@ int ovs_dist_sort_virtual(int world, const void* const* d_keys, const uint32_t* 
                 }
                 OVS_CK(cudaEventElapsedTime(&ms, fin[r].first, fin[r].second));
                 rank_ms[r] = tot + ms;
+                if (std::getenv("OVS_DIST_PHASES")) {  // experiments: the phase split of every rank
+                    float ph[4] = {0, 0, 0, ms};
+                    for (int g = 0; g < 3; ++g) OVS_CK(cudaEventElapsedTime(&ph[g], span[g][r].first, span[g][r].second));
+                    std::fprintf(stderr, "rank %d: sample %.3f select+count %.3f scatter %.3f finish %.3f ms\n", r, ph[0],
+                                 ph[1], ph[2], ph[3]);
+                }
             }
             for (auto e : evs) cudaEventDestroy(e);
         }

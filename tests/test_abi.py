@@ -105,3 +105,30 @@ def test_dist_plan_validation():
     assert dst.tolist() == [1, 3, 5, 1, 3, 5] and recv.tolist() == [6, 6]
     with pytest.raises(Exception):
         exchange_plan(np.ones((2, 5), dtype=np.uint32), 2, 5, 0)
+
+
+def test_workspace_bytes_new_dtypes_and_flags():
+    """Round-2 surface (host-only checks): 32-byte strings (OVS_S32) are ROS keys-only; the DRO merge
+    flag (OVS_DRO_MERGE) is accepted for DRO; unknown flags are rejected; every ps - 1 <= n is valid
+    (samples up to the whole input)."""
+    import paper_1608_08648_b200 as ovs
+    P = lambda **kw: _prm(ovs, **kw)
+    assert ovs.workspace_bytes(1 << 20, ovs.OVS_S32, False, P(p=256, s=32)) > 32 * (1 << 20)
+    assert ovs.workspace_bytes(1 << 20, ovs.OVS_S32, True, P(p=256, s=32)) == 0          # values
+    assert ovs.workspace_bytes(1 << 20, ovs.OVS_S32, False, P(method="dro", p=16, s=2)) == 0  # DRO
+    m = ovs.params("dro", 16, 2, 1, merge=True)
+    assert m.flags == ovs.OVS_DRO_MERGE
+    assert ovs.workspace_bytes(1 << 20, ovs.OVS_U32, False, m) > 0
+    bad = ovs.params("dro", 16, 2, 1)
+    bad.flags = 8
+    assert ovs.workspace_bytes(1 << 20, ovs.OVS_U32, False, bad) == 0
+    assert ovs.workspace_bytes(1 << 20, ovs.OVS_U32, False, P(p=64, s=(1 << 20) // 64)) > 0  # ps - 1 = n - 1
+    assert ovs.workspace_bytes(1 << 20, ovs.OVS_U32, False, P(p=1, s=1)) > 0
+    assert ovs.workspace_bytes((1 << 32) - 20, ovs.OVS_U32, False, P()) == 0            # n + 32 >= 2^32
+
+
+def test_device_status_rejects_null():
+    import paper_1608_08648_b200 as ovs
+    L = ovs.lib()
+    st = ctypes.c_uint32(7)
+    assert L.ovs_device_status(None, None, ctypes.byref(st), 0) == ovs.OVS_EINVAL

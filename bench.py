@@ -225,7 +225,8 @@ def main():
     ap.add_argument("--s", type=int, default=WORKLOAD["s"])
     ap.add_argument("--n", type=int, default=WORKLOAD["n"])
     ap.add_argument("--ref-n", type=int, default=1 << 22)
-    ap.add_argument("--cpu-n", type=int, default=1 << 26, help="keys of the cpu_baseline oracle run")
+    ap.add_argument("--cpu-n", type=int, default=1 << 27, help="keys of the cpu_baseline oracle run (default: "
+                    "the whole workload, ~20 s on one core)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--force-dist", action="store_true", help="run the distributed path even at N=1 (tests)")

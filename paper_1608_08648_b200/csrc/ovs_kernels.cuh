@@ -1755,33 +1755,6 @@ __global__ void __launch_bounds__(NT, 1) k_scatter_wc(Bufs<typename Codec<DT>::U
     if (DIST) __threadfence_system();
 }
 
-// ------------------------------------------------------------------ bulk async copies (TMA)
-// 1-D cp.async.bulk global -> shared with mbarrier completion (the Blackwell copy engine; one
-// thread issues a whole tile, the other threads wait on the barrier's phase).
-__device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(u64* bar, u32 count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ void mbar_expect_tx(u64* bar, u32 bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, u32 bytes, u64* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(u64* bar, u32 parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-
 // ------------------------------------------------------------------ level 1: buckets far over capacity
 // A list of buckets much larger than one SM's shared memory is re-split by the whole GPU ("the
 // split keys are to be sorted ... recursively by this same extended method"): every
@@ -1964,9 +1937,6 @@ __global__ void __launch_bounds__(1024) k_internal_sample(Bufs<typename Codec<DT
 #define OVS_BS_NT 512
 #endif
 constexpr int BS_NT = OVS_BS_NT;
-#ifndef OVS_BS_TMAHIST  // 32-bit keys: bucket bulk-copied to shared memory for the digit histogram
-#define OVS_BS_TMAHIST 0
-#endif
 #ifndef OVS_BS_PF2  // prefetch two buckets ahead into L2
 #define OVS_BS_PF2 0
 #endif
@@ -2180,9 +2150,6 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
     // memory; only resplit children go through the CTA's stack in global memory.
     __shared__ Bucket s_cur, s_nxt;
     __shared__ u32 s_base, s_first;
-    __shared__ __align__(8) u64 s_bar;  // bulk-copy completion (OVS_BS_TMAHIST)
-    u32 s_phase_bit = 0;                // its phase parity, tracked by every thread
-    if (OVS_BS_TMAHIST && threadIdx.x == 0) { mbar_init(&s_bar, 1); fence_mbar_init(); }
     if (threadIdx.x == 0) {
         s_first = 1;
         s_work = atomicAdd(ticket, 1u);
@@ -2461,39 +2428,10 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                 __syncthreads();
                 BS_PROBE(2)
                 // 1. digit histogram
-                bool hist_done = false;
-                if constexpr (!KV && sizeof(U) == 4 && OVS_BS_TMAHIST) {
-                    // the bucket's 16-byte-aligned cover copied into the (free) item array by one bulk
-                    // copy (TMA engine, mbarrier completion); the histogram then reads shared memory
-                    const uintptr_t a0 = (uintptr_t)(src + bk.beg) & ~(uintptr_t)15;
-                    const uintptr_t a1 = ((uintptr_t)(src + bk.beg + m) + 15) & ~(uintptr_t)15;
-                    const u32 bytes = (u32)(a1 - a0), off = (u32)(((uintptr_t)(src + bk.beg) & 15u) / 4u);
-                    if (bytes <= 4 * (cap + 16)) {
-                        if (threadIdx.x == 0) {
-                            fence_proxy_async();
-                            mbar_expect_tx(&s_bar, bytes);
-                            bulk_g2s(S.k, (const void*)a0, bytes, &s_bar);
-                        }
-                        mbar_wait(&s_bar, s_phase_bit);
-                        s_phase_bit ^= 1u;
-                        const uint4* s4 = (const uint4*)S.k;
-                        for (u32 v = threadIdx.x; v < bytes / 16; v += BS_NT) {
-                            const uint4 r = s4[v];
-                            const U* e = (const U*)&r;
-#pragma unroll
-                            for (u32 q = 0; q < 4; ++q) {
-                                const u32 li = 4 * v + q - off;
-                                if (li < m) atomicAdd(&Sa.cnt[digit(K(e[q]), 0u)], 1u);
-                            }
-                        }
-                        hist_done = true;
-                    }
-                }
-                if (!hist_done)
-                    for_items<U, BS_NT, OVS_BS_UNR>(src, bk.beg, m, [&](U kr, u32 o) {
-                        const u32 ix = KV ? IX(bk.beg + o) : 0u;
-                        atomicAdd(&Sa.cnt[digit(K(kr), ix)], 1u);
-                    });
+                for_items<U, BS_NT, OVS_BS_UNR>(src, bk.beg, m, [&](U kr, u32 o) {
+                    const u32 ix = KV ? IX(bk.beg + o) : 0u;
+                    atomicAdd(&Sa.cnt[digit(K(kr), ix)], 1u);
+                });
                 __syncthreads();
                 BS_PROBE(3)
                 if constexpr (!KV && sizeof(U) == 4 && OVS_BS_WIN16) {

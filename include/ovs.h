@@ -153,7 +153,8 @@ size_t ovs_dist_workspace_bytes(ovs_comm* c, size_t n_local, int dtype, int with
  * `stream` twice (the shard-size all-gather; the count matrix read-back, which decides capacity
  * and the exchange plan) and returns with the exchange and the local sort enqueued.  Errors are
  * decided from all-gathered data, so every rank returns the same code: OVS_EINVAL (p not a
- * multiple of world, DRO, flags, n_global >= 2^32-33), OVS_ESAMPLE (p*s-1 > n_global),
+ * multiple of world, flags, n_global >= 2^32-33; DRO: p not dividing n_global or unequal shards),
+ * OVS_ESAMPLE (ROS: p*s-1 > n_global; DRO: r*p > n_global/p),
  * OVS_EWORKSPACE (some rank's ws_bytes too small), OVS_ECAPACITY (some rank receives more items
  * than its out_capacity or the window holds: *n_out = this rank's requirement; grow and call
  * again), OVS_ENCCL, OVS_ECUDA.  rep (optional, host): the global splitters and bucket counts,
@@ -162,7 +163,14 @@ size_t ovs_dist_workspace_bytes(ovs_comm* c, size_t n_local, int dtype, int with
 int ovs_dist_sort_keys(ovs_comm* c, const void* d_in, size_t n_local, int dtype, const ovs_params* prm, void* d_out,
                        size_t out_capacity, size_t* n_out, void* d_ws, size_t ws_bytes, void* stream, ovs_report* rep);
 /* Stable key-value variant: uint32 values ride with their keys; equal keys keep their global
- * input order. */
+ * input order.
+ * DRO across GPUs (method OVS_DRO, s = r; SURVEY.md §8(e) DRO steps, the paper's McDet split,
+ * PAPER.md:664-670): every rank holds n_global / world keys, i.e. p/world whole sequences of
+ * Algorithm 1's baseline split (p must divide n_global); each rank sorts its sequences and stores
+ * their r p regular samples into every window, all ranks pick the same splitters, split their
+ * sequences, and every run X_{k,j} is stored straight into bucket j's owner, which sorts the bucket
+ * (the stable result of the paper's p-way merge).  Output, splitters (tags = global positions in the
+ * sorted sequences) and counts equal the single-process Algorithm 1 on the concatenation. */
 int ovs_dist_sort_pairs_stable(ovs_comm* c, const void* d_keys, const uint32_t* d_vals, size_t n_local, int dtype,
                                const ovs_params* prm, void* d_out_keys, uint32_t* d_out_vals, size_t out_capacity,
                                size_t* n_out, void* d_ws, size_t ws_bytes, void* stream, ovs_report* rep);

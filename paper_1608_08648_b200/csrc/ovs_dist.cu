@@ -72,8 +72,9 @@ int fail(int code, const std::string& msg) {
 int dist_args(int dtype, const ovs_params* prm, int world) {
     if (!prm) return OVS_EINVAL;
     if (dtype != OVS_U32 && dtype != OVS_I32 && dtype != OVS_F64) return OVS_EDTYPE;
-    if (prm->method != OVS_ROS) return OVS_EINVAL;  // DRO across GPUs: not in this revision
-    if (prm->flags != 0) return OVS_EINVAL;
+    if (prm->method != OVS_ROS && prm->method != OVS_DRO) return OVS_EINVAL;
+    if (prm->flags & ~(u32)OVS_DRO_PADDED_POSITIONS) return OVS_EINVAL;  // (no merge flag across GPUs)
+    if (prm->method == OVS_ROS && prm->flags) return OVS_EINVAL;
     if (prm->p < 2 || prm->p % (uint32_t)world != 0) return OVS_EINVAL;  // "p ... a multiple of m"
     if (prm->s == 0) return OVS_ESAMPLE;
     return OVS_OK;
@@ -81,8 +82,19 @@ int dist_args(int dtype, const ovs_params* prm, int world) {
 // checks on the global size (identical on every rank: the sizes are all-gathered)
 int dist_global(u64 n_global, const ovs_params* prm) {
     if (n_global >= 0xffffffffull - 32) return OVS_EINVAL;  // global indices are the u32 tags
+    if (prm->method == OVS_DRO) {
+        // every rank holds whole sequences of Algorithm 1's baseline split: p | n_global (the shard
+        // sizes are checked to be n_global / world by the caller of this), r p <= n / p
+        if (n_global % prm->p != 0) return OVS_EINVAL;
+        if ((u64)prm->s * prm->p > n_global / prm->p) return OVS_ESAMPLE;
+        return OVS_OK;
+    }
     if ((u64)prm->p * prm->s - 1 > n_global) return OVS_ESAMPLE;
     return OVS_OK;
+}
+// sample records in the window: ROS ps - 1, DRO r p^2
+u64 rec_count(const ovs_params* prm) {
+    return prm->method == OVS_DRO ? (u64)prm->s * prm->p * prm->p : (u64)prm->p * prm->s - 1;
 }
 
 DistCfg make_cfg(u64 n_local, u64 n_global, u64 offset, const ovs_params* prm, int world, int rank, u64 out_cap,
@@ -90,6 +102,7 @@ DistCfg make_cfg(u64 n_local, u64 n_global, u64 offset, const ovs_params* prm, i
     DistCfg g{};
     g.n_local = n_local; g.n_global = n_global; g.offset = offset;
     g.p = prm->p; g.s = prm->s; g.world = (u32)world; g.rank = (u32)rank; g.seed = prm->seed;
+    g.method = prm->method; g.flags = prm->flags;
     g.out_cap = out_cap; g.W = W;
     return g;
 }
@@ -154,14 +167,18 @@ int dist_impl(ovs_comm* c, const void* keys, const u32* vals, bool kv, size_t n_
             n_global += sz[3 * r];
         }
         v = dist_global(n_global, prm);
-        if (v != OVS_OK) return fail(v, "invalid global size or sample size (ps-1 <= n_global < 2^32-33)");
+        if (v != OVS_OK) return fail(v, "invalid global size or sample size (ps-1 <= n_global < 2^32-33; DRO: p | n)");
+        if (prm->method == OVS_DRO)
+            for (u32 r = 0; r < world; ++r)
+                if (sz[3 * r] != n_global / world)
+                    return fail(OVS_EINVAL, "DRO across GPUs: every rank holds n_global / world keys (whole sequences)");
         *n_out = 0;
         if (rep) {
             std::memset(rep->phase_ms, 0, sizeof(rep->phase_ms));
             rep->max_bucket = 0; rep->kernel_launches = 0; rep->device_status = 0;
         }
         const u32 kb = dtype == OVS_F64 ? 8 : 4;
-        const u64 m = (u64)p * prm->s - 1;
+        const u64 m = rec_count(prm);
         const WinLayout W = win_layout(c->win_bytes, m, kb, kv, world, p);
         if (W.end > c->win_bytes || W.cap == 0)
             return fail(OVS_ECAPACITY, "the window cannot hold the sample and the count matrix (ovs_comm_reserve)");
@@ -379,7 +396,7 @@ size_t ovs_comm_window_bytes(const ovs_comm* c) { return c ? c->win_bytes : 0; }
 size_t ovs_dist_window_bytes(size_t n_recv, int dtype, int with_values, const ovs_params* prm, int world) {
     if (!prm || world < 1 || prm->p < 1) return 0;
     const u32 kb = dtype == OVS_F64 ? 8 : 4;
-    const u64 m = (u64)prm->p * prm->s - 1;
+    const u64 m = rec_count(prm);
     const WinLayout L0 = win_layout(0, m, kb, with_values != 0, (u32)world, prm->p);
     return L0.rk + (size_t)n_recv * (kb + (with_values ? 8 : 0)) + 4 * 256;
 }
@@ -399,7 +416,7 @@ size_t ovs_dist_workspace_bytes(ovs_comm* c, size_t n_local, int dtype, int with
         }
         if (dist_global(n_global, prm) != OVS_OK) return 0;
         const u32 kb = dtype == OVS_F64 ? 8 : 4;
-        const WinLayout W = win_layout(c->win_bytes, (u64)prm->p * prm->s - 1, kb, with_values != 0, (u32)c->world, prm->p);
+        const WinLayout W = win_layout(c->win_bytes, rec_count(prm), kb, with_values != 0, (u32)c->world, prm->p);
         return ws_need(dtype, with_values != 0, make_cfg(n_local, n_global, offset, prm, c->world, c->rank, out_capacity, W));
     } catch (const std::exception& e) {
         g_err = e.what();
@@ -453,8 +470,11 @@ int ovs_dist_sort_virtual(int world, const void* const* d_keys, const uint32_t* 
         for (int r = 0; r < world; ++r) n_global += n_local[r];
         v = dist_global(n_global, prm);
         if (v != OVS_OK) return fail(v, "invalid global size");
+        if (prm->method == OVS_DRO)
+            for (int r = 0; r < world; ++r)
+                if (n_local[r] != n_global / world) return fail(OVS_EINVAL, "DRO: equal shards of whole sequences");
         const u32 kb = dtype == OVS_F64 ? 8 : 4, p = prm->p;
-        const WinLayout W = win_layout(win_bytes, (u64)p * prm->s - 1, kb, kv, (u32)world, p);
+        const WinLayout W = win_layout(win_bytes, rec_count(prm), kb, kv, (u32)world, p);
         if (W.end > win_bytes || W.cap == 0) return fail(OVS_ECAPACITY, "window too small");
         OVS_CK(cudaMalloc(&d_peer, sizeof(char*) * (size_t)world));
         OVS_CK(cudaMemcpyAsync(d_peer, d_win, sizeof(char*) * (size_t)world, cudaMemcpyHostToDevice, st));
@@ -578,7 +598,7 @@ size_t ovs_dist_virtual_workspace_bytes(int world, const size_t* n_local, int dt
         for (int r = 0; r < world; ++r) n_global += n_local[r];
         if (dist_global(n_global, prm) != OVS_OK) return 0;
         const u32 kb = dtype == OVS_F64 ? 8 : 4;
-        const WinLayout W = win_layout(win_bytes, (u64)prm->p * prm->s - 1, kb, with_values != 0, (u32)world, prm->p);
+        const WinLayout W = win_layout(win_bytes, rec_count(prm), kb, with_values != 0, (u32)world, prm->p);
         size_t mx = 0;
         u64 off = 0;
         for (int r = 0; r < world; ++r) {

@@ -997,7 +997,7 @@ template <int DT, bool KV> struct DroSort {
     void run_merge() {
         Bufs<U>& B = e.B;
         launch(c, k_dro_bounds<U>, cdiv((u64)p * (P + 1), 256), 256, 0, B.k[1], n, p, P, (const U*)fsk, (const u32*)fst,
-               bound);
+               bound, 0u);
         c.check();
         launch(c, k_dro_counts, cdiv((u64)p * P, 256), 256, 0, (const u32*)bound, p, P, cnt);
         c.check();
@@ -1070,7 +1070,7 @@ template <int DT, bool KV> struct DroSort {
         }
         c.mark(2);
         // a13: split every sorted sequence by binary search; bucket starts and run offsets
-        launch(c, k_dro_bounds<U>, cdiv((u64)p * (p + 1), 256), 256, 0, B.k[1], n, p, p, sk, st, bound);
+        launch(c, k_dro_bounds<U>, cdiv((u64)p * (p + 1), 256), 256, 0, B.k[1], n, p, p, sk, st, bound, 0u);
         c.check();
         launch(c, k_dro_counts, cdiv((u64)p * p, 256), 256, 0, bound, p, p, cnt);
         c.check();
@@ -1166,6 +1166,7 @@ inline void dist_plan_host(const u32* C, u32 world, u32 p, u32 rank, DistPlanHos
 struct DistCfg {
     const void* keys; const u32* vals; u64 n_local, n_global, offset;
     u32 p, s, world, rank; u64 seed;
+    u32 method, flags;  // OVS_ROS / OVS_DRO (s = r for DRO), OVS_DRO_PADDED_POSITIONS
     u64 out_cap;  // output items (d_out) the caller provides
     WinLayout W;
     void* out_k; u32* out_v;
@@ -1319,8 +1320,194 @@ Out plan_or_run(Ctx& c, void* keys, u32* vals, size_t n, const ovs_params* prm) 
 }
 
 
+// ---- DRO across GPUs (SURVEY.md §8(e) DRO steps 1-6; the paper's McDet): rank g owns the
+// p/G whole sequences [g p/G, (g+1) p/G) of Algorithm 1's baseline split (equal shards and p | n_global,
+// so every sequence is local).  Phases, as DistSort's:
+//   sample   a9: sort the local sequences (tags = global positions); a10: their r p regular samples
+//            (global s = r p per sequence) -> every rank's window, rank g's block of slots
+//   select   a11-a12: sort all r p^2 records, S[q] = T[(q+1) r p - 1] (identical on every rank)
+//   count    a13: split the local sequences, column prefix over them, bucket totals -> every window
+//   scatter  a14's exchange: every run X_{k,j} straight into the owner of bucket j (k_dro_send)
+//   finish   every owned bucket (runs in global sequence order) sorted into the output by (key,
+//            original index) - the stable result of the paper's p-way merge
+template <int DT, bool KV> struct DistDroSort : DistRun {
+    typedef typename Codec<DT>::U U;
+    Ctx& c;
+    DistCfg g;
+    Engine<DT, KV> e;   // local: buffer 0 = the shard (raw, read only), buffer 1 = sorted sequences
+    Engine<DT, KV> f;   // receive side (as DistSort)
+    typename Engine<DT, KV>::Lists l1, lb1, lf, lb;
+    u32 pl = 1, r = 1, s = 1, ns = 0;   // local sequences, r, s = r p, records r p^2
+    u64* t_pack = nullptr; u64* t_key = nullptr; u32* t_tag = nullptr;
+    InternalSort<false>* ts32 = nullptr;
+    InternalSort<true>* ts64 = nullptr;
+    U* sk = nullptr; u32* st = nullptr;
+    u32* bound = nullptr; u32* cnt = nullptr; u32* tot = nullptr; u32* nseg = nullptr; Seg* seg = nullptr;
+    u32* dst_off = nullptr; u32* desc = nullptr;
+    bool big = false;
+    Level1<DT, KV>* l1s = nullptr;   // local sequences far over capacity
+    Level1<DT, KV>* l1x = nullptr;   // owned buckets over capacity
+    DistDroSort(Ctx& ctx, const DistCfg& cfg) : c(ctx), g(cfg), e(ctx), f(ctx) {
+        const u32 nl = (u32)g.n_local, p = g.p;
+        pl = p / g.world;
+        r = g.s;
+        s = r * p;
+        ns = s * p;
+        e.n = nl;
+        e.ixbits = bits_for(g.n_global);
+        e.cap = bucket_cap<U, KV>(c.di);
+        e.B.k[0] = (U*)g.keys;
+        e.B.v[0] = (u32*)g.vals;
+        e.B.k[1] = c.take<U>(nl);
+        e.B.v[1] = KV ? c.take<u32>(nl) : nullptr;
+        e.B.i[0] = KV ? c.take<u32>(nl) : nullptr;
+        e.B.i[1] = KV ? c.take<u32>(nl) : nullptr;
+        sk = c.take<U>(p);
+        st = c.take<u32>(p);
+        if (sizeof(U) == 4) {
+            t_pack = c.take<u64>(ns);
+            ts32 = new InternalSort<false>(c, ns, t_pack, nullptr);
+        } else {
+            t_key = c.take<u64>(ns);
+            t_tag = c.take<u32>(ns);
+            ts64 = new InternalSort<true>(c, ns, t_key, t_tag);
+        }
+        bound = c.take<u32>((size_t)pl * (p + 1));
+        cnt = c.take<u32>((size_t)pl * p);
+        tot = c.take<u32>(p + 1);
+        seg = c.take<Seg>(1);
+        nseg = c.take<u32>(2);
+        dst_off = c.take<u32>(p);
+        desc = c.take<u32>(3 * (size_t)p);
+        e.carve_lists(l1, pl);
+        big = (nl / std::max<u32>(pl, 1)) > BS_WMAX * e.cap;
+        if (big) {
+            l1s = new Level1<DT, KV>(e, pl);
+            e.carve_lists(lb1, pl * Level1<DT, KV>::PS);
+        }
+        // receive side
+        const u32 oc = (u32)std::min<u64>(g.out_cap, 0xffffffffull - 64);
+        f.n = oc;
+        f.cap = e.cap;
+        f.ixbits = bits_for(g.n_global);
+        f.B.k[0] = (U*)g.out_k;
+        f.B.v[0] = g.out_v;
+        f.B.k[1] = nullptr; f.B.v[1] = nullptr; f.B.i[1] = nullptr;
+        f.B.i[0] = KV ? c.take<u32>(oc) : nullptr;
+        f.carve_lists(lf, p);
+        if (g.n_global / p > f.cap) {
+            l1x = new Level1<DT, KV>(f, p / g.world + 1);
+            f.carve_lists(lb, (p / g.world + 1) * Level1<DT, KV>::PS);
+        }
+    }
+    ~DistDroSort() { delete ts32; delete ts64; delete l1s; delete l1x; }
+    size_t ws() const override { return c.off + 256; }
+
+    void sample(char* const* d_peer) override {
+        if (c.dry) return;
+        Bufs<U>& B = e.B;
+        const u32 nl = (u32)g.n_local;
+        // a9: the local sequences sorted into buffer 1 (ordered keys; values, original indices)
+        fill_u32(c, l1.nfit, 0, 2);
+        launch(c, k_dro_segments, cdiv(pl, 256), 256, 0, l1.fit, l1.nfit, nl, pl);
+        c.check();
+        if (big) {
+            launch(c, k_to_ordered<DT, KV>, 4 * c.di.sms, 1024, 0, B, nl);
+            c.check();
+            launch(c, k_list_flip, cdiv(pl, 256), 256, 0, l1.fit, l1.nfit);
+            c.check();
+            fill_u32(c, lb1.nfit, 0, 2);
+            l1s->run(l1.fit, l1.nfit, lb1, 0x5e9u);
+            e.bucket_sort(lb1, 0x5e9u, B.k[1], KV ? B.v[1] : nullptr, KV ? B.i[1] : nullptr, false);
+        } else {
+            e.bucket_sort(l1, 0x5e9u, B.k[1], KV ? B.v[1] : nullptr, KV ? B.i[1] : nullptr, false);
+        }
+        if (KV && g.offset) {  // original indices of the shard -> global
+            launch(c, k_add_u32, cdiv(nl, 256), 256, 0, B.i[1], nl, (u32)g.offset);
+            c.check();
+        }
+        // a10: regular samples of the local sorted sequences -> every window (slots of this rank)
+        const u32 xpad = (u32)((((u64)g.n_global + g.p - 1) / g.p + s - 1) / s);
+        launch(c, k_dro_sample_dist<U>, cdiv((u64)s * pl, 256), 256, 0, (const U*)B.k[1], nl, pl, s,
+               (u32)((g.flags & OVS_DRO_PADDED_POSITIONS) ? 1 : 0), xpad, (u32)g.offset, g.rank * pl * s,
+               PeerOut{d_peer, g.W.rec, g.world});
+        c.check();
+    }
+    void select(const char* win) override {
+        if (c.dry) return;
+        const u32 words = sizeof(U) == 4 ? 1 : 2;
+        launch(c, k_dist_unpack, cdiv(ns, 256), 256, 0, (const u64*)(win + g.W.rec), ns, words, t_pack, t_key, t_tag);
+        c.check();
+        if (ts32) ts32->run(0xd0d0);
+        else ts64->run(0xd0d0);
+        launch(c, k_pick_splitters<U>, cdiv(g.p, 256), 256, 0, (const u64*)t_pack, (const u64*)t_key, (const u32*)t_tag,
+               g.p, s, 1u, sk, st);
+        c.check();
+    }
+    void count(char* const* d_peer) override {
+        if (c.dry) return;
+        const u32 nl = (u32)g.n_local, p = g.p;
+        launch(c, k_dro_bounds<U>, cdiv((u64)pl * (p + 1), 256), 256, 0, (const U*)e.B.k[1], nl, pl, p, (const U*)sk,
+               (const u32*)st, bound, (u32)g.offset);
+        c.check();
+        launch(c, k_dro_counts, cdiv((u64)pl * p, 256), 256, 0, (const u32*)bound, pl, p, cnt);
+        c.check();
+        launch(c, k_dro_seg<U>, 1, 1024, 0, (const U*)e.B.k[1], nl, pl, p, (const U*)sk, 0u, seg, nseg);
+        c.check();
+        launch(c, k_colscan, std::min<u32>(cdiv(p, 32), 4 * c.di.sms), 1024, 0, cnt, (const Seg*)seg,
+               (const u32*)nseg, p, tot);
+        c.check();
+        launch(c, k_put_counts32, cdiv(p * g.world, 256), 256, 0, (const u32*)tot, p, g.rank,
+               PeerOut{d_peer, g.W.C, g.world});
+        c.check();
+    }
+    void scatter(char* const* d_peer, const DistPlanHost& P, u32* h_stage) override {
+        if (c.dry) return;
+        std::memcpy(h_stage, P.dst_off.data(), 4 * (size_t)g.p);
+        if (!P.desc.empty()) std::memcpy(h_stage + g.p, P.desc.data(), 4 * P.desc.size());
+        OVS_CK(cudaMemcpyAsync(dst_off, h_stage, 4 * (size_t)g.p, cudaMemcpyHostToDevice, c.st));
+        if (!P.desc.empty())
+            OVS_CK(cudaMemcpyAsync(desc, h_stage + g.p, 4 * P.desc.size(), cudaMemcpyHostToDevice, c.st));
+        launch(c, k_dro_send<U, KV>, 8 * (u32)c.di.sms, 256, 0, e.B, (u32)g.n_local, pl, g.p, (const u32*)bound,
+               (const u32*)cnt, (const u32*)dst_off, PeerOut{d_peer, g.W.rk, g.world}, g.W.rv, g.W.ri);
+        c.check();
+    }
+    void finish(const char* win, u32 n_owned) override {
+        if (c.dry) return;
+        f.B.k[1] = (U*)(win + g.W.rk);
+        f.B.v[1] = KV ? (u32*)(win + g.W.rv) : nullptr;
+        f.B.i[1] = KV ? (u32*)(win + g.W.ri) : nullptr;
+        launch(c, k_dist_list<U>, std::max<u32>(1, cdiv(n_owned, 256)), 256, 0, (const u32*)desc, n_owned,
+               (const U*)sk, g.p, lf.fit, lf.nfit, 1u);
+        c.check();
+        fill_u32(c, lf.ticket, 0, 1);
+        if (l1x) {
+            fill_u32(c, lb.nfit, 0, 2);
+            l1x->run(lf.fit, lf.nfit, lb, g.seed ^ 0xf2);
+            f.bucket_sort(lb, g.seed ^ 0xf1);
+        } else {
+            f.bucket_sort(lf, g.seed ^ 0xf1);
+        }
+    }
+    void splitters(void* h_keys, uint64_t* h_tags) override {
+        if (c.dry || g.p < 2) return;
+        std::vector<U> kb(g.p - 1);
+        std::vector<u32> tb(g.p - 1);
+        OVS_CK(cudaMemcpyAsync(kb.data(), sk, sizeof(U) * (g.p - 1), cudaMemcpyDeviceToHost, c.st));
+        OVS_CK(cudaMemcpyAsync(tb.data(), st, 4 * (size_t)(g.p - 1), cudaMemcpyDeviceToHost, c.st));
+        OVS_CK(cudaStreamSynchronize(c.st));
+        for (u32 q = 0; q + 1 < g.p; ++q) {
+            if (h_keys) ((U*)h_keys)[q] = host_raw<DT>(kb[q]);
+            if (h_tags) h_tags[q] = tb[q];
+        }
+    }
+};
+
 // multi-GPU: one rank's distributed sort object (per (dtype, keys/pairs) translation unit)
-template <int DT, bool KV> DistRun* make_dist(Ctx& c, const DistCfg& cfg) { return new DistSort<DT, KV>(c, cfg); }
+template <int DT, bool KV> DistRun* make_dist(Ctx& c, const DistCfg& cfg) {
+    if (cfg.method == OVS_DRO) return new DistDroSort<DT, KV>(c, cfg);
+    return new DistSort<DT, KV>(c, cfg);
+}
 DistRun* dist_u32_k(Ctx& c, const DistCfg& cfg);
 DistRun* dist_u32_v(Ctx& c, const DistCfg& cfg);
 DistRun* dist_i32_k(Ctx& c, const DistCfg& cfg);

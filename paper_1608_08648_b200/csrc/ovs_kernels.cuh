@@ -3044,7 +3044,7 @@ __global__ void k_dro_sample(const U* xs, u32 n, u32 p, u32 s, u32 padded, u64* 
 // into the sorted X_k; count matrix cnt[k][j] = bound[k][j+1]-bound[k][j]
 // (P buckets: P - 1 splitters; P = p for the contract split, p*f for the fine split of f2)
 template <class U>
-__global__ void k_dro_bounds(const U* xs, u32 n, u32 p, u32 P, const U* sk, const u32* st, u32* bound) {
+__global__ void k_dro_bounds(const U* xs, u32 n, u32 p, u32 P, const U* sk, const u32* st, u32* bound, u32 tag0 = 0) {
     PDL_PROLOGUE();
     const u64 id = (u64)blockIdx.x * blockDim.x + threadIdx.x;
     if (id >= (u64)p * (P + 1)) return;
@@ -3062,7 +3062,7 @@ __global__ void k_dro_bounds(const U* xs, u32 n, u32 p, u32 P, const U* sk, cons
         while (cnt > 0) {
             const u32 half = cnt >> 1, mid = lo + half;
             const U x = xs[beg + mid];
-            const bool le = x < key || (x == key && beg + mid <= tag);
+            const bool le = x < key || (x == key && tag0 + beg + mid <= tag);  // tags: global positions
             if (le) { lo = mid + 1; cnt -= half + 1; } else cnt = half;
         }
         r = lo;
@@ -3280,6 +3280,73 @@ __global__ void k_put_counts(const u64* counts, u32 p, u32 rank, PeerOut po) {
     const u32 d = t / p, b = t % p;
     ((u32*)(po.peers[d] + po.off))[(size_t)rank * p + b] = (u32)counts[b];
     __threadfence_system();
+}
+
+// ---- DRO across GPUs (DRO steps; the paper's McDet split): rank g
+// holds the p/G whole sequences [g p/G, (g+1) p/G) of the global baseline split (equal shards, p | n).
+// a10 on the local sorted sequences: record (key, global tag = tag0 + local position) of sample j of
+// local sequence k goes to slot slot0 + k s + j of every rank's window (s = r p regular samples,
+// balanced or padded positions of the global Alg. 1)
+template <class U>
+__global__ void k_dro_sample_dist(const U* xs, u32 n, u32 p, u32 s, u32 padded, u32 xpad, u32 tag0, u32 slot0,
+                                  PeerOut po) {
+    PDL_PROLOGUE();
+    const u64 id = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (id >= (u64)s * p) return;
+    const u32 k = (u32)(id / s), j = (u32)(id % s);
+    const u32 q = n / p, rm = n % p;
+    const u32 beg = k * q + min(k, rm), m = q + (k < rm ? 1u : 0u);
+    u32 e;
+    if (padded) e = (j + 1 == s) ? m - 1 : (u32)min((u64)(j + 1) * xpad, (u64)m) - 1;
+    else {
+        const u32 qq = m / s, rr = m % s;
+        e = (j + 1) * qq + min(j + 1, rr) - 1;
+    }
+    put_rec<sizeof(U) == 8>(po, slot0 + (u32)id, (u64)xs[beg + e], (u64)(tag0 + beg + e));
+}
+
+// this rank's bucket totals (u32) -> row `rank` of every window's count matrix
+__global__ void k_put_counts32(const u32* tot, u32 p, u32 rank, PeerOut po) {
+    PDL_PROLOGUE();
+    const u32 t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= p * po.world) return;
+    const u32 d = t / p, b = t % p;
+    ((u32*)(po.peers[d] + po.off))[(size_t)rank * p + b] = tot[b];
+    __threadfence_system();
+}
+
+// a14's exchange: run (k, j) = X_k[bound[k][j] .. bound[k][j+1]) of local sorted sequence k goes to
+// bucket j's owner window at dst_off[j] + off[k][j] (the column prefix over the local sequences, so
+// runs arrive in global sequence order); keys ordered, values and original indices with them
+template <class U, bool KV>
+__global__ void k_dro_send(Bufs<U> B, u32 n, u32 p, u32 P, const u32* bound, const u32* off, const u32* dst_off,
+                           PeerOut pk, size_t off_v, size_t off_i) {
+    PDL_PROLOGUE();
+    const u32 lane = threadIdx.x & 31;
+    const u32 q = n / p, rm = n % p;
+    for (u64 w = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < (u64)p * P; w += ((u64)gridDim.x * blockDim.x) >> 5) {
+        const u32 k = (u32)(w / P), j = (u32)(w % P);
+        const u32 a = bound[(size_t)k * (P + 1) + j], b = bound[(size_t)k * (P + 1) + j + 1];
+        if (a == b) continue;
+        const u32 beg = k * q + min(k, rm);
+        const u32 d = dst_off[j] + off[(size_t)k * P + j];
+        char* const win = pk.peers[((u64)j * pk.world) / P];
+        U* dk = (U*)(win + pk.off);
+        for (u32 t = a + lane; t < b; t += 32) {
+            dk[d + t - a] = B.k[1][beg + t];
+            if (KV) {
+                ((u32*)(win + off_v))[d + t - a] = B.v[1][beg + t];
+                ((u32*)(win + off_i))[d + t - a] = B.i[1][beg + t];
+            }
+        }
+    }
+    __threadfence_system();
+}
+
+__global__ void k_add_u32(u32* a, u32 n, u32 v) {
+    PDL_PROLOGUE();
+    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) a[i] += v;
 }
 
 // the received (owned) buckets as a work list: desc[3j..3j+2] = (begin in the receive region,

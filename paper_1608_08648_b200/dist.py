@@ -100,7 +100,8 @@ class DistSorter:
     `group` constructs it and calls it the same number of times)."""
 
     def __init__(self, n_local: int, dtype, with_values: bool = False, p: int = 1024, s: int = 64, seed: int = 1,
-                 group=None, device=None, out_capacity: int | None = None, window_bytes: int | None = None):
+                 group=None, device=None, out_capacity: int | None = None, window_bytes: int | None = None,
+                 method: str = "ros", padded: bool = False):
         import torch
         import torch.distributed as dist
         self.L = _ensure_sigs()
@@ -109,7 +110,7 @@ class DistSorter:
         self.rank = dist.get_rank(group)
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.dtype, self.dt, self.kv = dtype, _dtcode(dtype), with_values
-        self.prm = params("ros", p, s, seed)
+        self.prm = params(method, p, s, seed, padded)  # DRO: s = r, equal shards of whole sequences
         self.p = p
         self.n_local = n_local
         # the NCCL unique id: rank 0 draws it, the process group broadcasts the 128 bytes
@@ -219,7 +220,8 @@ class DistSorter:
             pass
 
 
-def dist_sort_virtual(shards, vals=None, p: int = 1024, s: int = 64, seed: int = 1, win_items=None):
+def dist_sort_virtual(shards, vals=None, p: int = 1024, s: int = 64, seed: int = 1, win_items=None,
+                      method: str = "ros", padded: bool = False):
     """G ranks emulated on ONE GPU by one library call (ovs_dist_sort_virtual: the same phases
     and kernels, the fused scatter storing into the other emulated ranks' windows, phases run
     rank after rank so no kernel waits on another).  Returns (concatenated output, values,
@@ -230,7 +232,7 @@ def dist_sort_virtual(shards, vals=None, p: int = 1024, s: int = 64, seed: int =
     kv = vals is not None
     dev = shards[0].device
     dt = _dtcode(shards[0].dtype)
-    prm = params("ros", p, s, seed)
+    prm = params(method, p, s, seed, padded)
     n_local = np.array([int(x.numel()) for x in shards], dtype=np.uint64)
     n_global = int(n_local.sum())
     cap = int(win_items or (n_global // world + n_global // (2 * world) + 8192))

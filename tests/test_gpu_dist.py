@@ -177,3 +177,36 @@ def test_nccl_capacity_retry(orc, nccl_world1):
     check(ref, res.keys, None, res.counts, res.splitter_keys, res.splitter_tags)
     assert ds.out_cap >= n and ds.window_bytes() >= 4 * n
     ds.close()
+
+
+# ---------------------------------------------------------------- DRO across GPUs (§8(e) DRO steps)
+@pytest.mark.parametrize("G,dist_name,n_per,p,r,kv,padded", [
+    (1, "i32_uniform", 1 << 18, 64, 4, False, False), (2, "i32_gauss", 1 << 18, 64, 4, False, False),
+    (4, "u16key", 1 << 17, 32, 3, True, False), (2, "f64_normal", 1 << 17, 16, 5, True, True),
+    (8, "u32_few4", 1 << 16, 64, 2, False, False), (4, "u32", 1 << 20, 256, 8, False, True)])
+def test_virtual_ranks_dro(orc, G, dist_name, n_per, p, r, kv, padded):
+    """Rank g holds the p/G whole sequences of its shard; samples, splitters, split, exchange and the
+    owners' sorts equal the single-process Algorithm 1 on the concatenation (keys, values,
+    splitters, counts)."""
+    from paper_1608_08648_b200.dist import dist_sort_virtual
+    n = G * n_per
+    x = ovs_inputs.keys(dist_name, n, seed=19) if dist_name in ("i32_sorted",) else \
+        np.concatenate([ovs_inputs.keys(dist_name, n_per, seed=19, start=g * n_per) for g in range(G)])
+    v = ovs_inputs.index_values(n) if kv else None
+    xs = [torch.from_numpy(np.ascontiguousarray(x[g * n_per:(g + 1) * n_per])).cuda() for g in range(G)]
+    vs = [torch.from_numpy(np.ascontiguousarray(v[g * n_per:(g + 1) * n_per])).cuda() for g in range(G)] if kv else None
+    out, vout, counts, sk, st, _ = dist_sort_virtual(xs, vs, p, r, 0, method="dro", padded=padded)
+    ref = orc.dro_sort(x, p, r, vals=v, padded=padded)
+    check(ref, out, vout, counts, sk, st)
+
+
+def test_nccl_comm_world1_dro(orc, nccl_world1):
+    from paper_1608_08648_b200.dist import DistSorter
+    n, p, r = 1 << 20, 128, 6
+    x = ovs_inputs.keys("i32_gauss", n, seed=4)
+    v = ovs_inputs.index_values(n)
+    ds = DistSorter(n, torch.int32, True, p, r, 0, method="dro")
+    res = ds(torch.from_numpy(x).cuda(), torch.from_numpy(v).cuda(), report=True)
+    ref = orc.dro_sort(x, p, r, vals=v)
+    check(ref, res.keys, res.vals, res.counts, res.splitter_keys, res.splitter_tags)
+    ds.close()

@@ -356,6 +356,7 @@ def main():
                 "phases_frac": {k: PHASE_BYTES[k] * n / (phase_ms[k] * 1e-3) / 1e9 / peak for k in PHASE_BYTES}}
 
     cpu = None
+    cpu_extra = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         import oracle
         oracle.build()
@@ -366,6 +367,19 @@ def main():
         dt = time.perf_counter() - t0
         cpu = {"value": n_c / dt / 1e9, "unit": "Gkeys/s", "cores": 1, "kind": "oracle",
                "sample": f"{n_c} keys of the workload, ROS p={p_c} s={s}, one run, {dt:.1f} s"}
+        # the paper's multi-core variant (McRan) on every core of the process, and the
+        # standalone library sort column on one core: context for the oracle line
+        cores = len(os.sched_getaffinity(0))
+        t0 = time.perf_counter()
+        oracle.mcran_sort(x[:n_c], p_c, s, seed, cores)
+        dt_mc = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        np.sort(x[:n_c])
+        dt_np = time.perf_counter() - t0
+        cpu_extra = {"mcran": {"value": n_c / dt_mc / 1e9, "unit": "Gkeys/s", "cores": cores, "kind": "oracle-mcran",
+                               "sample": f"{n_c} keys, SqRan with steps 1/4/5 on {cores} threads, {dt_mc:.1f} s"},
+                     "standalone": {"value": n_c / dt_np / 1e9, "unit": "Gkeys/s", "cores": 1,
+                                    "kind": "numpy.sort", "sample": f"{n_c} keys, {dt_np:.1f} s"}}
 
     if rank == 0:
         line = {"metric": METRIC,
@@ -380,7 +394,7 @@ def main():
                            "l2": "input 512 MiB > 126 MB L2; 512 MiB restore copy before every step",
                            "launch": "timed steps replay the whole sort from a CUDA graph captured once "
                                      "(Sorter.graph); phases_ms from eager launches with phase events"},
-                "roofline": roofline, "cpu_baseline": cpu,
+                "roofline": roofline, "cpu_baseline": cpu, "cpu_baselines_context": cpu_extra,
                 "e2e": {"value": e2e_v, "unit": "Gkeys/s", "h2d_bytes_per_step": int(n * 4),
                         "d2h_bytes_per_step": int(n * 4), "ms_per_step": e2e_ms},
                 "gpu_launches": launches_per_step * args.steps, "launches_per_step": launches_per_step,

@@ -26,7 +26,7 @@ DRO_PADDED_POSITIONS = 1
 def build(force: bool = False) -> str:
     """Compile the oracle (plain g++, -O2, no fast-math: IEEE compares, Q18)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        subprocess.check_call(["g++", "-O2", "-std=c++17", "-fPIC", "-shared", "-o", _LIB, _SRC])
+        subprocess.check_call(["g++", "-O2", "-std=c++17", "-pthread", "-fPIC", "-shared", "-o", _LIB, _SRC])
     return _LIB
 
 
@@ -49,6 +49,8 @@ def lib():
         for f in (_lib.orc_ros_sort, _lib.orc_sqran_literal):
             f.restype = i32
             f.argtypes = sig
+        _lib.orc_mcran_sort.restype = i32
+        _lib.orc_mcran_sort.argtypes = [i32, vp, vp, u64, u32, u32, u64, u32, vp, vp, vp, vp, vp]
         _lib.orc_dro_sample_positions.restype = i32
         _lib.orc_dro_sample_positions.argtypes = [u64, u32, u32, u32, u32, vp]
         _lib.orc_dro_sort.restype = i32
@@ -126,6 +128,12 @@ def ros_sort(keys, p: int, s: int, seed: int, vals=None) -> Result:
 def sqran_literal(keys, p: int, s: int, seed: int, vals=None) -> Result:
     """Algorithm 2 (SqRan) as written."""
     return _run(lib().orc_sqran_literal, keys, vals, len(keys), p, s, (seed,))
+
+
+def mcran_sort(keys, p: int, s: int, seed: int, threads: int, vals=None) -> Result:
+    """McRan: Algorithm 2 with step 1's sorts, step 4's splits and step 5's merges on `threads`
+    threads; the multi-core CPU baseline."""
+    return _run(lib().orc_mcran_sort, keys, vals, len(keys), p, s, (seed, threads))
 
 
 def dro_sort(keys, p: int, r: int, vals=None, padded: bool = False) -> Result:

@@ -20,11 +20,16 @@
 // all permutations of tiny inputs, closed forms (exhaustive sample, sorted/reverse/constant
 // DRO inputs), Lemma 1, and agreement of the two independent ROS algorithms.
 #include <algorithm>
+#include <atomic>
+#include <thread>
 #include <cstdint>
 #include <cstring>
 #include <queue>
 #include <unordered_set>
 #include <vector>
+#ifdef EINVAL  // <thread> pulls in errno.h; the oracle's status codes are its own
+#undef EINVAL
+#endif
 
 namespace {
 
@@ -282,6 +287,106 @@ int sqran_literal(const K* x, const uint32_t* v, uint64_t n, uint32_t p, uint32_
     return OK;
 }
 
+// ---- McRan: Algorithm 2 with its independent work spread over t threads -------------------
+// The paper's multi-core variant: the p BaselineSorting sorts of step 1 (P:664-668,
+// "the p sorts ... over m cores"), the p binary-search splits of step 4 and the p bucket merges of
+// step 5 run on t std::threads; the sample, its sort and the splitters are the sequential steps.
+// Same results as sqran_literal (tests/test_oracle_pins.py); timed by bench.py as the multi-core CPU
+// baseline.
+template <class F>
+void parallel_for(uint32_t count, uint32_t threads, F&& f) {
+    std::atomic<uint32_t> next{0};
+    std::vector<std::thread> ts;
+    for (uint32_t t = 0; t < std::max<uint32_t>(threads, 1); ++t)
+        ts.emplace_back([&] {
+            for (uint32_t i; (i = next++) < count;) f(i);
+        });
+    for (auto& th : ts) th.join();
+}
+
+template <class K>
+int mcran_sort(const K* x, const uint32_t* v, uint64_t n, uint32_t p, uint32_t s, uint64_t seed, uint32_t threads,
+               K* out, uint32_t* outv, K* sk, uint64_t* st, uint64_t* counts) {
+    if (p == 0) return EINVAL;
+    if (n == 0) {
+        if (counts) for (uint32_t j = 0; j < p; ++j) counts[j] = 0;
+        return OK;
+    }
+    if (p == 1) {
+        plain_stable_sort(x, v, n, out, outv);
+        if (counts) counts[0] = n;
+        return OK;
+    }
+    if (s == 0) return ESAMPLE;
+    const uint64_t m = (uint64_t)p * s - 1;
+    if (m > n) return ESAMPLE;
+    // step 1 in parallel: X_k stably sorted, tags = original index
+    std::vector<Item<K>> X(n);
+    for (uint64_t i = 0; i < n; ++i) X[i] = {x[i], v ? v[i] : 0u, i};
+    parallel_for(p, threads, [&](uint32_t k) {
+        uint64_t a = seq_start(n, p, k), mk = seq_len(n, p, k);
+        std::stable_sort(X.begin() + a, X.begin() + a + mk,
+                         [](const Item<K>& A, const Item<K>& B) { return A.key < B.key; });
+    });
+    // steps 2-3: the sample (same index set I), sorted; splitters
+    std::vector<uint64_t> I = ros_sample_indices(n, m, seed, nullptr);
+    std::vector<Rec<K>> T(m);
+    for (uint64_t t = 0; t < m; ++t) T[t] = {x[I[t]], I[t]};
+    std::sort(T.begin(), T.end(), rec_less<K>);
+    std::vector<Rec<K>> S(p - 1);
+    for (uint32_t q = 0; q + 1 < p; ++q) S[q] = T[(uint64_t)(q + 1) * s - 1];
+    write_report(S, sk, st);
+    // step 4 in parallel: split every X_k around S by binary search
+    std::vector<uint64_t> bnd((uint64_t)p * (p + 1));
+    parallel_for(p, threads, [&](uint32_t k) {
+        uint64_t a = seq_start(n, p, k), mk = seq_len(n, p, k);
+        auto first = X.begin() + a, last = X.begin() + a + mk;
+        bnd[(uint64_t)k * (p + 1)] = 0;
+        for (uint32_t j = 0; j + 1 < p; ++j) {
+            auto it = std::upper_bound(first, last, S[j], [](const Rec<K>& sp, const Item<K>& e) {
+                return lex_less(sp.key, sp.tag, e.key, e.tag);
+            });
+            bnd[(uint64_t)k * (p + 1) + j + 1] = (uint64_t)(it - first);
+        }
+        bnd[(uint64_t)k * (p + 1) + p] = mk;
+    });
+    // step 5 in parallel: bucket j = the p-way merge of its runs (ties to the lower k), at its offset
+    std::vector<uint64_t> start(p + 1, 0);
+    for (uint32_t j = 0; j < p; ++j) {
+        uint64_t nj = 0;
+        for (uint32_t k = 0; k < p; ++k) nj += bnd[(uint64_t)k * (p + 1) + j + 1] - bnd[(uint64_t)k * (p + 1) + j];
+        start[j + 1] = start[j] + nj;
+        if (counts) counts[j] = nj;
+    }
+    struct Head { K key; uint32_t k; uint64_t pos, end; };
+    parallel_for(p, threads, [&](uint32_t j) {
+        auto worse = [](const Head& A, const Head& B) {
+            if (B.key < A.key) return true;
+            if (A.key < B.key) return false;
+            return A.k > B.k;
+        };
+        std::priority_queue<Head, std::vector<Head>, decltype(worse)> pq(worse);
+        for (uint32_t k = 0; k < p; ++k) {
+            uint64_t a = seq_start(n, p, k);
+            uint64_t lo = a + bnd[(uint64_t)k * (p + 1) + j], hi = a + bnd[(uint64_t)k * (p + 1) + j + 1];
+            if (lo < hi) pq.push({X[lo].key, k, lo, hi});
+        }
+        uint64_t o = start[j];
+        while (!pq.empty()) {
+            Head h = pq.top();
+            pq.pop();
+            out[o] = X[h.pos].key;
+            if (outv) outv[o] = X[h.pos].val;
+            ++o;
+            if (++h.pos < h.end) {
+                h.key = X[h.pos].key;
+                pq.push(h);
+            }
+        }
+    });
+    return OK;
+}
+
 // ---- DRO regular sample position (reading Q9) ----------------------------------
 // Position (0-based, in the sorted X_k of m keys) of the j-th of the s = rp samples.
 // Balanced (default): X_k is cut into s segments, the first (m mod s) of ceil(m/s) keys and
@@ -395,6 +500,16 @@ int orc_sqran_literal(int dtype, const void* keys, const uint32_t* vals, uint64_
         using K = std::remove_pointer_t<decltype(tag)>;
         return sqran_literal<K>((const K*)keys, vals, n, p, s, seed, (K*)out_keys, out_vals, (K*)split_keys,
                                 split_tags, counts);
+    });
+}
+
+int orc_mcran_sort(int dtype, const void* keys, const uint32_t* vals, uint64_t n, uint32_t p, uint32_t s,
+                   uint64_t seed, uint32_t threads, void* out_keys, uint32_t* out_vals, void* split_keys,
+                   uint64_t* split_tags, uint64_t* counts) {
+    return dispatch(dtype, [&](auto* tag) {
+        using K = std::remove_pointer_t<decltype(tag)>;
+        return mcran_sort<K>((const K*)keys, vals, n, p, s, seed, threads, (K*)out_keys, out_vals, (K*)split_keys,
+                             split_tags, counts);
     });
 }
 

@@ -391,3 +391,19 @@ def test_strings_exhaustive_sample_closed_form(orc, n, p, s):
     assert res.split_tags.tolist() == idx
     assert [bytes(v) for v in res.split_keys] == [bytes(x[i]) for i in idx]
     assert res.counts.tolist() == [s] * (p - 1) + [s - 1]
+
+
+@pytest.mark.parametrize("dist", ["u32_u31", "i32_few", "f64_normal", "u16key", "s32_prefix"])
+@pytest.mark.parametrize("threads", [1, 3, 8])
+def test_mcran_equals_sqran(orc, dist, threads):
+    """McRan (Algorithm 2 with the per-sequence and per-bucket steps on t threads) gives
+    the same splitters, counts and stable output as the sequential literal SqRan."""
+    n = 40_003
+    x = ovs_inputs.keys(dist, n, seed=23)
+    v = ovs_inputs.index_values(n)
+    a = orc.sqran_literal(x, 32, 16, 5, vals=v)
+    b = orc.mcran_sort(x, 32, 16, 5, threads, vals=v)
+    assert a.keys.tobytes() == b.keys.tobytes()
+    np.testing.assert_array_equal(a.vals, b.vals)
+    np.testing.assert_array_equal(a.split_tags, b.split_tags)
+    np.testing.assert_array_equal(a.counts, b.counts)

@@ -73,6 +73,7 @@ def keys(dist: str, n: int, seed: int, start: int = 0, world: int = 1, rank: int
       f64_normal   Box-Muller N(0,1), -0.0 -> +0.0          (C3)
       u16key       uint32 key = u >> 48 (uniform [0,2^16))  (C4 keys)
       u32_const    all keys equal (42)
+      u32_r26      uint32 uniform on [0, 2^26) (tests: dense bucket ranges with duplicates)
       u32_few4     u mod 4
       u32_staggered / u32_bucketsorted  C5 multi-GPU distributions (need world, rank)
       s32          32-byte strings of uniform random bytes (the paper's workload):
@@ -94,6 +95,8 @@ def keys(dist: str, n: int, seed: int, start: int = 0, world: int = 1, rank: int
     u = None if dist in ("i32_gauss", "f64_normal") else data_u64(seed, start, n)
     if dist == "u32_u31":
         return (u >> np.uint64(33)).astype(np.uint32)
+    if dist == "u32_r26":  # uniform on [0, 2^26): dense bucket ranges with duplicates (tests)
+        return (u >> np.uint64(38)).astype(np.uint32)
     if dist == "u32":
         return (u >> np.uint64(32)).astype(np.uint32)
     if dist == "i32_uniform":

@@ -360,3 +360,11 @@ def test_c2_full_merge(ovs, orc, dist, dseed):
 def test_c4_full_merge(ovs, orc):
     c = ovs_inputs.CONFIGS["C4"]
     dro_case(ovs, orc, ovs_inputs.keys("u16key", c["n"], seed=41), c["p"], c["s"], kv=True, merge=True)
+
+
+@pytest.mark.parametrize("dist,n,p,s", [("u32_r26", 1 << 21, 64, 32), ("u32_r26", 3_000_001, 100, 16),
+                                        ("i32_few", 2_000_000, 512, 8), ("u32", 1 << 22, 2048, 64)])
+def test_dense_range_buckets(ovs, orc, dist, n, p, s):
+    """Dense bucket key ranges with hundreds of duplicate keys per bucket (u32 uniform on [0, 2^26))
+    and few-distinct keys: the digit-group bucket sorter against the oracle."""
+    ros_case(ovs, orc, dist, n, p, s, seed=4, dseed=8)

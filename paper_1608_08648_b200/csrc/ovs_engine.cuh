@@ -139,6 +139,21 @@ static void launch(Ctx& c, void (*k)(KA...), dim3 grid, dim3 block, size_t smem,
     cfg.numAttrs = 1;
     OVS_CK(cudaLaunchKernelEx(&cfg, k, std::forward<AA>(args)...));
 }
+// cooperative launch (every CTA resident at once: the kernel uses grid-wide barriers)
+template <class... KA, class... AA>
+static void launch_coop(Ctx& c, void (*k)(KA...), dim3 grid, dim3 block, size_t smem, AA&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c.st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    OVS_CK(cudaLaunchKernelEx(&cfg, k, std::forward<AA>(args)...));
+}
 static inline u32 pow2_at_least(u32 x) {
     u32 p = 1;
     while (p < x) p <<= 1;
@@ -174,6 +189,9 @@ template <class U, bool KV> static size_t bucket_smem(u32 cap) {
 #define OVS_WC_TILE 8192
 #endif
 constexpr int WC_NT = OVS_WC_NT, WC_ITEMS = OVS_WC_TILE / OVS_WC_NT;
+#ifndef OVS_SEL_FUSED  // a3+a4 of 32-bit-key ROS samples in one cooperative launch (k_sel_fused)
+#define OVS_SEL_FUSED 1
+#endif
 #ifndef OVS_SEL_PER_BUCKET
 #define OVS_SEL_PER_BUCKET 2048u
 #endif
@@ -527,6 +545,24 @@ template <bool TAG> struct Selector {
         c.check();
         e.bucket_sort(l, seed);
     }
+    // 32-bit keys (packed records) drawn in random order: a3+a4 in one cooperative launch
+    // (its own coarse bucket count: <= 2048 records per bucket on average, one CTA each)
+    u32 fused_G() const {
+        u32 g = 1;
+        while ((u64)g * SF_NT * SF_IT < m) g *= 2;
+        return g;
+    }
+    bool fused_ok() const { return !TAG && stride == 1 && fused_G() <= std::min<u32>(SEL_GMAX, (u32)e.c.di.sms); }
+    template <int DT>
+    void run_fused(u32 P, u32 s, u32 f, typename Codec<DT>::U* sk, u32* st) {
+        Ctx& c = e.c;
+        if (c.dry) return;
+        const size_t sm = 16 * (size_t)SF_MAXB + 4 * (size_t)SF_NG;
+        auto k = k_sel_fused<DT>;
+        smem_limit(k, sm, c.di);
+        launch_coop(c, k, fused_G(), SF_NT, sm, tk, m, gcnt, gcur, e.B.k[1], e.B.k[0], P, s, f, sk, st, c.status);
+        c.check();
+    }
     // S[q] = T[(q+1)s - 1], q < P-1, from the sorted records
     template <class U> void pick(u32 P, u32 s, u32 f, U* sk, u32* st) {
         Ctx& c = e.c;
@@ -626,7 +662,13 @@ template <int DT, bool DIST> struct RosSampler {
         launch(c, k_ros_take<DT, DIST>, nb, TK_NT, 0, bits, bcnt, M, n, seed, m, x, offset, nl, tk, tt, c.status, po);
         c.check();
     }
-    void select(u32 P, u32 s, u32 f, u64 seed, U* sk, u32* st) { sel->template run<U>(P, s, f, seed, sk, st); }
+    void select(u32 P, u32 s, u32 f, u64 seed, U* sk, u32* st) {
+        if (OVS_SEL_FUSED && !DIST && !TAG && sel->fused_ok()) {
+            sel->template run_fused<DT>(P, s, f, sk, st);
+        } else {
+            sel->template run<U>(P, s, f, seed, sk, st);
+        }
+    }
 };
 
 // ------------------------------------------------------------------ ROS contract sort

@@ -418,32 +418,28 @@ __device__ void block_scan_small(u32* a, u32 cnt, u32* red) {
     __syncthreads();
 }
 
-// block_scan_small that also appends every index whose count is >= T to list[] (warp-aggregated;
-// *over set when the list is full) - the 32-bit keys-only bucket sorter lists its large groups here
+// block_scan_small that also lists every index whose count is >= T in list[] (ascending; *nlist =
+// their number, *over set when it exceeds cap).  Each thread marks its big elements in a 16-bit mask
+// and their number rides in the high half of the value the CTA scans (the counts sum to < 2^16:
+// cnt <= NT*16 elements of a bucket that fits on chip), so the list needs no shared atomics
+// (a shared counter bumped by every warp serialised this scan: 5.5K cycles per bucket).  The
+// 32-bit keys-only bucket sorter lists its large groups here.
 template <int NT>
 __device__ void block_scan_small_list(u32* a, u32 cnt, u32* red, u32 T, u32* list, u32* nlist, u32 cap, u32* over) {
     const u32 i0 = threadIdx.x * 16, r = (threadIdx.x >> 1) & 15;
-    const int lane = threadIdx.x & 31;
-    u32 v[16], s = 0, head = 0;
+    u32 v[16], s = 0, head = 0, bm = 0;
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
         const u32 e = (j + r) & 15;
         v[j] = (i0 + e < cnt) ? a[i0 + e] : 0u;
         s += v[j];
         if (e < r) head += v[j];
-        const bool big = v[j] >= T;
-        const u32 mb = __ballot_sync(0xffffffffu, big);
-        if (mb) {
-            u32 base = 0;
-            if (lane == 0) base = atomicAdd(nlist, __popc(mb));
-            base = __shfl_sync(0xffffffffu, base, 0) + __popc(mb & ((1u << lane) - 1));
-            if (big) {
-                if (base < cap) list[base] = i0 + e;
-                else atomicOr(over, 1u);
-            }
-        }
+        bm |= (v[j] >= T ? 1u : 0u) << e;
     }
-    const u32 base = block_exclusive_scan<NT>(s, red, nullptr);
+    u32 tot;
+    const u32 packed = block_exclusive_scan<NT>(s | ((u32)__popc(bm) << 16), red, &tot);
+    const u32 base = packed & 0xffffu;
+    u32 lb = packed >> 16;  // list slot of this thread's first big element
     u32 run = base + head;  // prefix of element r
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
@@ -451,6 +447,16 @@ __device__ void block_scan_small_list(u32* a, u32 cnt, u32* red, u32 T, u32* lis
         if (e == 0) run = base;
         if (i0 + e < cnt) a[i0 + e] = run;
         run += v[j];
+    }
+    while (bm) {
+        const u32 e = __ffs(bm) - 1;
+        bm &= bm - 1;
+        if (lb < cap) list[lb] = i0 + e;
+        ++lb;
+    }
+    if (threadIdx.x == 0) {
+        *nlist = tot >> 16;
+        if ((tot >> 16) > cap) *over = 1u;
     }
     __syncthreads();
 }
@@ -977,6 +983,263 @@ __global__ void __launch_bounds__(1024) k_sel_scatter(const u64* tk, const u32* 
         nlist[0] = nb;
         nlist[1] = 0;
     }
+}
+
+// a3+a4 in one launch (32-bit keys, packed records ord(key) << 32 | index, all distinct): the
+// same coarse buckets as k_sel_count / k_sel_scatter, then every coarse bucket sorted by one CTA
+// and S[q] = T[(q+1)s/f - 1] read off at once.  The steps are separated by grid-wide barriers
+// (cooperative launch: every CTA is resident) instead of four launches and the bucket sorter's
+// list machinery (sample phase 0.128 ms, most of it launch ramps and one-bucket-per-CTA tails).
+constexpr u32 SF_NT = 1024, SF_MAXB = 8192, SF_NG = 4096, SF_IT = 2, SF_BIG = 256;
+
+// grid-wide barrier number k (1, 2, ...) on a counter zeroed before the launch
+// (bounded wait: a CTA that is never scheduled cannot hang the device; status ST_LIST_OVER)
+__device__ __forceinline__ void grid_sync(u32* ctr, u32 k, u32* status) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(ctr, 1u);
+        for (u32 it = 0; *(volatile u32*)ctr < k * gridDim.x; ++it) {
+            if (it > (1u << 24)) { st_set(status, ST_LIST_OVER); break; }
+            __nanosleep(64);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// ascending sort of a[0..len) of distinct u64 (shared or global memory) by a bitonic network
+// whose comparators all point up (the first step of every merge compares i with its mirror), so
+// the virtual +inf padding beyond len never moves and len need not be a power of two
+template <int NT>
+__device__ void cta_sort_u64(u64* a, u32 len) {
+    u32 N = 1;
+    while (N < len) N <<= 1;
+    for (u32 kk = 2; kk <= N; kk <<= 1) {
+        const u32 hk = kk >> 1;
+        for (u32 t = threadIdx.x; t < N / 2; t += NT) {
+            const u32 x = (t / hk) * kk + (t % hk), y = (t / hk) * kk + kk - 1 - (t % hk);
+            if (y < len) { const u64 u = a[x], v = a[y]; if (v < u) { a[x] = v; a[y] = u; } }
+        }
+        __syncthreads();
+        for (u32 j = kk >> 2; j > 0; j >>= 1) {
+            for (u32 t = threadIdx.x; t < N / 2; t += NT) {
+                const u32 x = ((t & ~(j - 1)) << 1) | (t & (j - 1)), y = x + j;
+                if (y < len) { const u64 u = a[x], v = a[y]; if (v < u) { a[x] = v; a[y] = u; } }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// cta_bitonic_1pt for distinct u64 keys without tags (N == blockDim.x)
+__device__ void cta_bitonic_1pt_u64(u64* a, u32 N) {
+    const u32 e = threadIdx.x;
+    u64 k = a[e];
+    for (u32 kk = 2; kk <= N; kk <<= 1) {
+        for (u32 j = kk >> 1; j > 0; j >>= 1) {
+            u64 o;
+            if (j >= 32) {
+                __syncthreads();
+                a[e] = k;
+                __syncthreads();
+                o = a[e ^ j];
+            } else {
+                o = shfl_xor_any(k, (int)j);
+            }
+            k = (((e & kk) == 0) == ((e & j) == 0)) ? min(k, o) : max(k, o);
+        }
+    }
+    __syncthreads();
+    a[e] = k;
+    __syncthreads();
+}
+
+// grid = G CTAs (<= SEL_GMAX, m <= G * SF_NT * SF_IT); gcnt[G] and *gbar zeroed before the launch;
+// t2 = coarse-bucket order (workspace), ts = T sorted; S[q] = ts[(q+1)s/f - 1] for q < P-1
+#ifdef OVS_SF_PROF
+__device__ unsigned long long g_sfprof[8];
+#define SF_PROBE(i) if (threadIdx.x == 0) { const long long n_ = clock64(); atomicAdd(&g_sfprof[i], (unsigned long long)(n_ - sf_t_)); sf_t_ = n_; }
+#else
+#define SF_PROBE(i)
+#endif
+template <int DT>
+__global__ void __launch_bounds__(SF_NT, 1) k_sel_fused(const u64* tk, u32 m, u32* gcnt, u32* gbar, u64* t2, u64* ts,
+                                                        u32 P, u32 s, u32 f, typename Codec<DT>::U* sk, u32* st,
+                                                        u32* status) {
+    typedef typename Codec<DT>::U U;
+    extern __shared__ __align__(16) u64 sbuf[];  // 2 x SF_MAXB records, SF_NG group counters
+    __shared__ u64 qk[SEL_Q];
+    __shared__ u32 qt[SEL_Q];
+    __shared__ u32 h[SEL_GMAX], base[SEL_GMAX], start[SEL_GMAX + 1];
+    __shared__ u32 red[SF_NT / 32 + 1], big[SF_BIG], nbig, over;
+    __shared__ u64 rmn[SF_NT / 32], rmx[SF_NT / 32];
+#ifdef OVS_SF_PROF
+    long long sf_t_ = clock64();
+#endif
+    const u32 G = gridDim.x;
+    constexpr u32 RC = SF_IT;
+    u64 rc[RC];
+    u32 rv = 0;  // valid records of this thread (bit q)
+    u32 nbar = 0;
+    // 1. coarse splitters from the first Q records (T in draw order: a uniform random subset)
+    const u32 Q = min(m, SEL_Q);
+    if (G > 1) {
+        for (u32 i = threadIdx.x; i < SF_NT; i += SF_NT) qk[i] = i < Q ? tk[i] : ~0ull;  // padding sorts last
+        __syncthreads();
+        cta_bitonic_1pt_u64(qk, SF_NT);
+        u64 ck = 0;
+        if (threadIdx.x + 1 < G) ck = qk[(u32)(((u64)(threadIdx.x + 1) * Q) / G) - 1];
+        __syncthreads();
+        if (threadIdx.x + 1 < G) { qk[threadIdx.x] = ck; qt[threadIdx.x] = 0u; }
+    }
+    SF_PROBE(0)
+    for (u32 g = threadIdx.x; g < G; g += SF_NT) h[g] = 0;
+    __syncthreads();
+    // 2. this CTA's slice of T per coarse bucket; the CTA's run inside each bucket claimed
+    {
+        const u32 b0 = (u32)(((u64)m * blockIdx.x) / G), b1 = (u32)(((u64)m * (blockIdx.x + 1)) / G);
+#pragma unroll
+        for (u32 q = 0; q < RC; ++q) {
+            const u32 i = b0 + q * SF_NT + threadIdx.x;
+            if (i < b1) { rc[q] = tk[i]; rv |= 1u << q; }
+        }
+    }
+    u32 gg[RC], rr[RC];
+#pragma unroll
+    for (u32 q = 0; q < RC; ++q) {
+        if ((rv >> q) & 1u) {
+            gg[q] = coarse_of(qk, qt, G - 1, rc[q], 0u);
+            rr[q] = atomicAdd(&h[gg[q]], 1u);
+        }
+    }
+    __syncthreads();
+    for (u32 g = threadIdx.x; g < G; g += SF_NT) base[g] = h[g] ? atomicAdd(&gcnt[g], h[g]) : 0u;
+    SF_PROBE(1)
+    grid_sync(gbar, ++nbar, status);
+    SF_PROBE(2)
+    // 3. bucket starts (every CTA scans the G totals) and the scatter into coarse-bucket order
+    if (threadIdx.x < 32) {
+        u32 v[SEL_GMAX / 32], sum = 0;
+#pragma unroll
+        for (u32 j = 0; j < SEL_GMAX / 32; ++j) {
+            const u32 g = threadIdx.x * (SEL_GMAX / 32) + j;
+            v[j] = g < G ? __ldcg(&gcnt[g]) : 0u;
+            sum += v[j];
+        }
+        u32 x = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u32 y = __shfl_up_sync(0xffffffffu, x, o);
+            if ((int)threadIdx.x >= o) x += y;
+        }
+        u32 run = x - sum;
+#pragma unroll
+        for (u32 j = 0; j < SEL_GMAX / 32; ++j) {
+            const u32 g = threadIdx.x * (SEL_GMAX / 32) + j;
+            if (g < G) start[g] = run;
+            run += v[j];
+        }
+        if (threadIdx.x == 31) start[G] = x;  // = m
+    }
+    __syncthreads();
+#pragma unroll
+    for (u32 q = 0; q < RC; ++q)
+        if ((rv >> q) & 1u) t2[start[gg[q]] + base[gg[q]] + rr[q]] = rc[q];
+    SF_PROBE(3)
+    grid_sync(gbar, ++nbar, status);
+    SF_PROBE(4)
+    // 4. CTA b sorts coarse bucket b: a counting sort by a fine digit of (record - min) spreads it
+    // over ~len/2 groups (the records are a random sample: mostly 0-4 per group), then groups of
+    // <= 8 by one thread (Batcher network), larger ones (listed by the scan) by a warp or the CTA.
+    // A bucket over SF_MAXB records (the 8-records-per-splitter coarse sample makes that
+    // vanishingly rare) is sorted in place in global memory by the bitonic network instead.
+    const u32 bs = start[blockIdx.x], len = start[blockIdx.x + 1] - bs;
+    u64* a = t2 + bs;
+    if (len <= SF_MAXB) {
+        u64* A = sbuf;
+        u64* Bv = sbuf + SF_MAXB;
+        u32* cnt = (u32*)(sbuf + 2 * SF_MAXB);
+        u64 mn = ~0ull, mx = 0;
+        for (u32 i = threadIdx.x; i < len; i += SF_NT) {
+            const u64 v = __ldcg(t2 + bs + i);
+            A[i] = v;
+            mn = min(mn, v);
+            mx = max(mx, v);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) { mn = min(mn, shfl_xor_any(mn, o)); mx = max(mx, shfl_xor_any(mx, o)); }
+        if ((threadIdx.x & 31) == 0) { rmn[threadIdx.x >> 5] = mn; rmx[threadIdx.x >> 5] = mx; }
+        u32 ng = 32;
+        while (ng < SF_NG && ng * 2 < len) ng <<= 1;
+        for (u32 g = threadIdx.x; g < ng; g += SF_NT) cnt[g] = 0;
+        if (threadIdx.x == 0) over = 0;
+        __syncthreads();
+        mn = rmn[0]; mx = rmx[0];
+        for (u32 w = 1; w < SF_NT / 32; ++w) { mn = min(mn, rmn[w]); mx = max(mx, rmx[w]); }
+        // digit = floor((x - mn) * ng / (mx - mn + 1)), a fixed-point multiply-high: monotone
+        const double mq = (double)ng * 18446744073709551616.0 / ((double)(mx - mn) + 1.0);
+        const u64 mult = mq >= 18446744073709549568.0 ? 0xffffffffffffffffull : (u64)mq;
+        auto digit = [&](u64 x) -> u32 { return min((u32)__umul64hi(x - mn, mult), ng - 1); };
+        for (u32 i = threadIdx.x; i < len; i += SF_NT) atomicAdd(&cnt[digit(A[i])], 1u);
+        __syncthreads();
+        block_scan_small_list<SF_NT>(cnt, ng, red, 9u, big, &nbig, SF_BIG, &over);  // cnt[g] = start
+        for (u32 i = threadIdx.x; i < len; i += SF_NT) {
+            const u64 v = A[i];
+            Bv[atomicAdd(&cnt[digit(v)], 1u)] = v;  // afterwards cnt[g] = end of group g
+        }
+        __syncthreads();
+        typedef Elem<u64, false> E;
+        for (u32 g = threadIdx.x; g < ng; g += SF_NT) {
+            const u32 gs = g ? cnt[g - 1] : 0u, gl = cnt[g] - gs;
+            if (gl < 2 || gl > 8) continue;
+            E e[8];
+#pragma unroll
+            for (u32 q = 0; q < 8; ++q) e[q].k = q < gl ? Bv[gs + q] : ~0ull;
+            network8(e);
+#pragma unroll
+            for (u32 q = 0; q < 8; ++q)
+                if (q < gl) Bv[gs + q] = e[q].k;
+        }
+        const u32 nl = over ? ng : min(nbig, SF_BIG);  // list overflow: scan every group
+        const int lane = threadIdx.x & 31;
+        for (u32 q = threadIdx.x >> 5; q < nl; q += SF_NT / 32) {
+            const u32 g = over ? q : big[q];
+            const u32 gs = g ? cnt[g - 1] : 0u, gl = cnt[g] - gs;
+            if (gl <= 8 || gl > 256) continue;
+            E e[8];
+#pragma unroll
+            for (u32 r = 0; r < 8; ++r) { const u32 x = r * 32 + lane; e[r].k = x < gl ? Bv[gs + x] : ~0ull; }
+            warp_bitonic<E, 8>(e);
+#pragma unroll
+            for (u32 r = 0; r < 8; ++r) { const u32 x = r * 32 + lane; if (x < gl) Bv[gs + x] = e[r].k; }
+        }
+        __syncthreads();
+        for (u32 q = 0; q < nl; ++q) {  // groups over 256 records (heavy key repeats): the CTA
+            const u32 g = over ? q : big[q];
+            const u32 gs = g ? cnt[g - 1] : 0u, gl = cnt[g] - gs;
+            if (gl > 256) cta_sort_u64<SF_NT>(Bv + gs, gl);
+        }
+        __syncthreads();
+        a = Bv;
+    } else {
+        cta_sort_u64<SF_NT>(a, len);
+        __syncthreads();
+    }
+    SF_PROBE(5)
+    for (u32 i = threadIdx.x; i < len; i += SF_NT) ts[bs + i] = a[i];
+    // 5. the splitters whose rank falls in this bucket: r = (q+1)s/f - 1 in [bs, bs + len)
+    const u64 q0 = ((u64)bs * f + f) / s;  // first q+1 with (q+1)s/f - 1 >= bs, up to rounding
+    for (u64 q1 = (q0 > 0 ? q0 - 1 : 0) + threadIdx.x; q1 < P; q1 += SF_NT) {
+        const u64 r = q1 * s / f;  // (q+1) = q1 >= 1
+        if (q1 == 0 || r == 0) continue;
+        if (r - 1 < bs) continue;
+        if (r - 1 >= (u64)bs + len) break;
+        const u64 v = a[r - 1 - bs];
+        sk[q1 - 1] = (U)(v >> 32);
+        st[q1 - 1] = (u32)v;
+    }
+    SF_PROBE(6)
 }
 
 // a4: S[q] = T[(q+1)s - 1] (reading Q4); also the p-1 report arrays
@@ -2424,6 +2687,7 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                     }
                 };
                 const bool need_sort = KV || !direct;
+                constexpr bool FAST32 = !KV && sizeof(U) == 4 && OVS_BS_WIN16;
                 for (u32 g = threadIdx.x; g < ng; g += BS_NT) Sa.cnt[g] = 0;
                 __syncthreads();
                 BS_PROBE(2)
@@ -2434,7 +2698,7 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                 });
                 __syncthreads();
                 BS_PROBE(3)
-                if constexpr (!KV && sizeof(U) == 4 && OVS_BS_WIN16) {
+                if constexpr (FAST32) {
                     // (groups of >= 10 keys are listed here for the window networks below)
                     block_scan_small_list<BS_NT>(Sa.cnt, ng, red, need_sort ? 10u : 0xffffffffu, s_big, &s_nbig,
                                                  (u32)BS_BIGMAX, &s_over);
@@ -2442,7 +2706,7 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                     block_scan_small<BS_NT>(Sa.cnt, ng, red);  // cnt[g] = start of group g
                 }
                 BS_PROBE(4)
-                if constexpr (!KV && sizeof(U) == 4 && OVS_BS_WIN16) {
+                if constexpr (FAST32) {
                     // ---- 32-bit keys only: swizzled item array, windowed networks
                     u32* const kb = (u32*)S.k;  // 16-byte aligned; logical item x at kb[sw16(x + al)]
                     const u32 al = (u32)(((uintptr_t)(okeys + bk.beg)) / sizeof(U)) & 3u;

@@ -21,3 +21,8 @@ extern "C" int ovs_debug_bsprof_u32_k(unsigned long long* out, int reset) {
     return 0;
 }
 #endif
+#ifdef OVS_SF_PROF
+extern "C" int ovs_debug_sfprof(unsigned long long* out) {
+    return cudaMemcpyFromSymbol(out, ovs::g_sfprof, 8 * sizeof(unsigned long long)) != cudaSuccess;
+}
+#endif

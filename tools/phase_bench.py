@@ -43,10 +43,20 @@ for path in libs:
         continue
     arr = (ctypes.c_ulonglong * 16)()
     for dt in ("u32_k", "u32_v", "i32_k", "i32_v", "f64_k", "f64_v"):
-        getattr(L, "ovs_debug_bsprof_" + dt)(arr, 1)
+        if hasattr(L, "ovs_debug_bsprof_" + dt):
+            getattr(L, "ovs_debug_bsprof_" + dt)(arr, 1)
     srt = ovs.Sorter(n, torch.uint32, False, "ros", p, s, 1) if False else None
     names = ["resplit-push", "loose", "setup", "hist", "scan", "scatter", "net8", "net16+warp", "huge", "write", "rs-sample", "rs-count", "rs-scatter"]
     tot = arr[15]
     print("bucket sorter cycles (sum over CTAs, thread 0), share of kernel:",
           "  ".join(f"{nm} {arr[i] / tot * 100:.1f}%" for i, nm in enumerate(names)),
           f" other {(tot - sum(arr[:13])) / tot * 100:.1f}%")
+
+
+# fused sample-sort phase cycles (libraries built with -DOVS_SF_PROF)
+for path in libs:
+    L = ctypes.CDLL(path or ovs.LIB_PATH)
+    if hasattr(L, "ovs_debug_sfprof"):
+        a = (ctypes.c_ulonglong * 8)()
+        L.ovs_debug_sfprof(a)
+        print("k_sel_fused cycles (sum over CTAs and sorts, thread 0):", [a[i] for i in range(7)])

@@ -277,7 +277,7 @@ template <int DT, bool KV> struct Engine {
         z.log2L = ilog2(z.L);
         // chunks: one per resident CTA slot, whole sub-tiles
         const u32 ts = PT_NT * PartItems<U, KV>::v;
-        u32 want = (u32)c.di.sms;  // one chunk per SM: fewer concurrently open output lines
+        u32 want = (u32)c.di.sms * (wc ? OVS_WC_MINB : 1);  // one chunk per resident scatter CTA
         z.chunk = std::max<u32>(ts, cdiv(cdiv(n, want), ts) * ts);
         z.nchunk = std::max<u32>(1, cdiv(n, z.chunk));
         z.sk = c.take<U>(std::max<u32>(P, 1));

@@ -1776,8 +1776,14 @@ __global__ void __launch_bounds__(NT) k_scatter(Bufs<typename Codec<DT>::U> B, c
 //   P3: keys of the new, incomplete sector -> wc[b]
 // Ranks come from shared atomics: positions inside a (chunk, bucket) run are not in input
 // order, which the bucket sorter makes irrelevant (module notes).
+#ifndef OVS_WC_SB  // bytes of a write-combining sector (the DRAM sector is 32)
+#define OVS_WC_SB 32
+#endif
+#ifndef OVS_WC_MINB  // resident CTAs per SM of the write-combining scatter
+#define OVS_WC_MINB 1
+#endif
 template <class U> __host__ __device__ constexpr size_t wc_smem_bytes(u32 PS) {
-    return 32 * (size_t)PS + 8 * (size_t)PS;  // wc, q, sb
+    return OVS_WC_SB * (size_t)PS + 8 * (size_t)PS;  // wc, q, sb
 }
 
 // LEVEL0: the caller's raw keys in buffer 0 -> buffer 1; otherwise ordered keys of every chunk's
@@ -1786,20 +1792,20 @@ template <class U> __host__ __device__ constexpr size_t wc_smem_bytes(u32 PS) {
 // floor(b*world/P)'s receive window over NVLink (po.peers[owner] + po.off), at dst_off[b] (this
 // rank's run of b inside the owner's region, ovs_dist.cu) + the chunk's offset in the run.
 template <int DT, int NT, int ITEMS, bool LEVEL0, bool DIST = false>
-__global__ void __launch_bounds__(NT, 1) k_scatter_wc(Bufs<typename Codec<DT>::U> B, const Chunk* chunks,
+__global__ void __launch_bounds__(NT, OVS_WC_MINB) k_scatter_wc(Bufs<typename Codec<DT>::U> B, const Chunk* chunks,
                                                        const u32* nchunks, const Seg* segs, u32 PS, const u32* hist,
                                                        const u32* tot_pool, const u16* bid, const u32* dst_off = nullptr,
                                                        PeerOut po = PeerOut{nullptr, 0, 1}) {
     PDL_PROLOGUE();
     typedef typename Codec<DT>::U U;
-    constexpr u32 SV = 32 / sizeof(U);  // keys per 32-byte sector
+    constexpr u32 SV = OVS_WC_SB / sizeof(U);  // keys per write-combining sector
     constexpr u32 V = 16 / sizeof(U);   // keys per 16-byte vector
     constexpr u32 TS = NT * ITEMS;
     constexpr u32 NI = (ITEMS + 1) / 2;  // two u16 bucket ids per word
     static_assert(ITEMS % V == 0 && ITEMS <= 32, "whole vectors per thread, one mask bit per item");
     extern __shared__ __align__(16) char smem[];
     U* wc = (U*)smem;
-    u32* q = (u32*)(smem + 32 * (size_t)PS);
+    u32* q = (u32*)(smem + OVS_WC_SB * (size_t)PS);
     u32* sb = q + PS;
     const u32 nc = *nchunks;
     for (u32 c = blockIdx.x; c < nc; c += gridDim.x) {
@@ -1912,8 +1918,8 @@ __global__ void __launch_bounds__(NT, 1) k_scatter_wc(Bufs<typename Codec<DT>::U
                     if (front == 0) {
                         const uint4* w4 = (const uint4*)wb;
                         uint4* g4 = (uint4*)(db + s0);
-                        g4[0] = w4[0];
-                        g4[1] = w4[1];
+#pragma unroll
+                        for (u32 x = 0; x < OVS_WC_SB / 16; ++x) g4[x] = w4[x];
                     } else {
                         for (u32 x = front; x < SV; ++x) db[s0 + x] = wb[x];
                     }
@@ -1983,8 +1989,8 @@ __global__ void __launch_bounds__(NT, 1) k_scatter_wc(Bufs<typename Codec<DT>::U
                     if (front == 0) {
                         const uint4* w4 = (const uint4*)wb;
                         uint4* g4 = (uint4*)(db + s0);
-                        g4[0] = w4[0];
-                        g4[1] = w4[1];
+#pragma unroll
+                        for (u32 x = 0; x < OVS_WC_SB / 16; ++x) g4[x] = w4[x];
                     } else {
                         for (u32 x = front; x < SV; ++x) db[s0 + x] = wb[x];
                     }

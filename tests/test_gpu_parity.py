@@ -368,3 +368,17 @@ def test_dense_range_buckets(ovs, orc, dist, n, p, s):
     """Dense bucket key ranges with hundreds of duplicate keys per bucket (u32 uniform on [0, 2^26))
     and few-distinct keys: the digit-group bucket sorter against the oracle."""
     ros_case(ovs, orc, dist, n, p, s, seed=4, dseed=8)
+
+
+@pytest.mark.parametrize("dist,n,p,s", [
+    ("u32", 1 << 20, 64, 32),          # ps-1 = 2047: one coarse bucket
+    ("u32", 1 << 20, 1025, 2),         # 2049: two
+    ("i32_gauss", 1 << 20, 2049, 64),  # 131135: 128 coarse buckets of ~1K records
+    ("u32_few4", 1 << 20, 4096, 64),   # 262143 (the metric's sample): 128 buckets of ~2K, 4 key values
+    ("u32_const", 1 << 20, 4096, 64),  # every record has the same key word: ordered by index alone
+    ("u32", 1 << 21, 4097, 64),        # 262207 > 128 * 2048: the multi-launch sample sort instead
+])
+def test_fused_sample_sort_bounds(ovs, orc, dist, n, p, s):
+    """a3+a4 in one cooperative launch (k_sel_fused) at the edges of its coarse-bucket count
+    and past its limit: splitters (key and tag), counts and output against the oracle."""
+    ros_case(ovs, orc, dist, n, p, s, seed=6)

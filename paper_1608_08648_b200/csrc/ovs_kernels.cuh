@@ -2395,6 +2395,7 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
     __shared__ u32 s_big[BS_BIGMAX];
     __shared__ u32 s_huge[BS_HUGEMAX];
     __shared__ U s_mn[BS_NT / 32], s_mx[BS_NT / 32];
+    __shared__ u32 s_hl[4][BS_NT / 32];  // DT_U64 records: key-word and tag-word ranges
     __shared__ U sp_k[BS_SPMAX];
     __shared__ u32 sp_t[BS_SPMAX], sp_cnt[BS_SPMAX + 1], sp_cur[BS_SPMAX];
     __shared__ u32 rs_cnt[BS_SPMAX], rs_off[BS_SPMAX], s_w[4];
@@ -2653,7 +2654,46 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                 Sa.k = S.k + ((((uintptr_t)(okeys + bk.beg)) / sizeof(U)) & (16 / sizeof(U) - 1));
                 BS_PROBE(1)
                 U lo = (U)bk.lo, hi = (U)bk.hi;
-                if (bk.level & BK_LOOSE) {
+                // internal records (DT_U64: key word << 32 | tag) whose key words take few values
+                // (few distinct keys) sit in a few narrow clusters of the record range, so a digit
+                // over [lo, hi] puts each cluster in one or two huge groups: such buckets take a
+                // two-level digit instead, (key word - its min) * per + the tag's digit inside
+                // [min tag, max tag] over per groups (monotone in the record)
+                bool two = false;
+                u32 hmn = 0, per = 1, lmn = 0, multl = 0;
+                if constexpr (DT == DT_U64 && !KV) {
+                    u32 a = 0xffffffffu, b = 0, c2 = 0xffffffffu, d = 0;
+                    for_items<U, BS_NT, OVS_BS_UNR>(src, bk.beg, m, [&](U k, u32) {
+                        const u32 h = (u32)((u64)k >> 32), l = (u32)k;
+                        a = min(a, h); b = max(b, h); c2 = min(c2, l); d = max(d, l);
+                    });
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) {
+                        a = min(a, __shfl_xor_sync(0xffffffffu, a, o)); b = max(b, __shfl_xor_sync(0xffffffffu, b, o));
+                        c2 = min(c2, __shfl_xor_sync(0xffffffffu, c2, o)); d = max(d, __shfl_xor_sync(0xffffffffu, d, o));
+                    }
+                    if (lane == 0) { s_hl[0][wid] = a; s_hl[1][wid] = b; s_hl[2][wid] = c2; s_hl[3][wid] = d; }
+                    __syncthreads();
+                    a = s_hl[0][0]; b = s_hl[1][0]; c2 = s_hl[2][0]; d = s_hl[3][0];
+                    for (int q = 1; q < BS_NT / 32; ++q) {
+                        a = min(a, s_hl[0][q]); b = max(b, s_hl[1][q]); c2 = min(c2, s_hl[2][q]); d = max(d, s_hl[3][q]);
+                    }
+                    __syncthreads();
+                    lo = ((u64)a << 32) | c2;  // every record lies in [lo, hi] (tighter than the bounds)
+                    hi = ((u64)b << 32) | d;
+                    u32 ngt = 32;
+                    while (ngt < (u32)BS_NGMAX && ngt * 3 < m) ngt <<= 1;
+                    const u64 H = (u64)b - a + 1;
+                    if (H >= 2 && H * 4 <= ngt) {
+                        two = true;
+                        hmn = a;
+                        per = ngt / (u32)H;
+                        lmn = c2;
+                        const double mqt = (double)per * 4294967296.0 / ((double)(d - c2) + 1.0);
+                        multl = mqt >= 4294967295.0 ? 0xffffffffu : (u32)mqt;
+                    }
+                }
+                if ((bk.level & BK_LOOSE) && !(DT == DT_U64 && !KV)) {
                     U mn = umax_of<U>(), mx = 0;
                     for_items<U, BS_NT, OVS_BS_UNR>(src, bk.beg, m, [&](U kr, u32) { const U k = K(kr); mn = min(mn, k); mx = max(mx, k); });
     #pragma unroll
@@ -2688,11 +2728,15 @@ __global__ void __launch_bounds__(BS_NT, 1) k_bucket_sort(const Bucket* list, co
                         const u32 x = (u32)(k - lo);
                         return direct ? x : min(__umulhi(x, mult32), ng - 1);  // min: memory safety only
                     } else {
+                        if (DT == DT_U64 && !KV && two) {
+                            const u32 h = (u32)((u64)k >> 32) - hmn, l = (u32)k - lmn;
+                            return min(h * per + min(__umulhi(l, multl), per - 1), ng - 1);
+                        }
                         const u64 x = comp ? ((((u64)(k - lo)) << ixbits) | ix) : (u64)(U)(k - lo);
                         return direct ? (u32)x : min((u32)__umul64hi(x, mult), ng - 1);
                     }
                 };
-                const bool need_sort = KV || !direct;
+                const bool need_sort = KV || !direct || two;
                 constexpr bool FAST32 = !KV && sizeof(U) == 4 && OVS_BS_WIN16;
                 for (u32 g = threadIdx.x; g < ng; g += BS_NT) Sa.cnt[g] = 0;
                 __syncthreads();

@@ -189,6 +189,9 @@ template <class U, bool KV> static size_t bucket_smem(u32 cap) {
 #define OVS_WC_TILE 8192
 #endif
 constexpr int WC_NT = OVS_WC_NT, WC_ITEMS = OVS_WC_TILE / OVS_WC_NT;
+#ifndef OVS_REFINE_WC  // ROS refinement stays within the write-combining scatter's bucket count
+#define OVS_REFINE_WC 1
+#endif
 #ifndef OVS_SEL_FUSED  // a3+a4 of 32-bit-key ROS samples in one cooperative launch (k_sel_fused)
 #define OVS_SEL_FUSED 1
 #endif
@@ -710,7 +713,7 @@ template <int DT, bool KV> struct RosSort {
             // refine while the buckets exceed the on-chip capacity, within the bucket count the
             // fast scatter handles (keys only: the write-combining one)
             u32 pmax = std::min<u32>(8192, e.max_p_one_level());
-            if (!KV && e.use_wc(p)) while (pmax > p && !e.use_wc(pmax)) --pmax;
+            if (OVS_REFINE_WC && !KV && e.use_wc(p)) while (pmax > p && !e.use_wc(pmax)) --pmax;
             while (s / (2 * f) >= 8 && (u64)p * 2 * f <= pmax && (u64)n > (u64)p * f * e.cap)
                 f *= 2;
             P0 = p * f;

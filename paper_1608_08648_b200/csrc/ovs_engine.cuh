@@ -38,6 +38,7 @@ struct StatusFail {
 struct DevInfo {
     int sms = 148;
     int smem_optin = 232448;
+    long long l2_bytes = 126ll << 20;
 };
 
 inline DevInfo dev_info_impl() {
@@ -48,6 +49,7 @@ inline DevInfo dev_info_impl() {
     if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0) d.sms = v;
     if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) == cudaSuccess && v > 0)
         d.smem_optin = v;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, dev) == cudaSuccess && v > 0) d.l2_bytes = v;
     cudaGetLastError();
     return d;
 }
@@ -495,6 +497,50 @@ template <bool KV> struct InternalSort {
             e.level0(z, l, nullptr);
         }
         e.bucket_sort(l, seed);
+    }
+};
+
+// DRO's sample T (p sorted runs of s records): merged (SampleMerge) while the merge's two arrays
+// fit in half the L2, else sorted by the generic internal sort — measured on B200: C2 (12.6 MB of
+// records) 0.20 -> 0.11 ms merged; C4 (56.6 MB) 0.43 ms sorted, 0.48 ms merged (9 levels that
+// miss L2).  OVS_DRO_SAMPLE_SORT=1 / =0 forces the sort / the merge (experiments and tests).
+static inline bool sample_sorted(const DevInfo& di, u64 ns, bool w64) {
+    const char* v = getenv("OVS_DRO_SAMPLE_SORT");
+    if (v && (v[0] == '0' || v[0] == '1')) return v[0] == '1';
+    return 2 * ns * (w64 ? 12 : 8) > (u64)di.l2_bytes / 2;
+}
+// ------------------------------------------------------------------ a11: merge of the DRO sample
+// The p sorted regular samples T_k (s records each, contiguous, run k at k*s) merged into T by
+// ceil(lg p) levels of the pairwise merge k_sample_merge (Algorithm 1 step 2, PAPER.md:266,
+// PAPER.md:359-364), ping-ponging between the sample arrays and one scratch pair.  T is identical
+// to a sort of the sample (records are unique by their tag).  run() returns the buffer holding T.
+struct SampleMerge {
+    Ctx& c;
+    u32 ns, s;
+    bool w64;
+    u64* k[2] = {nullptr, nullptr};
+    u32* t[2] = {nullptr, nullptr};
+    SampleMerge(Ctx& c_, u32 ns_, u32 s_, u64* k0, u32* t0, bool w64_) : c(c_), ns(ns_), s(s_), w64(w64_) {
+        k[0] = k0;
+        t[0] = t0;
+        k[1] = c.take<u64>(ns);
+        t[1] = w64 ? c.take<u32>(ns) : nullptr;
+    }
+    int run() {
+        int cur = 0;
+        if (c.dry || ns == 0 || s == 0) return cur;
+        for (u64 L = s; L < ns; L *= 2) {
+            const u32 tpp = (u32)cdiv(2 * L, (u64)MS_TILE), pairs = (u32)cdiv((u64)ns, 2 * L);
+            if (w64)
+                launch(c, k_sample_merge<true>, pairs * tpp, MS_NT, 0, (const u64*)k[cur], (const u32*)t[cur], k[cur ^ 1],
+                       t[cur ^ 1], ns, (u32)L, tpp);
+            else
+                launch(c, k_sample_merge<false>, pairs * tpp, MS_NT, 0, (const u64*)k[cur], (const u32*)nullptr,
+                       k[cur ^ 1], (u32*)nullptr, ns, (u32)L, tpp);
+            c.check();
+            cur ^= 1;
+        }
+        return cur;
     }
 };
 
@@ -962,6 +1008,8 @@ template <int DT, bool KV> struct DroSort {
     u64* t_pack = nullptr; u64* t_key = nullptr; u32* t_tag = nullptr;
     InternalSort<false>* ts32 = nullptr;
     InternalSort<true>* ts64 = nullptr;
+    SampleMerge* smg = nullptr;
+    const u64* fin_pack = nullptr; const u64* fin_key = nullptr; const u32* fin_tag = nullptr;  // sorted T
     u32* bound = nullptr; u32* cnt = nullptr; u32* tot = nullptr; u32* nseg = nullptr;
     Seg* seg = nullptr;
     // sequences and buckets of n/p keys far over the on-chip capacity: level 1 re-splits them
@@ -994,13 +1042,13 @@ template <int DT, bool KV> struct DroSort {
         st = c.take<u32>(p);
         // (the sample of sorted runs is sorted by the generic internal sort; the ROS coarse-bucket
         // selector measured slower here: its buckets of ~n/(128 r p) records overflow the chip)
-        if (sizeof(U) == 4) {
-            t_pack = c.take<u64>(ns);
-            ts32 = new InternalSort<false>(c, ns, t_pack, nullptr);
+        if (sizeof(U) == 4) t_pack = c.take<u64>(ns);
+        else { t_key = c.take<u64>(ns); t_tag = c.take<u32>(ns); }
+        if (sample_sorted(c.di, ns, sizeof(U) == 8)) {
+            if (sizeof(U) == 4) ts32 = new InternalSort<false>(c, ns, t_pack, nullptr);
+            else ts64 = new InternalSort<true>(c, ns, t_key, t_tag);
         } else {
-            t_key = c.take<u64>(ns);
-            t_tag = c.take<u32>(ns);
-            ts64 = new InternalSort<true>(c, ns, t_key, t_tag);
+            smg = new SampleMerge(c, ns, s, sizeof(U) == 4 ? t_pack : t_key, t_tag, sizeof(U) == 8);
         }
         if (merge) {
             // merge capacity (items in shared memory, two buffers) and the refinement f: the
@@ -1035,7 +1083,7 @@ template <int DT, bool KV> struct DroSort {
             e.carve_lists(lb, p * Level1<DT, KV>::PS);
         }
     }
-    ~DroSort() { delete ts32; delete ts64; delete l1x; }
+    ~DroSort() { delete ts32; delete ts64; delete smg; delete l1x; }
 
     // f2: a13 against the P - 1 fine splitters, then a14 as an on-chip p-way merge per fine
     // bucket (k_dro_merge); fine buckets over the merge capacity: gather + bucket sorter
@@ -1100,13 +1148,18 @@ template <int DT, bool KV> struct DroSort {
         launch(c, k_dro_sample<U>, cdiv((u64)ns, 256), 256, 0, B.k[1], n, p, s, flags & OVS_DRO_PADDED_POSITIONS,
                                                              t_pack, t_key, t_tag);
         c.check();
-        if (ts32) ts32->run(0xd0d0);
+        fin_pack = t_pack; fin_key = t_key; fin_tag = t_tag;
+        if (smg) {
+            const int b = smg->run();
+            if (sizeof(U) == 4) fin_pack = smg->k[b];
+            else { fin_key = smg->k[b]; fin_tag = smg->t[b]; }
+        } else if (ts32) ts32->run(0xd0d0);
         else ts64->run(0xd0d0);
-        launch(c, k_pick_splitters<U>, cdiv(p, 256), 256, 0, t_pack, t_key, t_tag, p, s, 1u, sk, st);
+        launch(c, k_pick_splitters<U>, cdiv(p, 256), 256, 0, fin_pack, fin_key, fin_tag, p, s, 1u, sk, st);
         c.check();
         if (merge) {
             // fine splitters T[floor((i+1) s / f) - 1]: the contract's S[q] is fine splitter (q+1)f - 1
-            launch(c, k_pick_splitters<U>, cdiv(P, 256), 256, 0, t_pack, t_key, t_tag, P, s, f, fsk, fst);
+            launch(c, k_pick_splitters<U>, cdiv(P, 256), 256, 0, fin_pack, fin_key, fin_tag, P, s, f, fsk, fst);
             c.check();
             c.mark(2);
             run_merge();
@@ -1386,6 +1439,8 @@ template <int DT, bool KV> struct DistDroSort : DistRun {
     u64* t_pack = nullptr; u64* t_key = nullptr; u32* t_tag = nullptr;
     InternalSort<false>* ts32 = nullptr;
     InternalSort<true>* ts64 = nullptr;
+    SampleMerge* smg = nullptr;
+    const u64* fin_pack = nullptr; const u64* fin_key = nullptr; const u32* fin_tag = nullptr;  // sorted T
     U* sk = nullptr; u32* st = nullptr;
     u32* bound = nullptr; u32* cnt = nullptr; u32* tot = nullptr; u32* nseg = nullptr; Seg* seg = nullptr;
     u32* dst_off = nullptr; u32* desc = nullptr;
@@ -1409,13 +1464,13 @@ template <int DT, bool KV> struct DistDroSort : DistRun {
         e.B.i[1] = KV ? c.take<u32>(nl) : nullptr;
         sk = c.take<U>(p);
         st = c.take<u32>(p);
-        if (sizeof(U) == 4) {
-            t_pack = c.take<u64>(ns);
-            ts32 = new InternalSort<false>(c, ns, t_pack, nullptr);
+        if (sizeof(U) == 4) t_pack = c.take<u64>(ns);
+        else { t_key = c.take<u64>(ns); t_tag = c.take<u32>(ns); }
+        if (sample_sorted(c.di, ns, sizeof(U) == 8)) {
+            if (sizeof(U) == 4) ts32 = new InternalSort<false>(c, ns, t_pack, nullptr);
+            else ts64 = new InternalSort<true>(c, ns, t_key, t_tag);
         } else {
-            t_key = c.take<u64>(ns);
-            t_tag = c.take<u32>(ns);
-            ts64 = new InternalSort<true>(c, ns, t_key, t_tag);
+            smg = new SampleMerge(c, ns, s, sizeof(U) == 4 ? t_pack : t_key, t_tag, sizeof(U) == 8);
         }
         bound = c.take<u32>((size_t)pl * (p + 1));
         cnt = c.take<u32>((size_t)pl * p);
@@ -1445,7 +1500,7 @@ template <int DT, bool KV> struct DistDroSort : DistRun {
             f.carve_lists(lb, (p / g.world + 1) * Level1<DT, KV>::PS);
         }
     }
-    ~DistDroSort() { delete ts32; delete ts64; delete l1s; delete l1x; }
+    ~DistDroSort() { delete ts32; delete ts64; delete smg; delete l1s; delete l1x; }
     size_t ws() const override { return c.off + 256; }
 
     void sample(char* const* d_peer) override {
@@ -1483,9 +1538,14 @@ template <int DT, bool KV> struct DistDroSort : DistRun {
         const u32 words = sizeof(U) == 4 ? 1 : 2;
         launch(c, k_dist_unpack, cdiv(ns, 256), 256, 0, (const u64*)(win + g.W.rec), ns, words, t_pack, t_key, t_tag);
         c.check();
-        if (ts32) ts32->run(0xd0d0);
+        fin_pack = t_pack; fin_key = t_key; fin_tag = t_tag;
+        if (smg) {
+            const int b = smg->run();
+            if (sizeof(U) == 4) fin_pack = smg->k[b];
+            else { fin_key = smg->k[b]; fin_tag = smg->t[b]; }
+        } else if (ts32) ts32->run(0xd0d0);
         else ts64->run(0xd0d0);
-        launch(c, k_pick_splitters<U>, cdiv(g.p, 256), 256, 0, (const u64*)t_pack, (const u64*)t_key, (const u32*)t_tag,
+        launch(c, k_pick_splitters<U>, cdiv(g.p, 256), 256, 0, fin_pack, fin_key, fin_tag,
                g.p, s, 1u, sk, st);
         c.check();
     }

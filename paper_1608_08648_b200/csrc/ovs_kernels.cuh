@@ -3354,6 +3354,136 @@ __global__ void k_dro_sample(const U* xs, u32 n, u32 p, u32 s, u32 padded, u64* 
     else { t_key[id] = (u64)key; t_tag[id] = tag; }
 }
 
+// a11: "Merge all T_k into a sorted sequence T of rp^2 keys" (Algorithm 1 step 2, PAPER.md:266;
+// the p sorted sample sequences "are then merged or sorted into T", cost
+// B p^2 r lg p).  One level of a pairwise merge: runs of L records, runs 2i and 2i+1 merged into one
+// run of 2L (an odd last run is copied).  Records compare by (key, tag): 32-bit keys one u64 word
+// (ord key << 32 | tag), 64-bit keys the key word with the tag as tie-break (W64).  Merge path:
+// each CTA writes MS_TILE outputs of one pair; warps 0 and 1 find the tile's two diagonal splits
+// by a 32-ary search (a handful of dependent L2 reads), both input ranges are staged in shared
+// memory, each thread merges MS_IT consecutive outputs (odd: bank-conflict-free transposes), the tile is stored coalesced.
+constexpr u32 MS_NT = 256, MS_IT = 9, MS_TILE = MS_NT * MS_IT;  // odd MS_IT: the per-thread runs of u64 records start on distinct bank pairs
+template <bool W64> __device__ __forceinline__ bool ms_less(u64 ka, u32 ta, u64 kb, u32 tb) {
+    return ka < kb || (W64 && ka == kb && ta < tb);
+}
+// number of A records among the first d outputs of merge(A, B) (A first on ties): the smallest
+// a with !(B[d-1-a] < A[a]) false, i.e. pred(m) = !(B[d-1-m] < A[m]) holds exactly for m < a
+template <bool W64>
+__device__ __forceinline__ u32 ms_split_warp(const u64* A, const u32* At, u32 la, const u64* B, const u32* Bt,
+                                             u32 lb, u32 d, u32 lane) {
+    u32 lo = d > lb ? d - lb : 0, hi = min(d, la);
+    while (hi > lo) {
+        const u32 step = (hi - lo + 31) / 32;
+        const u32 m = lo + lane * step;
+        bool pr = false;
+        if (m < hi) pr = !ms_less<W64>(B[d - 1 - m], W64 ? Bt[d - 1 - m] : 0u, A[m], W64 ? At[m] : 0u);
+        const u32 cnt = __popc(__ballot_sync(~0u, pr));
+        if (cnt == 0) hi = lo;
+        else {
+            lo = lo + (cnt - 1) * step + 1;
+            hi = min(hi, lo - 1 + step);
+        }
+    }
+    return lo;
+}
+template <bool W64>
+__global__ void __launch_bounds__(MS_NT) k_sample_merge(const u64* __restrict__ ik, const u32* __restrict__ it,
+                                                        u64* __restrict__ ok, u32* __restrict__ ot, u32 N, u32 L,
+                                                        u32 tpp) {
+    PDL_PROLOGUE();
+    __shared__ u64 sk[MS_TILE];
+    __shared__ u32 stg[W64 ? MS_TILE : 1];
+    __shared__ u32 spl[2];
+    const u32 pair = blockIdx.x / tpp, tile = blockIdx.x % tpp;
+    const u64 base = (u64)pair * 2 * L;
+    if (base >= N) return;
+    const u32 la = (u32)min((u64)L, N - base);
+    const u32 lb = (u32)min((u64)L, N - base - la);
+    const u32 d0 = tile * MS_TILE;
+    if (d0 >= la + lb) return;
+    const u32 d1 = min(d0 + MS_TILE, la + lb);
+    const u64* A = ik + base;
+    const u64* B = A + la;
+    const u32* At = W64 ? it + base : nullptr;
+    const u32* Bt = W64 ? At + la : nullptr;
+    const u32 tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (warp < 2) {
+        const u32 a = ms_split_warp<W64>(A, At, la, B, Bt, lb, warp ? d1 : d0, lane);
+        if (lane == 0) spl[warp] = a;
+    }
+    __syncthreads();
+    const u32 a0 = spl[0], a1 = spl[1], b0 = d0 - a0, b1 = d1 - a1;
+    const u32 na = a1 - a0, nb = b1 - b0, nt = na + nb;
+    {  // all MS_IT loads of a thread in flight before the shared stores
+        u64 v[MS_IT];
+        u32 vt[MS_IT];
+#pragma unroll
+        for (u32 q = 0; q < MS_IT; ++q) {
+            const u32 i = tid + q * MS_NT;
+            const bool fa = i < na;
+            const u32 g = fa ? a0 + i : b0 + (i - na);
+            if (i < nt) {
+                v[q] = *((fa ? A : B) + g);
+                if (W64) vt[q] = *((fa ? At : Bt) + g);
+            }
+        }
+#pragma unroll
+        for (u32 q = 0; q < MS_IT; ++q) {
+            const u32 i = tid + q * MS_NT;
+            if (i < nt) {
+                sk[i] = v[q];
+                if (W64) stg[i] = vt[q];
+            }
+        }
+    }
+    __syncthreads();
+    // this thread's outputs [dl, dl + MS_IT) of the tile: split by a binary search in shared memory
+    const u32 dl = min(tid * MS_IT, nt);
+    u32 lo = dl > nb ? dl - nb : 0, hi = min(dl, na);
+    while (lo < hi) {
+        const u32 m = (lo + hi) >> 1;
+        if (!ms_less<W64>(sk[na + dl - 1 - m], W64 ? stg[na + dl - 1 - m] : 0u, sk[m], W64 ? stg[m] : 0u)) lo = m + 1;
+        else hi = m;
+    }
+    u32 i = lo, j = dl - lo;
+    u64 rk[MS_IT];
+    u32 rt[MS_IT];
+    // the two heads stay in registers: one shared read per output (the side just consumed)
+    u64 ka = i < na ? sk[i] : 0ull, kb = j < nb ? sk[na + j] : 0ull;
+    u32 ta_ = (W64 && i < na) ? stg[i] : 0u, tb_ = (W64 && j < nb) ? stg[na + j] : 0u;
+#pragma unroll
+    for (u32 q = 0; q < MS_IT; ++q) {
+        const bool ta = j >= nb || (i < na && !ms_less<W64>(kb, tb_, ka, ta_));
+        rk[q] = ta ? ka : kb;
+        rt[q] = ta ? ta_ : tb_;
+        if (ta) {
+            ++i;
+            ka = i < na ? sk[i] : 0ull;
+            if (W64) ta_ = i < na ? stg[i] : 0u;
+        } else {
+            ++j;
+            kb = j < nb ? sk[na + j] : 0ull;
+            if (W64) tb_ = j < nb ? stg[na + j] : 0u;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (u32 q = 0; q < MS_IT; ++q) {
+        const u32 o = tid * MS_IT + q;
+        if (o < nt) {
+            sk[o] = rk[q];
+            if (W64) stg[o] = rt[q];
+        }
+    }
+    __syncthreads();
+    u64* O = ok + base + d0;
+    u32* Ot = W64 ? ot + base + d0 : nullptr;
+    for (u32 q = tid; q < nt; q += MS_NT) {
+        O[q] = sk[q];
+        if (W64) Ot[q] = stg[q];
+    }
+}
+
 // a13: bound[k][j+1] = #{t : (X_k[t], start_k + t) <=lex S[j]} by binary search of splitter j
 // into the sorted X_k; count matrix cnt[k][j] = bound[k][j+1]-bound[k][j]
 // (P buckets: P - 1 splitters; P = p for the contract split, p*f for the fine split of f2)

@@ -264,6 +264,22 @@ def test_c4_full(ovs, orc):
     dro_case(ovs, orc, ovs_inputs.keys("u16key", c["n"], seed=41), c["p"], c["s"], kv=True)
 
 
+@pytest.mark.parametrize("force,dist,dseed", [("0", None, 41), ("1", "i32_uniform", 21), ("1", "f64_normal", 2)])
+def test_dro_sample_merge_and_sort(ovs, orc, monkeypatch, force, dist, dseed):
+    """a11 both ways (Algorithm 1 step 2: the p sorted T_k "merged or sorted" into T,
+    PAPER.md:359-364): C4 with its sample merged (it is sorted by default, 56.6 MB > L2/4), and
+    C2 / an f64 case with their samples sorted (merged by default); same splitters and output."""
+    monkeypatch.setenv("OVS_DRO_SAMPLE_SORT", force)
+    if dist is None:
+        c = ovs_inputs.CONFIGS["C4"]
+        dro_case(ovs, orc, ovs_inputs.keys("u16key", c["n"], seed=dseed), c["p"], c["s"], kv=True)
+    elif dist == "f64_normal":
+        dro_case(ovs, orc, ovs_inputs.keys(dist, 300_001, seed=dseed), 64, 2)
+    else:
+        c = ovs_inputs.CONFIGS["C2"]
+        dro_case(ovs, orc, ovs_inputs.keys(dist, c["n"], seed=dseed), c["p"], c["s"])
+
+
 # ---------------------------------------------------------------- samples that are a large fraction of n
 @pytest.mark.parametrize("dist,n,p,s,kv", [
     ("u32", 1_000_000, 64, 12_000, False),      # ps-1 = 0.77 n: the direct-address sample table

@@ -223,6 +223,48 @@ class Sorter:
         return g.replay
 
 
+class HostPipeline:
+    """Sorts a stream of host key arrays (pinned, n keys each) with one Sorter: step k's host->device
+    copy and step k-1's device->host copy run on their own streams (the two PCIe directions and
+    copy engines) while the sorts run one after another on a third, so a stream of host sorts is
+    bound by the slower copy direction instead of the sum of both copies and the sort.  Two device
+    buffers alternate; a buffer is refilled only after its previous result has left the device."""
+
+    def __init__(self, sorter: "Sorter", dtype):
+        import torch
+        assert not sorter.kv, "keys-only sorter"
+        dev = sorter.ws.device
+        self.sorter = sorter
+        self.buf = [torch.empty(sorter.n, dtype=dtype, device=dev) for _ in range(2)]
+        self.s_in, self.s_sort, self.s_out = (torch.cuda.Stream(device=dev) for _ in range(3))
+        self.freed = [None, None]
+        self.k = 0
+
+    def submit(self, host_in, host_out):
+        """Enqueue: host_in -> device, sort, device -> host_out (both pinned host tensors of n keys).
+        Returns the event that completes when host_out holds the sorted keys."""
+        import torch
+        b = self.k & 1
+        self.k += 1
+        if self.freed[b] is not None:
+            self.s_in.wait_event(self.freed[b])
+        with torch.cuda.stream(self.s_in):
+            self.buf[b].copy_(host_in, non_blocking=True)
+        loaded = torch.cuda.Event()
+        loaded.record(self.s_in)
+        self.s_sort.wait_event(loaded)
+        self.sorter(self.buf[b], stream=self.s_sort)
+        sorted_ = torch.cuda.Event()
+        sorted_.record(self.s_sort)
+        self.s_out.wait_event(sorted_)
+        with torch.cuda.stream(self.s_out):
+            host_out.copy_(self.buf[b], non_blocking=True)
+        done = torch.cuda.Event(enable_timing=True)
+        done.record(self.s_out)
+        self.freed[b] = done
+        return done
+
+
 def sort_keys(keys, method: str = "ros", p: int = 64, s: int = 32, seed: int = 1, padded: bool = False,
               report: bool = True):
     """Sort a CUDA tensor (uint32 / int32 / float64) in place; returns the report."""

@@ -502,8 +502,8 @@ template <bool KV> struct InternalSort {
 
 // DRO's sample T (p sorted runs of s records): merged (SampleMerge) while the merge's two arrays
 // fit in half the L2, else sorted by the generic internal sort — measured on B200: C2 (12.6 MB of
-// records) 0.20 -> 0.11 ms merged; C4 (56.6 MB) 0.43 ms sorted, 0.48 ms merged (9 levels that
-// miss L2).  OVS_DRO_SAMPLE_SORT=1 / =0 forces the sort / the merge (experiments and tests).
+// records) 0.20 -> 0.11 ms merged; C4 (56.6 MB, 9 levels that miss L2) 0.43 ms sorted, 0.42 ms
+// merged (break-even).  OVS_DRO_SAMPLE_SORT=1 / =0 forces the sort / the merge (experiments and tests).
 static inline bool sample_sorted(const DevInfo& di, u64 ns, bool w64) {
     const char* v = getenv("OVS_DRO_SAMPLE_SORT");
     if (v && (v[0] == '0' || v[0] == '1')) return v[0] == '1';

@@ -3362,7 +3362,7 @@ __global__ void k_dro_sample(const U* xs, u32 n, u32 p, u32 s, u32 padded, u64* 
 // each CTA writes MS_TILE outputs of one pair; warps 0 and 1 find the tile's two diagonal splits
 // by a 32-ary search (a handful of dependent L2 reads), both input ranges are staged in shared
 // memory, each thread merges MS_IT consecutive outputs (odd: bank-conflict-free transposes), the tile is stored coalesced.
-constexpr u32 MS_NT = 256, MS_IT = 9, MS_TILE = MS_NT * MS_IT;  // odd MS_IT: the per-thread runs of u64 records start on distinct bank pairs
+constexpr u32 MS_NT = 256, MS_IT = 15, MS_TILE = MS_NT * MS_IT;  // odd MS_IT: the per-thread runs of u64 records start on distinct bank pairs
 template <bool W64> __device__ __forceinline__ bool ms_less(u64 ka, u32 ta, u64 kb, u32 tb) {
     return ka < kb || (W64 && ka == kb && ta < tb);
 }

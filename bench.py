@@ -409,8 +409,9 @@ def main():
                 "roofline": roofline, "cpu_baseline": cpu, "cpu_baselines_context": cpu_extra,
                 "e2e": {"value": e2e_v, "unit": "Gkeys/s", "h2d_bytes_per_step": int(n * 4),
                         "d2h_bytes_per_step": int(n * 4), "ms_per_step": e2e_ms,
-                        "how": f"{args.e2e_steps} host-to-host sorts streamed through ovs.HostPipeline (H2D of step k "
-                               "overlaps D2H of step k-1 and the sorts), device-timed first H2D start to last D2H end",
+                        "how": f"{args.e2e_steps} host-to-host sorts streamed through ovs.HostPipeline (three rotating "
+                               "device buffers: H2D of step k overlaps D2H of step k-1 and the sorts), device-timed "
+                               "first H2D start to last D2H end",
                         "serial_ms_per_step": e2e_serial_ms,
                         "serial_value": n * world / (e2e_serial_ms * 1e-3) / 1e9},
                 "gpu_launches": launches_per_step * args.steps, "launches_per_step": launches_per_step,

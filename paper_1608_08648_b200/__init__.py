@@ -227,24 +227,27 @@ class HostPipeline:
     """Sorts a stream of host key arrays (pinned, n keys each) with one Sorter: step k's host->device
     copy and step k-1's device->host copy run on their own streams (the two PCIe directions and
     copy engines) while the sorts run one after another on a third, so a stream of host sorts is
-    bound by the slower copy direction instead of the sum of both copies and the sort.  Two device
-    buffers alternate; a buffer is refilled only after its previous result has left the device."""
+    bound by the slower copy direction instead of the sum of both copies and the sort.  nbuf device
+    buffers rotate; a buffer is refilled only after its previous result has left the device.  With two
+    buffers step k+1's copy-in waits for step k-1's copy-out, which started a sort's time after step
+    k's copy-in, so every step pays the sort once more; with three (the default) the copy-in never waits."""
 
-    def __init__(self, sorter: "Sorter", dtype):
+    def __init__(self, sorter: "Sorter", dtype, nbuf: int = 3):
         import torch
         assert not sorter.kv, "keys-only sorter"
         dev = sorter.ws.device
         self.sorter = sorter
-        self.buf = [torch.empty(sorter.n, dtype=dtype, device=dev) for _ in range(2)]
+        assert nbuf >= 1
+        self.buf = [torch.empty(sorter.n, dtype=dtype, device=dev) for _ in range(nbuf)]
         self.s_in, self.s_sort, self.s_out = (torch.cuda.Stream(device=dev) for _ in range(3))
-        self.freed = [None, None]
+        self.freed = [None] * nbuf
         self.k = 0
 
     def submit(self, host_in, host_out):
         """Enqueue: host_in -> device, sort, device -> host_out (both pinned host tensors of n keys).
         Returns the event that completes when host_out holds the sorted keys."""
         import torch
-        b = self.k & 1
+        b = self.k % len(self.buf)
         self.k += 1
         if self.freed[b] is not None:
             self.s_in.wait_event(self.freed[b])

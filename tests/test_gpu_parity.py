@@ -135,14 +135,16 @@ def test_determinism_and_streams(ovs):
     np.testing.assert_array_equal(a[2].splitter_tags, b[2].splitter_tags)
 
 
-def test_host_pipeline(ovs, orc):
-    """ovs.HostPipeline (the e2e path bench.py times): five different host arrays streamed through
-    two device buffers and three streams; every host result equals the oracle's output for its input
-    (no step reads another step's buffer)."""
+@pytest.mark.parametrize("nbuf", [1, 2, 3])
+def test_host_pipeline(ovs, orc, nbuf):
+    """ovs.HostPipeline (the e2e path bench.py times): seven different host arrays streamed through
+    nbuf rotating device buffers (3 is the default) and three streams; every host result equals the
+    oracle's output for its input (no step reads another step's buffer)."""
     n, p, s, seed = (1 << 20) + 77, 64, 32, 3
     srt = ovs.Sorter(n, torch.uint32, False, "ros", p, s, seed)
-    pipe = ovs.HostPipeline(srt, torch.uint32)
-    xs = [ovs_inputs.keys(d, n, seed=10 + i) for i, d in enumerate(["u32", "u32_u31", "u32_few4", "u32", "u32_const"])]
+    pipe = ovs.HostPipeline(srt, torch.uint32, nbuf)
+    xs = [ovs_inputs.keys(d, n, seed=10 + i)
+          for i, d in enumerate(["u32", "u32_u31", "u32_few4", "u32", "u32_const", "u32_u31", "u32"])]
     hin = [torch.from_numpy(x).pin_memory() for x in xs]
     hout = [torch.empty_like(h).pin_memory() for h in hin]
     evs = [pipe.submit(a, b) for a, b in zip(hin, hout)]

@@ -199,6 +199,36 @@ size_t ovs_dist_virtual_workspace_bytes(int world, const size_t* n_local, int dt
  * host computation from the device's shared-memory size (no launch). */
 int ovs_auto_params(size_t n, int dtype, int with_values, int method, ovs_params* out);
 
+/* ---------------------------------------------------------------------------------------
+ * Host buffers (the end-to-end path): a stream of keys-only sorts of n keys
+ * each, from and to PINNED host memory, the problem statement of PAPER.md:254 with the keys
+ * starting and ending in host memory.  Every submitted step copies its whole input to the device,
+ * sorts it there (ovs_sort_keys, same splitters and counts) and copies the whole result back; the
+ * pipe runs step k's host->device copy, the sorts, and step k-1's device->host copy on three CUDA
+ * streams of its own, so a stream of sorts is bound by the slower PCIe direction, not by the sum
+ * of both copies and the sort.
+ *   ovs_host_pipe_create: d_bufs[0..nbuf) are nbuf (1..16; 3 lets a copy-in never wait) device
+ *     buffers of n keys each and d_ws a workspace of ws_bytes >= ovs_workspace_bytes(n, dtype, 0,
+ *     prm); all stay the caller's, must outlive the pipe and must not be used by the caller while
+ *     steps are in flight.  The pipe owns only its streams and events (on the device current at
+ *     creation).  OVS_EINVAL / OVS_EDTYPE / OVS_EWORKSPACE / OVS_ECUDA.
+ *   ovs_host_pipe_submit: enqueue one step h_in -> device -> sort -> h_out (host pointers, n keys
+ *     each, page-locked so the copies are asynchronous; h_in may equal h_out; h_in must stay
+ *     unchanged and h_out unread until the next ovs_host_pipe_wait).  Returns without waiting for
+ *     the device (a buffer is refilled only after its previous result has left the device; that
+ *     wait is on the device).  Errors as ovs_sort_keys.
+ *   ovs_host_pipe_wait: blocks until every submitted step's result is in host memory; *ms (may be
+ *     NULL) = device time from the start of the first copy-in submitted since the previous wait to
+ *     the end of the last copy-out.  Returns OVS_OK, or OVS_EINTERNAL if a device-side check of
+ *     any of those sorts failed (ovs_device_status semantics; the sticky word is reset).
+ *   ovs_host_pipe_destroy: waits for the pipe's streams and releases them (NULL is allowed). */
+typedef struct ovs_host_pipe ovs_host_pipe;
+int ovs_host_pipe_create(ovs_host_pipe** out, size_t n, int dtype, const ovs_params* prm, void* const* d_bufs,
+                         int nbuf, void* d_ws, size_t ws_bytes);
+int ovs_host_pipe_submit(ovs_host_pipe* hp, const void* h_in, void* h_out);
+int ovs_host_pipe_wait(ovs_host_pipe* hp, float* ms);
+int ovs_host_pipe_destroy(ovs_host_pipe* hp);
+
 /* Profiling hook (thread-local): subsequent sort calls on this thread record events[k]
  * (cudaEvent_t passed as void*) on their stream at phase boundary k, without synchronising:
  *   0 start, 1 after the sample draw + gather (a1-a2), 2 after the sample sort + splitters

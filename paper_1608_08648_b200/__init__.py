@@ -69,6 +69,15 @@ def lib() -> ctypes.CDLL:
         L.ovs_auto_params.argtypes = [sz, i32, i32, i32, ctypes.POINTER(Params)]
         L.ovs_device_status.restype = i32
         L.ovs_device_status.argtypes = [vp, vp, ctypes.POINTER(ctypes.c_uint32), i32]
+        L.ovs_host_pipe_create.restype = i32
+        L.ovs_host_pipe_create.argtypes = [ctypes.POINTER(vp), sz, i32, ctypes.POINTER(Params),
+                                           ctypes.POINTER(vp), i32, vp, sz]
+        L.ovs_host_pipe_submit.restype = i32
+        L.ovs_host_pipe_submit.argtypes = [vp, vp, vp]
+        L.ovs_host_pipe_wait.restype = i32
+        L.ovs_host_pipe_wait.argtypes = [vp, ctypes.POINTER(ctypes.c_float)]
+        L.ovs_host_pipe_destroy.restype = i32
+        L.ovs_host_pipe_destroy.argtypes = [vp]
         L.ovs_last_error.restype = ctypes.c_char_p
         L.ovs_version.restype = ctypes.c_char_p
         _lib = L
@@ -224,48 +233,57 @@ class Sorter:
 
 
 class HostPipeline:
-    """Sorts a stream of host key arrays (pinned, n keys each) with one Sorter: step k's host->device
-    copy and step k-1's device->host copy run on their own streams (the two PCIe directions and
-    copy engines) while the sorts run one after another on a third, so a stream of host sorts is
-    bound by the slower copy direction instead of the sum of both copies and the sort.  nbuf device
-    buffers rotate; a buffer is refilled only after its previous result has left the device.  With two
-    buffers step k+1's copy-in waits for step k-1's copy-out, which started a sort's time after step
-    k's copy-in, so every step pays the sort once more; with three (the default) the copy-in never waits."""
+    """ovs_host_pipe_* (include/ovs.h): sorts a stream of pinned host key arrays (n keys each) with one
+    Sorter's parameters and workspace.  The library runs step k's host->device copy, the sorts and step
+    k-1's device->host copy on its own three streams over nbuf rotating device buffers (allocated here
+    as torch tensors; three let a copy-in never wait), so a stream of host sorts is bound by the slower
+    PCIe direction instead of the sum of both copies and the sort.  This class only marshals arguments."""
 
     def __init__(self, sorter: "Sorter", dtype, nbuf: int = 3):
         import torch
         assert not sorter.kv, "keys-only sorter"
         dev = sorter.ws.device
         self.sorter = sorter
-        assert nbuf >= 1
-        self.buf = [torch.empty(sorter.n, dtype=dtype, device=dev) for _ in range(nbuf)]
-        self.s_in, self.s_sort, self.s_out = (torch.cuda.Stream(device=dev) for _ in range(3))
-        self.freed = [None] * nbuf
-        self.k = 0
+        self.bytes = sorter.n * {OVS_F64: 8, OVS_S32: 32}.get(sorter.dt, 4)
+        with torch.cuda.device(dev):
+            self.buf = [torch.empty(self.bytes, dtype=torch.uint8, device=dev) for _ in range(nbuf)]
+            torch.cuda.synchronize(dev)  # the pipe's streams do not wait for torch's
+            ptrs = (ctypes.c_void_p * nbuf)(*[b.data_ptr() for b in self.buf])
+            self.h = ctypes.c_void_p()
+            rc = lib().ovs_host_pipe_create(ctypes.byref(self.h), sorter.n, sorter.dt, ctypes.byref(sorter.prm), ptrs,
+                                            nbuf, sorter.ws.data_ptr(), sorter.ws_bytes)
+        if rc != OVS_OK:
+            sorter._raise(rc)
 
-    def submit(self, host_in, host_out):
-        """Enqueue: host_in -> device, sort, device -> host_out (both pinned host tensors of n keys).
-        Returns the event that completes when host_out holds the sorted keys."""
-        import torch
-        b = self.k % len(self.buf)
-        self.k += 1
-        if self.freed[b] is not None:
-            self.s_in.wait_event(self.freed[b])
-        with torch.cuda.stream(self.s_in):
-            self.buf[b].copy_(host_in, non_blocking=True)
-        loaded = torch.cuda.Event()
-        loaded.record(self.s_in)
-        self.s_sort.wait_event(loaded)
-        self.sorter(self.buf[b], stream=self.s_sort)
-        sorted_ = torch.cuda.Event()
-        sorted_.record(self.s_sort)
-        self.s_out.wait_event(sorted_)
-        with torch.cuda.stream(self.s_out):
-            host_out.copy_(self.buf[b], non_blocking=True)
-        done = torch.cuda.Event(enable_timing=True)
-        done.record(self.s_out)
-        self.freed[b] = done
-        return done
+    def submit(self, host_in, host_out) -> None:
+        """Enqueue: host_in -> device, sort, device -> host_out (pinned host tensors of n keys each);
+        returns at once.  host_out is valid after wait()."""
+        assert host_in.is_pinned() and host_out.is_pinned() and host_in.is_contiguous() and host_out.is_contiguous()
+        assert host_in.numel() * host_in.element_size() == self.bytes == host_out.numel() * host_out.element_size()
+        rc = lib().ovs_host_pipe_submit(self.h, host_in.data_ptr(), host_out.data_ptr())
+        if rc != OVS_OK:
+            self.sorter._raise(rc)
+
+    def wait(self) -> float:
+        """Block until every submitted result is in host memory; returns the device time (ms) from the
+        first copy-in submitted since the previous wait to the last copy-out.  Raises if a device-side
+        check of any of those sorts failed."""
+        ms = ctypes.c_float(0.0)
+        rc = lib().ovs_host_pipe_wait(self.h, ctypes.byref(ms))
+        if rc != OVS_OK:
+            self.sorter._raise(rc)
+        return float(ms.value)
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            lib().ovs_host_pipe_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def sort_keys(keys, method: str = "ros", p: int = 64, s: int = 32, seed: int = 1, padded: bool = False,

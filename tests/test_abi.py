@@ -132,3 +132,30 @@ def test_device_status_rejects_null():
     L = ovs.lib()
     st = ctypes.c_uint32(7)
     assert L.ovs_device_status(None, None, ctypes.byref(st), 0) == ovs.OVS_EINVAL
+
+
+def test_host_pipe_rejects_bad_arguments_before_any_cuda_call():
+    """ovs_host_pipe_* (host-buffer entry): argument checks run before the first CUDA call."""
+    import paper_1608_08648_b200 as ovs
+    L = ovs.lib()
+    prm = _prm(ovs)
+    h = ctypes.c_void_p()
+    bufs = (ctypes.c_void_p * 2)(0x1000, 0x2000)  # never dereferenced: every call below fails validation
+    ws = ctypes.c_void_p(0x3000)
+    need = ovs.workspace_bytes(1 << 16, ovs.OVS_U32, False, prm)
+    C = L.ovs_host_pipe_create
+    assert C(None, 1 << 16, ovs.OVS_U32, ctypes.byref(prm), bufs, 2, ws, need) == ovs.OVS_EINVAL
+    assert C(ctypes.byref(h), 0, ovs.OVS_U32, ctypes.byref(prm), bufs, 2, ws, need) == ovs.OVS_EINVAL
+    assert C(ctypes.byref(h), 1 << 16, ovs.OVS_U32, ctypes.byref(prm), bufs, 0, ws, need) == ovs.OVS_EINVAL
+    assert C(ctypes.byref(h), 1 << 16, ovs.OVS_U32, ctypes.byref(prm), bufs, 17, ws, need) == ovs.OVS_EINVAL
+    assert C(ctypes.byref(h), 1 << 16, 9, ctypes.byref(prm), bufs, 2, ws, need) == ovs.OVS_EDTYPE
+    assert C(ctypes.byref(h), 1 << 16, ovs.OVS_U32, ctypes.byref(prm), bufs, 2, ws, need - 1) == ovs.OVS_EWORKSPACE
+    assert L.ovs_last_error().decode() == "workspace too small"
+    hole = (ctypes.c_void_p * 2)(0x1000, None)
+    assert C(ctypes.byref(h), 1 << 16, ovs.OVS_U32, ctypes.byref(prm), hole, 2, ws, need) == ovs.OVS_EINVAL
+    bad = _prm(ovs, p=0)
+    assert C(ctypes.byref(h), 1 << 16, ovs.OVS_U32, ctypes.byref(bad), bufs, 2, ws, need) == ovs.OVS_EINVAL
+    assert not h.value
+    assert L.ovs_host_pipe_submit(None, None, None) == ovs.OVS_EINVAL
+    assert L.ovs_host_pipe_wait(None, None) == ovs.OVS_EINVAL
+    assert L.ovs_host_pipe_destroy(None) == ovs.OVS_OK

@@ -137,7 +137,7 @@ def test_determinism_and_streams(ovs):
 
 @pytest.mark.parametrize("nbuf", [1, 2, 3])
 def test_host_pipeline(ovs, orc, nbuf):
-    """ovs.HostPipeline (the e2e path bench.py times): seven different host arrays streamed through
+    """ovs.HostPipeline = ovs_host_pipe_* of the C ABI (the e2e path bench.py times): seven different host arrays streamed through
     nbuf rotating device buffers (3 is the default) and three streams; every host result equals the
     oracle's output for its input (no step reads another step's buffer)."""
     n, p, s, seed = (1 << 20) + 77, 64, 32, 3
@@ -147,10 +147,16 @@ def test_host_pipeline(ovs, orc, nbuf):
           for i, d in enumerate(["u32", "u32_u31", "u32_few4", "u32", "u32_const", "u32_u31", "u32"])]
     hin = [torch.from_numpy(x).pin_memory() for x in xs]
     hout = [torch.empty_like(h).pin_memory() for h in hin]
-    evs = [pipe.submit(a, b) for a, b in zip(hin, hout)]
-    evs[-1].synchronize()
+    for a, b in zip(hin, hout):
+        pipe.submit(a, b)
+    assert pipe.wait() > 0.0
+    assert pipe.wait() == 0.0  # nothing submitted since
     for x, h in zip(xs, hout):
         np.testing.assert_array_equal(h.numpy(), orc.ros_sort(x, p, s, seed).keys)
+    pipe.submit(hin[1], hin[1])  # in place in host memory, after a wait
+    pipe.wait()
+    np.testing.assert_array_equal(hin[1].numpy(), orc.ros_sort(xs[1], p, s, seed).keys)
+    pipe.close()
 
 
 def test_error_codes(ovs):

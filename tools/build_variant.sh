@@ -8,7 +8,7 @@ C=${SRC:-/root/repo/paper_1608_08648_b200/csrc}
 NC=$(python -c "import nvidia.nccl as m; print(list(m.__path__)[0])")
 ARCH="-gencode arch=compute_100a,code=sm_100a"
 # ONLY="ovs_u32_k ..." compiles just those units with the flags and links the in-tree build's other objects
-ALL="ovs_api ovs_dist ovs_s32_k ovs_u32_k ovs_u32_v ovs_i32_k ovs_i32_v ovs_f64_k ovs_f64_v"
+ALL="ovs_api ovs_host ovs_dist ovs_s32_k ovs_u32_k ovs_u32_v ovs_i32_k ovs_i32_v ovs_f64_k ovs_f64_v"
 for f in $ALL; do
   if [ -n "$ONLY" ] && ! echo " $ONLY " | grep -q " $f "; then cp $C/build/$f.o $D/$f.o; continue; fi
   nvcc -O3 -std=c++17 $ARCH -lineinfo -Xcompiler -fPIC -I/root/repo/include -I$NC/include $FLAGS -c -o $D/$f.o $C/$f.cu &

@@ -159,6 +159,23 @@ def test_host_pipeline(ovs, orc, nbuf):
     pipe.close()
 
 
+def test_host_pipeline_f64_dro(ovs, orc):
+    """The host pipe with 8-byte keys and DRO (Algorithm 1) parameters: three host arrays through two
+    device buffers, each result equal to the oracle's DRO output."""
+    n, p, r = 64 * 4099, 64, 12
+    srt = ovs.Sorter(n, torch.float64, False, "dro", p, r, 1)
+    pipe = ovs.HostPipeline(srt, torch.float64, 2)
+    xs = [ovs_inputs.keys(d, n, seed=40 + i) for i, d in enumerate(["f64_uniform", "f64_normal", "f64_uniform"])]
+    hin = [torch.from_numpy(x).pin_memory() for x in xs]
+    hout = [torch.empty_like(h).pin_memory() for h in hin]
+    for a, b in zip(hin, hout):
+        pipe.submit(a, b)
+    pipe.wait()
+    for x, h in zip(xs, hout):
+        np.testing.assert_array_equal(h.numpy(), orc.dro_sort(x, p, r).keys)
+    pipe.close()
+
+
 def test_error_codes(ovs):
     x = torch.zeros(100, dtype=torch.uint32, device="cuda")
     with pytest.raises(ovs.OvsError) as e:
